@@ -1,0 +1,186 @@
+/*
+ * hivf.h -- C-ABI of the B200-native IVF retrieval hot path
+ *           (HedraRAG, arXiv 2507.09138: coarse assign -> list scan -> top-k).
+ *
+ * Plain C: pointers, sizes and status codes only (no C++ types, no torch types,
+ * no exceptions cross this boundary).  Every entry point names the reference
+ * interface it replaces; reference paths are relative to /root/reference/.
+ *
+ * Error mapping (reference exceptions -> status):
+ *   std::invalid_argument  -> HIVF_EINVAL    (caller misuse: nprobe/k out of range,
+ *                                             dim mismatch, duplicate doc id, ...)
+ *   std::runtime_error     -> HIVF_EINTERNAL (cluster out of plan order, cursor
+ *                                             exhausted mid-batch, ...)
+ *   plus HIVF_ECUDA / HIVF_ENOMEM / HIVF_EUNSUPPORTED for the device side.
+ * hivf_last_error() returns a thread-local message for the last failure.
+ *
+ * Threading: an hivf_ctx has one owning host thread at a time (the reference's
+ * single retrieval-worker context, proj/include/hedra/retrieval_engine.hpp:76-79).
+ * All device work is issued on the context's stream.
+ *
+ * Arithmetic contract: every distance returned is the bit-exact double the
+ * reference computes (proj/include/hedra/embedding.hpp:27-34); ids and plan
+ * orders follow the reference's (distance, id) total order
+ * (proj/include/hedra/vector_index.hpp:41-44).
+ */
+#ifndef HIVF_H_
+#define HIVF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HIVF_OK = 0,
+  HIVF_EINVAL = 1,
+  HIVF_EINTERNAL = 2,
+  HIVF_ECUDA = 3,
+  HIVF_ENOMEM = 4,
+  HIVF_EUNSUPPORTED = 5
+} hivf_status;
+
+/* Metric ids match hedra::Metric (proj/include/hedra/embedding.hpp:14). */
+enum { HIVF_METRIC_L2 = 0, HIVF_METRIC_COSINE = 1 };
+
+typedef struct hivf_ctx hivf_ctx;
+typedef struct hivf_index hivf_index;
+
+/* Thread-local description of the most recent failure ("" if none). */
+const char* hivf_last_error(void);
+const char* hivf_version(void);
+
+/* ---- context --------------------------------------------------------------
+ * Owns the device, the stream and per-call scratch.  Replaces the retrieval
+ * worker context that owns a RetrievalEngine
+ * (proj/include/hedra/retrieval_engine.hpp:80-84).  `stream` may be NULL
+ * (the context creates its own) or a cudaStream_t the caller owns. */
+hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out);
+hivf_status hivf_ctx_destroy(hivf_ctx* ctx);
+hivf_status hivf_ctx_set_stream(hivf_ctx* ctx, void* stream);
+hivf_status hivf_ctx_synchronize(hivf_ctx* ctx);
+
+/* ---- index ----------------------------------------------------------------
+ * Replaces ivf::index_from_assignments (proj/src/vector_index.cpp:210-235) and
+ * the IvfIndex it returns (proj/include/hedra/vector_index.hpp:83-113): the
+ * caller passes the lists in CSR form (list c owns rows
+ * [list_offsets[c], list_offsets[c+1]) of vectors/ids, row-major, list order
+ * as index_from_assignments leaves it).  Vectors must already be in search
+ * space (normalized for cosine, as build_index does at :245-252).  The
+ * library copies everything into HBM (chunk-major 16B-aligned list layout,
+ * see DESIGN.md); the caller keeps ownership of its arrays.
+ * EINVAL: dim == 0, n_clusters == 0, offsets not monotone, duplicate doc ids
+ * (build_index, :240-244), non-finite values. */
+hivf_status hivf_index_upload(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
+                              const float* centroids, const uint64_t* list_offsets,
+                              const float* vectors, const uint64_t* ids, hivf_index** out);
+/* Same, with `vectors`/`ids`/`centroids` in device memory (list_offsets on host).
+ * Used to build large indexes directly in HBM. */
+hivf_status hivf_index_upload_device(hivf_ctx* ctx, uint32_t dim, int metric,
+                                     uint32_t n_clusters, const float* d_centroids,
+                                     const uint64_t* list_offsets, const float* d_vectors,
+                                     const uint64_t* d_ids, hivf_index** out);
+/* Incremental build for indexes too large to stage twice (the same packing,
+ * fed in row chunks of the list-ordered CSR): begin (centroids on host or
+ * device per `centroids_on_device`, offsets on host), add_rows any number of
+ * times with device rows [first_row, first_row+n_rows) in list order, then
+ * finish (duplicate-id / finiteness checks, EINVAL on failure). */
+hivf_status hivf_index_begin(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
+                             const float* centroids, int centroids_on_device,
+                             const uint64_t* list_offsets, hivf_index** out);
+hivf_status hivf_index_add_rows_device(hivf_index* idx, uint64_t first_row, uint64_t n_rows,
+                                       const float* d_rows, const uint64_t* d_ids);
+hivf_status hivf_index_finish(hivf_index* idx);
+hivf_status hivf_index_destroy(hivf_index* idx);
+/* k_clusters / cluster_size / total_vectors / mean_assigned_distance
+ * (vector_index.hpp:92-98).  Any output pointer may be NULL. */
+hivf_status hivf_index_info(const hivf_index* idx, uint32_t* dim, uint32_t* n_clusters,
+                            uint64_t* n_vectors, uint64_t* hbm_bytes,
+                            double* mean_assigned_distance);
+hivf_status hivf_index_cluster_sizes(const hivf_index* idx, uint64_t* sizes_out);
+
+/* ---- coarse assign --------------------------------------------------------
+ * Batched ivf::select_clusters (proj/src/vector_index.cpp:261-278): for each
+ * query, the nprobe nearest centroids in exact (double distance, cluster id)
+ * order.  Queries are raw (normalized internally for cosine, :270).
+ * plans_out[n_queries*nprobe]; dists_out (optional) gets the exact doubles.
+ * EINVAL: nprobe not in [1, n_clusters] (:264). */
+hivf_status hivf_assign(hivf_index* idx, const float* queries, uint32_t n_queries,
+                        uint32_t nprobe, uint32_t* plans_out, double* dists_out);
+
+/* ---- per-request search ---------------------------------------------------
+ * Batched make_cursor + search_step over the full plan
+ * (proj/src/vector_index.cpp:280-289,319-328, per-query top-k with the
+ * TopKResult semantics of :38-53).  Host buffers: queries[n_queries*dim];
+ * ids_out / dists_out [n_queries*k] (entries past counts_out[b] are zero);
+ * counts_out[n_queries] = heap size (min(k, rows probed)).
+ * EINVAL: k == 0 (:281), nprobe out of range. */
+hivf_status hivf_search(hivf_index* idx, const float* queries, uint32_t n_queries,
+                        uint32_t nprobe, uint32_t k, uint64_t* ids_out, double* dists_out,
+                        uint32_t* counts_out);
+/* Device-pointer variant: all buffers in HBM, asynchronous on the context
+ * stream (no host synchronisation; CUDA-graph capturable after one warm call
+ * with the same (n_queries, nprobe, k)). */
+hivf_status hivf_search_device(hivf_index* idx, const float* d_queries, uint32_t n_queries,
+                               uint32_t nprobe, uint32_t k, uint64_t* d_ids_out,
+                               double* d_dists_out, uint32_t* d_counts_out);
+
+/* ---- node-split sub-search --------------------------------------------------
+ * Many cursors advanced by one sub-stage: ivf::search_clusters
+ * (proj/src/vector_index.cpp:291-317) for every item of a SubStageBatch, as
+ * RetrievalEngine::execute runs it (proj/src/retrieval_engine.cpp:94-103).
+ *   queries[n_items*dim]     the cursor query of each item, already in search
+ *                            space (SearchCursor::query, vector_index.hpp:119)
+ *   cluster_off[n_items+1], clusters[]  each item's clusters, in plan order
+ *   k[n_items]               each cursor's heap bound (SearchCursor::k)
+ *   heap_ids/heap_dists [n_items*heap_stride], heap_counts[n_items]:
+ *                            the cursor heaps, read and updated in place
+ *                            (entries sorted by (dist, id), size <= k)
+ *   changed_out[len(clusters)] per-cluster `changed` flag (:300-313), from
+ *                            which the caller derives heap_changed and
+ *                            unchanged_streak exactly as the reference does.
+ * Validation that clusters match plan order stays with the caller (the
+ * adapter), which owns the plans (EINTERNAL there, as :295-298). */
+hivf_status hivf_scan_items(hivf_index* idx, const float* queries, uint32_t n_items,
+                            const uint32_t* cluster_off, const uint32_t* clusters,
+                            const uint32_t* k, uint64_t* heap_ids, double* heap_dists,
+                            uint32_t* heap_counts, uint32_t heap_stride,
+                            uint8_t* changed_out);
+
+/* ---- multi-GPU merge ------------------------------------------------------
+ * merge_topk (proj/src/vector_index.cpp:71-91) of n_parts per-shard top-k
+ * lists per query, on device: parts laid out [n_parts][n_queries][k]
+ * (ids u64, dists f64, counts u32 [n_parts][n_queries]) as an all-gather
+ * leaves them.  Output [n_queries][k] + counts. */
+hivf_status hivf_merge_parts_device(hivf_ctx* ctx, uint32_t n_parts, uint32_t n_queries,
+                                    uint32_t k, const uint64_t* d_ids, const double* d_dists,
+                                    const uint32_t* d_counts, uint64_t* d_ids_out,
+                                    double* d_dists_out, uint32_t* d_counts_out);
+
+/* ---- hot-cluster residency set ---------------------------------------------
+ * Device side of cache::ClusterCacheState (proj/include/hedra/tiered_cache.hpp
+ * :37-78): the host adapter keeps the reference's bookkeeping; these calls
+ * apply a residency set to the device (hot lists are scheduled first and kept
+ * L2-persistent while resident). */
+hivf_status hivf_residency_set(hivf_index* idx, const uint32_t* clusters, uint32_t n);
+hivf_status hivf_residency_get(const hivf_index* idx, uint8_t* resident_out);
+
+/* ---- introspection (bench / tests) ----------------------------------------- */
+typedef struct {
+  uint32_t kernels_launched;   /* kernels issued by the last search call */
+  uint32_t n_work_items;       /* grouped-scan work items of the last call */
+  uint32_t n_fallback;         /* queries that took the exact fallback path */
+  uint32_t n_unique_lists;     /* distinct lists probed by the last batch */
+  uint64_t scan_bytes;         /* algorithmic list bytes of the last batch */
+} hivf_stats;
+hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
+/* Tuning knobs (0 = default): rows per scan segment, force exact path. */
+hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HIVF_H_ */

@@ -1,0 +1,103 @@
+"""ctypes binding of libhivf.so (include/hivf.h).
+
+The library is the product: there is no Python/CPU fallback.  Loading fails
+loudly if the in-tree libhivf.so is missing (build it with
+``python -m paper_2507_09138_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libhivf.so")
+
+HIVF_OK, HIVF_EINVAL, HIVF_EINTERNAL, HIVF_ECUDA, HIVF_ENOMEM, HIVF_EUNSUPPORTED = range(6)
+
+# header-declared symbols (tests check every one is exported)
+SYMBOLS = [
+    "hivf_last_error", "hivf_version", "hivf_ctx_create", "hivf_ctx_destroy",
+    "hivf_ctx_set_stream", "hivf_ctx_synchronize", "hivf_index_upload",
+    "hivf_index_upload_device", "hivf_index_begin", "hivf_index_add_rows_device",
+    "hivf_index_finish", "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
+    "hivf_assign", "hivf_search", "hivf_search_device", "hivf_scan_items",
+    "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get", "hivf_last_stats",
+    "hivf_set_option",
+]
+
+
+class HivfError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"hivf status {status}: {msg}")
+        self.status = status
+
+
+class InvalidArgument(HivfError, ValueError):
+    """std::invalid_argument of the reference."""
+
+
+class InternalError(HivfError):
+    """std::runtime_error of the reference."""
+
+
+class Stats(C.Structure):
+    _fields_ = [("kernels_launched", C.c_uint32), ("n_work_items", C.c_uint32),
+                ("n_fallback", C.c_uint32), ("n_unique_lists", C.c_uint32),
+                ("scan_bytes", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build it with `python -m paper_2507_09138_b200.build`"
+                          " (the CUDA path is the only path; there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, u32, u64, i32, f64 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_double
+    P = C.POINTER
+    sig = {
+        "hivf_last_error": (C.c_char_p, []),
+        "hivf_version": (C.c_char_p, []),
+        "hivf_ctx_create": (i32, [i32, vp, P(vp)]),
+        "hivf_ctx_destroy": (i32, [vp]),
+        "hivf_ctx_set_stream": (i32, [vp, vp]),
+        "hivf_ctx_synchronize": (i32, [vp]),
+        "hivf_index_upload": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, P(vp)]),
+        "hivf_index_upload_device": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, P(vp)]),
+        "hivf_index_begin": (i32, [vp, u32, i32, u32, vp, i32, vp, P(vp)]),
+        "hivf_index_add_rows_device": (i32, [vp, u64, u64, vp, vp]),
+        "hivf_index_finish": (i32, [vp]),
+        "hivf_index_destroy": (i32, [vp]),
+        "hivf_index_info": (i32, [vp, P(u32), P(u32), P(u64), P(u64), P(f64)]),
+        "hivf_index_cluster_sizes": (i32, [vp, vp]),
+        "hivf_assign": (i32, [vp, vp, u32, u32, vp, vp]),
+        "hivf_search": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
+        "hivf_search_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
+        "hivf_scan_items": (i32, [vp, vp, u32, vp, vp, vp, vp, vp, vp, u32, vp]),
+        "hivf_merge_parts_device": (i32, [vp, u32, u32, u32, vp, vp, vp, vp, vp, vp]),
+        "hivf_residency_set": (i32, [vp, vp, u32]),
+        "hivf_residency_get": (i32, [vp, vp]),
+        "hivf_last_stats": (i32, [vp, P(Stats)]),
+        "hivf_set_option": (i32, [vp, C.c_char_p, C.c_int64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status == HIVF_OK:
+        return
+    msg = lib().hivf_last_error().decode(errors="replace")
+    if status == HIVF_EINVAL:
+        raise InvalidArgument(status, msg)
+    if status == HIVF_EINTERNAL:
+        raise InternalError(status, msg)
+    raise HivfError(status, msg)

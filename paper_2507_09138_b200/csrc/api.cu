@@ -1,0 +1,812 @@
+// api.cu -- the C-ABI (include/hivf.h): contexts, HBM index, batched search,
+// coarse assign, node-split sub-search, shard merge, residency.
+//
+// No exceptions and no CPU fallback: every compute entry point runs the
+// device kernels of this library; failures come back as hivf_status with a
+// thread-local message.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/hivf.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace hivf;
+
+namespace {
+
+thread_local std::string g_err;
+
+hivf_status fail(hivf_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? HIVF_ENOMEM : HIVF_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                    \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(HIVF_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                             \
+  } while (0)
+
+// Grow-only device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    want = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct HBuf {  // grow-only pinned host buffer
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(want, 256));
+    if (e == cudaSuccess) bytes = std::max<size_t>(want, 256);
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct hivf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 148;
+  // options
+  uint32_t opt_seg_rows = 4096;
+  int opt_force_exact = 0;
+  int opt_scan_ctas = 0;
+  // scratch
+  DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
+      list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
+      cand_n, out_ids, out_d, out_cnt, qin, it_off, it_cl, it_k, heap_ids, heap_d, heap_n,
+      changed;
+  HBuf hstage;
+  hivf_stats stats{};
+  uint32_t last_nq = 0;
+  ~hivf_ctx() {
+    for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq, &pl,
+                    &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items, &n_items,
+                    &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &out_d, &out_cnt,
+                    &qin, &it_off, &it_cl, &it_k, &heap_ids, &heap_d, &heap_n, &changed})
+      b->release();
+    hstage.release();
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+struct hivf_index {
+  hivf_ctx* ctx = nullptr;
+  uint32_t dim = 0, dpad = 0, K = 0;
+  int metric = 0;
+  uint64_t N = 0;
+  std::vector<uint64_t> list_off;  // host copy
+  float* vec = nullptr;
+  uint64_t* ids = nullptr;
+  float* xnorm2 = nullptr;
+  uint64_t* d_list_off = nullptr;
+  uint32_t* maxnorm_bits = nullptr;
+  float* cent = nullptr;
+  float* cnorm2 = nullptr;
+  float* cnorm = nullptr;
+  uint32_t* list_order = nullptr;
+  int* d_err = nullptr;
+  uint64_t rows_added = 0;
+  bool finished = false;
+  double mean_assigned = -1.0;
+  uint32_t seg_rows = 4096, s_max = 1;
+  std::vector<uint8_t> resident;
+  IndexView view() const {
+    IndexView v{};
+    v.vec = vec;
+    v.ids = ids;
+    v.xnorm2 = xnorm2;
+    v.list_off = d_list_off;
+    v.maxnorm = reinterpret_cast<const float*>(maxnorm_bits);
+    v.cent = cent;
+    v.cnorm2 = cnorm2;
+    v.cnorm = cnorm;
+    v.list_order = list_order;
+    v.dim = dim;
+    v.dpad = dpad;
+    v.K = K;
+    v.N = N;
+    v.seg_rows = seg_rows;
+    v.s_max = s_max;
+    v.metric = metric;
+    return v;
+  }
+  ~hivf_index() {
+    for (void* p : {(void*)vec, (void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits,
+                    (void*)cent, (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err})
+      if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+const char* hivf_last_error(void) { return g_err.c_str(); }
+const char* hivf_version(void) { return "hivf 0.1.0 (sm_100a)"; }
+
+hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
+  if (!out) return fail(HIVF_EINVAL, "hivf_ctx_create: out is NULL");
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(HIVF_EINVAL, "hivf_ctx_create: no device %d", device);
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(HIVF_EUNSUPPORTED, "hivf: device %d is sm_%d%d, this build is sm_100a only", device,
+                prop.major, prop.minor);
+  auto* c = new hivf_ctx;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      return fail(HIVF_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+    c->own_stream = true;
+  }
+  *out = c;
+  return HIVF_OK;
+}
+
+hivf_status hivf_ctx_destroy(hivf_ctx* ctx) {
+  if (!ctx) return HIVF_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+  return HIVF_OK;
+}
+
+hivf_status hivf_ctx_set_stream(hivf_ctx* ctx, void* stream) {
+  if (!ctx) return fail(HIVF_EINVAL, "ctx is NULL");
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  ctx->own_stream = false;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  if (!stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  return HIVF_OK;
+}
+
+hivf_status hivf_ctx_synchronize(hivf_ctx* ctx) {
+  if (!ctx) return fail(HIVF_EINVAL, "ctx is NULL");
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HIVF_OK;
+}
+
+hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
+  if (!ctx || !name) return fail(HIVF_EINVAL, "hivf_set_option: NULL argument");
+  if (!strcmp(name, "seg_rows")) {
+    if (value == 0) value = 4096;
+    if (value < kRowBlock || value % kRowBlock) return fail(HIVF_EINVAL, "seg_rows must be a multiple of %d", kRowBlock);
+    ctx->opt_seg_rows = (uint32_t)value;
+  } else if (!strcmp(name, "force_exact")) {
+    ctx->opt_force_exact = value != 0;
+  } else if (!strcmp(name, "scan_ctas")) {
+    ctx->opt_scan_ctas = (int)value;
+  } else {
+    return fail(HIVF_EINVAL, "hivf_set_option: unknown option '%s'", name);
+  }
+  return HIVF_OK;
+}
+
+hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
+  if (!ctx || !out) return fail(HIVF_EINVAL, "NULL argument");
+  CK(cudaStreamSynchronize(ctx->stream));
+  hivf_stats s = ctx->stats;
+  if (ctx->n_items.p) CK(cudaMemcpy(&s.n_work_items, ctx->n_items.p, 4, cudaMemcpyDeviceToHost));
+  if (ctx->last_nq && ctx->flags_f.p && ctx->flags_c.p) {
+    std::vector<int> f(ctx->last_nq), g(ctx->last_nq);
+    CK(cudaMemcpy(f.data(), ctx->flags_f.p, 4ull * ctx->last_nq, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(g.data(), ctx->flags_c.p, 4ull * ctx->last_nq, cudaMemcpyDeviceToHost));
+    s.n_fallback = 0;
+    for (uint32_t i = 0; i < ctx->last_nq; ++i) s.n_fallback += (f[i] != 0) + (g[i] != 0);
+  }
+  *out = s;
+  return HIVF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// index build
+// ---------------------------------------------------------------------------
+
+hivf_status hivf_index_begin(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
+                             const float* centroids, int centroids_on_device,
+                             const uint64_t* list_offsets, hivf_index** out) {
+  if (!ctx || !out || !centroids || !list_offsets) return fail(HIVF_EINVAL, "hivf_index_begin: NULL argument");
+  if (dim == 0) return fail(HIVF_EINVAL, "index: dim must be >= 1");
+  if (n_clusters == 0) return fail(HIVF_EINVAL, "index: n_clusters must be >= 1");
+  if (metric != HIVF_METRIC_L2 && metric != HIVF_METRIC_COSINE) return fail(HIVF_EINVAL, "index: unknown metric %d", metric);
+  if (list_offsets[0] != 0) return fail(HIVF_EINVAL, "index: list_offsets[0] must be 0");
+  for (uint32_t c = 0; c < n_clusters; ++c)
+    if (list_offsets[c + 1] < list_offsets[c]) return fail(HIVF_EINVAL, "index: list_offsets not monotone at %u", c);
+  const uint64_t N = list_offsets[n_clusters];
+  if (N >= 0xffffffffull) return fail(HIVF_EUNSUPPORTED, "index: more than 2^32-2 vectors per device");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  auto* ix = new hivf_index;
+  ix->ctx = ctx;
+  ix->dim = dim;
+  ix->dpad = (dim + kChunk - 1) / kChunk * kChunk;
+  ix->K = n_clusters;
+  ix->metric = metric;
+  ix->N = N;
+  ix->list_off.assign(list_offsets, list_offsets + n_clusters + 1);
+  ix->resident.assign(n_clusters, 0);
+  uint64_t maxn = 0;
+  for (uint32_t c = 0; c < n_clusters; ++c) maxn = std::max(maxn, list_offsets[c + 1] - list_offsets[c]);
+  ix->seg_rows = ctx->opt_seg_rows;
+  ix->s_max = (uint32_t)std::max<uint64_t>(1, (maxn + ix->seg_rows - 1) / ix->seg_rows);
+  auto bail = [&](cudaError_t e, const char* what) {
+    delete ix;
+    return fail(e == cudaErrorMemoryAllocation ? HIVF_ENOMEM : HIVF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&ix->vec, std::max<uint64_t>(16, N * ix->dpad * 4))) != cudaSuccess) return bail(e, "alloc lists");
+  if ((e = cudaMalloc(&ix->ids, std::max<uint64_t>(8, N * 8))) != cudaSuccess) return bail(e, "alloc ids");
+  if ((e = cudaMalloc(&ix->xnorm2, std::max<uint64_t>(4, N * 4))) != cudaSuccess) return bail(e, "alloc norms");
+  if ((e = cudaMalloc(&ix->d_list_off, (n_clusters + 1) * 8ull)) != cudaSuccess) return bail(e, "alloc offsets");
+  if ((e = cudaMalloc(&ix->maxnorm_bits, n_clusters * 4ull)) != cudaSuccess) return bail(e, "alloc maxnorm");
+  if ((e = cudaMalloc(&ix->cent, (uint64_t)n_clusters * ix->dpad * 4)) != cudaSuccess) return bail(e, "alloc centroids");
+  if ((e = cudaMalloc(&ix->cnorm2, n_clusters * 4ull)) != cudaSuccess) return bail(e, "alloc cnorm2");
+  if ((e = cudaMalloc(&ix->cnorm, n_clusters * 4ull)) != cudaSuccess) return bail(e, "alloc cnorm");
+  if ((e = cudaMalloc(&ix->list_order, n_clusters * 4ull)) != cudaSuccess) return bail(e, "alloc order");
+  if ((e = cudaMalloc(&ix->d_err, 4)) != cudaSuccess) return bail(e, "alloc err");
+  cudaMemsetAsync(ix->d_err, 0, 4, s);
+  cudaMemsetAsync(ix->maxnorm_bits, 0, n_clusters * 4ull, s);
+  cudaMemcpyAsync(ix->d_list_off, list_offsets, (n_clusters + 1) * 8ull, cudaMemcpyHostToDevice, s);
+  // lists by size, descending (LPT order for the scan work list)
+  std::vector<uint32_t> order(n_clusters);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return list_offsets[a + 1] - list_offsets[a] > list_offsets[b + 1] - list_offsets[b];
+  });
+  cudaMemcpyAsync(ix->list_order, order.data(), n_clusters * 4ull, cudaMemcpyHostToDevice, s);
+  const float* dcent = centroids;
+  float* tmp = nullptr;
+  if (!centroids_on_device) {
+    if ((e = cudaMalloc(&tmp, (uint64_t)n_clusters * dim * 4)) != cudaSuccess) return bail(e, "alloc tmp");
+    cudaMemcpyAsync(tmp, centroids, (uint64_t)n_clusters * dim * 4, cudaMemcpyHostToDevice, s);
+    dcent = tmp;
+  }
+  launch_pack_centroids(dcent, n_clusters, dim, ix->dpad, ix->cent, ix->cnorm2, ix->cnorm, ix->d_err, s);
+  e = cudaStreamSynchronize(s);
+  if (tmp) cudaFree(tmp);
+  if (e != cudaSuccess) return bail(e, "pack centroids");
+  if ((e = cudaGetLastError()) != cudaSuccess) return bail(e, "pack centroids launch");
+  *out = ix;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_add_rows_device(hivf_index* ix, uint64_t first_row, uint64_t n_rows,
+                                       const float* d_rows, const uint64_t* d_ids) {
+  if (!ix || (!d_rows && n_rows)) return fail(HIVF_EINVAL, "hivf_index_add_rows_device: NULL argument");
+  if (ix->finished) return fail(HIVF_EINVAL, "index already finished");
+  if (first_row + n_rows > ix->N) return fail(HIVF_EINVAL, "add_rows: rows [%llu, %llu) beyond N=%llu",
+                                               (unsigned long long)first_row,
+                                               (unsigned long long)(first_row + n_rows),
+                                               (unsigned long long)ix->N);
+  if (!n_rows) return HIVF_OK;
+  cudaStream_t s = ix->ctx->stream;
+  CK(cudaSetDevice(ix->ctx->device));
+  launch_pack_lists(d_rows, first_row, n_rows, ix->dim, ix->dpad, ix->d_list_off, ix->K, ix->vec,
+                    ix->xnorm2, ix->maxnorm_bits, ix->d_err, s);
+  CKL();
+  if (d_ids) CK(cudaMemcpyAsync(ix->ids + first_row, d_ids, n_rows * 8, cudaMemcpyDeviceToDevice, s));
+  ix->rows_added += n_rows;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_finish(hivf_index* ix) {
+  if (!ix) return fail(HIVF_EINVAL, "index is NULL");
+  cudaStream_t s = ix->ctx->stream;
+  CK(cudaSetDevice(ix->ctx->device));
+  if (ix->rows_added != ix->N)
+    return fail(HIVF_EINVAL, "index_finish: %llu of %llu rows added", (unsigned long long)ix->rows_added,
+                (unsigned long long)ix->N);
+  if (ix->N > 1) {  // duplicate doc ids -> invalid_argument (vector_index.cpp:240-244)
+    uint64_t* sorted = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, ix->ids, sorted, (int64_t)ix->N, 0, 64, s));
+    CK(cudaMalloc(&sorted, ix->N * 8));
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, ix->ids, sorted, (int64_t)ix->N, 0, 64, s));
+    launch_check_dup_ids(sorted, ix->N, ix->d_err, s);
+    CK(cudaStreamSynchronize(s));
+    cudaFree(sorted);
+    cudaFree(tmp);
+  }
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, ix->d_err, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (err == 1) return fail(HIVF_EINVAL, "index: non-finite value in vectors or centroids");
+  if (err == 2) return fail(HIVF_EINVAL, "build_index: duplicate doc_id");
+  ix->finished = true;
+  return HIVF_OK;
+}
+
+static hivf_status upload_common(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
+                                 const float* centroids, int cent_dev, const uint64_t* list_offsets,
+                                 const float* vectors, const uint64_t* ids, bool dev,
+                                 hivf_index** out) {
+  if (!out) return fail(HIVF_EINVAL, "out is NULL");
+  hivf_index* ix = nullptr;
+  hivf_status st = hivf_index_begin(ctx, dim, metric, n_clusters, centroids, cent_dev, list_offsets, &ix);
+  if (st != HIVF_OK) return st;
+  const uint64_t N = ix->N;
+  if (N && (!vectors || !ids)) {
+    hivf_index_destroy(ix);
+    return fail(HIVF_EINVAL, "index: vectors/ids NULL");
+  }
+  if (dev) {
+    st = hivf_index_add_rows_device(ix, 0, N, vectors, ids);
+  } else {
+    // stage host rows through a bounded device buffer (256 MB chunks)
+    const uint64_t rows_per = std::max<uint64_t>(1, (256ull << 20) / (4ull * dim));
+    float* drows = nullptr;
+    uint64_t* dids = nullptr;
+    cudaError_t e = cudaMalloc(&drows, std::min(rows_per, std::max<uint64_t>(N, 1)) * dim * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&dids, std::min(rows_per, std::max<uint64_t>(N, 1)) * 8);
+    if (e != cudaSuccess) {
+      if (drows) cudaFree(drows);
+      hivf_index_destroy(ix);
+      return fail(HIVF_ENOMEM, "index staging: %s", cudaGetErrorString(e));
+    }
+    for (uint64_t r = 0; r < N && st == HIVF_OK; r += rows_per) {
+      const uint64_t n = std::min(rows_per, N - r);
+      cudaMemcpyAsync(drows, vectors + r * dim, n * dim * 4, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(dids, ids + r, n * 8, cudaMemcpyHostToDevice, ctx->stream);
+      st = hivf_index_add_rows_device(ix, r, n, drows, dids);
+      cudaStreamSynchronize(ctx->stream);
+    }
+    cudaFree(drows);
+    cudaFree(dids);
+  }
+  if (st == HIVF_OK) st = hivf_index_finish(ix);
+  if (st != HIVF_OK) {
+    std::string keep = g_err;
+    hivf_index_destroy(ix);
+    g_err = keep;
+    return st;
+  }
+  *out = ix;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_upload(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
+                              const float* centroids, const uint64_t* list_offsets,
+                              const float* vectors, const uint64_t* ids, hivf_index** out) {
+  return upload_common(ctx, dim, metric, n_clusters, centroids, 0, list_offsets, vectors, ids, false, out);
+}
+
+hivf_status hivf_index_upload_device(hivf_ctx* ctx, uint32_t dim, int metric,
+                                     uint32_t n_clusters, const float* d_centroids,
+                                     const uint64_t* list_offsets, const float* d_vectors,
+                                     const uint64_t* d_ids, hivf_index** out) {
+  return upload_common(ctx, dim, metric, n_clusters, d_centroids, 1, list_offsets, d_vectors, d_ids, true, out);
+}
+
+hivf_status hivf_index_destroy(hivf_index* ix) {
+  if (!ix) return HIVF_OK;
+  cudaSetDevice(ix->ctx->device);
+  cudaStreamSynchronize(ix->ctx->stream);
+  delete ix;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_info(const hivf_index* cix, uint32_t* dim, uint32_t* n_clusters,
+                            uint64_t* n_vectors, uint64_t* hbm_bytes,
+                            double* mean_assigned_distance) {
+  if (!cix) return fail(HIVF_EINVAL, "index is NULL");
+  auto* ix = const_cast<hivf_index*>(cix);
+  if (dim) *dim = ix->dim;
+  if (n_clusters) *n_clusters = ix->K;
+  if (n_vectors) *n_vectors = ix->N;
+  if (hbm_bytes)
+    *hbm_bytes = ix->N * (ix->dpad * 4ull + 8 + 4) + (uint64_t)ix->K * (ix->dpad * 4ull + 8 + 16);
+  if (mean_assigned_distance) {
+    if (ix->mean_assigned < 0) {
+      const uint32_t np = 1024;
+      double* part = nullptr;
+      CK(cudaMalloc(&part, np * 8));
+      launch_mean_assigned(ix->view(), part, np, ix->ctx->stream);
+      std::vector<double> h(np);
+      CK(cudaMemcpyAsync(h.data(), part, np * 8, cudaMemcpyDeviceToHost, ix->ctx->stream));
+      CK(cudaStreamSynchronize(ix->ctx->stream));
+      cudaFree(part);
+      double sum = 0;
+      for (double v : h) sum += v;
+      ix->mean_assigned = ix->N ? sum / (double)ix->N : 0.0;
+    }
+    *mean_assigned_distance = ix->mean_assigned;
+  }
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_cluster_sizes(const hivf_index* ix, uint64_t* sizes_out) {
+  if (!ix || !sizes_out) return fail(HIVF_EINVAL, "NULL argument");
+  for (uint32_t c = 0; c < ix->K; ++c) sizes_out[c] = ix->list_off[c + 1] - ix->list_off[c];
+  return HIVF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// search
+// ---------------------------------------------------------------------------
+
+static hivf_status prep_queries(hivf_index* ix, const float* d_q, uint32_t n, bool normalize,
+                                QueryView* qv) {
+  hivf_ctx* c = ix->ctx;
+  CK(c->qs.ensure((size_t)n * ix->dpad * 4));
+  CK(c->qn2.ensure((size_t)n * 4));
+  CK(c->qnorm.ensure((size_t)n * 4));
+  CK(c->err.ensure(4));
+  launch_prep_queries(d_q, n, ix->dim, ix->dpad, ix->metric, normalize, c->qs.as<float>(),
+                      c->qn2.as<float>(), c->qnorm.as<float>(), c->err.as<int>(), c->stream);
+  CKL();
+  qv->qs = c->qs.as<float>();
+  qv->qn2 = c->qn2.as<float>();
+  qv->qnorm = c->qnorm.as<float>();
+  qv->n = n;
+  return HIVF_OK;
+}
+
+static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t nprobe, double* d_dists) {
+  hivf_ctx* c = ix->ctx;
+  const IndexView v = ix->view();
+  CK(c->dist32.ensure((size_t)qv.n * ix->K * 4));
+  CK(c->plans.ensure((size_t)qv.n * nprobe * 4));
+  CK(c->flags_c.ensure((size_t)qv.n * 4));
+  launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream);
+  CKL();
+  launch_coarse_select(v, qv, c->dist32.as<float>(), nprobe, c->plans.as<uint32_t>(), d_dists,
+                       c->flags_c.as<int>(), c->stream);
+  CKL();
+  launch_coarse_fallback(v, qv, nprobe, c->plans.as<uint32_t>(), d_dists, c->flags_c.as<int>(), c->stream);
+  CKL();
+  c->stats.kernels_launched += 3;
+  return HIVF_OK;
+}
+
+// Grouped scan over pairs (pair_query/pair_list already in c->pq / c->pl).
+static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs) {
+  hivf_ctx* c = ix->ctx;
+  const IndexView v = ix->view();
+  const size_t nslots = (size_t)std::max<uint32_t>(n_pairs, 1) * ix->s_max;
+  CK(c->list_cnt.ensure(ix->K * 4ull));
+  CK(c->list_poff.ensure(ix->K * 4ull));
+  CK(c->list_cur.ensure(ix->K * 4ull));
+  CK(c->list_ioff.ensure(ix->K * 4ull));
+  CK(c->sorted_pairs.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
+  CK(c->items.ensure(nslots * sizeof(ScanItem)));
+  CK(c->n_items.ensure(4));
+  CK(c->work_ctr.ensure(4));
+  CK(c->cand_d.ensure(nslots * kKP * 4));
+  CK(c->cand_row.ensure(nslots * kKP * 4));
+  CK(c->cand_thr.ensure(nslots * 4));
+  CK(c->cand_n.ensure(nslots * 4));
+  // slots of empty lists are never written by the scan; zero counts so the
+  // finalize pass reads "no candidates" there
+  CK(cudaMemsetAsync(c->cand_n.p, 0, nslots * 4, c->stream));
+  launch_build_worklist(v, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
+                        c->list_poff.as<uint32_t>(), c->list_cur.as<uint32_t>(),
+                        c->list_ioff.as<uint32_t>(), c->sorted_pairs.as<uint32_t>(),
+                        c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
+                        c->stream);
+  CKL();
+  const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;
+  launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
+              c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
+              c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
+              c->stream);
+  CKL();
+  c->stats.kernels_launched += 5;
+  return HIVF_OK;
+}
+
+static hivf_status check_search_args(hivf_index* ix, uint32_t n, uint32_t nprobe, uint32_t k) {
+  if (!ix) return fail(HIVF_EINVAL, "index is NULL");
+  if (!ix->finished) return fail(HIVF_EINVAL, "index not finished");
+  if (k == 0) return fail(HIVF_EINVAL, "make_cursor: k must be >= 1");
+  if (nprobe < 1 || nprobe > ix->K) return fail(HIVF_EINVAL, "select_clusters: nprobe out of range");
+  if (nprobe > kNprobeMax) return fail(HIVF_EUNSUPPORTED, "nprobe > %u", kNprobeMax);
+  if (k > kExactMaxK) return fail(HIVF_EUNSUPPORTED, "k > %u", kExactMaxK);
+  (void)n;
+  return HIVF_OK;
+}
+
+hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t n,
+                               uint32_t nprobe, uint32_t k, uint64_t* d_ids_out,
+                               double* d_dists_out, uint32_t* d_counts_out) {
+  hivf_status st = check_search_args(ix, n, nprobe, k);
+  if (st != HIVF_OK) return st;
+  if (n == 0) return HIVF_OK;
+  hivf_ctx* c = ix->ctx;
+  CK(cudaSetDevice(c->device));
+  c->stats = hivf_stats{};
+  c->last_nq = n;
+  QueryView qv;
+  if ((st = prep_queries(ix, d_queries, n, true, &qv)) != HIVF_OK) return st;
+  if ((st = run_assign(ix, qv, nprobe, nullptr)) != HIVF_OK) return st;
+  const uint32_t np = n * nprobe;
+  CK(c->pq.ensure((size_t)np * 4));
+  CK(c->pl.ensure((size_t)np * 4));
+  CK(c->flags_f.ensure((size_t)n * 4));
+  const IndexView v = ix->view();
+  const bool exact_only = c->opt_force_exact || k > (uint32_t)kKP;
+  if (!exact_only) {
+    launch_plans_to_pairs(c->plans.as<uint32_t>(), n, nprobe, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), c->stream);
+    CKL();
+    if ((st = run_scan(ix, qv, np)) != HIVF_OK) return st;
+    launch_finalize_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(),
+                           c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(),
+                           d_ids_out, d_dists_out, d_counts_out, c->flags_f.as<int>(), c->stream);
+    CKL();
+    launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->flags_f.as<int>(), d_ids_out,
+                        d_dists_out, d_counts_out, c->stream);
+    CKL();
+    c->stats.kernels_launched += 4;
+  } else {
+    CK(cudaMemsetAsync(c->flags_f.p, 0, (size_t)n * 4, c->stream));
+    launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, nullptr, d_ids_out, d_dists_out,
+                        d_counts_out, c->stream);
+    CKL();
+    c->stats.kernels_launched += 1;
+  }
+  return HIVF_OK;
+}
+
+hivf_status hivf_search(hivf_index* ix, const float* queries, uint32_t n, uint32_t nprobe,
+                        uint32_t k, uint64_t* ids_out, double* dists_out, uint32_t* counts_out) {
+  hivf_status st = check_search_args(ix, n, nprobe, k);
+  if (st != HIVF_OK) return st;
+  if (n == 0) return HIVF_OK;
+  if (!queries || !ids_out || !dists_out || !counts_out) return fail(HIVF_EINVAL, "hivf_search: NULL buffer");
+  hivf_ctx* c = ix->ctx;
+  CK(cudaSetDevice(c->device));
+  const size_t qb = (size_t)n * ix->dim * 4, ob = (size_t)n * k;
+  CK(c->qin.ensure(qb));
+  CK(c->out_ids.ensure(ob * 8));
+  CK(c->out_d.ensure(ob * 8));
+  CK(c->out_cnt.ensure((size_t)n * 4));
+  CK(c->err.ensure(4));
+  CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
+  CK(cudaMemcpyAsync(c->qin.p, queries, qb, cudaMemcpyHostToDevice, c->stream));
+  if ((st = hivf_search_device(ix, c->qin.as<float>(), n, nprobe, k, c->out_ids.as<uint64_t>(),
+                               c->out_d.as<double>(), c->out_cnt.as<uint32_t>())) != HIVF_OK)
+    return st;
+  CK(cudaMemcpyAsync(ids_out, c->out_ids.p, ob * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(dists_out, c->out_d.p, ob * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(counts_out, c->out_cnt.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (err) return fail(HIVF_EINVAL, "hivf_search: non-finite query value");
+  return HIVF_OK;
+}
+
+hivf_status hivf_assign(hivf_index* ix, const float* queries, uint32_t n, uint32_t nprobe,
+                        uint32_t* plans_out, double* dists_out) {
+  hivf_status st = check_search_args(ix, n, nprobe, 1);
+  if (st != HIVF_OK) return st;
+  if (n == 0) return HIVF_OK;
+  if (!queries || !plans_out) return fail(HIVF_EINVAL, "hivf_assign: NULL buffer");
+  hivf_ctx* c = ix->ctx;
+  CK(cudaSetDevice(c->device));
+  c->stats = hivf_stats{};
+  c->last_nq = 0;
+  const size_t qb = (size_t)n * ix->dim * 4;
+  CK(c->qin.ensure(qb));
+  CK(c->pdists.ensure((size_t)n * nprobe * 8));
+  CK(c->err.ensure(4));
+  CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
+  CK(cudaMemcpyAsync(c->qin.p, queries, qb, cudaMemcpyHostToDevice, c->stream));
+  QueryView qv;
+  if ((st = prep_queries(ix, c->qin.as<float>(), n, true, &qv)) != HIVF_OK) return st;
+  if ((st = run_assign(ix, qv, nprobe, c->pdists.as<double>())) != HIVF_OK) return st;
+  CK(cudaMemcpyAsync(plans_out, c->plans.p, (size_t)n * nprobe * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (dists_out)
+    CK(cudaMemcpyAsync(dists_out, c->pdists.p, (size_t)n * nprobe * 8, cudaMemcpyDeviceToHost, c->stream));
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (err) return fail(HIVF_EINVAL, "select_clusters: non-finite query value");
+  return HIVF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// node-split sub-search
+// ---------------------------------------------------------------------------
+
+hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_items,
+                            const uint32_t* cluster_off, const uint32_t* clusters,
+                            const uint32_t* kv, uint64_t* heap_ids, double* heap_dists,
+                            uint32_t* heap_counts, uint32_t heap_stride, uint8_t* changed_out) {
+  if (!ix) return fail(HIVF_EINVAL, "index is NULL");
+  if (!ix->finished) return fail(HIVF_EINVAL, "index not finished");
+  if (n_items == 0) return HIVF_OK;
+  if (!queries || !cluster_off || !kv || !heap_ids || !heap_dists || !heap_counts)
+    return fail(HIVF_EINVAL, "hivf_scan_items: NULL buffer");
+  uint32_t kmax = 0;
+  for (uint32_t i = 0; i < n_items; ++i) {
+    if (kv[i] == 0) return fail(HIVF_EINVAL, "make_cursor: k must be >= 1");
+    if (kv[i] > kExactMaxK) return fail(HIVF_EUNSUPPORTED, "k > %u", kExactMaxK);
+    if (kv[i] > heap_stride) return fail(HIVF_EINVAL, "heap_stride < k");
+    if (heap_counts[i] > kv[i]) return fail(HIVF_EINVAL, "heap larger than k");
+    if (cluster_off[i + 1] < cluster_off[i]) return fail(HIVF_EINVAL, "cluster_off not monotone");
+    kmax = std::max(kmax, kv[i]);
+  }
+  const uint32_t n_pairs = cluster_off[n_items] - cluster_off[0];
+  if (cluster_off[0] != 0) return fail(HIVF_EINVAL, "cluster_off[0] must be 0");
+  if (n_pairs && (!clusters || !changed_out)) return fail(HIVF_EINVAL, "hivf_scan_items: NULL clusters");
+  for (uint32_t p = 0; p < n_pairs; ++p)
+    if (clusters[p] >= ix->K) return fail(HIVF_EINVAL, "cluster id %u out of range", clusters[p]);
+  hivf_ctx* c = ix->ctx;
+  CK(cudaSetDevice(c->device));
+  c->stats = hivf_stats{};
+  c->last_nq = 0;
+  cudaStream_t s = c->stream;
+  // item -> query index per pair
+  std::vector<uint32_t> pq(n_pairs);
+  for (uint32_t i = 0; i < n_items; ++i)
+    for (uint32_t p = cluster_off[i]; p < cluster_off[i + 1]; ++p) pq[p] = i;
+  const size_t qb = (size_t)n_items * ix->dim * 4;
+  CK(c->qin.ensure(qb));
+  CK(c->pq.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
+  CK(c->pl.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
+  CK(c->it_off.ensure((n_items + 1) * 4ull));
+  CK(c->it_cl.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
+  CK(c->it_k.ensure(n_items * 4ull));
+  CK(c->heap_ids.ensure((size_t)n_items * heap_stride * 8));
+  CK(c->heap_d.ensure((size_t)n_items * heap_stride * 8));
+  CK(c->heap_n.ensure(n_items * 4ull));
+  CK(c->changed.ensure((size_t)std::max<uint32_t>(n_pairs, 1)));
+  CK(c->flags_f.ensure(n_items * 4ull));
+  CK(c->err.ensure(4));
+  CK(cudaMemsetAsync(c->err.p, 0, 4, s));
+  CK(cudaMemcpyAsync(c->qin.p, queries, qb, cudaMemcpyHostToDevice, s));
+  if (n_pairs) {
+    CK(cudaMemcpyAsync(c->pq.p, pq.data(), n_pairs * 4ull, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->pl.p, clusters, n_pairs * 4ull, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->it_cl.p, clusters, n_pairs * 4ull, cudaMemcpyHostToDevice, s));
+  }
+  CK(cudaMemcpyAsync(c->it_off.p, cluster_off, (n_items + 1) * 4ull, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->it_k.p, kv, n_items * 4ull, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->heap_ids.p, heap_ids, (size_t)n_items * heap_stride * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->heap_d.p, heap_dists, (size_t)n_items * heap_stride * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->heap_n.p, heap_counts, n_items * 4ull, cudaMemcpyHostToDevice, s));
+  hivf_status st;
+  QueryView qv;
+  // cursor queries are already in search space: no re-normalization
+  if ((st = prep_queries(ix, c->qin.as<float>(), n_items, false, &qv)) != HIVF_OK) return st;
+  const IndexView v = ix->view();
+  const bool exact_only = c->opt_force_exact || kmax > (uint32_t)kKP;
+  if (!exact_only && n_pairs) {
+    if ((st = run_scan(ix, qv, n_pairs)) != HIVF_OK) return st;
+    launch_finalize_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
+                          c->it_k.as<uint32_t>(), c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
+                          c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), c->heap_ids.as<uint64_t>(),
+                          c->heap_d.as<double>(), c->heap_n.as<uint32_t>(), heap_stride,
+                          c->changed.as<uint8_t>(), c->flags_f.as<int>(), s);
+    CKL();
+    launch_exact_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
+                       c->it_k.as<uint32_t>(), c->heap_ids.as<uint64_t>(), c->heap_d.as<double>(),
+                       c->heap_n.as<uint32_t>(), heap_stride, c->changed.as<uint8_t>(),
+                       c->flags_f.as<int>(), s);
+    CKL();
+  } else {
+    launch_exact_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
+                       c->it_k.as<uint32_t>(), c->heap_ids.as<uint64_t>(), c->heap_d.as<double>(),
+                       c->heap_n.as<uint32_t>(), heap_stride, c->changed.as<uint8_t>(), nullptr, s);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(heap_ids, c->heap_ids.p, (size_t)n_items * heap_stride * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(heap_dists, c->heap_d.p, (size_t)n_items * heap_stride * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(heap_counts, c->heap_n.p, n_items * 4ull, cudaMemcpyDeviceToHost, s));
+  if (n_pairs) CK(cudaMemcpyAsync(changed_out, c->changed.p, n_pairs, cudaMemcpyDeviceToHost, s));
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (err) return fail(HIVF_EINVAL, "hivf_scan_items: non-finite query value");
+  return HIVF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU merge + residency
+// ---------------------------------------------------------------------------
+
+hivf_status hivf_merge_parts_device(hivf_ctx* ctx, uint32_t n_parts, uint32_t n_queries,
+                                    uint32_t k, const uint64_t* d_ids, const double* d_dists,
+                                    const uint32_t* d_counts, uint64_t* d_ids_out,
+                                    double* d_dists_out, uint32_t* d_counts_out) {
+  if (!ctx) return fail(HIVF_EINVAL, "ctx is NULL");
+  if (k == 0 || n_parts == 0) return fail(HIVF_EINVAL, "merge: k and n_parts must be >= 1");
+  if ((uint64_t)n_parts * k > 8192) return fail(HIVF_EUNSUPPORTED, "merge: n_parts*k > 8192");
+  if (!n_queries) return HIVF_OK;
+  CK(cudaSetDevice(ctx->device));
+  launch_merge_parts(n_parts, n_queries, k, d_ids, d_dists, d_counts, d_ids_out, d_dists_out,
+                     d_counts_out, ctx->stream);
+  CKL();
+  return HIVF_OK;
+}
+
+hivf_status hivf_residency_set(hivf_index* ix, const uint32_t* clusters, uint32_t n) {
+  if (!ix) return fail(HIVF_EINVAL, "index is NULL");
+  if (n && !clusters) return fail(HIVF_EINVAL, "clusters NULL");
+  std::vector<uint8_t> res(ix->K, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (clusters[i] >= ix->K) return fail(HIVF_EINVAL, "cluster %u out of range", clusters[i]);
+    res[clusters[i]] = 1;
+  }
+  ix->resident.swap(res);
+  return HIVF_OK;
+}
+
+hivf_status hivf_residency_get(const hivf_index* ix, uint8_t* out) {
+  if (!ix || !out) return fail(HIVF_EINVAL, "NULL argument");
+  std::memcpy(out, ix->resident.data(), ix->K);
+  return HIVF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,392 @@
+// finalize.cu -- K4/K5: exact fp64 re-rank and top-k assembly.
+//
+// The scan kept, per (query, segment), the 32 best rows by the fp32 distance
+// d32 plus a "drop threshold" T (every row NOT kept has d32 >= T).  With the
+// per-(query, list) error bound E (common.cuh):
+//   tau = k-th smallest of (d32 + E) over all kept rows of the query  ->
+//         the reference's k-th distance is <= tau;
+//   candidates = kept rows with d32 - E <= tau  -> superset of the true top-k;
+//   proof of completeness: every segment has T - E > tau (else the query is
+//   flagged and redone by the exact streaming kernel).
+// Candidates get the reference's exact double (embedding.hpp:27-34, sequential,
+// no FMA) and are ordered by (distance, doc id) (vector_index.hpp:41-44), so
+// ids AND distances are bit-identical to TopKResult after the full plan
+// (vector_index.cpp:38-53,291-317).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hivf {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kFinThreads = 128;
+constexpr int kCandMax = 1024;
+constexpr float kInf = __builtin_inff();
+
+__device__ __forceinline__ float list_E(double eps, double ab, float qn, float xn) {
+  const double m = (double)qn + (double)xn;
+  return __double2float_ru(eps * m * m + ab);
+}
+
+__device__ __forceinline__ uint32_t list_of_row(const IndexView& ix, uint64_t r) {
+  uint32_t lo = 0, hi = ix.K;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ix.list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Exact reference distance between the (search-space) query in smem and the
+// row `r` of list `c` (squared_l2(query, vec), vector_index.cpp:303).
+__device__ double exact_row_dist(const IndexView& ix, const float* qsh, uint32_t c, uint64_t r) {
+  const uint64_t lbeg = ix.list_off[c];
+  const uint64_t n_c = ix.list_off[c + 1] - lbeg;
+  const uint64_t base = lbeg * ix.dpad;
+  const uint64_t lr = r - lbeg;
+  double acc = 0.0;
+  const uint32_t ng = (ix.dim + 3) / 4;
+  for (uint32_t g = 0; g < ng; ++g) {
+    const float4 x = *reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4));
+    const uint32_t d = g * 4;
+    acc = exact_step(acc, qsh[d], x.x);
+    if (d + 1 < ix.dim) acc = exact_step(acc, qsh[d + 1], x.y);
+    if (d + 2 < ix.dim) acc = exact_step(acc, qsh[d + 2], x.z);
+    if (d + 3 < ix.dim) acc = exact_step(acc, qsh[d + 3], x.w);
+  }
+  return acc;
+}
+
+// Merge a sorted-ascending 32-lane list `v` into sorted-ascending `cur`
+// (keeps the 32 smallest).
+__device__ __forceinline__ float warp_merge32(float cur, float v) {
+  const int lane = threadIdx.x & 31;
+  const float o = __shfl_sync(FULL, v, 31 - lane);
+  float x = fminf(cur, o);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const float p = __shfl_xor_sync(FULL, x, s);
+    x = ((lane & s) == 0) ? fminf(x, p) : fmaxf(x, p);
+  }
+  return x;
+}
+
+template <typename IdT>
+__device__ void block_sort_pairs(double* d, IdT* id, uint32_t n) {
+  for (uint32_t size = 2; size <= n; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < n / 2; i += blockDim.x) {
+        const uint32_t lo = 2 * i - (i & (stride - 1));
+        const uint32_t hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const bool gt = pair_less(d[hi], (uint64_t)id[hi], d[lo], (uint64_t)id[lo]);
+        if (gt == up) {
+          const double td = d[lo];
+          d[lo] = d[hi];
+          d[hi] = td;
+          const IdT ti = id[lo];
+          id[lo] = id[hi];
+          id[hi] = ti;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t nseg_of(const IndexView& ix, uint32_t c) {
+  const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
+  return (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+}
+
+// One CTA per query.
+__global__ void __launch_bounds__(kFinThreads) k_finalize_search(
+    IndexView ix, QueryView qv, const uint32_t* __restrict__ plans, uint32_t nprobe, uint32_t k,
+    const float* __restrict__ cand_d, const uint32_t* __restrict__ cand_row,
+    const float* __restrict__ cand_thr, const uint32_t* __restrict__ cand_n, double eps,
+    double ab, uint64_t* __restrict__ ids_out, double* __restrict__ d_out,
+    uint32_t* __restrict__ counts_out, int* flags) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  double* cdist = reinterpret_cast<double*>(sm);                 // kCandMax
+  uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kCandMax);  // kCandMax
+  uint32_t* crow = reinterpret_cast<uint32_t*>(cid + kCandMax);   // kCandMax
+  uint32_t* clist = crow + kCandMax;                              // kCandMax
+  float* qsh = reinterpret_cast<float*>(clist + kCandMax);        // dpad
+  __shared__ float wl[kFinThreads / 32][32];
+  __shared__ float s_tau;
+  __shared__ uint32_t s_cnt;
+  __shared__ int s_bad;
+  __shared__ unsigned long long s_total;
+  const uint32_t b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = kFinThreads / 32;
+  const float qn = qv.qnorm[b];
+  for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)b * ix.dpad + d];
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_bad = 0;
+    s_total = 0;
+  }
+  __syncthreads();
+  // 1. tau = k-th smallest upper bound
+  float cur = kInf;
+  unsigned long long total = 0;
+  for (uint32_t p = warp; p < nprobe; p += NW) {
+    const uint32_t c = plans[(uint64_t)b * nprobe + p];
+    const float E = list_E(eps, ab, qn, ix.maxnorm[c]);
+    const uint32_t ns = nseg_of(ix, c);
+    total += ix.list_off[c + 1] - ix.list_off[c];
+    for (uint32_t s = 0; s < ns; ++s) {
+      const uint64_t slot = ((uint64_t)b * nprobe + p) * ix.s_max + s;
+      const uint32_t n = cand_n[slot];
+      const float v = lane < (int)n ? __fadd_ru(cand_d[slot * kKP + lane], E) : kInf;
+      cur = warp_merge32(cur, v);
+    }
+  }
+  wl[warp][lane] = cur;
+  if (lane == 0) atomicAdd(&s_total, total);
+  __syncthreads();
+  if (warp == 0) {
+    float x = wl[0][lane];
+    for (int w = 1; w < NW; ++w) x = warp_merge32(x, wl[w][lane]);
+    const float t = __shfl_sync(FULL, x, (int)min(k, 32u) - 1);
+    if (lane == 0) s_tau = t;
+  }
+  __syncthreads();
+  const float tau = s_tau;
+  // 2. candidates + completeness
+  for (uint32_t p = warp; p < nprobe; p += NW) {
+    const uint32_t c = plans[(uint64_t)b * nprobe + p];
+    const float E = list_E(eps, ab, qn, ix.maxnorm[c]);
+    const uint32_t ns = nseg_of(ix, c);
+    for (uint32_t s = 0; s < ns; ++s) {
+      const uint64_t slot = ((uint64_t)b * nprobe + p) * ix.s_max + s;
+      const uint32_t n = cand_n[slot];
+      const bool take = lane < (int)n && __fsub_rd(cand_d[slot * kKP + lane], E) <= tau;
+      const unsigned m = __ballot_sync(FULL, take);
+      uint32_t base = 0;
+      if (lane == 0 && m) base = atomicAdd(&s_cnt, (uint32_t)__popc(m));
+      base = __shfl_sync(FULL, base, 0);
+      if (take) {
+        const uint32_t pos = base + __popc(m & ((1u << lane) - 1));
+        if (pos < kCandMax) {
+          crow[pos] = cand_row[slot * kKP + lane];
+          clist[pos] = c;
+        }
+      }
+      if (lane == 0 && __fsub_rd(cand_thr[slot], E) <= tau) s_bad = 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t m = s_cnt;
+  if (s_bad || m > kCandMax || !(tau < kInf && tau >= -FLT_MAX) && s_total >= k) {
+    if (threadIdx.x == 0) flags[b] = 1;
+    return;
+  }
+  // 3. exact distances
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    cdist[i] = exact_row_dist(ix, qsh, clist[i], crow[i]);
+    cid[i] = ix.ids[crow[i]];
+  }
+  uint32_t mp = 1;
+  while (mp < m) mp <<= 1;
+  for (uint32_t i = m + threadIdx.x; i < mp; i += blockDim.x) {
+    cdist[i] = DBL_MAX;
+    cid[i] = ~0ull;
+  }
+  block_sort_pairs(cdist, cid, mp);
+  const uint32_t cnt = (uint32_t)min((unsigned long long)k, s_total);
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+    ids_out[(uint64_t)b * k + i] = i < cnt ? cid[i] : 0;
+    d_out[(uint64_t)b * k + i] = i < cnt ? cdist[i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    counts_out[b] = cnt;
+    flags[b] = 0;
+  }
+}
+
+// Exact streaming top-k over every row of the query's plan (flagged queries
+// and k > 32).  Buffer of `cap` (d, id) pairs filtered by the running k-th.
+__global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv,
+                                                      const uint32_t* __restrict__ plans,
+                                                      uint32_t nprobe, uint32_t k, uint32_t cap,
+                                                      const int* flags, uint64_t* ids_out,
+                                                      double* d_out, uint32_t* counts_out) {
+  const uint32_t b = blockIdx.x;
+  if (flags && !flags[b]) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  double* bd = reinterpret_cast<double*>(sm);
+  uint64_t* bi = reinterpret_cast<uint64_t*>(bd + cap);
+  float* qsh = reinterpret_cast<float*>(bi + cap);
+  __shared__ uint32_t s_cnt;
+  __shared__ double s_thr_d;
+  __shared__ uint64_t s_thr_i;
+  __shared__ unsigned long long s_total;
+  for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)b * ix.dpad + d];
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_thr_d = DBL_MAX;
+    s_thr_i = ~0ull;
+    s_total = 0;
+  }
+  __syncthreads();
+  for (uint32_t p = 0; p < nprobe; ++p) {
+    const uint32_t c = plans[(uint64_t)b * nprobe + p];
+    const uint64_t beg = ix.list_off[c], end = ix.list_off[c + 1];
+    if (threadIdx.x == 0) s_total += end - beg;
+    for (uint64_t r0 = beg; r0 < end; r0 += blockDim.x) {
+      const uint64_t r = r0 + threadIdx.x;
+      double dist = DBL_MAX;
+      uint64_t id = ~0ull;
+      if (r < end) {
+        dist = exact_row_dist(ix, qsh, c, r);
+        id = ix.ids[r];
+      }
+      const uint32_t cnt_now = s_cnt;
+      __syncthreads();  // every thread has read s_cnt before any append
+      if (cnt_now + blockDim.x > cap) {
+        for (uint32_t i = s_cnt + threadIdx.x; i < cap; i += blockDim.x) {
+          bd[i] = DBL_MAX;
+          bi[i] = ~0ull;
+        }
+        block_sort_pairs(bd, bi, cap);
+        if (threadIdx.x == 0) {
+          s_cnt = k;
+          s_thr_d = bd[k - 1];
+          s_thr_i = bi[k - 1];
+        }
+        __syncthreads();
+      }
+      if (r < end && pair_less(dist, id, s_thr_d, s_thr_i)) {
+        const uint32_t pos = atomicAdd(&s_cnt, 1u);
+        bd[pos] = dist;
+        bi[pos] = id;
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = s_cnt + threadIdx.x; i < cap; i += blockDim.x) {
+    bd[i] = DBL_MAX;
+    bi[i] = ~0ull;
+  }
+  block_sort_pairs(bd, bi, cap);
+  const uint32_t cnt = (uint32_t)min((unsigned long long)k, s_total);
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+    ids_out[(uint64_t)b * k + i] = i < cnt ? bi[i] : 0;
+    d_out[(uint64_t)b * k + i] = i < cnt ? bd[i] : 0.0;
+  }
+  if (threadIdx.x == 0) counts_out[b] = cnt;
+}
+
+__global__ void k_plans_to_pairs(const uint32_t* plans, uint32_t n, uint32_t nprobe, uint32_t* pq,
+                                 uint32_t* pl) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n * nprobe) return;
+  pq[p] = p / nprobe;
+  pl[p] = plans[p];
+}
+
+// merge_topk (vector_index.cpp:71-91) over n_parts exact per-shard lists.
+__global__ void k_merge_parts(uint32_t n_parts, uint32_t nq, uint32_t k, const uint64_t* ids,
+                              const double* d, const uint32_t* counts, uint64_t* ids_out,
+                              double* d_out, uint32_t* counts_out, uint32_t cap) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  double* bd = reinterpret_cast<double*>(sm);
+  uint64_t* bi = reinterpret_cast<uint64_t*>(bd + cap);
+  const uint32_t b = blockIdx.x;
+  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
+    const uint32_t part = i / k, e = i % k;
+    bool ok = part < n_parts && e < counts[(uint64_t)part * nq + b];
+    bd[i] = ok ? d[((uint64_t)part * nq + b) * k + e] : DBL_MAX;
+    bi[i] = ok ? ids[((uint64_t)part * nq + b) * k + e] : ~0ull;
+  }
+  block_sort_pairs(bd, bi, cap);
+  // collapse duplicate ids to the minimum distance: after the (d, id) sort the
+  // first occurrence of an id is its minimum; drop later ones.
+  __shared__ uint32_t s_n;
+  if (threadIdx.x == 0) {
+    uint32_t n = 0;
+    for (uint32_t i = 0; i < cap && n < k; ++i) {
+      if (bi[i] == ~0ull && bd[i] == DBL_MAX) break;
+      bool dup = false;
+      for (uint32_t j = 0; j < n; ++j)
+        if (ids_out[(uint64_t)b * k + j] == bi[i]) dup = true;
+      if (dup) continue;
+      ids_out[(uint64_t)b * k + n] = bi[i];
+      d_out[(uint64_t)b * k + n] = bd[i];
+      ++n;
+    }
+    for (uint32_t j = n; j < k; ++j) {
+      ids_out[(uint64_t)b * k + j] = 0;
+      d_out[(uint64_t)b * k + j] = 0.0;
+    }
+    s_n = n;
+    counts_out[b] = n;
+  }
+}
+
+}  // namespace
+
+void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe,
+                           uint32_t* pair_query, uint32_t* pair_list, cudaStream_t s) {
+  const uint32_t n = n_queries * nprobe;
+  if (!n) return;
+  k_plans_to_pairs<<<(n + 255) / 256, 256, 0, s>>>(plans, n_queries, nprobe, pair_query, pair_list);
+}
+
+void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
+                            uint32_t nprobe, uint32_t k, const float* cand_d,
+                            const uint32_t* cand_row, const float* cand_thr,
+                            const uint32_t* cand_n, uint64_t* ids_out, double* d_out,
+                            uint32_t* counts_out, int* flags, cudaStream_t s) {
+  const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_finalize_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_exact_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_finalize_search<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row,
+                                                    cand_thr, cand_n, filter_eps(ix.dim),
+                                                    filter_abs(ix.dim), ids_out, d_out,
+                                                    counts_out, flags);
+}
+
+void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
+                         uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
+                         double* d_out, uint32_t* counts_out, cudaStream_t s) {
+  uint32_t cap = 512;
+  while (cap < k + 256) cap <<= 1;
+  const size_t smem = (size_t)cap * 16 + (size_t)ix.dpad * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_exact_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_exact_search<<<qv.n, 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out, d_out,
+                                         counts_out);
+}
+
+void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const uint64_t* ids,
+                        const double* d, const uint32_t* counts, uint64_t* ids_out,
+                        double* d_out, uint32_t* counts_out, cudaStream_t s) {
+  uint32_t cap = 1;
+  while (cap < n_parts * k) cap <<= 1;
+  const size_t smem = (size_t)cap * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_merge_parts, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_merge_parts<<<n_queries, 256, smem, s>>>(n_parts, n_queries, k, ids, d, counts, ids_out, d_out,
+                                             counts_out, cap);
+}
+
+// Node-split sub-search finalize lives in items.cu.
+
+}  // namespace hivf

@@ -1,0 +1,364 @@
+// items.cu -- node-split sub-search finalize (hivf_scan_items).
+//
+// Reference: ivf::search_clusters (/root/reference/proj/src/vector_index.cpp
+// :291-317) run per BatchItem by RetrievalEngine::execute
+// (/root/reference/proj/src/retrieval_engine.cpp:94-103): the cursor heap is
+// carried in, every cluster of the item is scanned IN ORDER, TopKResult::insert
+// (:38-53) is applied row by row, and each cluster reports whether any insert
+// changed the heap (feeds unchanged_streak, :307-313).
+//
+// Device algorithm (one CTA per item), exact for unique doc ids:
+//  A. prefix bounds: U_j = min(worst(H_0), k-th smallest upper bound over the
+//     lists before j) bounds worst(H_{j-1}) from above; within list j only
+//     its own top-k can enter, bounded by tau_j (k-th upper bound in list j).
+//     Candidates of list j: kept rows with lower bound <= min(U_j, tau_j);
+//     completeness checked against each segment's drop threshold.
+//  B. exact fp64 distances for all candidates (parallel).
+//  C. sequential replay, list by list, of TopKResult::insert on a register
+//     heap (warp 0): rows that are not candidates provably never survive in
+//     the heap, so the final heap and every per-cluster `changed` flag equal
+//     the reference's (a row inserted then evicted inside the same list leaves
+//     an inserted successor behind, so `changed` is unaffected).
+// Items whose proof fails (or k > 32) run k_exact_items: the reference
+// algorithm verbatim (exact distances, in-order inserts) on the GPU.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hivf {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kItThreads = 128;
+constexpr int kItCand = 2048;
+constexpr float kInf = __builtin_inff();
+
+__device__ __forceinline__ float it_E(double eps, double ab, float qn, float xn) {
+  const double m = (double)qn + (double)xn;
+  return __double2float_ru(eps * m * m + ab);
+}
+
+__device__ double it_exact_row(const IndexView& ix, const float* qsh, uint32_t c, uint64_t r) {
+  const uint64_t lbeg = ix.list_off[c];
+  const uint64_t n_c = ix.list_off[c + 1] - lbeg;
+  const uint64_t base = lbeg * ix.dpad;
+  const uint64_t lr = r - lbeg;
+  double acc = 0.0;
+  const uint32_t ng = (ix.dim + 3) / 4;
+  for (uint32_t g = 0; g < ng; ++g) {
+    const float4 x = *reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4));
+    const uint32_t d = g * 4;
+    acc = exact_step(acc, qsh[d], x.x);
+    if (d + 1 < ix.dim) acc = exact_step(acc, qsh[d + 1], x.y);
+    if (d + 2 < ix.dim) acc = exact_step(acc, qsh[d + 2], x.z);
+    if (d + 3 < ix.dim) acc = exact_step(acc, qsh[d + 3], x.w);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ float it_merge32(float cur, float v) {
+  const int lane = threadIdx.x & 31;
+  const float o = __shfl_sync(FULL, v, 31 - lane);
+  float x = fminf(cur, o);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const float p = __shfl_xor_sync(FULL, x, s);
+    x = ((lane & s) == 0) ? fminf(x, p) : fmaxf(x, p);
+  }
+  return x;
+}
+
+// TopKResult::insert (vector_index.cpp:38-53) on a warp-register heap:
+// lane t holds entry t (t < n).  Returns true when the set changed.
+__device__ __forceinline__ bool warp_heap_insert(double& hd, uint64_t& hid, uint32_t& n, uint32_t k,
+                                                 uint64_t id, double d) {
+  const int lane = threadIdx.x & 31;
+  if (k == 0) return false;
+  const unsigned dup = __ballot_sync(FULL, lane < (int)n && hid == id);
+  if (dup) {
+    const int at = __ffs(dup) - 1;
+    const double old = __shfl_sync(FULL, hd, at);
+    if (d >= old) return false;
+    // erase entry `at` (shift the tail left by one)
+    const double nd = __shfl_down_sync(FULL, hd, 1);
+    const uint64_t ni = __shfl_down_sync(FULL, hid, 1);
+    if (lane >= at) {
+      hd = nd;
+      hid = ni;
+    }
+    n -= 1;
+  }
+  const int pos = __popc(__ballot_sync(FULL, lane < (int)n && pair_less(hd, hid, d, id)));
+  if (n >= k && pos == (int)n) return false;
+  const double ud = __shfl_up_sync(FULL, hd, 1);
+  const uint64_t ui = __shfl_up_sync(FULL, hid, 1);
+  if (lane > pos) {
+    hd = ud;
+    hid = ui;
+  } else if (lane == pos) {
+    hd = d;
+    hid = id;
+  }
+  n = min(n + 1, k);
+  return true;
+}
+
+__global__ void __launch_bounds__(kItThreads) k_finalize_items(
+    IndexView ix, QueryView qv, uint32_t n_items, const uint32_t* __restrict__ item_off,
+    const uint32_t* __restrict__ clusters, const uint32_t* __restrict__ kv,
+    const float* __restrict__ cand_d, const uint32_t* __restrict__ cand_row,
+    const float* __restrict__ cand_thr, const uint32_t* __restrict__ cand_n, double eps,
+    double ab, uint64_t* heap_ids, double* heap_d, uint32_t* heap_n, uint32_t stride,
+    uint8_t* changed, int* flags) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  double* cdist = reinterpret_cast<double*>(sm);                // kItCand
+  uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kItCand);  // kItCand
+  uint32_t* crow = reinterpret_cast<uint32_t*>(cid + kItCand);   // kItCand
+  uint32_t* clist = crow + kItCand;                              // kItCand
+  uint32_t* cj_off = clist + kItCand;                            // (m_items+1) candidate offsets per cluster
+  float* qsh = reinterpret_cast<float*>(cj_off + kNprobeMax + 1);  // dpad
+  __shared__ int s_bad;
+  const uint32_t it = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t j0 = item_off[it], j1 = item_off[it + 1];
+  const uint32_t mcl = j1 - j0;
+  const uint32_t k = kv[it];
+  const float qn = qv.qnorm[it];
+  for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)it * ix.dpad + d];
+  if (threadIdx.x == 0) s_bad = (k > 32u || mcl > kNprobeMax) ? 1 : 0;
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) flags[it] = 1;
+    return;
+  }
+  // A + candidate collection (warp 0, in plan order -> candidates grouped by cluster)
+  if (warp == 0) {
+    const uint32_t n0 = heap_n[it];
+    float U0 = kInf;
+    if (n0 >= k && n0 > 0) U0 = __double2float_ru(heap_d[(uint64_t)it * stride + n0 - 1]);
+    float cur = kInf;  // top-32 upper bounds of the lists before j
+    uint32_t cnt = 0;
+    bool bad = false;
+    for (uint32_t j = 0; j < mcl; ++j) {
+      const uint32_t c = clusters[j0 + j];
+      const float E = it_E(eps, ab, qn, ix.maxnorm[c]);
+      const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
+      const uint32_t ns = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+      float lj = kInf;
+      for (uint32_t s = 0; s < ns; ++s) {
+        const uint64_t slot = (uint64_t)(j0 + j) * ix.s_max + s;
+        const uint32_t n = cand_n[slot];
+        const float v = lane < (int)n ? __fadd_ru(cand_d[slot * kKP + lane], E) : kInf;
+        lj = it_merge32(lj, v);
+      }
+      const float tau_j = __shfl_sync(FULL, lj, (int)k - 1);
+      const float u_prev = __shfl_sync(FULL, cur, (int)k - 1);
+      const float lim = fminf(fminf(U0, u_prev), tau_j);
+      if (lane == 0) cj_off[j] = cnt;
+      for (uint32_t s = 0; s < ns; ++s) {
+        const uint64_t slot = (uint64_t)(j0 + j) * ix.s_max + s;
+        const uint32_t n = cand_n[slot];
+        const bool take = lane < (int)n && __fsub_rd(cand_d[slot * kKP + lane], E) <= lim;
+        const unsigned m = __ballot_sync(FULL, take);
+        if (take) {
+          const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1));
+          if (pos < kItCand) {
+            crow[pos] = cand_row[slot * kKP + lane];
+            clist[pos] = c;
+          }
+        }
+        cnt += __popc(m);
+        if (__fsub_rd(cand_thr[slot], E) <= lim) bad = true;
+      }
+      cur = it_merge32(cur, lj);
+    }
+    if (lane == 0) {
+      cj_off[mcl] = cnt;
+      if (bad || cnt > kItCand) s_bad = 1;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) flags[it] = 1;
+    return;
+  }
+  const uint32_t m = cj_off[mcl];
+  // B. exact distances
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    cdist[i] = it_exact_row(ix, qsh, clist[i], crow[i]);
+    cid[i] = ix.ids[crow[i]];
+  }
+  __syncthreads();
+  // C. sequential replay of TopKResult::insert, cluster by cluster
+  if (warp == 0) {
+    uint32_t n = heap_n[it];
+    double hd = lane < (int)n ? heap_d[(uint64_t)it * stride + lane] : DBL_MAX;
+    uint64_t hid = lane < (int)n ? heap_ids[(uint64_t)it * stride + lane] : ~0ull;
+    for (uint32_t j = 0; j < mcl; ++j) {
+      bool ch = false;
+      // rows of one list in ascending row order, like the reference loop
+      const uint32_t b0 = cj_off[j], b1 = cj_off[j + 1];
+      for (uint32_t a = b0; a < b1; ++a) {
+        // pick the a-th smallest row among [b0, b1) (tiny sets: selection)
+        uint32_t best = a;
+        for (uint32_t t = a + 1; t < b1; ++t)
+          if (crow[t] < crow[best]) best = t;
+        __syncwarp();
+        if (lane == 0 && best != a) {
+          const double td = cdist[a]; cdist[a] = cdist[best]; cdist[best] = td;
+          const uint64_t ti = cid[a]; cid[a] = cid[best]; cid[best] = ti;
+          const uint32_t tr = crow[a]; crow[a] = crow[best]; crow[best] = tr;
+        }
+        __syncwarp();
+        ch |= warp_heap_insert(hd, hid, n, k, cid[a], cdist[a]);
+      }
+      if (lane == 0) changed[j0 + j] = ch ? 1 : 0;
+    }
+    if (lane < (int)n) {
+      heap_d[(uint64_t)it * stride + lane] = hd;
+      heap_ids[(uint64_t)it * stride + lane] = hid;
+    }
+    if (lane == 0) {
+      heap_n[it] = n;
+      flags[it] = 0;
+    }
+  }
+}
+
+// The reference algorithm verbatim for flagged items / k > 32: every row of
+// every cluster, exact distance, TopKResult::insert in row order.
+__global__ void __launch_bounds__(256) k_exact_items(IndexView ix, QueryView qv, uint32_t n_items,
+                                                     const uint32_t* __restrict__ item_off,
+                                                     const uint32_t* __restrict__ clusters,
+                                                     const uint32_t* __restrict__ kv,
+                                                     uint64_t* heap_ids, double* heap_d,
+                                                     uint32_t* heap_n, uint32_t stride,
+                                                     uint8_t* changed, const int* flags) {
+  const uint32_t it = blockIdx.x;
+  if (flags && !flags[it]) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint32_t k = kv[it];
+  double* hd = reinterpret_cast<double*>(sm);            // k+1
+  uint64_t* hi = reinterpret_cast<uint64_t*>(hd + k + 1);  // k+1
+  double* td = reinterpret_cast<double*>(hi + k + 1);     // 256
+  uint64_t* ti = reinterpret_cast<uint64_t*>(td + 256);   // 256
+  float* qsh = reinterpret_cast<float*>(ti + 256);        // dpad
+  __shared__ uint32_t s_n;
+  __shared__ int s_ch;
+  for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)it * ix.dpad + d];
+  if (threadIdx.x == 0) {
+    s_n = heap_n[it];
+    for (uint32_t i = 0; i < s_n; ++i) {
+      hd[i] = heap_d[(uint64_t)it * stride + i];
+      hi[i] = heap_ids[(uint64_t)it * stride + i];
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = item_off[it]; j < item_off[it + 1]; ++j) {
+    const uint32_t c = clusters[j];
+    const uint64_t beg = ix.list_off[c], end = ix.list_off[c + 1];
+    if (threadIdx.x == 0) s_ch = 0;
+    for (uint64_t r0 = beg; r0 < end; r0 += blockDim.x) {
+      const uint64_t r = r0 + threadIdx.x;
+      if (r < end) {
+        td[threadIdx.x] = it_exact_row(ix, qsh, c, r);
+        ti[threadIdx.x] = ix.ids[r];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t n = s_n;
+        const uint32_t lim = (uint32_t)min((uint64_t)blockDim.x, end - r0);
+        for (uint32_t t = 0; t < lim; ++t) {
+          const double d = td[t];
+          const uint64_t id = ti[t];
+          if (k == 0) break;
+          // TopKResult::insert
+          bool skip = false;
+          for (uint32_t i = 0; i < n; ++i) {
+            if (hi[i] == id) {
+              if (d >= hd[i]) {
+                skip = true;
+              } else {
+                for (uint32_t q = i; q + 1 < n; ++q) {
+                  hd[q] = hd[q + 1];
+                  hi[q] = hi[q + 1];
+                }
+                --n;
+              }
+              break;
+            }
+          }
+          if (skip) continue;
+          uint32_t lo = 0, up = n;
+          while (lo < up) {
+            const uint32_t mid = (lo + up) >> 1;
+            if (pair_less(hd[mid], hi[mid], d, id)) lo = mid + 1; else up = mid;
+          }
+          if (n >= k && lo == n) continue;
+          for (uint32_t q = n; q > lo; --q) {
+            hd[q] = hd[q - 1];
+            hi[q] = hi[q - 1];
+          }
+          hd[lo] = d;
+          hi[lo] = id;
+          ++n;
+          if (n > k) n = k;
+          s_ch = 1;
+        }
+        s_n = n;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) changed[j] = (uint8_t)s_ch;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    heap_n[it] = s_n;
+    for (uint32_t i = 0; i < s_n; ++i) {
+      heap_d[(uint64_t)it * stride + i] = hd[i];
+      heap_ids[(uint64_t)it * stride + i] = hi[i];
+    }
+  }
+}
+
+}  // namespace
+
+void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
+                           const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
+                           const float* cand_d, const uint32_t* cand_row, const float* cand_thr,
+                           const uint32_t* cand_n, uint64_t* heap_ids, double* heap_d,
+                           uint32_t* heap_n, uint32_t heap_stride, uint8_t* changed, int* flags,
+                           cudaStream_t s) {
+  if (!n_items) return;
+  const size_t smem = (size_t)kItCand * (8 + 8 + 4 + 4) + (kNprobeMax + 1) * 4 + (size_t)ix.dpad * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_finalize_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    cudaFuncSetAttribute(k_exact_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    attr = true;
+  }
+  k_finalize_items<<<n_items, kItThreads, smem, s>>>(ix, qv, n_items, item_off, clusters, k, cand_d,
+                                                     cand_row, cand_thr, cand_n, filter_eps(ix.dim),
+                                                     filter_abs(ix.dim), heap_ids, heap_d, heap_n,
+                                                     heap_stride, changed, flags);
+}
+
+void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
+                        const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
+                        uint64_t* heap_ids, double* heap_d, uint32_t* heap_n,
+                        uint32_t heap_stride, uint8_t* changed, const int* flags,
+                        cudaStream_t s) {
+  if (!n_items) return;
+  const size_t smem = (size_t)(kExactMaxK + 1) * 16 + 256 * 16 + (size_t)ix.dpad * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_exact_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    attr = true;
+  }
+  k_exact_items<<<n_items, 256, smem, s>>>(ix, qv, n_items, item_off, clusters, k, heap_ids, heap_d,
+                                           heap_n, heap_stride, changed, flags);
+}
+
+}  // namespace hivf

@@ -1,0 +1,111 @@
+// kernels.h -- internal launcher interface between the C-ABI (api.cu) and the
+// kernel translation units.  Host-only C++; not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hivf {
+
+// One grouped-scan work item: rows [row0, row0+nrows) of list `list` (local
+// row numbers) against up to kQMax queries listed in item_pairs[pair0, pair0+nq).
+struct ScanItem {
+  uint32_t list;
+  uint32_t seg;    // segment index within the list
+  uint32_t row0;   // first local row of the segment
+  uint32_t nrows;  // rows in the segment
+  uint32_t pair0;  // offset into the list-sorted pair array
+  uint32_t nq;     // queries in the group (1..kQMax)
+};
+
+// Device view of an uploaded index.
+struct IndexView {
+  const float* vec;         // chunk-major swizzled lists
+  const uint64_t* ids;      // [N] doc ids, list order
+  const float* xnorm2;      // [N] fp32(|x|^2)
+  const uint64_t* list_off; // [K+1] row offsets
+  const float* maxnorm;     // [K] upper bound of max |x| in the list
+  const float* cent;        // [K][dpad] row-major, zero padded
+  const float* cnorm2;      // [K] fp32(|c|^2)
+  const float* cnorm;       // [K] upper bound of |c|
+  const uint32_t* list_order;  // [K] lists by size, descending
+  uint32_t dim, dpad, K;
+  uint64_t N;
+  uint32_t seg_rows;        // rows per scan segment (multiple of kRowBlock)
+  uint32_t s_max;           // max segments per list
+  int metric;
+};
+
+// Per-batch query state (search space).
+struct QueryView {
+  const float* qs;      // [nq][dpad] search-space queries, zero padded
+  const float* qn2;     // [nq] fp32(|q|^2)
+  const float* qnorm;   // [nq] upper bound of |q|
+  uint32_t n;
+};
+
+// ---- layout.cu
+void launch_pack_lists(const float* src_rows, uint64_t r_first, uint64_t n_rows, uint32_t dim,
+                       uint32_t dpad, const uint64_t* d_list_off, uint32_t K, float* dst,
+                       float* xnorm2, uint32_t* maxnorm_bits, int* err, cudaStream_t s);
+void launch_pack_centroids(const float* src, uint32_t K, uint32_t dim, uint32_t dpad, float* dst,
+                           float* cnorm2, float* cnorm, int* err, cudaStream_t s);
+void launch_mean_assigned(const IndexView& ix, double* partial, uint32_t n_partial,
+                          cudaStream_t s);
+void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cudaStream_t s);
+
+// ---- assign.cu
+void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t dpad, int metric,
+                         bool normalize, float* qs, float* qn2, float* qnorm, int* err,
+                         cudaStream_t s);
+void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s);
+void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
+                          uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
+                          cudaStream_t s);
+void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t nprobe,
+                            uint32_t* plans, double* dists, const int* flags, cudaStream_t s);
+
+// ---- scan.cu
+// Pair p = (query pair_query[p], cluster pair_list[p]); output slots
+// [p*s_max, p*s_max + nseg(list)).
+void launch_build_worklist(const IndexView& ix, const uint32_t* pair_query,
+                           const uint32_t* pair_list, uint32_t n_pairs, uint32_t* list_cnt,
+                           uint32_t* list_pair_off, uint32_t* list_cursor,
+                           uint32_t* list_item_off, uint32_t* sorted_pairs, ScanItem* items,
+                           uint32_t* n_items, uint32_t* work_ctr, cudaStream_t s);
+void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items,
+                 const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
+                 const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
+                 uint32_t* out_n, int n_ctas, cudaStream_t s);
+int scan_smem_bytes(uint32_t dpad);
+
+// ---- finalize.cu
+void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe,
+                           uint32_t* pair_query, uint32_t* pair_list, cudaStream_t s);
+void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
+                            uint32_t nprobe, uint32_t k, const float* cand_d,
+                            const uint32_t* cand_row, const float* cand_thr,
+                            const uint32_t* cand_n, uint64_t* ids_out, double* d_out,
+                            uint32_t* counts_out, int* flags, cudaStream_t s);
+void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
+                         uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
+                         double* d_out, uint32_t* counts_out, cudaStream_t s);
+void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
+                           const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
+                           const float* cand_d, const uint32_t* cand_row, const float* cand_thr,
+                           const uint32_t* cand_n, uint64_t* heap_ids, double* heap_d,
+                           uint32_t* heap_n, uint32_t heap_stride, uint8_t* changed, int* flags,
+                           cudaStream_t s);
+void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
+                        const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
+                        uint64_t* heap_ids, double* heap_d, uint32_t* heap_n,
+                        uint32_t heap_stride, uint8_t* changed, const int* flags,
+                        cudaStream_t s);
+void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const uint64_t* ids,
+                        const double* d, const uint32_t* counts, uint64_t* ids_out,
+                        double* d_out, uint32_t* counts_out, cudaStream_t s);
+
+constexpr uint32_t kExactMaxK = 1024;     // exact-path heap bound
+constexpr uint32_t kNprobeMax = 4096;     // exact coarse-assign bound
+
+}  // namespace hivf

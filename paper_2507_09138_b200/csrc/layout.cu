@@ -1,0 +1,143 @@
+// layout.cu -- K6: inverted-list packing into HBM.
+//
+// Replaces the host-side list building of ivf::index_from_assignments
+// (/root/reference/proj/src/vector_index.cpp:210-235).  Input rows arrive
+// row-major in list order (exactly the order index_from_assignments appends
+// them); output is the chunk-major, 16B-group-swizzled layout the scan kernel
+// streams with 1-D bulk copies (common.cuh).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hivf {
+
+namespace {
+
+// One thread per (row, 4-dim group).  Also computes fp32 |x|^2 (from an fp64
+// sum; only used by the error-bounded filter) and the per-list max |x|.
+__global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first, uint64_t n_rows,
+                             uint32_t dim,
+                             uint32_t dpad, const uint64_t* __restrict__ list_off, uint32_t K,
+                             float* __restrict__ dst, float* __restrict__ xnorm2,
+                             uint32_t* __restrict__ maxnorm_bits, int* err) {
+  const uint32_t groups = dpad / 4;
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n_rows * groups) return;
+  const uint64_t lrow = gid / groups;        // row within this chunk
+  const uint64_t r = r_first + lrow;          // global row (list order)
+  const uint32_t g = (uint32_t)(gid % groups);
+  // list of row r: upper_bound(list_off, r) - 1
+  uint32_t lo = 0, hi = K;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
+  }
+  const uint32_t c = lo;
+  const uint64_t base = list_off[c] * (uint64_t)dpad;
+  const uint64_t n_c = list_off[c + 1] - list_off[c];
+  const uint64_t lr = r - list_off[c];
+  float v[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t d = g * 4 + e;
+    v[e] = d < dim ? src[lrow * dim + d] : 0.f;
+    if (!isfinite(v[e])) *err = 1;
+  }
+  const uint64_t o = swz_offset(base, n_c, lr, g * 4);
+  *reinterpret_cast<float4*>(dst + o) = make_float4(v[0], v[1], v[2], v[3]);
+  if (g == 0) {
+    double acc = 0.0;
+    for (uint32_t d = 0; d < dim; ++d) {
+      const double x = (double)src[lrow * dim + d];
+      acc = __dadd_rn(acc, __dmul_rn(x, x));
+    }
+    xnorm2[r] = __double2float_rn(acc);
+    const float nrm = __double2float_ru(sqrt(acc) * (1.0 + 1e-6));
+    atomicMax(maxnorm_bits + c, __float_as_uint(nrm));  // non-negative floats order as uints
+  }
+}
+
+__global__ void k_pack_centroids(const float* __restrict__ src, uint32_t K, uint32_t dim,
+                                 uint32_t dpad, float* __restrict__ dst, float* cnorm2,
+                                 float* cnorm, int* err) {
+  const uint32_t c = blockIdx.x;
+  for (uint32_t d = threadIdx.x; d < dpad; d += blockDim.x) {
+    const float v = d < dim ? src[(uint64_t)c * dim + d] : 0.f;
+    if (!isfinite(v)) *err = 1;
+    dst[(uint64_t)c * dpad + d] = v;
+  }
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (uint32_t d = 0; d < dim; ++d) {
+      const double x = (double)src[(uint64_t)c * dim + d];
+      acc = __dadd_rn(acc, __dmul_rn(x, x));
+    }
+    cnorm2[c] = __double2float_rn(acc);
+    cnorm[c] = __double2float_ru(sqrt(acc) * (1.0 + 1e-6));
+  }
+}
+
+// mean_assigned_distance (vector_index.cpp:222-233): exact per-row distance to
+// its centroid, reduced in a fixed tree (deterministic; the reference sums in
+// corpus order, so the last bits may differ -- the value is informational).
+__global__ void k_mean_assigned(IndexView ix, double* partial) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ix.N;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = ix.K;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (ix.list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t base = ix.list_off[lo] * (uint64_t)ix.dpad;
+    const uint64_t n_c = ix.list_off[lo + 1] - ix.list_off[lo];
+    const uint64_t lr = r - ix.list_off[lo];
+    double d = 0.0;
+    for (uint32_t k = 0; k < ix.dim; ++k)
+      d = exact_step(d, ix.vec[swz_offset(base, n_c, lr, k)], ix.cent[(uint64_t)lo * ix.dpad + k]);
+    acc += d;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void k_check_dup(const uint64_t* sorted, uint64_t n, int* err) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (i < n && sorted[i] == sorted[i - 1]) *err = 2;
+}
+
+}  // namespace
+
+void launch_pack_lists(const float* src_rows, uint64_t r_first, uint64_t n_rows, uint32_t dim,
+                       uint32_t dpad, const uint64_t* d_list_off, uint32_t K, float* dst,
+                       float* xnorm2, uint32_t* maxnorm_bits, int* err, cudaStream_t s) {
+  const uint64_t total = n_rows * (dpad / 4);
+  if (total == 0) return;
+  const uint32_t bs = 256;
+  k_pack_lists<<<(unsigned)((total + bs - 1) / bs), bs, 0, s>>>(
+      src_rows, r_first, n_rows, dim, dpad, d_list_off, K, dst, xnorm2, maxnorm_bits, err);
+}
+
+void launch_pack_centroids(const float* src, uint32_t K, uint32_t dim, uint32_t dpad, float* dst,
+                           float* cnorm2, float* cnorm, int* err, cudaStream_t s) {
+  k_pack_centroids<<<K, 128, 0, s>>>(src, K, dim, dpad, dst, cnorm2, cnorm, err);
+}
+
+void launch_mean_assigned(const IndexView& ix, double* partial, uint32_t n_partial,
+                          cudaStream_t s) {
+  k_mean_assigned<<<n_partial, 256, 0, s>>>(ix, partial);
+}
+
+void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cudaStream_t s) {
+  if (n < 2) return;
+  k_check_dup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sorted_ids, n, err);
+}
+
+}  // namespace hivf

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+Oracles: the golden fixtures produced by the reference itself
+(tests/golden/*.npz, make_golden.py) and the C restatement (oracle/) on the
+same seeded inputs.  Bar: ids bit-exact, distances bit-equal doubles, plans
+equal in order (stronger than the north_star's 1e-5 relative).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2507_09138_b200 import Context
+    c = Context(0)
+    yield c
+
+
+def golden_index(ctx, g):
+    from paper_2507_09138_b200 import IvfIndex
+    rows = ((g["list_ids"] - 3) // 7).astype(np.int64)
+    vec = g["corpus"][rows]
+    if int(g["metric"]) == 1:
+        vec = np.stack([oracle.normalized(r) for r in vec])
+    return IvfIndex.upload(ctx, g["centroids"], g["list_off"], vec, g["list_ids"], int(g["metric"]))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_golden_search_and_plans(ctx, path):
+    g = np.load(path)
+    ix = golden_index(ctx, g)
+    Q = g["queries"]
+    for key in g.files:
+        if key.startswith("plan_np"):
+            npb = int(key[len("plan_np"):])
+            plans = ix.select_clusters(Q, npb)
+            np.testing.assert_array_equal(plans, g[key])
+        if key.startswith("ids_np"):
+            npb, k = key[len("ids_np"):].split("_k")
+            npb, k = int(npb), int(k)
+            ids, d, cnt = ix.search(Q, npb, k)
+            np.testing.assert_array_equal(cnt, g[f"count_np{npb}_k{k}"])
+            np.testing.assert_array_equal(ids, g[key])
+            assert np.array_equal(d.view(np.uint64), g[f"dist_np{npb}_k{k}"].view(np.uint64))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_golden_nprobe_all_equals_brute_force(ctx, path):
+    # test_vector_index.cpp:196-208 / acceptance criterion 1
+    g = np.load(path)
+    ix = golden_index(ctx, g)
+    ids, d, cnt = ix.search(g["queries"], ix.k_clusters, 10)
+    np.testing.assert_array_equal(ids, g["brute_ids_k10"])
+    assert np.array_equal(d.view(np.uint64), g["brute_dist_k10"].view(np.uint64))
+
+
+def _mixture(rng, n, dim, topics, spread):
+    centers = rng.standard_normal((topics, dim)).astype(np.float32)
+    X = centers[np.arange(n) % topics] + rng.standard_normal((n, dim)).astype(np.float32) * spread
+    return X.astype(np.float32), centers
+
+
+def _random_index(ctx, rng, n, dim, K, spread=0.3, topics=None, metric=0, skew=False):
+    """Random centroids picked from the data, exact (oracle) assignment."""
+    from paper_2507_09138_b200 import IvfIndex
+    X, centers = _mixture(rng, n, dim, topics or max(2, K // 2), spread)
+    if metric == 1:
+        X = np.stack([oracle.normalized(r) for r in X])
+    cents = X[rng.choice(n, K, replace=False)].copy()
+    if skew:  # make one list huge (multi-segment) and several empty
+        cents[1:4] = cents[0] + 50.0
+    assign = oracle.compute_assignments(X, cents)
+    ids = rng.permutation(n).astype(np.uint64) * 3 + 11
+    csr = oracle.CsrIndex.from_assignments(X, ids, cents, assign, metric)
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids, metric)
+    return ix, csr, X, centers
+
+
+def _check_search(ix, csr, Q, nprobe, k):
+    ids, d, cnt = ix.search(Q, nprobe, k)
+    oi, od, oc = csr.search(Q, nprobe, k)
+    np.testing.assert_array_equal(cnt, oc)
+    np.testing.assert_array_equal(ids, oi)
+    assert np.array_equal(d.view(np.uint64), od.view(np.uint64))
+
+
+@pytest.mark.parametrize("dim,n,K,nprobe,k,B", [
+    (2, 300, 4, 2, 3, 5),
+    (5, 800, 10, 3, 7, 17),
+    (16, 3000, 32, 8, 10, 40),
+    (64, 6000, 48, 12, 20, 70),
+    (128, 20000, 64, 8, 10, 64),
+    (768, 20000, 64, 16, 10, 48),
+    (100, 4000, 20, 20, 1, 33),
+    (48, 5000, 16, 4, 32, 24),
+])
+def test_random_search_vs_oracle(ctx, dim, n, K, nprobe, k, B):
+    rng = np.random.default_rng(dim * 1000 + K)
+    ix, csr, X, centers = _random_index(ctx, rng, n, dim, K)
+    Q = (centers[rng.integers(0, len(centers), B)] +
+         rng.standard_normal((B, dim)).astype(np.float32) * 0.3).astype(np.float32)
+    plans = ix.select_clusters(Q, nprobe)
+    oplans, _ = csr.assign(Q, nprobe)
+    np.testing.assert_array_equal(plans, oplans)
+    _check_search(ix, csr, Q, nprobe, k)
+
+
+def test_many_queries_per_list_and_segments(ctx):
+    """>16 queries per list (several query groups), lists larger than a
+    segment (several segments), empty lists."""
+    rng = np.random.default_rng(7)
+    ctx.set_option("seg_rows", 512)
+    try:
+        ix, csr, X, centers = _random_index(ctx, rng, 12000, 32, 12, spread=0.5, skew=True)
+        sizes = ix.cluster_sizes()
+        assert sizes.max() > 1024 and (sizes == 0).any()
+        Q = X[rng.choice(len(X), 100)] + 0.01
+        for nprobe, k in [(1, 10), (3, 5), (12, 32)]:
+            _check_search(ix, csr, Q.astype(np.float32), nprobe, k)
+    finally:
+        ctx.set_option("seg_rows", 0)
+
+
+def test_large_k_exact_path(ctx):
+    rng = np.random.default_rng(9)
+    ix, csr, X, centers = _random_index(ctx, rng, 3000, 24, 16)
+    Q = rng.standard_normal((9, 24)).astype(np.float32)
+    _check_search(ix, csr, Q, 5, 100)
+    _check_search(ix, csr, Q, 16, 64)
+
+
+def test_force_exact_matches(ctx):
+    rng = np.random.default_rng(10)
+    ix, csr, X, centers = _random_index(ctx, rng, 4000, 40, 16)
+    Q = rng.standard_normal((20, 40)).astype(np.float32)
+    ctx.set_option("force_exact", 1)
+    try:
+        _check_search(ix, csr, Q, 6, 10)
+    finally:
+        ctx.set_option("force_exact", 0)
+
+
+def test_cosine_metric(ctx):
+    rng = np.random.default_rng(11)
+    ix, csr, X, centers = _random_index(ctx, rng, 3000, 24, 12, metric=1)
+    Q = (rng.standard_normal((15, 24)) * 3).astype(np.float32)
+    _check_search(ix, csr, Q, 4, 8)
+    _check_search(ix, csr, Q, 12, 5)
+
+
+def test_ties_equal_distances(ctx):
+    """Duplicate vectors under different ids: ties broken by doc id."""
+    from paper_2507_09138_b200 import IvfIndex
+    rng = np.random.default_rng(12)
+    base = rng.standard_normal((50, 8)).astype(np.float32)
+    X = np.repeat(base, 8, axis=0)  # 8 copies of each vector
+    ids = rng.permutation(len(X)).astype(np.uint64)
+    cents = base[:6].copy()
+    assign = oracle.compute_assignments(X, cents)
+    csr = oracle.CsrIndex.from_assignments(X, ids, cents, assign)
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
+    Q = base[:10] + 0.0
+    _check_search(ix, csr, Q, 3, 12)
+    _check_search(ix, csr, Q, 6, 20)
+
+
+def test_centroid_ties_lower_id(ctx):
+    # test_vector_index.cpp:91-102 (tie -> lower cluster id) and plan order
+    from paper_2507_09138_b200 import IvfIndex
+    cents = np.array([[-1.0], [1.0], [1.0], [-1.0]], np.float32)
+    X = np.array([[0.0], [0.5], [-0.5], [2.0]], np.float32)
+    assign = oracle.compute_assignments(X, cents)
+    csr = oracle.CsrIndex.from_assignments(X, np.arange(4, dtype=np.uint64), cents, assign)
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
+    plans = ix.select_clusters(np.array([[0.0]], np.float32), 4)
+    np.testing.assert_array_equal(plans[0], [0, 1, 2, 3])
+
+
+def test_errors(ctx):
+    from paper_2507_09138_b200 import InvalidArgument, IvfIndex
+    rng = np.random.default_rng(13)
+    ix, csr, X, centers = _random_index(ctx, rng, 500, 8, 8)
+    Q = rng.standard_normal((2, 8)).astype(np.float32)
+    with pytest.raises(InvalidArgument):
+        ix.select_clusters(Q, 0)
+    with pytest.raises(InvalidArgument):
+        ix.select_clusters(Q, 9)
+    with pytest.raises(InvalidArgument):
+        ix.search(Q, 2, 0)
+    with pytest.raises(InvalidArgument):  # duplicate doc ids (vector_index.cpp:240-244)
+        IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, np.zeros(len(csr.ids), np.uint64))
+    bad = csr.vectors.copy()
+    bad[3, 2] = np.nan
+    with pytest.raises(InvalidArgument):
+        IvfIndex.upload(ctx, csr.centroids, csr.off, bad, csr.ids)
+
+
+def test_corpus_a_known_answers(ctx):
+    # test_vector_index.cpp:116-125,145-155 (CORPUS-A)
+    from paper_2507_09138_b200 import IvfIndex
+    pts = np.array([[0, 0], [.1, 0], [0, .1], [.1, .1], [10, 10], [10.1, 10], [9.9, 10.05],
+                    [10, 10.05]], np.float32)
+    cents = np.array([[0.05, 0.05], [10.0, 10.025]], np.float32)
+    assign = oracle.compute_assignments(pts, cents)
+    csr = oracle.CsrIndex.from_assignments(pts, np.arange(8, dtype=np.uint64), cents, assign)
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
+    np.testing.assert_array_equal(ix.cluster_sizes(), [4, 4])
+    assert list(ix.select_clusters(np.array([[1.0, 0.0]], np.float32), 1)[0]) == [0]
+    assert list(ix.select_clusters(np.array([[1.0, 0.0]], np.float32), 2)[0]) == [0, 1]
+    ids, d, cnt = ix.search(np.array([[0.0, 0.0]], np.float32), 2, 1)
+    assert cnt[0] == 1 and ids[0, 0] == 0 and d[0, 0] == 0.0
+    ids, d, cnt = ix.search(np.array([[0.0, 0.0]], np.float32), 2, 100)
+    assert cnt[0] == 8
