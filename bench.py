@@ -1,0 +1,502 @@
+#!/usr/bin/env python
+"""bench.py -- IVF queries/sec on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl hivf|reference]
+
+Workload (default `c3`, BASELINE.json configs[2]): 21M x 768 fp32 synthetic
+Gaussian mixture, IVF-4096, nprobe=128, k=10, 256-query batches (bench_workload.py).
+
+A step = one batched search (coarse assign -> grouped list scan -> exact top-k)
+of one 256-query batch.  `value` = queries/s with queries already in HBM
+(hivf_search_device), CUDA events on the library's stream, max over ranks.
+`e2e` = the same through the host-buffer C-ABI call hivf_search (pinned host
+queries in, results out, copies inside the timed region).  The 64 GB index is
+far larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): lists are sharded across ranks by
+LPT on bytes; each rank searches its shard (exact local top-k), the per-query
+candidates are all-gathered with NCCL and merged on device
+(hivf_merge_parts_device = merge_topk).  Total index size is fixed as N grows
+("scaling": "strong").
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref: /root/reference/proj sources compiled unmodified) on the box's
+host cores: make_cursor per query + RetrievalEngine::execute(live_math=true),
+on a restricted index holding every list probed by a fixed 16-query sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IVF queries/sec (21M×768, nprobe=128, k=10) at 1/2/4/8 B200; % HBM peak"
+UNIT = "queries/s"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits", "-lms", "100"],
+                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        p.terminate()
+        try:
+            p.wait(timeout=2)
+        except Exception:
+            p.kill()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=3)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torch.distributed over NCCL; one process per GPU)
+# ---------------------------------------------------------------------------
+
+def dist_setup(n_gpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# index construction (GPU, chunked, exact same data on every rank)
+# ---------------------------------------------------------------------------
+
+def build_shard(wl, ctx, rank, world):
+    """Centroids + assignments on GPU, then pack this rank's lists into HBM."""
+    import torch
+    from bench_workload import list_layout, shard_lists
+    from paper_2507_09138_b200 import IvfIndex
+    cfg = wl.cfg
+    t0 = time.time()
+    cents = wl.train_centroids()
+    assign = wl.assign_all(cents)
+    off, pos, order = list_layout(assign, cfg.k_clusters)
+    sizes = (off[1:] - off[:-1]).cpu().numpy()
+    owner = shard_lists(sizes, world) if world > 1 else np.zeros(cfg.k_clusters, np.int64)
+    own_t = torch.from_numpy(owner == rank).to(wl.device)
+    # shard-local CSR: lists not owned by this rank are empty
+    my_sizes = torch.where(own_t, off[1:] - off[:-1], torch.zeros_like(off[1:]))
+    my_off = torch.zeros_like(off)
+    my_off[1:] = torch.cumsum(my_sizes, 0)
+    mine_row = own_t[assign]
+    # position of each owned row inside the shard CSR
+    local_pos = my_off[assign] + (pos - off[assign])
+    log(f"rank {rank}: centroids+assign {time.time() - t0:.1f}s; lists {cfg.k_clusters}, "
+        f"sizes min {sizes.min()} mean {sizes.mean():.0f} max {sizes.max()}")
+
+    def chunks():
+        from bench_workload import CHUNK
+        for ci in range(wl.n_chunks()):
+            rows = wl.chunk(ci)
+            sl = slice(ci * CHUNK, ci * CHUNK + rows.shape[0])
+            m = mine_row[sl]
+            if world > 1:
+                idx = torch.nonzero(m).squeeze(1)
+                rows = rows[idx].contiguous()
+                p = local_pos[sl][idx].contiguous()
+                ids = (idx + ci * CHUNK).contiguous()
+            else:
+                p = local_pos[sl].contiguous()
+                ids = torch.arange(sl.start, sl.stop, device=wl.device, dtype=torch.int64)
+            if rows.shape[0]:
+                yield p, rows, ids
+
+    t1 = time.time()
+    ix = IvfIndex.build_scatter(ctx, cents, my_off.cpu().numpy().astype(np.uint64), 0,
+                                int(my_off[-1].item()), chunks())
+    log(f"rank {rank}: packed {int(my_off[-1].item())} rows into HBM in {time.time() - t1:.1f}s")
+    return ix, cents, sizes, owner, assign, order, off
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_hivf(args):
+    import torch
+    from bench_workload import CONFIGS, Workload, algorithmic_bytes, list_bytes
+    from paper_2507_09138_b200 import Context
+    rank, world, local = dist_setup(args.gpus)
+    cfg = CONFIGS[args.config]
+    if args.batch:
+        cfg.batch = args.batch
+    wl = Workload(cfg, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+    ctx = Context(local, stream)
+    ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, rank, world)
+    B, npb, k = cfg.batch, cfg.nprobe, cfg.k
+    pool = [wl.queries(i) for i in range(args.pool)]
+    ids = torch.empty(B, k, dtype=torch.int64, device=wl.device)
+    dd = torch.empty(B, k, dtype=torch.float64, device=wl.device)
+    cnt = torch.empty(B, dtype=torch.int32, device=wl.device)
+    if world > 1:
+        g_ids = torch.empty(world, B, k, dtype=torch.int64, device=wl.device)
+        g_d = torch.empty(world, B, k, dtype=torch.float64, device=wl.device)
+        g_cnt = torch.empty(world, B, dtype=torch.int32, device=wl.device)
+        m_ids, m_d, m_cnt = torch.empty_like(ids), torch.empty_like(dd), torch.empty_like(cnt)
+    import torch.distributed as dist
+
+    def step(i):
+        ix.search_device(pool[i % len(pool)], npb, k, ids, dd, cnt)
+        if world > 1:
+            dist.all_gather_into_tensor(g_ids, ids)
+            dist.all_gather_into_tensor(g_d, dd)
+            dist.all_gather_into_tensor(g_cnt, cnt)
+            ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    st = ctx.stats()
+    kernels_per_step = st["kernels_launched"] + (1 if world > 1 else 0)
+    # ---- timed region (value) ----------------------------------------------------
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    ms_per_step = ms / args.steps
+    value = B * args.steps / (ms / 1e3)
+    # ---- per-kernel timing pass (events around each phase, inside the library) ----
+    ctx.set_option("time_kernels", 1)
+    ctx.set_option("reset_timers", 1)
+    for i in range(args.steps):
+        step(i)
+    torch.cuda.synchronize()
+    st = ctx.stats()
+    ctx.set_option("time_kernels", 0)
+    scan_ms = st["scan_ms"] / max(1, st["timed_calls"])
+    assign_ms = st["assign_ms"] / max(1, st["timed_calls"])
+    fin_ms = st["finalize_ms"] / max(1, st["timed_calls"])
+    # algorithmic bytes of the steps (distinct lists per batch)
+    plans = [ix.select_clusters(q.cpu().numpy(), npb) for q in pool]
+    my_sizes = np.where(owner == rank, sizes, 0)
+    lb = [list_bytes(p, my_sizes, cfg.dim) for p in plans]
+    ab = [algorithmic_bytes(p, my_sizes, cfg.dim, cfg.k_clusters) for p in plans]
+    steps_lb = [lb[i % len(pool)] for i in range(args.steps)]
+    steps_ab = [ab[i % len(pool)] for i in range(args.steps)]
+    scan_bytes = float(np.mean(steps_lb))
+    peak, peak_kind = measured_peaks()
+    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
+    step_gbs = float(np.mean(steps_ab)) / (ms_per_step / 1e3) / 1e9
+    # ---- e2e: host buffers through the C-ABI ------------------------------------
+    e2e = None
+    if world == 1:
+        qh = [torch.empty(B, cfg.dim, dtype=torch.float32, pin_memory=True) for _ in pool]
+        for a, b in zip(qh, pool):
+            a.copy_(b.cpu())
+        qn = [a.numpy() for a in qh]
+        for i in range(args.warmup):
+            ix.search(qn[i % len(qn)], npb, k)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for i in range(args.steps):
+            ix.search(qn[i % len(qn)], npb, k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e2e_ms = max(e0.elapsed_time(e1), wall * 1e3)
+        e2e = {"value": B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": B * cfg.dim * 4,
+               "d2h_bytes_per_step": B * k * (8 + 8) + B * 4,
+               "api": "hivf_search (host buffers, pinned)"}
+    # ---- CPU baseline + full-scale parity sample (rank 0, N=1) -------------------
+    cpu = None
+    parity = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        cpu, parity = cpu_baseline_and_parity(ix, wl, cents, pool[0], cfg, args)
+    if rank != 0:
+        return
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic gaussian mixture (bench_workload.py), generated on device",
+        "config": {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
+                   "k_clusters": cfg.k_clusters, "nprobe": npb, "k": k, "batch": B,
+                   "query_pool_batches": len(pool), "parallelism": f"list-sharded x{world}",
+                   "l2": "index (%.1f GB) >> 126 MB L2: no flush needed" % (
+                       cfg.n * cfg.dim * 4 / 1e9)},
+        "e2e": e2e,
+        "gpu_launches": kernels_per_step * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_scan (grouped list scan)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     "traffic": None,
+                     "bytes_per_launch": int(scan_bytes), "launch_ms": round(scan_ms, 4),
+                     "step_hbm_frac": round(step_gbs / peak, 4),
+                     "phase_ms": {"assign": round(assign_ms, 4), "scan": round(scan_ms, 4),
+                                  "finalize": round(fin_ms, 4)}},
+        "cpu_baseline": cpu,
+        "parity_sample": parity,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _ref_restricted_index(rows_by_list, cents, k_clusters):
+    """A reference IvfIndex (index_from_assignments, vector_index.cpp:210-235)
+    holding only the given lists; select_clusters only reads centroids, so plans
+    and results equal the full index's for queries whose plans it covers."""
+    import oracle
+    corpus = np.concatenate([r for r, _ in rows_by_list.values()]) if rows_by_list else \
+        np.zeros((0, cents.shape[1]), np.float32)
+    ids = np.concatenate([i for _, i in rows_by_list.values()]) if rows_by_list else \
+        np.zeros(0, np.uint64)
+    assign = np.concatenate([np.full(len(i), c, np.uint32) for c, (_, i) in rows_by_list.items()]) \
+        if rows_by_list else np.zeros(0, np.uint32)
+    # index_from_assignments keeps corpus order inside a list: order rows by doc id
+    o = np.argsort(ids, kind="stable")
+    return oracle.RefIndex.from_assignments(corpus[o], ids[o], cents, assign[o], 0)
+
+
+def cpu_baseline_and_parity(ix, wl, cents, q0, cfg, args):
+    """Reference CPU path (oracle/_ref) on a bounded sample, timed on this host's
+    cores, plus a bit-exact check of our results for the same queries."""
+    import oracle
+    if not oracle.ref_available():
+        try:
+            oracle.build()
+        except Exception:
+            pass
+    if not oracle.ref_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}, None
+    S = min(args.cpu_sample, q0.shape[0])
+    Q = q0[:S].cpu().numpy()
+    cents_np = cents.cpu().numpy()
+    plans = ix.select_clusters(Q, cfg.nprobe)
+    lists = np.unique(plans)
+    sizes = ix.cluster_sizes()
+    off = np.zeros(len(sizes) + 1, np.uint64)
+    off[1:] = np.cumsum(sizes)
+    t0 = time.time()
+    rows_by_list = {}
+    for c in lists:
+        r, i = ix.get_rows(int(off[c]), int(sizes[c]))
+        rows_by_list[int(c)] = (r, i)
+    ri = _ref_restricted_index(rows_by_list, cents_np, cfg.k_clusters)
+    log(f"cpu baseline: restricted reference index of {len(lists)} lists "
+        f"({sum(len(i) for _, i in rows_by_list.values())} rows) in {time.time() - t0:.1f}s")
+    cores = os.cpu_count() or 1
+    times = []
+    for rep in range(args.cpu_reps):
+        ms, oi, od, oc = ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
+        times.append(ms)
+    best = min(times)
+    gi, gd, gc = ix.search(Q, cfg.nprobe, cfg.k)
+    exact = bool(np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint64), od.view(np.uint64))
+                 and np.array_equal(gc, oc))
+    cpu = {"value": round(S / (best / 1e3), 3), "unit": UNIT, "cores": cores, "kind": "reference",
+           "sample": f"{S} queries of the timed workload (full plans, nprobe={cfg.nprobe}) on a "
+                     f"restricted index of the {len(lists)} probed lists; make_cursor xS + "
+                     f"RetrievalEngine::execute(live_math=true), best of {len(times)} "
+                     f"({', '.join(f'{t / 1e3:.2f}s' for t in times)})"}
+    parity = {"queries": S, "bit_exact_vs_reference": exact, "nprobe": cfg.nprobe, "k": cfg.k}
+    return cpu, parity
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    import oracle
+    from bench_workload import CHUNK, CONFIGS, Workload
+    cfg = CONFIGS[args.config]
+    if args.batch:
+        cfg.batch = args.batch
+    if not oracle.ref_available():
+        try:
+            oracle.build()
+        except Exception:
+            pass
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference sources "
+                                                              "compiled) missing"}))
+        return
+    torch.cuda.set_device(0)
+    wl = Workload(cfg)
+    t0 = time.time()
+    cents = wl.train_centroids()
+    assign = wl.assign_all(cents)
+    cents_np = cents.cpu().numpy()
+    S = min(args.cpu_sample, cfg.batch)
+    Q = wl.queries(0)[:S].cpu().numpy()
+    # plans from the reference's own select_clusters on a centroid-only index
+    empty = oracle.RefIndex.from_assignments(np.zeros((0, cfg.dim), np.float32),
+                                             np.zeros(0, np.uint64), cents_np,
+                                             np.zeros(0, np.uint32))
+    plans = np.stack([empty.select_clusters(q, cfg.nprobe) for q in Q])
+    want = torch.zeros(cfg.k_clusters, dtype=torch.bool, device=wl.device)
+    want[torch.from_numpy(np.unique(plans).astype(np.int64)).to(wl.device)] = True
+    rows, ids, asg = [], [], []
+    for ci in range(wl.n_chunks()):
+        x = wl.chunk(ci)
+        a = assign[ci * CHUNK: ci * CHUNK + x.shape[0]]
+        m = torch.nonzero(want[a]).squeeze(1)
+        rows.append(x[m].cpu().numpy())
+        ids.append((m + ci * CHUNK).cpu().numpy().astype(np.uint64))
+        asg.append(a[m].cpu().numpy().astype(np.uint32))
+    ri = oracle.RefIndex.from_assignments(np.concatenate(rows), np.concatenate(ids), cents_np,
+                                          np.concatenate(asg))
+    log(f"reference: restricted index ({int(sum(len(i) for i in ids))} rows) in "
+        f"{time.time() - t0:.1f}s")
+    for _ in range(args.warmup):
+        ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
+    times = []
+    for _ in range(args.steps):
+        ms, *_ = ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
+        times.append(ms)
+    tot = sum(times)
+    value = S * len(times) / (tot / 1e3)
+    cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tot / len(times), 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic gaussian mixture (bench_workload.py)",
+        "config": {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
+                   "k_clusters": cfg.k_clusters, "nprobe": cfg.nprobe, "k": cfg.k,
+                   "batch": cfg.batch, "parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
+                         "kind": "reference",
+                         "sample": f"{S} queries per step (full plans) on a restricted index of "
+                                   f"the {len(np.unique(plans))} probed lists"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--impl", default="hivf", choices=["hivf", "reference"])
+    ap.add_argument("--pool", type=int, default=8, help="distinct query batches cycled")
+    ap.add_argument("--cpu-sample", type=int, default=8)
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        with torch.cuda.stream(torch.cuda.Stream()):  # one explicit stream for torch + hivf
+            run_hivf(args)
+
+
+if __name__ == "__main__":
+    main()

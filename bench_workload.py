@@ -1,0 +1,184 @@
+"""Synthetic IVF workloads for bench.py (bench infrastructure, not product).
+
+Distribution follows the reference generator's design
+(/root/reference/proj/src/workload.cpp:23-35,135-164): topic centers on the
+unit sphere, point i belongs to topic i mod T, per-dim N(0, spread^2) noise,
+doc_id = i; queries = topic center + the same noise, topics uniform
+(workload.cpp:241-309 samples topics; Zipf for skewed streams).  Generated on
+the GPU with torch's counter-based Philox generator, one fixed seed per
+262144-row chunk, so any chunk can be regenerated bit-identically (the index
+build regenerates chunks instead of holding the 64 GB corpus twice).
+
+Centroids: k-means (Lloyd) on a sample, deterministic (fp64 segment sums).
+Assignments: fp32 argmin over centroids (the same assignment vector is handed
+to both the GPU index and the reference's index_from_assignments, so both
+search the identical index -- SURVEY.md 8(d)).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+CHUNK = 1 << 18
+
+
+@dataclass
+class Config:
+    name: str
+    n: int
+    dim: int
+    k_clusters: int
+    nprobe: int
+    k: int
+    batch: int
+    spread: float
+    zipf: float = 0.0
+
+    def describe(self) -> str:
+        return (f"{self.n // 1_000_000 if self.n >= 1_000_000 else self.n}"
+                f"{'M' if self.n >= 1_000_000 else ''}x{self.dim} IVF-{self.k_clusters} "
+                f"nprobe={self.nprobe} k={self.k} batch={self.batch}")
+
+
+CONFIGS = {
+    # BASELINE.json configs[0..2] (configs[3]/[4] are multi-GPU / stream workloads)
+    "c1": Config("c1", 100_000, 128, 256, 8, 10, 64, 0.25),
+    "c2": Config("c2", 1_000_000, 768, 1024, 32, 10, 256, 0.03),
+    "c3": Config("c3", 21_000_000, 768, 4096, 128, 10, 256, 0.03),
+    # small configs for tests
+    "tiny": Config("tiny", 60_000, 64, 64, 8, 10, 48, 0.3),
+}
+
+
+class Workload:
+    def __init__(self, cfg: Config, device="cuda", corpus_seed=1, query_seed=2):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.corpus_seed = corpus_seed
+        self.query_seed = query_seed
+        self.topics = max(1, cfg.k_clusters // 4)
+        g = torch.Generator(device=self.device).manual_seed(corpus_seed)
+        c = torch.randn(self.topics, cfg.dim, generator=g, device=self.device, dtype=torch.float64)
+        c = c / c.norm(dim=1, keepdim=True).clamp_min(1e-300)
+        self.centers = c.float()
+
+    # -- corpus -----------------------------------------------------------------
+    def n_chunks(self) -> int:
+        return (self.cfg.n + CHUNK - 1) // CHUNK
+
+    def chunk(self, ci: int) -> torch.Tensor:
+        """Rows [ci*CHUNK, min(n, (ci+1)*CHUNK)) as a [rows, dim] float32 tensor."""
+        first = ci * CHUNK
+        rows = min(CHUNK, self.cfg.n - first)
+        g = torch.Generator(device=self.device).manual_seed(self.corpus_seed * 1_000_003 + ci + 17)
+        z = torch.randn(rows, self.cfg.dim, generator=g, device=self.device, dtype=torch.float32)
+        topic = torch.arange(first, first + rows, device=self.device) % self.topics
+        return self.centers[topic] + z * self.cfg.spread
+
+    # -- queries ----------------------------------------------------------------
+    def queries(self, batch_index: int, b: int | None = None) -> torch.Tensor:
+        b = b or self.cfg.batch
+        g = torch.Generator(device=self.device).manual_seed(self.query_seed * 7919 + batch_index)
+        if self.cfg.zipf > 0:
+            w = 1.0 / torch.arange(1, self.topics + 1, device=self.device,
+                                   dtype=torch.float64) ** self.cfg.zipf
+            t = torch.multinomial(w, b, replacement=True, generator=g)
+        else:
+            t = torch.randint(0, self.topics, (b,), generator=g, device=self.device)
+        z = torch.randn(b, self.cfg.dim, generator=g, device=self.device, dtype=torch.float32)
+        return (self.centers[t] + z * self.cfg.spread).contiguous()
+
+    # -- centroids ----------------------------------------------------------------
+    @staticmethod
+    def _assign(x: torch.Tensor, cents: torch.Tensor, cn2: torch.Tensor) -> torch.Tensor:
+        return torch.argmin(cn2[None, :] - 2.0 * (x @ cents.T), dim=1)
+
+    def train_centroids(self, iters: int = 6, sample_per_centroid: int = 48) -> torch.Tensor:
+        K = self.cfg.k_clusters
+        want = min(self.cfg.n, max(K, sample_per_centroid * K))
+        parts, got, ci = [], 0, 0
+        while got < want:
+            c = self.chunk(ci)[: want - got]
+            parts.append(c)
+            got += c.shape[0]
+            ci += 1
+        x = torch.cat(parts)
+        g = torch.Generator(device=self.device).manual_seed(self.corpus_seed + 99)
+        cents = x[torch.randperm(x.shape[0], generator=g, device=self.device)[:K]].clone()
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            for _ in range(iters):
+                a = self._assign(x, cents, (cents * cents).sum(1))
+                order = torch.sort(a, stable=True).indices
+                counts = torch.bincount(a, minlength=K)
+                cs = torch.zeros(x.shape[0] + 1, x.shape[1], device=self.device, dtype=torch.float64)
+                cs[1:] = torch.cumsum(x[order].double(), dim=0)
+                ends = torch.cumsum(counts, 0)
+                starts = ends - counts
+                sums = cs[ends] - cs[starts]
+                nz = counts > 0
+                cents[nz] = (sums[nz] / counts[nz, None].double()).float()
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        return cents.contiguous()
+
+    def assign_all(self, cents: torch.Tensor) -> torch.Tensor:
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        cn2 = (cents * cents).sum(1)
+        out = torch.empty(self.cfg.n, dtype=torch.int64, device=self.device)
+        try:
+            for ci in range(self.n_chunks()):
+                x = self.chunk(ci)
+                out[ci * CHUNK: ci * CHUNK + x.shape[0]] = self._assign(x, cents, cn2)
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        return out
+
+
+def list_layout(assign: torch.Tensor, k_clusters: int):
+    """index_from_assignments order: list offsets + each row's list-order position."""
+    counts = torch.bincount(assign, minlength=k_clusters)
+    off = torch.zeros(k_clusters + 1, dtype=torch.int64, device=assign.device)
+    off[1:] = torch.cumsum(counts, 0)
+    order = torch.sort(assign, stable=True).indices
+    pos = torch.empty_like(order)
+    pos[order] = torch.arange(assign.shape[0], device=assign.device)
+    return off, pos, order
+
+
+def shard_lists(sizes: np.ndarray, world: int) -> np.ndarray:
+    """LPT assignment of lists to ranks by bytes; owner[c]."""
+    owner = np.zeros(len(sizes), np.int64)
+    load = np.zeros(world, np.float64)
+    for c in np.argsort(-sizes.astype(np.float64), kind="stable"):
+        r = int(np.argmin(load))
+        owner[c] = r
+        load[r] += float(sizes[c])
+    return owner
+
+
+def algorithmic_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int, k_clusters: int) -> int:
+    """distinct probed lists streamed once + centroids + queries."""
+    uniq = np.unique(plans)
+    return int(sizes[uniq].sum()) * 4 * dim + k_clusters * 4 * dim + plans.shape[0] * 4 * dim
+
+
+def list_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int) -> int:
+    return int(sizes[np.unique(plans)].sum()) * 4 * dim
+
+
+def human(n: float) -> str:
+    for u in ["", "K", "M", "G", "T"]:
+        if abs(n) < 1000:
+            return f"{n:.3g}{u}"
+        n /= 1000
+    return f"{n:.3g}P"
+
+
+__all__ = ["CHUNK", "CONFIGS", "Config", "Workload", "list_layout", "shard_lists",
+           "algorithmic_bytes", "list_bytes", "human", "math"]

@@ -92,7 +92,16 @@ hivf_status hivf_index_begin(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n
                              const uint64_t* list_offsets, hivf_index** out);
 hivf_status hivf_index_add_rows_device(hivf_index* idx, uint64_t first_row, uint64_t n_rows,
                                        const float* d_rows, const uint64_t* d_ids);
+/* Same, rows scattered to explicit list-order positions d_positions[n_rows]
+ * (index_from_assignments order: list offset + rank within the list). */
+hivf_status hivf_index_add_rows_at_device(hivf_index* idx, uint64_t n_rows,
+                                          const uint64_t* d_positions, const float* d_rows,
+                                          const uint64_t* d_ids);
 hivf_status hivf_index_finish(hivf_index* idx);
+/* Read rows [first_row, first_row+n_rows) back (list order, row-major host
+ * floats + doc ids); the IvfIndex::doc_embedding of vector_index.hpp:105-108. */
+hivf_status hivf_index_get_rows(hivf_index* idx, uint64_t first_row, uint64_t n_rows,
+                                float* rows_out, uint64_t* ids_out);
 hivf_status hivf_index_destroy(hivf_index* idx);
 /* k_clusters / cluster_size / total_vectors / mean_assigned_distance
  * (vector_index.hpp:92-98).  Any output pointer may be NULL. */
@@ -171,12 +180,18 @@ hivf_status hivf_residency_get(const hivf_index* idx, uint8_t* resident_out);
 typedef struct {
   uint32_t kernels_launched;   /* kernels issued by the last search call */
   uint32_t n_work_items;       /* grouped-scan work items of the last call */
-  uint32_t n_fallback;         /* queries that took the exact fallback path */
+  uint32_t n_fallback;         /* queries that took an exact fallback path (last call) */
   uint32_t n_unique_lists;     /* distinct lists probed by the last batch */
-  uint64_t scan_bytes;         /* algorithmic list bytes of the last batch */
+  uint64_t scan_bytes;         /* algorithmic list bytes of the last batch (sum n_c*dim*4) */
+  uint32_t timed_calls;        /* calls accumulated below (option "time_kernels") */
+  double assign_ms;            /* accumulated CUDA-event time: coarse assign kernels */
+  double scan_ms;              /* accumulated CUDA-event time: grouped list scan kernel */
+  double finalize_ms;          /* accumulated CUDA-event time: re-rank + fallback kernels */
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
-/* Tuning knobs (0 = default): rows per scan segment, force exact path. */
+/* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
+ * "scan_ctas", "time_kernels" (record events around each phase and
+ * accumulate into hivf_stats), "reset_timers". */
 hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
 
 #ifdef __cplusplus

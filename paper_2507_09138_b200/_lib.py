@@ -19,7 +19,8 @@ SYMBOLS = [
     "hivf_last_error", "hivf_version", "hivf_ctx_create", "hivf_ctx_destroy",
     "hivf_ctx_set_stream", "hivf_ctx_synchronize", "hivf_index_upload",
     "hivf_index_upload_device", "hivf_index_begin", "hivf_index_add_rows_device",
-    "hivf_index_finish", "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
+    "hivf_index_add_rows_at_device", "hivf_index_finish", "hivf_index_get_rows",
+    "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
     "hivf_assign", "hivf_search", "hivf_search_device", "hivf_scan_items",
     "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get", "hivf_last_stats",
     "hivf_set_option",
@@ -43,7 +44,8 @@ class InternalError(HivfError):
 class Stats(C.Structure):
     _fields_ = [("kernels_launched", C.c_uint32), ("n_work_items", C.c_uint32),
                 ("n_fallback", C.c_uint32), ("n_unique_lists", C.c_uint32),
-                ("scan_bytes", C.c_uint64)]
+                ("scan_bytes", C.c_uint64), ("timed_calls", C.c_uint32),
+                ("assign_ms", C.c_double), ("scan_ms", C.c_double), ("finalize_ms", C.c_double)]
 
 
 _lib = None
@@ -70,7 +72,9 @@ def lib():
         "hivf_index_upload_device": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, P(vp)]),
         "hivf_index_begin": (i32, [vp, u32, i32, u32, vp, i32, vp, P(vp)]),
         "hivf_index_add_rows_device": (i32, [vp, u64, u64, vp, vp]),
+        "hivf_index_add_rows_at_device": (i32, [vp, u64, vp, vp, vp]),
         "hivf_index_finish": (i32, [vp]),
+        "hivf_index_get_rows": (i32, [vp, u64, u64, vp, vp]),
         "hivf_index_destroy": (i32, [vp]),
         "hivf_index_info": (i32, [vp, P(u32), P(u32), P(u64), P(u64), P(f64)]),
         "hivf_index_cluster_sizes": (i32, [vp, vp]),

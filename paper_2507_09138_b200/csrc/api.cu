@@ -117,7 +117,43 @@ struct hivf_ctx {
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;
+  uint32_t last_K = 0;
+  const hivf_index* last_index = nullptr;
+  // phase timing (option "time_kernels"): one event set per call, resolved lazily
+  int opt_time = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  uint32_t timed_calls = 0;
+  double acc_assign = 0, acc_scan = 0, acc_fin = 0;
+  cudaEvent_t next_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  void mark(int slot) {  // slot 0..3 of the current set
+    if (!opt_time) return;
+    cudaEventRecord(next_event(), stream);
+    (void)slot;
+  }
+  void resolve_timers() {
+    for (size_t i = 0; i + 4 <= ev_used; i += 4) {
+      float a = 0, b = 0, c = 0;
+      cudaEventSynchronize(ev_pool[i + 3]);
+      cudaEventElapsedTime(&a, ev_pool[i], ev_pool[i + 1]);
+      cudaEventElapsedTime(&b, ev_pool[i + 1], ev_pool[i + 2]);
+      cudaEventElapsedTime(&c, ev_pool[i + 2], ev_pool[i + 3]);
+      acc_assign += a;
+      acc_scan += b;
+      acc_fin += c;
+      ++timed_calls;
+    }
+    ev_used = 0;
+  }
   ~hivf_ctx() {
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq, &pl,
                     &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items, &n_items,
                     &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &out_d, &out_cnt,
@@ -245,6 +281,15 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->opt_force_exact = value != 0;
   } else if (!strcmp(name, "scan_ctas")) {
     ctx->opt_scan_ctas = (int)value;
+  } else if (!strcmp(name, "time_kernels")) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->resolve_timers();
+    ctx->opt_time = value != 0;
+  } else if (!strcmp(name, "reset_timers")) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->ev_used = 0;
+    ctx->timed_calls = 0;
+    ctx->acc_assign = ctx->acc_scan = ctx->acc_fin = 0;
   } else {
     return fail(HIVF_EINVAL, "hivf_set_option: unknown option '%s'", name);
   }
@@ -254,8 +299,25 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
   if (!ctx || !out) return fail(HIVF_EINVAL, "NULL argument");
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->resolve_timers();
   hivf_stats s = ctx->stats;
+  s.timed_calls = ctx->timed_calls;
+  s.assign_ms = ctx->acc_assign;
+  s.scan_ms = ctx->acc_scan;
+  s.finalize_ms = ctx->acc_fin;
   if (ctx->n_items.p) CK(cudaMemcpy(&s.n_work_items, ctx->n_items.p, 4, cudaMemcpyDeviceToHost));
+  if (ctx->last_index && ctx->list_cnt.p && ctx->last_K == ctx->last_index->K) {
+    std::vector<uint32_t> cnt(ctx->last_K);
+    CK(cudaMemcpy(cnt.data(), ctx->list_cnt.p, 4ull * ctx->last_K, cudaMemcpyDeviceToHost));
+    s.n_unique_lists = 0;
+    s.scan_bytes = 0;
+    const auto& off = ctx->last_index->list_off;
+    for (uint32_t c = 0; c < ctx->last_K; ++c)
+      if (cnt[c]) {
+        ++s.n_unique_lists;
+        s.scan_bytes += (off[c + 1] - off[c]) * (uint64_t)ctx->last_index->dim * 4;
+      }
+  }
   if (ctx->last_nq && ctx->flags_f.p && ctx->flags_c.p) {
     std::vector<int> f(ctx->last_nq), g(ctx->last_nq);
     CK(cudaMemcpy(f.data(), ctx->flags_f.p, 4ull * ctx->last_nq, cudaMemcpyDeviceToHost));
@@ -350,11 +412,54 @@ hivf_status hivf_index_add_rows_device(hivf_index* ix, uint64_t first_row, uint6
   if (!n_rows) return HIVF_OK;
   cudaStream_t s = ix->ctx->stream;
   CK(cudaSetDevice(ix->ctx->device));
-  launch_pack_lists(d_rows, first_row, n_rows, ix->dim, ix->dpad, ix->d_list_off, ix->K, ix->vec,
-                    ix->xnorm2, ix->maxnorm_bits, ix->d_err, s);
+  launch_pack_lists(d_rows, first_row, nullptr, n_rows, ix->dim, ix->dpad, ix->d_list_off, ix->K,
+                    ix->vec, ix->xnorm2, ix->maxnorm_bits, ix->d_err, s);
   CKL();
   if (d_ids) CK(cudaMemcpyAsync(ix->ids + first_row, d_ids, n_rows * 8, cudaMemcpyDeviceToDevice, s));
   ix->rows_added += n_rows;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_add_rows_at_device(hivf_index* ix, uint64_t n_rows,
+                                          const uint64_t* d_positions, const float* d_rows,
+                                          const uint64_t* d_ids) {
+  if (!ix || (n_rows && (!d_rows || !d_positions)))
+    return fail(HIVF_EINVAL, "hivf_index_add_rows_at_device: NULL argument");
+  if (ix->finished) return fail(HIVF_EINVAL, "index already finished");
+  if (ix->rows_added + n_rows > ix->N) return fail(HIVF_EINVAL, "add_rows_at: more rows than N");
+  if (!n_rows) return HIVF_OK;
+  cudaStream_t s = ix->ctx->stream;
+  CK(cudaSetDevice(ix->ctx->device));
+  launch_pack_lists(d_rows, 0, d_positions, n_rows, ix->dim, ix->dpad, ix->d_list_off, ix->K,
+                    ix->vec, ix->xnorm2, ix->maxnorm_bits, ix->d_err, s);
+  CKL();
+  if (d_ids) {
+    launch_scatter_ids(d_ids, d_positions, n_rows, ix->ids, s);
+    CKL();
+  }
+  ix->rows_added += n_rows;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_get_rows(hivf_index* ix, uint64_t first_row, uint64_t n_rows,
+                                float* rows_out, uint64_t* ids_out) {
+  if (!ix) return fail(HIVF_EINVAL, "index is NULL");
+  if (first_row + n_rows > ix->N) return fail(HIVF_EINVAL, "get_rows: range beyond N");
+  if (!n_rows) return HIVF_OK;
+  cudaStream_t s = ix->ctx->stream;
+  CK(cudaSetDevice(ix->ctx->device));
+  const uint64_t per = std::max<uint64_t>(1, (256ull << 20) / (4ull * ix->dim));
+  float* tmp = nullptr;
+  CK(cudaMalloc(&tmp, std::min(per, n_rows) * ix->dim * 4));
+  for (uint64_t r = 0; r < n_rows; r += per) {
+    const uint64_t n = std::min(per, n_rows - r);
+    launch_unpack_rows(ix->vec, ix->d_list_off, ix->K, ix->dim, ix->dpad, first_row + r, n, tmp, s);
+    if (rows_out) cudaMemcpyAsync(rows_out + r * ix->dim, tmp, n * ix->dim * 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+  }
+  cudaFree(tmp);
+  if (ids_out) CK(cudaMemcpyAsync(ids_out, ix->ids + first_row, n_rows * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return HIVF_OK;
 }
 
@@ -530,7 +635,7 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
 }
 
 // Grouped scan over pairs (pair_query/pair_list already in c->pq / c->pl).
-static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs) {
+static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs, bool timed) {
   hivf_ctx* c = ix->ctx;
   const IndexView v = ix->view();
   const size_t nslots = (size_t)std::max<uint32_t>(n_pairs, 1) * ix->s_max;
@@ -556,6 +661,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
                         c->stream);
   CKL();
   const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;
+  if (timed) c->mark(1);
   launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
               c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
               c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
@@ -586,7 +692,10 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
   CK(cudaSetDevice(c->device));
   c->stats = hivf_stats{};
   c->last_nq = n;
+  c->last_index = ix;
+  c->last_K = ix->K;
   QueryView qv;
+  c->mark(0);
   if ((st = prep_queries(ix, d_queries, n, true, &qv)) != HIVF_OK) return st;
   if ((st = run_assign(ix, qv, nprobe, nullptr)) != HIVF_OK) return st;
   const uint32_t np = n * nprobe;
@@ -598,7 +707,8 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
   if (!exact_only) {
     launch_plans_to_pairs(c->plans.as<uint32_t>(), n, nprobe, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), c->stream);
     CKL();
-    if ((st = run_scan(ix, qv, np)) != HIVF_OK) return st;
+    if ((st = run_scan(ix, qv, np, true)) != HIVF_OK) return st;
+    c->mark(2);
     launch_finalize_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(),
                            c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(),
                            d_ids_out, d_dists_out, d_counts_out, c->flags_f.as<int>(), c->stream);
@@ -607,12 +717,16 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
                         d_dists_out, d_counts_out, c->stream);
     CKL();
     c->stats.kernels_launched += 4;
+    c->mark(3);
   } else {
     CK(cudaMemsetAsync(c->flags_f.p, 0, (size_t)n * 4, c->stream));
+    c->mark(1);
+    c->mark(2);
     launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, nullptr, d_ids_out, d_dists_out,
                         d_counts_out, c->stream);
     CKL();
     c->stats.kernels_launched += 1;
+    c->mark(3);
   }
   return HIVF_OK;
 }
@@ -706,6 +820,8 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
   CK(cudaSetDevice(c->device));
   c->stats = hivf_stats{};
   c->last_nq = 0;
+  c->last_index = ix;
+  c->last_K = ix->K;
   cudaStream_t s = c->stream;
   // item -> query index per pair
   std::vector<uint32_t> pq(n_pairs);
@@ -743,7 +859,7 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
   const IndexView v = ix->view();
   const bool exact_only = c->opt_force_exact || kmax > (uint32_t)kKP;
   if (!exact_only && n_pairs) {
-    if ((st = run_scan(ix, qv, n_pairs)) != HIVF_OK) return st;
+    if ((st = run_scan(ix, qv, n_pairs, false)) != HIVF_OK) return st;
     launch_finalize_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
                           c->it_k.as<uint32_t>(), c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
                           c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), c->heap_ids.as<uint64_t>(),

@@ -16,8 +16,8 @@ namespace {
 
 // One thread per (row, 4-dim group).  Also computes fp32 |x|^2 (from an fp64
 // sum; only used by the error-bounded filter) and the per-list max |x|.
-__global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first, uint64_t n_rows,
-                             uint32_t dim,
+__global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first,
+                             const uint64_t* __restrict__ pos, uint64_t n_rows, uint32_t dim,
                              uint32_t dpad, const uint64_t* __restrict__ list_off, uint32_t K,
                              float* __restrict__ dst, float* __restrict__ xnorm2,
                              uint32_t* __restrict__ maxnorm_bits, int* err) {
@@ -25,7 +25,7 @@ __global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first, ui
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= n_rows * groups) return;
   const uint64_t lrow = gid / groups;        // row within this chunk
-  const uint64_t r = r_first + lrow;          // global row (list order)
+  const uint64_t r = pos ? pos[lrow] : r_first + lrow;  // global row (list order)
   const uint32_t g = (uint32_t)(gid % groups);
   // list of row r: upper_bound(list_off, r) - 1
   uint32_t lo = 0, hi = K;
@@ -56,6 +56,24 @@ __global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first, ui
     const float nrm = __double2float_ru(sqrt(acc) * (1.0 + 1e-6));
     atomicMax(maxnorm_bits + c, __float_as_uint(nrm));  // non-negative floats order as uints
   }
+}
+
+// Inverse of the packing: rows [first, first+n) back to row-major.
+__global__ void k_unpack_rows(const float* __restrict__ vec, const uint64_t* __restrict__ list_off,
+                              uint32_t K, uint32_t dim, uint32_t dpad, uint64_t first, uint64_t n,
+                              float* __restrict__ out) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n * dim) return;
+  const uint64_t lrow = gid / dim;
+  const uint32_t d = (uint32_t)(gid % dim);
+  const uint64_t r = first + lrow;
+  uint32_t lo = 0, hi = K;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
+  }
+  const uint64_t n_c = list_off[lo + 1] - list_off[lo];
+  out[gid] = vec[swz_offset(list_off[lo] * (uint64_t)dpad, n_c, r - list_off[lo], d)];
 }
 
 __global__ void k_pack_centroids(const float* __restrict__ src, uint32_t K, uint32_t dim,
@@ -115,14 +133,23 @@ __global__ void k_check_dup(const uint64_t* sorted, uint64_t n, int* err) {
 
 }  // namespace
 
-void launch_pack_lists(const float* src_rows, uint64_t r_first, uint64_t n_rows, uint32_t dim,
-                       uint32_t dpad, const uint64_t* d_list_off, uint32_t K, float* dst,
-                       float* xnorm2, uint32_t* maxnorm_bits, int* err, cudaStream_t s) {
+void launch_pack_lists(const float* src_rows, uint64_t r_first, const uint64_t* pos,
+                       uint64_t n_rows, uint32_t dim, uint32_t dpad, const uint64_t* d_list_off,
+                       uint32_t K, float* dst, float* xnorm2, uint32_t* maxnorm_bits, int* err,
+                       cudaStream_t s) {
   const uint64_t total = n_rows * (dpad / 4);
   if (total == 0) return;
   const uint32_t bs = 256;
   k_pack_lists<<<(unsigned)((total + bs - 1) / bs), bs, 0, s>>>(
-      src_rows, r_first, n_rows, dim, dpad, d_list_off, K, dst, xnorm2, maxnorm_bits, err);
+      src_rows, r_first, pos, n_rows, dim, dpad, d_list_off, K, dst, xnorm2, maxnorm_bits, err);
+}
+
+void launch_unpack_rows(const float* vec, const uint64_t* d_list_off, uint32_t K, uint32_t dim,
+                        uint32_t dpad, uint64_t first, uint64_t n, float* out, cudaStream_t s) {
+  const uint64_t total = n * dim;
+  if (!total) return;
+  k_unpack_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(vec, d_list_off, K, dim, dpad, first,
+                                                               n, out);
 }
 
 void launch_pack_centroids(const float* src, uint32_t K, uint32_t dim, uint32_t dpad, float* dst,
@@ -140,4 +167,17 @@ void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cuda
   k_check_dup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sorted_ids, n, err);
 }
 
+}  // namespace hivf
+
+namespace hivf {
+namespace {
+__global__ void k_scatter_ids(const uint64_t* ids, const uint64_t* pos, uint64_t n, uint64_t* out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[pos[i]] = ids[i];
+}
+}  // namespace
+void launch_scatter_ids(const uint64_t* ids, const uint64_t* pos, uint64_t n, uint64_t* out,
+                        cudaStream_t s) {
+  if (n) k_scatter_ids<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ids, pos, n, out);
+}
 }  // namespace hivf

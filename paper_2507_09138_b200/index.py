@@ -28,16 +28,24 @@ class Context:
     """Owns a device + stream (hivf_ctx)."""
 
     def __init__(self, device: int = 0, stream=None):
+        """stream: None -> the context owns a non-blocking stream; a torch
+        stream (or raw handle) -> all work is issued on it.  torch's default
+        stream has handle 0, which the C-ABI reads as "create one", so it is
+        passed as cudaStreamLegacy (0x1)."""
         h = C.c_void_p()
         s = None
         if stream is not None:
             s = stream if isinstance(stream, int) else stream.cuda_stream
+            if s == 0:
+                s = 1  # cudaStreamLegacy
         check(lib().hivf_ctx_create(device, s, C.byref(h)))
         self.h = h
         self.device = device
 
     def set_stream(self, stream):
         s = stream if (stream is None or isinstance(stream, int)) else stream.cuda_stream
+        if s == 0:
+            s = 1  # cudaStreamLegacy
         check(lib().hivf_ctx_set_stream(self.h, s))
 
     def synchronize(self):
@@ -132,6 +140,37 @@ class IvfIndex:
             del rows, rid
         check(lib().hivf_index_finish(h))
         return ix
+
+    @staticmethod
+    def build_scatter(ctx: Context, centroids, list_offsets, metric, n_rows, chunks):
+        """Incremental HBM build from corpus-order chunks: ``chunks`` yields
+        (positions uint64 [n], rows float32 [n,dim], ids uint64 [n]) torch CUDA
+        tensors; positions are list-order row indices (index_from_assignments
+        order)."""
+        import torch
+        cents = centroids
+        dev = isinstance(cents, torch.Tensor) and cents.is_cuda
+        if not dev:
+            cents = np.ascontiguousarray(cents, np.float32)
+        K, dim = cents.shape
+        off = np.ascontiguousarray(list_offsets, np.uint64)
+        h = C.c_void_p()
+        check(lib().hivf_index_begin(ctx.h, dim, metric, K, _ptr(cents), 1 if dev else 0,
+                                     off.ctypes.data, C.byref(h)))
+        ix = IvfIndex(ctx, h, dim, K, metric)
+        for pos, rows, rid in chunks:
+            check(lib().hivf_index_add_rows_at_device(h, pos.shape[0], pos.data_ptr(),
+                                                      rows.data_ptr(), rid.data_ptr()))
+            ctx.synchronize()
+        check(lib().hivf_index_finish(h))
+        return ix
+
+    def get_rows(self, first, n):
+        """Rows [first, first+n) in list order (row-major float32) + doc ids."""
+        rows = np.zeros((n, self.dim), np.float32)
+        ids = np.zeros(n, np.uint64)
+        check(lib().hivf_index_get_rows(self.h, first, n, rows.ctypes.data, ids.ctypes.data))
+        return rows, ids
 
     def close(self):
         # an index must not outlive its context (the C-ABI contract); if the
