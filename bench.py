@@ -273,6 +273,10 @@ def run_hivf(args):
     steps_lb = [lb[i % len(pool)] for i in range(args.steps)]
     steps_ab = [ab[i % len(pool)] for i in range(args.steps)]
     scan_bytes = float(np.mean(steps_lb))
+    pp = np.bincount(plans[0].ravel(), minlength=cfg.k_clusters)
+    pp = pp[pp > 0]
+    probes_per_list = {"mean": round(float(pp.mean()), 2), "p50": int(np.percentile(pp, 50)),
+                       "p90": int(np.percentile(pp, 90)), "max": int(pp.max())}
     peak, peak_kind = measured_peaks()
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
     step_gbs = float(np.mean(steps_ab)) / (ms_per_step / 1e3) / 1e9
@@ -314,6 +318,7 @@ def run_hivf(args):
         "config": {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
                    "k_clusters": cfg.k_clusters, "nprobe": npb, "k": k, "batch": B,
                    "query_pool_batches": len(pool), "parallelism": f"list-sharded x{world}",
+                   "probes_per_probed_list": probes_per_list,
                    "l2": "index (%.1f GB) >> 126 MB L2: no flush needed" % (
                        cfg.n * cfg.dim * 4 / 1e9)},
         "e2e": e2e,
@@ -328,6 +333,8 @@ def run_hivf(args):
                                   "finalize": round(fin_ms, 4)}},
         "cpu_baseline": cpu,
         "parity_sample": parity,
+        "scan_stats": {"work_items": st["n_work_items"], "fallback_queries": st["n_fallback"],
+                       "unique_lists": st["n_unique_lists"]},
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

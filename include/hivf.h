@@ -61,6 +61,10 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out);
 hivf_status hivf_ctx_destroy(hivf_ctx* ctx);
 hivf_status hivf_ctx_set_stream(hivf_ctx* ctx, void* stream);
 hivf_status hivf_ctx_synchronize(hivf_ctx* ctx);
+/* SM count and the tensor core's fp32->tf32 operand conversion as probed on
+ * this device at first context creation (0 truncation, 1 round-to-nearest-
+ * even, 2 unknown -> the FFMA scan is used). */
+hivf_status hivf_device_info(hivf_ctx* ctx, int* sm_count, int* tc_tf32_conversion);
 
 /* ---- index ----------------------------------------------------------------
  * Replaces ivf::index_from_assignments (proj/src/vector_index.cpp:210-235) and
@@ -187,11 +191,13 @@ typedef struct {
   double assign_ms;            /* accumulated CUDA-event time: coarse assign kernels */
   double scan_ms;              /* accumulated CUDA-event time: grouped list scan kernel */
   double finalize_ms;          /* accumulated CUDA-event time: re-rank + fallback kernels */
+  uint32_t scan_kernel;        /* last call: 0 exact only, 1 FFMA, 2 tcgen05 split, 3 tcgen05 single */
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
- * "scan_ctas", "time_kernels" (record events around each phase and
- * accumulate into hivf_stats), "reset_timers". */
+ * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
+ * 3 tcgen05 single-pass), "tc_qmax", "time_kernels" (record events around each
+ * phase and accumulate into hivf_stats), "reset_timers". */
 hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
 
 #ifdef __cplusplus

@@ -17,7 +17,7 @@ HIVF_OK, HIVF_EINVAL, HIVF_EINTERNAL, HIVF_ECUDA, HIVF_ENOMEM, HIVF_EUNSUPPORTED
 # header-declared symbols (tests check every one is exported)
 SYMBOLS = [
     "hivf_last_error", "hivf_version", "hivf_ctx_create", "hivf_ctx_destroy",
-    "hivf_ctx_set_stream", "hivf_ctx_synchronize", "hivf_index_upload",
+    "hivf_ctx_set_stream", "hivf_ctx_synchronize", "hivf_device_info", "hivf_index_upload",
     "hivf_index_upload_device", "hivf_index_begin", "hivf_index_add_rows_device",
     "hivf_index_add_rows_at_device", "hivf_index_finish", "hivf_index_get_rows",
     "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
@@ -45,7 +45,8 @@ class Stats(C.Structure):
     _fields_ = [("kernels_launched", C.c_uint32), ("n_work_items", C.c_uint32),
                 ("n_fallback", C.c_uint32), ("n_unique_lists", C.c_uint32),
                 ("scan_bytes", C.c_uint64), ("timed_calls", C.c_uint32),
-                ("assign_ms", C.c_double), ("scan_ms", C.c_double), ("finalize_ms", C.c_double)]
+                ("assign_ms", C.c_double), ("scan_ms", C.c_double), ("finalize_ms", C.c_double),
+                ("scan_kernel", C.c_uint32)]
 
 
 _lib = None
@@ -68,6 +69,7 @@ def lib():
         "hivf_ctx_destroy": (i32, [vp]),
         "hivf_ctx_set_stream": (i32, [vp, vp]),
         "hivf_ctx_synchronize": (i32, [vp]),
+        "hivf_device_info": (i32, [vp, P(i32), P(i32)]),
         "hivf_index_upload": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, P(vp)]),
         "hivf_index_upload_device": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, P(vp)]),
         "hivf_index_begin": (i32, [vp, u32, i32, u32, vp, i32, vp, P(vp)]),

@@ -108,17 +108,23 @@ struct hivf_ctx {
   // options
   uint32_t opt_seg_rows = 4096;
   int opt_force_exact = 0;
+  // 0 auto (tensor cores when the dim fits; single-pass tf32, escalating to the
+  // split kernel when the data makes its bound too loose), 1 FFMA, 2 tcgen05
+  // split-precision, 3 tcgen05 single-pass
+  int opt_scan_kernel = 0;
   int opt_scan_ctas = 0;
   // scratch
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
       cand_n, out_ids, out_d, out_cnt, qin, it_off, it_cl, it_k, heap_ids, heap_d, heap_n,
-      changed;
+      changed, x_ids, x_d, x_cnt, x_tot;
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;
   uint32_t last_K = 0;
   const hivf_index* last_index = nullptr;
+  uint32_t last_kind = 0;
+  bool stats_adapted = false;
   // phase timing (option "time_kernels"): one event set per call, resolved lazily
   int opt_time = 0;
   std::vector<cudaEvent_t> ev_pool;
@@ -157,7 +163,8 @@ struct hivf_ctx {
     for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq, &pl,
                     &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items, &n_items,
                     &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &out_d, &out_cnt,
-                    &qin, &it_off, &it_cl, &it_k, &heap_ids, &heap_d, &heap_n, &changed})
+                    &qin, &it_off, &it_cl, &it_k, &heap_ids, &heap_d, &heap_n, &changed, &x_ids,
+                    &x_d, &x_cnt, &x_tot})
       b->release();
     hstage.release();
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -185,8 +192,16 @@ struct hivf_index {
   double mean_assigned = -1.0;
   uint32_t seg_rows = 4096, s_max = 1;
   std::vector<uint8_t> resident;
+  int auto_split = 0;  // auto policy: 0 single-pass tf32, 1 split-precision
+  uint32_t adapt_seen = 0, adapt_fallback = 0;
+  // scan kernel for the next call: 1 FFMA, 2 tensor-core split, 3 tensor-core single pass
+  int scan_kind() const;
   IndexView view() const {
     IndexView v{};
+    const int kind = scan_kind();
+    if (kind == 2) bound_tc(dim, &v.e_a, &v.e_b, &v.e_c);
+    else if (kind == 3) bound_tc1(dim, &v.e_a, &v.e_b, &v.e_c);
+    else bound_ffma(dim, &v.e_a, &v.e_b, &v.e_c);
     v.vec = vec;
     v.ids = ids;
     v.xnorm2 = xnorm2;
@@ -211,6 +226,26 @@ struct hivf_index {
       if (p) cudaFree(p);
   }
 };
+
+int hivf_index::scan_kind() const {
+  const int k = ctx->opt_scan_kernel;
+  if (k == 1) return 1;
+  if (tc_conversion_mode() > 1) return 1;  // unknown tensor-core conversion: FFMA scan
+  const int want = k == 2 ? 2 : k == 3 ? 3 : (auto_split ? 2 : 3);
+  if (scan_tc_qmax(dpad, want == 2) > 0) return want;
+  return 1;  // too wide for the tensor-core scan
+}
+
+// Auto policy: the single-pass tf32 bound is 2^-9|x||q| (Cauchy-Schwarz on the
+// operand truncation).  When the data's norms are large against its neighbor
+// gaps, too many queries miss the proof and take the exact fallback; once
+// that exceeds 2% of the queries seen, switch this index to the split kernel.
+static void adapt_scan(hivf_index* ix, uint32_t n_queries, uint32_t n_fallback) {
+  if (ix->ctx->opt_scan_kernel != 0 || ix->auto_split) return;
+  ix->adapt_seen += n_queries;
+  ix->adapt_fallback += n_fallback;
+  if (ix->adapt_fallback * 50 > ix->adapt_seen && ix->adapt_fallback >= 2) ix->auto_split = 1;
+}
 
 extern "C" {
 
@@ -241,7 +276,15 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
     }
     c->own_stream = true;
   }
+  if (tc_conversion_mode() < 0) set_tc_conversion_mode(tc_probe_conversion(c->stream));
   *out = c;
+  return HIVF_OK;
+}
+
+hivf_status hivf_device_info(hivf_ctx* ctx, int* sm_count, int* tc_tf32_conversion) {
+  if (!ctx) return fail(HIVF_EINVAL, "ctx is NULL");
+  if (sm_count) *sm_count = ctx->sm_count;
+  if (tc_tf32_conversion) *tc_tf32_conversion = tc_conversion_mode();
   return HIVF_OK;
 }
 
@@ -281,6 +324,15 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->opt_force_exact = value != 0;
   } else if (!strcmp(name, "scan_ctas")) {
     ctx->opt_scan_ctas = (int)value;
+  } else if (!strcmp(name, "scan_kernel")) {
+    if (value < 0 || value > 3)
+      return fail(HIVF_EINVAL, "scan_kernel: 0 auto, 1 ffma, 2 tc split, 3 tc single-pass");
+    ctx->opt_scan_kernel = (int)value;
+  } else if (!strcmp(name, "tc_variant")) {  // debug only: results are inexact when != 0
+    set_tc_variant((int)value);
+  } else if (!strcmp(name, "tc_qmax")) {  // tuning: queries per tensor-core work item
+    if (value < 0 || value > 32 || value % 8) return fail(HIVF_EINVAL, "tc_qmax: 0 or 8..32 step 8");
+    set_tc_qmax((uint32_t)value);
   } else if (!strcmp(name, "time_kernels")) {
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->resolve_timers();
@@ -323,8 +375,17 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
     CK(cudaMemcpy(f.data(), ctx->flags_f.p, 4ull * ctx->last_nq, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(g.data(), ctx->flags_c.p, 4ull * ctx->last_nq, cudaMemcpyDeviceToHost));
     s.n_fallback = 0;
-    for (uint32_t i = 0; i < ctx->last_nq; ++i) s.n_fallback += (f[i] != 0) + (g[i] != 0);
+    uint32_t scan_fb = 0;
+    for (uint32_t i = 0; i < ctx->last_nq; ++i) {
+      s.n_fallback += (f[i] != 0) + (g[i] != 0);
+      scan_fb += f[i] != 0;
+    }
+    if (ctx->last_index && !ctx->stats_adapted) {
+      adapt_scan(const_cast<hivf_index*>(ctx->last_index), ctx->last_nq, scan_fb);
+      ctx->stats_adapted = true;
+    }
   }
+  s.scan_kernel = ctx->last_kind;
   *out = s;
   return HIVF_OK;
 }
@@ -654,7 +715,10 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   // slots of empty lists are never written by the scan; zero counts so the
   // finalize pass reads "no candidates" there
   CK(cudaMemsetAsync(c->cand_n.p, 0, nslots * 4, c->stream));
-  launch_build_worklist(v, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
+  const int kind = ix->scan_kind();
+  const bool tc = kind != 1;
+  const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2) : (uint32_t)kQMax;
+  launch_build_worklist(v, group, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
                         c->list_poff.as<uint32_t>(), c->list_cur.as<uint32_t>(),
                         c->list_ioff.as<uint32_t>(), c->sorted_pairs.as<uint32_t>(),
                         c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
@@ -662,10 +726,16 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   CKL();
   const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;
   if (timed) c->mark(1);
-  launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
-              c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
-              c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
-              c->stream);
+  if (tc)
+    launch_scan_tc(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
+                   c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
+                   c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
+                   kind == 2, c->stream);
+  else
+    launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
+                c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
+                c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
+                c->stream);
   CKL();
   c->stats.kernels_launched += 5;
   return HIVF_OK;
@@ -694,6 +764,8 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
   c->last_nq = n;
   c->last_index = ix;
   c->last_K = ix->K;
+  c->last_kind = (c->opt_force_exact || k > (uint32_t)kKP) ? 0 : ix->scan_kind();
+  c->stats_adapted = false;
   QueryView qv;
   c->mark(0);
   if ((st = prep_queries(ix, d_queries, n, true, &qv)) != HIVF_OK) return st;
@@ -704,6 +776,13 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
   CK(c->flags_f.ensure((size_t)n * 4));
   const IndexView v = ix->view();
   const bool exact_only = c->opt_force_exact || k > (uint32_t)kKP;
+  {
+    const size_t parts = (size_t)n * exact_search_parts(nprobe, k);
+    CK(c->x_ids.ensure(parts * k * 8));
+    CK(c->x_d.ensure(parts * k * 8));
+    CK(c->x_cnt.ensure(parts * 4));
+    CK(c->x_tot.ensure(parts * 8));
+  }
   if (!exact_only) {
     launch_plans_to_pairs(c->plans.as<uint32_t>(), n, nprobe, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), c->stream);
     CKL();
@@ -714,7 +793,8 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
                            d_ids_out, d_dists_out, d_counts_out, c->flags_f.as<int>(), c->stream);
     CKL();
     launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->flags_f.as<int>(), d_ids_out,
-                        d_dists_out, d_counts_out, c->stream);
+                        d_dists_out, d_counts_out, c->x_ids.as<uint64_t>(), c->x_d.as<double>(),
+                        c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), c->stream);
     CKL();
     c->stats.kernels_launched += 4;
     c->mark(3);
@@ -723,7 +803,8 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
     c->mark(1);
     c->mark(2);
     launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, nullptr, d_ids_out, d_dists_out,
-                        d_counts_out, c->stream);
+                        d_counts_out, c->x_ids.as<uint64_t>(), c->x_d.as<double>(),
+                        c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), c->stream);
     CKL();
     c->stats.kernels_launched += 1;
     c->mark(3);
@@ -755,8 +836,16 @@ hivf_status hivf_search(hivf_index* ix, const float* queries, uint32_t n, uint32
   CK(cudaMemcpyAsync(counts_out, c->out_cnt.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
   int err = 0;
   CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<int> fb(c->opt_scan_kernel == 0 && !ix->auto_split ? n : 0);
+  if (!fb.empty()) CK(cudaMemcpyAsync(fb.data(), c->flags_f.p, 4ull * n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (err) return fail(HIVF_EINVAL, "hivf_search: non-finite query value");
+  if (!fb.empty()) {
+    uint32_t nf = 0;
+    for (int v : fb) nf += v != 0;
+    adapt_scan(ix, n, nf);
+    c->stats_adapted = true;
+  }
   return HIVF_OK;
 }
 

@@ -47,6 +47,13 @@ __host__ __device__ inline double filter_eps(uint32_t dim) {
 }
 __host__ __device__ inline double filter_abs(uint32_t dim) { return 1e-36 * (dim + 8.0); }
 
+// Per-(query, list) filter bound from the IndexView coefficients (rounded up).
+template <typename View>
+__device__ __forceinline__ float seg_bound(const View& ix, float qn, float xn) {
+  const double q = qn, x = xn;
+  return __double2float_ru(ix.e_a * q * x + ix.e_b * (q * q + x * x) + ix.e_c);
+}
+
 // ---- exact reference arithmetic (embedding.hpp:27-34) -------------------------
 // d = (double)a - (double)b ; acc += d * d  -- sequential, every op rounded,
 // never contracted into an FMA.

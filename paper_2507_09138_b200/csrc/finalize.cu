@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   unsigned long long total = 0;
   for (uint32_t p = warp; p < nprobe; p += NW) {
     const uint32_t c = plans[(uint64_t)b * nprobe + p];
-    const float E = list_E(eps, ab, qn, ix.maxnorm[c]);
+    const float E = seg_bound(ix, qn, ix.maxnorm[c]);
     const uint32_t ns = nseg_of(ix, c);
     total += ix.list_off[c + 1] - ix.list_off[c];
     for (uint32_t s = 0; s < ns; ++s) {
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   // 2. candidates + completeness
   for (uint32_t p = warp; p < nprobe; p += NW) {
     const uint32_t c = plans[(uint64_t)b * nprobe + p];
-    const float E = list_E(eps, ab, qn, ix.maxnorm[c]);
+    const float E = seg_bound(ix, qn, ix.maxnorm[c]);
     const uint32_t ns = nseg_of(ix, c);
     for (uint32_t s = 0; s < ns; ++s) {
       const uint64_t slot = ((uint64_t)b * nprobe + p) * ix.s_max + s;
@@ -210,15 +210,24 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   }
 }
 
-// Exact streaming top-k over every row of the query's plan (flagged queries
-// and k > 32).  Buffer of `cap` (d, id) pairs filtered by the running k-th.
+// Exact streaming top-k (the reference algorithm on the GPU: every row of the
+// plan, exact distance, (d, id) order) for flagged queries and k > 32.
+// Grid (query, part): part y covers plan positions [y*per, (y+1)*per); with
+// more than one part each CTA writes its exact partial top-k and
+// k_exact_merge combines them (lists are disjoint, so the merge is exact).
+// Buffer of `cap` (d, id) pairs filtered by the running k-th.
 __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv,
                                                       const uint32_t* __restrict__ plans,
                                                       uint32_t nprobe, uint32_t k, uint32_t cap,
                                                       const int* flags, uint64_t* ids_out,
-                                                      double* d_out, uint32_t* counts_out) {
+                                                      double* d_out, uint32_t* counts_out,
+                                                      uint64_t* part_total) {
   const uint32_t b = blockIdx.x;
   if (flags && !flags[b]) return;
+  const uint32_t nsplit = gridDim.y, y = blockIdx.y;
+  const uint32_t per = (nprobe + nsplit - 1) / nsplit;
+  const uint32_t p_beg = min(nprobe, y * per), p_end = min(nprobe, p_beg + per);
+  const uint64_t out_row = nsplit > 1 ? (uint64_t)b * nsplit + y : b;
   extern __shared__ __align__(16) uint8_t sm[];
   double* bd = reinterpret_cast<double*>(sm);
   uint64_t* bi = reinterpret_cast<uint64_t*>(bd + cap);
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
     s_total = 0;
   }
   __syncthreads();
-  for (uint32_t p = 0; p < nprobe; ++p) {
+  for (uint32_t p = p_beg; p < p_end; ++p) {
     const uint32_t c = plans[(uint64_t)b * nprobe + p];
     const uint64_t beg = ix.list_off[c], end = ix.list_off[c + 1];
     if (threadIdx.x == 0) s_total += end - beg;
@@ -273,6 +282,44 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
   for (uint32_t i = s_cnt + threadIdx.x; i < cap; i += blockDim.x) {
     bd[i] = DBL_MAX;
     bi[i] = ~0ull;
+  }
+  block_sort_pairs(bd, bi, cap);
+  const uint32_t cnt = (uint32_t)min((unsigned long long)k, s_total);
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+    ids_out[out_row * k + i] = i < cnt ? bi[i] : 0;
+    d_out[out_row * k + i] = i < cnt ? bd[i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    counts_out[out_row] = cnt;
+    if (part_total) part_total[out_row] = s_total;
+  }
+}
+
+// Combine the exact partial top-k lists of k_exact_search (nsplit parts).
+__global__ void __launch_bounds__(256) k_exact_merge(uint32_t nsplit, uint32_t k, uint32_t cap,
+                                                     const int* flags, const uint64_t* part_ids,
+                                                     const double* part_d,
+                                                     const uint32_t* part_cnt,
+                                                     const uint64_t* part_total,
+                                                     uint64_t* ids_out, double* d_out,
+                                                     uint32_t* counts_out) {
+  const uint32_t b = blockIdx.x;
+  if (flags && !flags[b]) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  double* bd = reinterpret_cast<double*>(sm);
+  uint64_t* bi = reinterpret_cast<uint64_t*>(bd + cap);
+  __shared__ unsigned long long s_total;
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (uint32_t y = 0; y < nsplit; ++y) t += part_total[(uint64_t)b * nsplit + y];
+    s_total = t;
+  }
+  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
+    const uint32_t y = i / k, e = i % k;
+    const uint64_t row = (uint64_t)b * nsplit + y;
+    const bool ok = y < nsplit && e < part_cnt[row];
+    bd[i] = ok ? part_d[row * k + e] : DBL_MAX;
+    bi[i] = ok ? part_ids[row * k + e] : ~0ull;
   }
   block_sort_pairs(bd, bi, cap);
   const uint32_t cnt = (uint32_t)min((unsigned long long)k, s_total);
@@ -357,19 +404,39 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                                                     counts_out, flags);
 }
 
+uint32_t exact_search_parts(uint32_t nprobe, uint32_t k) {
+  uint32_t ns = nprobe < 64 ? nprobe : 64;
+  while (ns > 1 && (uint64_t)ns * k > 8192) ns >>= 1;
+  return ns ? ns : 1;
+}
+
 void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
                          uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
-                         double* d_out, uint32_t* counts_out, cudaStream_t s) {
+                         double* d_out, uint32_t* counts_out, uint64_t* part_ids,
+                         double* part_d, uint32_t* part_cnt, uint64_t* part_total,
+                         cudaStream_t s) {
   uint32_t cap = 512;
   while (cap < k + 256) cap <<= 1;
   const size_t smem = (size_t)cap * 16 + (size_t)ix.dpad * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_exact_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_exact_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_exact_search<<<qv.n, 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out, d_out,
-                                         counts_out);
+  const uint32_t ns = part_ids ? exact_search_parts(nprobe, k) : 1;
+  if (ns <= 1) {
+    k_exact_search<<<dim3(qv.n, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
+                                                    d_out, counts_out, nullptr);
+    return;
+  }
+  k_exact_search<<<dim3(qv.n, ns), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, part_ids,
+                                                   part_d, part_cnt, part_total);
+  uint32_t mcap = 1;
+  while (mcap < ns * k) mcap <<= 1;
+  k_exact_merge<<<qv.n, 256, (size_t)mcap * 16, s>>>(ns, k, mcap, flags, part_ids, part_d,
+                                                     part_cnt, part_total, ids_out, d_out,
+                                                     counts_out);
 }
 
 void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const uint64_t* ids,

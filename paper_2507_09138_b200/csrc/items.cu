@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     bool bad = false;
     for (uint32_t j = 0; j < mcl; ++j) {
       const uint32_t c = clusters[j0 + j];
-      const float E = it_E(eps, ab, qn, ix.maxnorm[c]);
+      const float E = seg_bound(ix, qn, ix.maxnorm[c]);
       const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
       const uint32_t ns = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
       float lj = kInf;

@@ -34,6 +34,9 @@ struct IndexView {
   uint32_t seg_rows;        // rows per scan segment (multiple of kRowBlock)
   uint32_t s_max;           // max segments per list
   int metric;
+  // filter bound of the scan kernel that produced the candidates:
+  // |d32 - delta| <= e_a*|q|*|x| + e_b*(|q|^2 + |x|^2) + e_c
+  double e_a, e_b, e_c;
 };
 
 // Per-batch query state (search space).
@@ -73,7 +76,7 @@ void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t n
 // ---- scan.cu
 // Pair p = (query pair_query[p], cluster pair_list[p]); output slots
 // [p*s_max, p*s_max + nseg(list)).
-void launch_build_worklist(const IndexView& ix, const uint32_t* pair_query,
+void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* pair_query,
                            const uint32_t* pair_list, uint32_t n_pairs, uint32_t* list_cnt,
                            uint32_t* list_pair_off, uint32_t* list_cursor,
                            uint32_t* list_item_off, uint32_t* sorted_pairs, ScanItem* items,
@@ -83,6 +86,21 @@ void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items
                  const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                  uint32_t* out_n, int n_ctas, cudaStream_t s);
 int scan_smem_bytes(uint32_t dpad);
+// ---- scan_tc.cu (tcgen05 tensor-core scan)
+void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
+                    const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
+                    const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
+                    uint32_t* out_n, int n_ctas, int split, cudaStream_t s);
+uint32_t scan_tc_qmax(uint32_t dpad, int split);
+void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)
+int tc_probe_conversion(cudaStream_t s);  // 0 trunc, 1 RNE, 2 unsupported
+void set_tc_conversion_mode(int m);
+void set_tc_variant(int v);  // debug knob (inexact results when nonzero)
+int tc_conversion_mode();
+int scan_tc_smem_bytes(uint32_t dpad, int split);
+void bound_ffma(uint32_t dim, double* a, double* b, double* c);
+void bound_tc(uint32_t dim, double* a, double* b, double* c);   // 3-pass split
+void bound_tc1(uint32_t dim, double* a, double* b, double* c);  // single pass
 
 // ---- finalize.cu
 void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe,
@@ -92,9 +110,14 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                             const uint32_t* cand_row, const float* cand_thr,
                             const uint32_t* cand_n, uint64_t* ids_out, double* d_out,
                             uint32_t* counts_out, int* flags, cudaStream_t s);
+// part_* scratch (n_queries x exact_search_parts() x k) enables the multi-CTA
+// path; pass nullptr for one CTA per query.
+uint32_t exact_search_parts(uint32_t nprobe, uint32_t k);
 void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
                          uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
-                         double* d_out, uint32_t* counts_out, cudaStream_t s);
+                         double* d_out, uint32_t* counts_out, uint64_t* part_ids,
+                         double* part_d, uint32_t* part_cnt, uint64_t* part_total,
+                         cudaStream_t s);
 void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
                            const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
                            const float* cand_d, const uint32_t* cand_row, const float* cand_thr,

@@ -283,7 +283,8 @@ __global__ void k_count_pairs(const uint32_t* pair_list, uint32_t n_pairs, uint3
 
 // Single CTA: exclusive scans (in list_order, largest lists first) of the pair
 // counts and of the work items each list generates.
-__global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, const uint32_t* cnt,
+__global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t group,
+                                                       const uint32_t* cnt,
                                                        uint32_t* pair_off, uint32_t* cursor,
                                                        uint32_t* item_off, uint32_t* n_items,
                                                        uint32_t* work_ctr) {
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, const uint3
     const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
     const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
     tp += n;
-    ti += n ? nseg * ((n + kQMax - 1) / kQMax) : 0;
+    ti += n ? nseg * ((n + group - 1) / group) : 0;
   }
   sp[threadIdx.x] = tp;
   si[threadIdx.x] = ti;
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, const uint3
     item_off[c] = oi;
     cursor[c] = 0;
     op += n;
-    oi += n ? nseg * ((n + kQMax - 1) / kQMax) : 0;
+    oi += n ? nseg * ((n + group - 1) / group) : 0;
   }
   if (threadIdx.x == 1023) {
     *n_items = si[1023];
@@ -337,7 +338,8 @@ __global__ void k_scatter_pairs(const uint32_t* pair_list, uint32_t n_pairs, con
   sorted_pairs[pair_off[c] + pos] = p;
 }
 
-__global__ void k_make_items(IndexView ix, const uint32_t* cnt, const uint32_t* pair_off,
+__global__ void k_make_items(IndexView ix, uint32_t group, const uint32_t* cnt,
+                             const uint32_t* pair_off,
                              const uint32_t* item_off, ScanItem* items) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ix.K) return;
@@ -345,7 +347,7 @@ __global__ void k_make_items(IndexView ix, const uint32_t* cnt, const uint32_t* 
   if (!n) return;
   const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
   const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
-  const uint32_t ng = (n + kQMax - 1) / kQMax;
+  const uint32_t ng = (n + group - 1) / group;
   uint32_t o = item_off[c];
   for (uint32_t s = 0; s < nseg; ++s) {
     const uint32_t row0 = s * ix.seg_rows;
@@ -356,8 +358,8 @@ __global__ void k_make_items(IndexView ix, const uint32_t* cnt, const uint32_t* 
       it.seg = s;
       it.row0 = row0;
       it.nrows = nr;
-      it.pair0 = pair_off[c] + g * kQMax;
-      it.nq = min((uint32_t)kQMax, n - g * kQMax);
+      it.pair0 = pair_off[c] + g * group;
+      it.nq = min(group, n - g * group);
       items[o++] = it;
     }
   }
@@ -369,7 +371,7 @@ int scan_smem_bytes(uint32_t dpad) {
   return kStages * kStageBytes + (int)dpad * kQMax * 4 + 2 * kStages * 8;
 }
 
-void launch_build_worklist(const IndexView& ix, const uint32_t* pair_query,
+void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* pair_query,
                            const uint32_t* pair_list, uint32_t n_pairs, uint32_t* list_cnt,
                            uint32_t* list_pair_off, uint32_t* list_cursor,
                            uint32_t* list_item_off, uint32_t* sorted_pairs, ScanItem* items,
@@ -377,12 +379,12 @@ void launch_build_worklist(const IndexView& ix, const uint32_t* pair_query,
   (void)pair_query;
   cudaMemsetAsync(list_cnt, 0, sizeof(uint32_t) * ix.K, s);
   if (n_pairs) k_count_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_cnt);
-  k_list_offsets<<<1, 1024, 0, s>>>(ix, list_cnt, list_pair_off, list_cursor, list_item_off,
+  k_list_offsets<<<1, 1024, 0, s>>>(ix, group, list_cnt, list_pair_off, list_cursor, list_item_off,
                                     n_items, work_ctr);
   if (n_pairs)
     k_scatter_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_pair_off,
                                                           list_cursor, sorted_pairs);
-  k_make_items<<<(ix.K + 255) / 256, 256, 0, s>>>(ix, list_cnt, list_pair_off, list_item_off, items);
+  k_make_items<<<(ix.K + 255) / 256, 256, 0, s>>>(ix, group, list_cnt, list_pair_off, list_item_off, items);
 }
 
 void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items,
@@ -399,4 +401,41 @@ void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items
   k_scan<<<n_ctas, (kScanWarps + 1) * 32, smem, s>>>(P);
 }
 
+}  // namespace hivf
+
+namespace hivf {
+// Filter bounds: coefficients of
+//   |d32 - delta| <= a*|q|*|x| + b*(|q|^2 + |x|^2) + c.
+// FFMA scan: sequential fp32 FMA dot, eps(D)*(|q|+|x|)^2 (common.cuh).
+void bound_ffma(uint32_t dim, double* a, double* b, double* c) {
+  const double e = filter_eps(dim);
+  *a = 2.0 * e;
+  *b = e;
+  *c = filter_abs(dim);
+}
+// Tensor-core scan (3-pass split tf32): dropped lo*lo and lo conversion
+// (4*2^-20 |x||q| by Cauchy-Schwarz) + fp32 tensor-core accumulation bounded at
+// 4x round-to-nearest per MMA step over 3*D/8 steps, plus the norm/combine
+// roundings; x1.5 headroom.
+void bound_tc(uint32_t dim, double* a, double* b, double* c) {
+  const double u = 5.9604644775390625e-08, u53 = 1.1102230246251565e-16;
+  const double alpha = (4.0 * 0x1p-20 + 1.5 * (double)dim * 0x1p-22) * 1.01;
+  *a = 1.5 * (2.0 * alpha + 4.0 * u + 2.0 * (3.0 * dim + 6.0) * u53);
+  *b = 1.5 * (4.0 * u + (3.0 * dim + 6.0) * u53);
+  *c = filter_abs(dim);
+}
+}  // namespace hivf
+
+namespace hivf {
+// Tensor-core scan, single pass: tf32 operand truncation (<= 2^-10 relative
+// per element, both operands) bounded by Cauchy-Schwarz: (2^-9 + 2^-20)|x||q|,
+// plus fp32 accumulation at 4x round-to-nearest per MMA step (D/8 steps) and
+// the norm/combine roundings; x1.5 headroom.
+void bound_tc1(uint32_t dim, double* a, double* b, double* c) {
+  const double u = 5.9604644775390625e-08, u53 = 1.1102230246251565e-16;
+  const double alpha = (0x1p-9 + 0x1p-20 + 0.5 * (double)dim * 0x1p-22) * 1.01;
+  *a = 1.5 * (2.0 * alpha + 4.0 * u + 2.0 * (3.0 * dim + 6.0) * u53);
+  *b = 1.5 * (4.0 * u + (3.0 * dim + 6.0) * u53);
+  *c = filter_abs(dim);
+}
 }  // namespace hivf

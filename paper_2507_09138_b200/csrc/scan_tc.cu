@@ -1,0 +1,628 @@
+// scan_tc.cu -- K2 on the 5th-gen tensor cores: grouped inverted-list scan
+// with tcgen05.mma (kind::tf32), TMEM accumulators and a bulk-copy/mbarrier
+// pipeline.  Same work items and same output contract as scan.cu (32 best
+// (dist32, row) per (query, segment) + drop threshold), so finalize.cu /
+// items.cu re-rank its candidates exactly as for the FFMA kernel.
+//
+// Replaces the inner loop of ivf::search_clusters
+// (/root/reference/proj/src/vector_index.cpp:302-306).  Why tensor cores: the
+// FFMA scan (scan.cu) is issue-bound at ~50% of HBM (profiles/); here the
+// B x rows dot products run on tcgen05 and the SMs only stream + select.
+//
+// Precision: error-compensated split.  The tensor core reads every fp32
+// operand x as hi = tf32(x) (its own conversion, measured once per process by
+// hivf_tc_probe: truncation or RNE); splitter warps write lo = x - hi (exact in
+// fp32) for the list rows, the query group carries [q ; lo(q)] rows, and each
+// 8-dim k-step issues A x [q ; lo(q)] (N = 2 npad: hi*hi and hi*lo in separate
+// TMEM columns) and lo(A) x q (accumulated onto hi*hi; lo(A) is written by the
+// splitters straight into TMEM and read from there by the MMA, so the split
+// costs one extra smem read of the stage and no smem writes).  The
+// dropped lo*lo term and the tf32 conversion of lo are each <= 2^-20 per
+// element, so by Cauchy-Schwarz the operand error is <= 4*2^-20 |x||q|; the
+// fp32 tensor-core accumulation is bounded at 4x the round-to-nearest bound
+// per MMA step ((3D/2) * 2^-22 |x||q|).  finalize.cu uses that bound
+// (IndexView::e_*), so every id/distance is still the reference's exact double.
+//
+// CTA (1 per SM, persistent) = 6 warps:
+//   warp 0   producer: 1-D bulk copies of (<=128 rows x 16 dims) list slices --
+//            contiguous in the chunk-major HBM layout, whose 16-B XOR swizzle
+//            IS the canonical SWIZZLE_64B K-major UMMA layout -- into a deep
+//            ring (3-8 stages of 4 chunks = 64 dims) sized from the smem left
+//            after the resident query group
+//   warp 1   TMEM allocator + single-thread MMA issuer: per 128-row tile and
+//            per 8-dim k-step one tcgen05.mma M=128 x N=ceil8(nq) x K=8 into
+//            a double-buffered TMEM accumulator; tcgen05.commit frees smem
+//            stages and publishes finished tiles
+//   warps 2-5 splitters: lo(A) of each stage, one row per thread, into TMEM
+//   warps 6-9 epilogue: tcgen05.ld of the tile (one row per thread, one column
+//            per query), fp32 expansion distance, per-warp register top-32 per
+//            query; at item end a bitonic merge across the four warps.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hivf {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kTcTile = 128;       // rows per MMA tile (M)
+constexpr int kTcCps = 4;          // 16-dim chunks per pipeline stage (64 dims)
+constexpr int kTcMaxA = 8;         // max depth of the A landing ring
+constexpr int kTcLo = 4;           // depth of the A_lo ring (in TMEM, 64 columns per slot)
+constexpr int kTcChunkBytes = kTcTile * kChunk * 4;       // 8 KB
+constexpr int kTcStageBytes = kTcCps * kTcChunkBytes;     // 32 KB
+constexpr int kTcSplitWarps = 4;
+constexpr int kTcEpiWarps = 4;
+constexpr int kTcThreads = (2 + kTcSplitWarps + kTcEpiWarps) * 32;
+constexpr uint32_t kTmemAcc = 128;  // 2 accumulator buffers x 64 columns ([hi*hi|hi*lo])
+constexpr uint32_t kTmemLoCols = kTcCps * kChunk;            // 64 columns of A_lo per slot
+constexpr uint32_t kTmemCols = 512;  // 128 accumulator + kTcLo x 64 lo columns (pow2)
+
+struct TcParams {
+  IndexView ix;
+  QueryView qv;
+  const ScanItem* items;
+  const uint32_t* n_items;
+  uint32_t* work_ctr;
+  const uint32_t* sorted_pairs;
+  const uint32_t* pair_query;
+  float* out_d;
+  uint32_t* out_row;
+  float* out_thr;
+  uint32_t* out_n;
+  uint32_t qmax;  // queries per item (8..32)
+  uint32_t sa;    // A landing-ring depth (16 KB stages)
+  int conv;       // tensor-core tf32 conversion (0 trunc, 1 RNE)
+  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA (results then inexact)
+  int split;      // 1: 3-pass split precision, 0: single-pass tf32 (looser bound)
+};
+
+// ---- tcgen05 PTX wrappers ------------------------------------------------------
+__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);  // start address (16-B units)
+  d |= (uint64_t)1u << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512u >> 4) << 32;         // SBO: 8 rows x 64 B between row groups
+  d |= (uint64_t)1u << 46;                  // descriptor version (sm_100)
+  d |= (uint64_t)4u << 61;                  // SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ uint32_t tf32_idesc(uint32_t n) {
+  return (1u << 4)            // D = f32
+         | (2u << 7)          // A = tf32
+         | (2u << 10)         // B = tf32
+         | ((n >> 3) << 17)   // N
+         | ((uint32_t)(kTcTile >> 4) << 24);  // M = 128
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+#define TMEM_ST32(taddr, r)                                                                    \
+  asm volatile(                                                                                \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"  \
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"     \
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),         \
+      "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),          \
+      "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]),      \
+      "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),      \
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                    \
+  asm volatile(                                                                                \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"      \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),             \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),          \
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),          \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),          \
+        "=r"(r[31])                                                                            \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- the kernel ------------------------------------------------------------------
+// smem carve-out (1024-B aligned): per stage [A_hi 16K | A_lo 16K | B_hi | B_lo],
+// then the resident (unsplit) query group, then the mbarriers.
+__device__ __forceinline__ float tf32_trunc(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+// The tensor core's own fp32 -> tf32 operand conversion, as measured by
+// hivf_tc_probe (mode 0: truncation, 1: round-to-nearest-even).
+__device__ __forceinline__ float tf32_conv(float x, int mode) {
+  if (mode == 0) return tf32_trunc(x);
+  const uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;  // inf / nan untouched
+  const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) & 0xffffe000u;
+  return __uint_as_float(r);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t dpad = P.ix.dpad;
+  const uint32_t nch = dpad / kChunk;
+  const uint32_t qmax = P.qmax;
+  const uint32_t SA = P.sa;
+  const bool split = P.split != 0;
+  const uint32_t qblk = (split ? 2 : 1) * qmax * 64;                // per chunk: [raw rows | lo rows]
+  uint8_t* aring = smem;                                            // SA x 16 KB (raw A)
+  uint8_t* qsm = smem + SA * kTcStageBytes;                         // nch x qblk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qsm + (size_t)nch * qblk);
+  uint64_t* full = bars;                        // [SA] TMA -> splitter
+  uint64_t* empty = bars + kTcMaxA;             // [SA] MMA -> TMA
+  uint64_t* lfull = bars + 2 * kTcMaxA;         // [kTcLo] splitter -> MMA
+  uint64_t* lempty = lfull + kTcLo;             // [kTcLo] MMA -> splitter
+  uint64_t* tfull = lempty + kTcLo;             // [2] MMA -> epilogue
+  uint64_t* tempty = tfull + 2;                 // [2] epilogue -> MMA
+  __shared__ ScanItem s_item;
+  __shared__ int s_valid;
+  __shared__ uint32_t s_tmem;
+  __shared__ float s_qn2[32];
+  __shared__ uint32_t s_slot[32];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < SA; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < kTcLo; ++i) {
+      mbar_init(&lfull[i], kTcSplitWarps);
+      mbar_init(&lempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kTcEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = s_tmem;
+
+  // ring positions (each role keeps its own copy): A ring slot/phase, lo ring slot/phase
+  uint32_t ra = 0, rpa = 0, rl = 0, rpl = 0;
+  uint32_t tb = 0, tph = 0;   // TMEM accumulator ring
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const uint32_t it = atomicAdd(P.work_ctr, 1u);
+      s_valid = it < *P.n_items;
+      if (s_valid) s_item = P.items[it];
+    }
+    __syncthreads();
+    if (!s_valid) break;
+    const ScanItem item = s_item;
+    const uint32_t nq = item.nq;
+    const uint32_t npad = (nq + 7) & ~7u;
+    const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
+    const uint32_t nstg = (nch + kTcCps - 1) / kTcCps;
+    const uint64_t lbeg = P.ix.list_off[item.list];
+    if (warp == 0) {
+      // ---------------- producer: list slices -> A_hi ----------------
+      if (lane == 0) {
+        const uint64_t n_c = P.ix.list_off[item.list + 1] - lbeg;
+        const float* lbase = P.ix.vec + lbeg * dpad;
+        for (uint32_t t = 0; t < ntiles; ++t) {
+          const uint32_t r0 = item.row0 + t * kTcTile;
+          const uint32_t nr = min((uint32_t)kTcTile, item.nrows - t * kTcTile);
+          for (uint32_t sg = 0; sg < nstg; ++sg) {
+            const uint32_t c0 = sg * kTcCps, cn = min((uint32_t)kTcCps, nch - c0);
+            const uint32_t a = ra, pa = rpa;
+            mbar_wait(&empty[a], pa ^ 1);
+            mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4);
+            for (uint32_t c = 0; c < cn; ++c)
+              bulk_g2s(aring + a * kTcStageBytes + c * kTcChunkBytes,
+                       lbase + (uint64_t)(c0 + c) * n_c * kChunk + (uint64_t)r0 * kChunk,
+                       nr * kChunk * 4, &full[a]);
+            if (++ra == SA) { ra = 0; rpa ^= 1; }
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------- MMA issuer: tf32, single pass or 3-pass split ----------------
+      named_bar_sync(1, (kTcEpiWarps + kTcSplitWarps + 1) * 32);  // queries staged
+      if (lane == 0) {
+        const uint32_t idesc2 = tf32_idesc(split ? 2 * npad : npad);
+        const uint32_t idesc1 = tf32_idesc(npad);
+        const uint32_t q_base = smem_u32(qsm);
+        for (uint32_t t = 0; t < ntiles; ++t) {
+          mbar_wait(&tempty[tb], tph ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + tb * 64;  // accumulator columns [0, 128)
+          for (uint32_t sg = 0; sg < nstg; ++sg) {
+            const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
+            const uint32_t a = ra, pa = rpa, l = rl, pl = rpl;
+            if (split) mbar_wait(&lfull[l], pl);  // split done (implies A landed)
+            else mbar_wait(&full[a], pa);
+            tc_fence_after();
+            const uint32_t ahi = smem_u32(aring + a * kTcStageBytes);
+            const uint32_t alo = tmem_base + kTmemAcc + l * kTmemLoCols;  // A_lo in TMEM, lane = row
+            const uint32_t c0 = sg * kTcCps;
+            for (uint32_t c = 0; c < cn; ++c) {
+              const uint32_t qb = q_base + (c0 + c) * qblk;  // [raw rows | lo rows], lo at +npad rows
+#pragma unroll
+              for (uint32_t k2 = 0; k2 < 2; ++k2) {
+                const uint32_t ao = c * kTcChunkBytes + k2 * 32;
+                const uint32_t first = (sg | c | k2) == 0;
+                // cols [0,npad): hi(A) hi(q);  cols [npad,2npad): hi(A) lo(q)
+                mma_tf32(d_tmem, sw64_kmajor_desc(ahi + ao), sw64_kmajor_desc(qb + k2 * 32), idesc2, !first);
+                // cols [0,npad) += lo(A) hi(q), A from TMEM (8 columns per k-step)
+                if (split && !(P.variant & 2))
+                  mma_tf32_ta(d_tmem, alo + c * 16 + k2 * 8, sw64_kmajor_desc(qb + k2 * 32), idesc1, 1);
+              }
+            }
+            mma_commit(&empty[a]);   // A slot reusable by TMA
+            if (split) {
+              mma_commit(&lempty[l]);  // lo slot reusable by the splitters
+              if (++rl == kTcLo) { rl = 0; rpl ^= 1; }
+            }
+            if (++ra == SA) { ra = 0; rpa ^= 1; }
+          }
+          mma_commit(&tfull[tb]);
+          if (++tb == 2) {
+            tb = 0;
+            tph ^= 1;
+          }
+        }
+      }
+      __syncwarp();
+    } else if (warp < 2 + kTcSplitWarps) {
+      // ---------------- splitters: lo(A) rows -> TMEM ----------------
+      named_bar_sync(1, (kTcEpiWarps + kTcSplitWarps + 1) * 32);  // queries staged
+      const uint32_t quad = warp & 3;              // TMEM lane quadrant of this warp
+      const uint32_t row = quad * 32 + lane;       // tile row owned by this thread
+      const uint32_t swz = (row >> 1) & 3;
+      const int cm = P.conv;
+      for (uint32_t t = 0; split && t < ntiles; ++t) {
+        for (uint32_t sg = 0; sg < nstg; ++sg) {
+          const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
+          const uint32_t a = ra, pa = rpa, l = rl, pl = rpl;
+          mbar_wait(&full[a], pa);
+          mbar_wait(&lempty[l], pl ^ 1);
+          tc_fence_after();
+          const uint8_t* sb = aring + a * kTcStageBytes + row * 64;
+          if (!(P.variant & 1))
+#pragma unroll
+          for (uint32_t h2 = 0; h2 < kTcCps / 2; ++h2) {  // 2 chunks (32 columns) per TMEM store
+            uint32_t lo[32];
+#pragma unroll
+            for (uint32_t cc = 0; cc < 2; ++cc) {
+              const uint32_t c = h2 * 2 + cc;
+#pragma unroll
+              for (uint32_t g = 0; g < 4; ++g) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (c < cn) v = *reinterpret_cast<const float4*>(sb + c * kTcChunkBytes + ((g ^ swz) << 4));
+                lo[cc * 16 + g * 4 + 0] = __float_as_uint(v.x - tf32_conv(v.x, cm));
+                lo[cc * 16 + g * 4 + 1] = __float_as_uint(v.y - tf32_conv(v.y, cm));
+                lo[cc * 16 + g * 4 + 2] = __float_as_uint(v.z - tf32_conv(v.z, cm));
+                lo[cc * 16 + g * 4 + 3] = __float_as_uint(v.w - tf32_conv(v.w, cm));
+              }
+            }
+            TMEM_ST32(tmem_base + ((quad * 32) << 16) + kTmemAcc + l * kTmemLoCols + h2 * 32, lo);
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lfull[l]);
+          if (++ra == SA) { ra = 0; rpa ^= 1; }
+          if (++rl == kTcLo) { rl = 0; rpl ^= 1; }
+        }
+      }
+    } else {
+      // ---------------- epilogue warps ----------------
+      const int et = threadIdx.x - (2 + kTcSplitWarps) * 32;  // 0..127
+      const uint32_t ng = dpad / 4;
+      for (uint32_t idx = et; idx < qmax * ng; idx += kTcEpiWarps * 32) {
+        const uint32_t n = idx / ng, g4 = idx % ng;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (n < nq) {
+          const uint32_t qi = P.pair_query[P.sorted_pairs[item.pair0 + n]];
+          v = *reinterpret_cast<const float4*>(P.qv.qs + (uint64_t)qi * dpad + g4 * 4);
+        }
+        const uint32_t ch = g4 >> 2, g = g4 & 3;
+        if (n < npad && !split) {
+          uint8_t* blk = qsm + ch * qblk;
+          *reinterpret_cast<float4*>(blk + n * 64 + ((g ^ ((n >> 1) & 3)) << 4)) = v;
+        } else if (n < npad) {
+          const int cm = P.conv;
+          const float4 lo = make_float4(v.x - tf32_conv(v.x, cm), v.y - tf32_conv(v.y, cm),
+                                        v.z - tf32_conv(v.z, cm), v.w - tf32_conv(v.w, cm));
+          uint8_t* blk = qsm + ch * qblk;
+          *reinterpret_cast<float4*>(blk + n * 64 + ((g ^ ((n >> 1) & 3)) << 4)) = v;
+          const uint32_t nl = npad + n;  // lo rows follow the npad raw rows
+          *reinterpret_cast<float4*>(blk + nl * 64 + ((g ^ ((nl >> 1) & 3)) << 4)) = lo;
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+      if (et < (int)nq) {
+        const uint32_t pair = P.sorted_pairs[item.pair0 + et];
+        s_qn2[et] = P.qv.qn2[P.pair_query[pair]];
+        s_slot[et] = pair * P.ix.s_max + item.seg;
+      }
+      named_bar_sync(1, (kTcEpiWarps + kTcSplitWarps + 1) * 32);
+      const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+      float ld[32];
+      uint32_t lr[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        ld[j] = __int_as_float(0x7f800000);
+        lr[j] = kNoRow;
+      }
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        mbar_wait(&tfull[tb], tph);
+        tc_fence_after();
+        uint32_t acc[32], acc2[32];
+        TMEM_LD32(tmem_base + ((quad * 32) << 16) + tb * 64, acc);
+        if (split) TMEM_LD32(tmem_base + ((quad * 32) << 16) + tb * 64 + npad, acc2);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[tb]);
+        if (++tb == 2) {
+          tb = 0;
+          tph ^= 1;
+        }
+        const uint32_t srow = t * kTcTile + quad * 32 + lane;
+        const bool valid = srow < item.nrows;
+        const float xn = valid ? P.ix.xnorm2[lbeg + item.row0 + srow] : 0.f;
+        const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j >= (int)nq) break;
+          const float dot = split ? __fadd_rn(__uint_as_float(acc[j]), __uint_as_float(acc2[j]))
+                                  : __uint_as_float(acc[j]);
+          const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, s_qn2[j]))
+                                : __int_as_float(0x7f800000);
+          float th = __shfl_sync(FULL, ld[j], 31);
+          unsigned m = __ballot_sync(FULL, v < th);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            const float cv = __shfl_sync(FULL, v, src);
+            const uint32_t crow = __shfl_sync(FULL, grow, src);
+            const bool before = (ld[j] < cv) || (ld[j] == cv && lr[j] < crow);
+            const int pos = __popc(__ballot_sync(FULL, before));
+            const float upd = __shfl_up_sync(FULL, ld[j], 1);
+            const uint32_t upr = __shfl_up_sync(FULL, lr[j], 1);
+            if (lane > pos) {
+              ld[j] = upd;
+              lr[j] = upr;
+            } else if (lane == pos) {
+              ld[j] = cv;
+              lr[j] = crow;
+            }
+            th = __shfl_sync(FULL, ld[j], 31);
+            m &= ~(1u << src);
+            m &= __ballot_sync(FULL, v < th);
+          }
+        }
+      }
+      // cross-warp merge (the smem stages are idle: every MMA of this item retired)
+      named_bar_sync(2, kTcEpiWarps * 32);
+      float* md = reinterpret_cast<float*>(aring);
+      uint32_t* mr = reinterpret_cast<uint32_t*>(aring + kTcEpiWarps * 32 * 32 * 4);
+      const uint32_t ew = warp - (2 + kTcSplitWarps);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j >= (int)nq) break;
+        md[(ew * 32 + j) * 32 + lane] = ld[j];
+        mr[(ew * 32 + j) * 32 + lane] = lr[j];
+      }
+      named_bar_sync(2, kTcEpiWarps * 32);
+      for (uint32_t j = ew; j < nq; j += kTcEpiWarps) {
+        float v = md[j * 32 + lane];
+        uint32_t r = mr[j * 32 + lane];
+        for (uint32_t w2 = 1; w2 < kTcEpiWarps; ++w2) {
+          const float o = md[(w2 * 32 + j) * 32 + 31 - lane];
+          const uint32_t orr = mr[(w2 * 32 + j) * 32 + 31 - lane];
+          if (o < v || (o == v && orr < r)) {
+            v = o;
+            r = orr;
+          }
+#pragma unroll
+          for (int s = 16; s > 0; s >>= 1) {
+            const float pv = __shfl_xor_sync(FULL, v, s);
+            const uint32_t pr = __shfl_xor_sync(FULL, r, s);
+            const bool keep_min = (lane & s) == 0;
+            const bool p_less = (pv < v) || (pv == v && pr < r);
+            if (keep_min == p_less) {
+              v = pv;
+              r = pr;
+            }
+          }
+        }
+        const uint32_t slot = s_slot[j];
+        P.out_d[(uint64_t)slot * kKP + lane] = v;
+        P.out_row[(uint64_t)slot * kKP + lane] = r;
+        const uint32_t n_valid = __popc(__ballot_sync(FULL, r != kNoRow));
+        const float last = __shfl_sync(FULL, v, 31);
+        if (lane == 0) {
+          P.out_thr[slot] = n_valid == kKP ? last : __int_as_float(0x7f800000);
+          P.out_n[slot] = n_valid;
+        }
+      }
+      fence_proxy_async_smem();  // generic writes (merge buffers) before the next bulk copies
+    }
+    __syncthreads();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace
+
+// Shared-memory plan: the unsplit query group stays resident for the whole
+// item; what is left feeds the A landing ring (bytes in flight per SM).
+static constexpr int kTcBudget = 225 * 1024;
+static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
+  return 1024 + (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64 +
+         8 * (2 * kTcMaxA + 2 * kTcLo + 4);
+}
+static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
+  const int left = kTcBudget - tc_fixed_bytes(dpad, qmax, split);
+  return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / kTcStageBytes);
+}
+static uint32_t g_tc_qmax_override = 0;
+void set_tc_qmax(uint32_t q) { g_tc_qmax_override = q; }
+
+uint32_t scan_tc_qmax(uint32_t dpad, int split) {
+  const uint32_t o = g_tc_qmax_override;
+  if (o && tc_ring(dpad, o, split) >= 2) return o;
+  for (uint32_t q : {32u, 24u, 16u})
+    if (tc_ring(dpad, q, split) >= 3) return q;
+  if (tc_ring(dpad, 8, split) >= 2) return 8;
+  return 0;  // too wide for the tensor-core scan: caller uses the FFMA scan
+}
+static int g_tc_variant = 0;
+void set_tc_variant(int v) { g_tc_variant = v; }
+
+static int g_tc_conv = -1;  // set by tc_probe_conversion()
+void set_tc_conversion_mode(int m) { g_tc_conv = m; }
+int tc_conversion_mode() { return g_tc_conv; }
+
+int scan_tc_smem_bytes(uint32_t dpad, int split) {
+  const uint32_t q = scan_tc_qmax(dpad, split);
+  return tc_fixed_bytes(dpad, q, split) + (int)tc_ring(dpad, q, split) * kTcStageBytes;
+}
+
+void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
+                    const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
+                    const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
+                    uint32_t* out_n, int n_ctas, int split, cudaStream_t s) {
+  const uint32_t q = scan_tc_qmax(ix.dpad, split);
+  TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
+             out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
+             split};
+  const int smem = scan_tc_smem_bytes(ix.dpad, split);
+  static int attr_bytes = 0;
+  if (attr_bytes < smem) {
+    cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_bytes = smem;
+  }
+  k_scan_tc<<<n_ctas, kTcThreads, smem, s>>>(P);
+}
+
+}  // namespace hivf
+
+// ---------------------------------------------------------------------------
+// hivf_tc_probe: how does this tensor core convert fp32 operands to tf32?
+// One M=128 x N=8 x K=8 MMA with A[r][0] = probe value, B[0][0] = 1: the
+// accumulator then holds conv(v_r) exactly.  Result: 0 truncation, 1 RNE,
+// 2 neither (the split-precision scan is then disabled).
+// ---------------------------------------------------------------------------
+namespace hivf {
+namespace {
+__global__ void __launch_bounds__(128, 1) k_tc_probe(int* out) {
+  __shared__ __align__(1024) uint8_t a[kTcChunkBytes];
+  __shared__ __align__(1024) uint8_t b[8 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t s_tmem;
+  __shared__ int votes[3];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // probe values: 1.x with every interesting low-13-bit pattern (below, at, above the tie)
+  const uint32_t lows[8] = {0x0000u, 0x0001u, 0x0fffu, 0x1000u, 0x1001u, 0x1fffu, 0x0800u, 0x17ffu};
+  const uint32_t u = 0x3f800000u | ((uint32_t)(tid >> 3) << 13) | lows[tid & 7];
+  const float v = __uint_as_float(u);
+  for (int i = tid; i < kTcChunkBytes / 4; i += 128) reinterpret_cast<float*>(a)[i] = 0.f;
+  for (int i = tid; i < 8 * 16; i += 128) reinterpret_cast<float*>(b)[i] = 0.f;
+  if (tid < 3) votes[tid] = 0;
+  __syncthreads();
+  // row tid, dim 0 -> 16-B group 0 at swizzled position (0 ^ ((r>>1)&3))
+  reinterpret_cast<float*>(a + tid * 64 + (((tid >> 1) & 3) << 4))[0] = v;
+  if (tid == 0) reinterpret_cast<float*>(b)[0] = 1.0f;  // B row 0, group 0 (swizzle 0)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  if (tid == 0) {
+    mma_tf32(tmem, sw64_kmajor_desc(smem_u32(a)), sw64_kmajor_desc(smem_u32(b)), tf32_idesc(8), 0);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  uint32_t r[32];
+  TMEM_LD32(tmem + ((warp * 32) << 16), r);
+  tmem_wait_ld();
+  const float got = __uint_as_float(r[0]);
+  const uint32_t rne = (u + 0xfffu + ((u >> 13) & 1u)) & 0xffffe000u;
+  if (got == tf32_trunc(v)) atomicAdd(&votes[0], 1);
+  if (__float_as_uint(got) == rne) atomicAdd(&votes[1], 1);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32));
+  }
+  if (tid == 0) *out = votes[0] == 128 ? 0 : (votes[1] == 128 ? 1 : 2);
+}
+}  // namespace
+
+int tc_probe_conversion(cudaStream_t s) {
+  int* d = nullptr;
+  int h = 2;
+  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 2;
+  k_tc_probe<<<1, 128, 0, s>>>(d);
+  if (cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    h = 2;
+  cudaFree(d);
+  return h;
+}
+}  // namespace hivf

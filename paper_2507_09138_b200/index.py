@@ -51,6 +51,12 @@ class Context:
     def synchronize(self):
         check(lib().hivf_ctx_synchronize(self.h))
 
+    def device_info(self) -> dict:
+        sm, conv = C.c_int(), C.c_int()
+        check(lib().hivf_device_info(self.h, C.byref(sm), C.byref(conv)))
+        return {"sm_count": sm.value, "tc_tf32_conversion": ["truncate", "rne", "unknown"][conv.value]
+                if 0 <= conv.value <= 2 else "unknown"}
+
     def set_option(self, name: str, value: int):
         check(lib().hivf_set_option(self.h, name.encode(), int(value)))
 
