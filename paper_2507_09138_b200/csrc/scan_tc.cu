@@ -390,7 +390,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         ld[j] = __int_as_float(0x7f800000);
         lr[j] = kNoRow;
       }
+      // row norms for tile t are fetched one tile ahead (global latency off the
+      // critical path)
+      float xn_next = 0.f;
+      {
+        const uint32_t srow0 = quad * 32 + lane;
+        if (srow0 < item.nrows) xn_next = __ldg(P.ix.xnorm2 + lbeg + item.row0 + srow0);
+      }
       for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t srow = t * kTcTile + quad * 32 + lane;
+        const bool valid = srow < item.nrows;
+        const float xn = xn_next;
+        {
+          const uint32_t nrow = srow + kTcTile;
+          xn_next = (nrow < item.nrows) ? __ldg(P.ix.xnorm2 + lbeg + item.row0 + nrow) : 0.f;
+        }
         mbar_wait(&tfull[tb], tph);
         tc_fence_after();
         uint32_t acc[32], acc2[32];
@@ -404,9 +418,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           tb = 0;
           tph ^= 1;
         }
-        const uint32_t srow = t * kTcTile + quad * 32 + lane;
-        const bool valid = srow < item.nrows;
-        const float xn = valid ? P.ix.xnorm2[lbeg + item.row0 + srow] : 0.f;
         const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -417,6 +428,49 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
                                 : __int_as_float(0x7f800000);
           float th = __shfl_sync(FULL, ld[j], 31);
           unsigned m = __ballot_sync(FULL, v < th);
+          if (__popc(m) > 2) {
+            // many candidates (early tiles): bitonic-sort this tile's 32 values and
+            // min-merge them into the running top-32 (about 25 shuffle steps instead
+            // of up to 32 serial insertions)
+            float sv = (v < th) ? v : __int_as_float(0x7f800000);
+            uint32_t sr = (v < th) ? grow : kNoRow;
+#pragma unroll
+            for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+              for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const float pv = __shfl_xor_sync(FULL, sv, jj);
+                const uint32_t pr = __shfl_xor_sync(FULL, sr, jj);
+                const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
+                const bool p_less = (pv < sv) || (pv == sv && pr < sr);
+                if (keep_min == p_less) {
+                  sv = pv;
+                  sr = pr;
+                }
+              }
+            }
+            const float ov = __shfl_sync(FULL, sv, 31 - lane);
+            const uint32_t orr = __shfl_sync(FULL, sr, 31 - lane);
+            float xv = ld[j];
+            uint32_t xr = lr[j];
+            if (ov < xv || (ov == xv && orr < xr)) {
+              xv = ov;
+              xr = orr;
+            }
+#pragma unroll
+            for (int jj = 16; jj > 0; jj >>= 1) {
+              const float pv = __shfl_xor_sync(FULL, xv, jj);
+              const uint32_t pr = __shfl_xor_sync(FULL, xr, jj);
+              const bool keep_min = (lane & jj) == 0;
+              const bool p_less = (pv < xv) || (pv == xv && pr < xr);
+              if (keep_min == p_less) {
+                xv = pv;
+                xr = pr;
+              }
+            }
+            ld[j] = xv;
+            lr[j] = xr;
+            continue;
+          }
           while (m) {
             const int src = __ffs(m) - 1;
             const float cv = __shfl_sync(FULL, v, src);
