@@ -1,0 +1,447 @@
+// hedra_gpu.cpp -- host side of the drop-in (see hedra_gpu.hpp).  Bookkeeping
+// only; every distance, scan and selection is a libhivf (sm_100a) call.
+#include "hedra_gpu.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <numeric>
+
+namespace hedra_gpu {
+
+Embedding normalized(Embedding v) {
+  double norm = 0.0;
+  for (float x : v) norm += static_cast<double>(x) * static_cast<double>(x);
+  norm = std::sqrt(norm);
+  if (norm == 0.0) return v;
+  for (float& x : v) x = static_cast<float>(static_cast<double>(x) / norm);
+  return v;
+}
+
+void check(hivf_status st) {
+  if (st == HIVF_OK) return;
+  const std::string msg = hivf_last_error();
+  if (st == HIVF_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+namespace ivf {
+
+// ---- TopKResult ------------------------------------------------------------
+void TopKResult::set_k(std::size_t k) {
+  k_ = k;
+  if (entries_.size() > k_) entries_.resize(k_);
+}
+
+bool TopKResult::insert(DocId doc_id, double distance) {
+  if (k_ == 0) return false;
+  auto same = std::find_if(entries_.begin(), entries_.end(),
+                           [&](const TopKEntry& e) { return e.doc_id == doc_id; });
+  if (same != entries_.end()) {
+    if (!(distance < same->distance)) return false;  // keep the minimum
+    entries_.erase(same);
+  }
+  const TopKEntry e{doc_id, distance};
+  const auto at = std::lower_bound(entries_.begin(), entries_.end(), e, topk_less);
+  if (at == entries_.end() && entries_.size() >= k_) return false;
+  entries_.insert(at, e);
+  if (entries_.size() > k_) entries_.pop_back();
+  return true;
+}
+
+TopKResult TopKResult::truncated(std::size_t k) const {
+  TopKResult out(k);
+  out.entries_.assign(entries_.begin(), entries_.begin() + std::min(k, entries_.size()));
+  return out;
+}
+
+std::vector<DocId> TopKResult::doc_ids() const {
+  std::vector<DocId> out(entries_.size());
+  std::transform(entries_.begin(), entries_.end(), out.begin(),
+                 [](const TopKEntry& e) { return e.doc_id; });
+  return out;
+}
+
+bool TopKResult::operator==(const TopKResult& o) const {
+  if (entries_.size() != o.entries_.size()) return false;
+  for (std::size_t i = 0; i < entries_.size(); ++i)
+    if (entries_[i].doc_id != o.entries_[i].doc_id || entries_[i].distance != o.entries_[i].distance)
+      return false;
+  return true;
+}
+
+void TopKResult::assign_sorted(const std::uint64_t* ids, const double* d, std::size_t n) {
+  entries_.resize(n);
+  for (std::size_t i = 0; i < n; ++i) entries_[i] = TopKEntry{ids[i], d[i]};
+}
+
+TopKResult merge_topk(const TopKResult& a, const TopKResult& b, std::size_t k) {
+  // best distance per id, then (distance, id) order, first k
+  std::map<DocId, double> best;
+  for (const auto* r : {&a, &b})
+    for (const auto& e : r->entries()) {
+      auto it = best.find(e.doc_id);
+      if (it == best.end() || e.distance < it->second) best[e.doc_id] = e.distance;
+    }
+  std::vector<TopKEntry> all;
+  all.reserve(best.size());
+  for (const auto& [id, d] : best) all.push_back(TopKEntry{id, d});
+  std::sort(all.begin(), all.end(), topk_less);
+  TopKResult out(k);
+  for (std::size_t i = 0; i < all.size() && i < k; ++i) out.insert(all[i].doc_id, all[i].distance);
+  return out;
+}
+
+// ---- Context / IvfIndex ---------------------------------------------------------
+Context::Context(int device, void* stream) { check(hivf_ctx_create(device, stream, &ctx_)); }
+Context::~Context() { hivf_ctx_destroy(ctx_); }
+
+std::shared_ptr<IvfIndex> IvfIndex::from_assignments(Context& ctx, const std::vector<float>& corpus,
+                                                     const std::vector<DocId>& ids, std::uint32_t dim,
+                                                     Metric metric,
+                                                     const std::vector<std::vector<float>>& centroids,
+                                                     const std::vector<ClusterId>& assign) {
+  if (assign.size() != ids.size() || corpus.size() != ids.size() * dim)
+    throw std::invalid_argument("index_from_assignments: assignment count mismatch");
+  const std::size_t K = centroids.size();
+  std::vector<std::uint64_t> off(K + 1, 0);
+  for (ClusterId c : assign) {
+    if (c >= K) throw std::invalid_argument("index_from_assignments: cluster id out of range");
+    ++off[c + 1];
+  }
+  std::partial_sum(off.begin(), off.end(), off.begin());
+  std::vector<std::uint64_t> cursor(off.begin(), off.end() - 1);
+  std::vector<float> rows(corpus.size());
+  std::vector<DocId> lids(ids.size());
+  for (std::size_t i = 0; i < ids.size(); ++i) {  // stable: corpus order inside a list
+    const std::uint64_t r = cursor[assign[i]]++;
+    std::copy(corpus.begin() + i * dim, corpus.begin() + (i + 1) * dim, rows.begin() + r * dim);
+    lids[r] = ids[i];
+  }
+  std::vector<float> cents;
+  cents.reserve(K * dim);
+  for (const auto& c : centroids) {
+    if (c.size() != dim) throw std::invalid_argument("build_index: dimension mismatch");
+    cents.insert(cents.end(), c.begin(), c.end());
+  }
+  auto ix = std::shared_ptr<IvfIndex>(new IvfIndex);
+  ix->ctx_ = &ctx;
+  ix->dim_ = dim;
+  ix->metric_ = metric;
+  ix->total_ = ids.size();
+  ix->sizes_.resize(K);
+  for (std::size_t c = 0; c < K; ++c) ix->sizes_[c] = off[c + 1] - off[c];
+  check(hivf_index_upload(ctx.raw(), dim, static_cast<int>(metric), static_cast<std::uint32_t>(K),
+                          cents.data(), off.data(), rows.data(), lids.data(), &ix->ix_));
+  return ix;
+}
+
+IvfIndex::~IvfIndex() { hivf_index_destroy(ix_); }
+
+double IvfIndex::mean_assigned_distance() const {
+  double m = 0.0;
+  check(hivf_index_info(ix_, nullptr, nullptr, nullptr, nullptr, &m));
+  return m;
+}
+
+// ---- search API ---------------------------------------------------------------
+std::vector<ClusterId> select_clusters(const IvfIndex& index, const Embedding& query,
+                                       std::size_t nprobe) {
+  if (nprobe < 1 || nprobe > index.k_clusters())
+    throw std::invalid_argument("select_clusters: nprobe out of range");
+  if (query.size() != index.dim()) throw std::invalid_argument("select_clusters: dimension mismatch");
+  std::vector<ClusterId> plan(nprobe);
+  check(hivf_assign(index.raw(), query.data(), 1, static_cast<std::uint32_t>(nprobe), plan.data(),
+                    nullptr));
+  return plan;
+}
+
+SearchCursor make_cursor(const IvfIndex& index, const Embedding& query, std::size_t nprobe,
+                         std::size_t k) {
+  if (k == 0) throw std::invalid_argument("make_cursor: k must be >= 1");
+  SearchCursor c;
+  c.query = index.metric() == Metric::Cosine ? normalized(query) : query;
+  c.plan = select_clusters(index, query, nprobe);
+  c.k = k;
+  c.heap.set_k(k);
+  return c;
+}
+
+std::vector<SearchStepReport> search_clusters_batch(
+    const IvfIndex& index, const std::vector<SearchCursor*>& cursors,
+    const std::vector<std::span<const ClusterId>>& clusters) {
+  const std::size_t n = cursors.size();
+  if (clusters.size() != n) throw std::invalid_argument("search_clusters_batch: size mismatch");
+  std::vector<SearchStepReport> out(n);
+  if (n == 0) return out;
+  // plan-order validation (vector_index.cpp:295-298) before any state changes
+  std::size_t kmax = 1;
+  for (std::size_t i = 0; i < n; ++i) {
+    const SearchCursor& c = *cursors[i];
+    for (std::size_t j = 0; j < clusters[i].size(); ++j) {
+      if (c.next_pos + j >= c.plan.size())
+        throw std::runtime_error("search_clusters: cursor exhausted mid-batch");
+      if (c.plan[c.next_pos + j] != clusters[i][j])
+        throw std::runtime_error("search_clusters: cluster does not match plan order");
+    }
+    kmax = std::max(kmax, c.k);
+  }
+  const std::uint32_t dim = index.dim();
+  std::vector<float> q(n * dim);
+  std::vector<std::uint32_t> off(n + 1, 0), kk(n), hn(n), cl;
+  std::vector<std::uint64_t> hid(n * kmax, 0);
+  std::vector<double> hd(n * kmax, 0.0);
+  for (std::size_t i = 0; i < n; ++i) {
+    const SearchCursor& c = *cursors[i];
+    if (c.query.size() != dim) throw std::invalid_argument("search_clusters: dimension mismatch");
+    std::copy(c.query.begin(), c.query.end(), q.begin() + i * dim);
+    cl.insert(cl.end(), clusters[i].begin(), clusters[i].end());
+    off[i + 1] = static_cast<std::uint32_t>(cl.size());
+    kk[i] = static_cast<std::uint32_t>(c.k);
+    const auto& e = c.heap.entries();
+    hn[i] = static_cast<std::uint32_t>(e.size());
+    for (std::size_t j = 0; j < e.size(); ++j) {
+      hid[i * kmax + j] = e[j].doc_id;
+      hd[i * kmax + j] = e[j].distance;
+    }
+  }
+  std::vector<std::uint8_t> changed(std::max<std::size_t>(1, cl.size()));
+  check(hivf_scan_items(index.raw(), q.data(), static_cast<std::uint32_t>(n), off.data(), cl.data(),
+                        kk.data(), hid.data(), hd.data(), hn.data(),
+                        static_cast<std::uint32_t>(kmax), changed.data()));
+  for (std::size_t i = 0; i < n; ++i) {
+    SearchCursor& c = *cursors[i];
+    c.heap.assign_sorted(hid.data() + i * kmax, hd.data() + i * kmax, hn[i]);
+    for (std::uint32_t j = off[i]; j < off[i + 1]; ++j) {
+      ++c.next_pos;
+      ++c.clusters_searched;
+      c.unchanged_streak = changed[j] ? 0 : c.unchanged_streak + 1;
+      out[i].heap_changed |= changed[j] != 0;
+      out[i].searched.push_back(cl[j]);
+    }
+  }
+  return out;
+}
+
+SearchStepReport search_clusters(const IvfIndex& index, SearchCursor& cursor,
+                                 std::span<const ClusterId> clusters) {
+  return search_clusters_batch(index, {&cursor}, {clusters})[0];
+}
+
+SearchStepReport search_step(const IvfIndex& index, SearchCursor& cursor,
+                             std::size_t cluster_budget) {
+  if (cursor.done()) return {};
+  if (cluster_budget == 0) throw std::invalid_argument("search_step: cluster_budget must be >= 1");
+  const std::size_t take = std::min(cluster_budget, cursor.remaining());
+  const std::vector<ClusterId> slice(cursor.plan.begin() + cursor.next_pos,
+                                     cursor.plan.begin() + cursor.next_pos + take);
+  return search_clusters(index, cursor, slice);
+}
+
+std::vector<TopKResult> search(const IvfIndex& index, const std::vector<Embedding>& queries,
+                               std::size_t nprobe, std::size_t k) {
+  if (k == 0) throw std::invalid_argument("make_cursor: k must be >= 1");
+  const std::uint32_t dim = index.dim();
+  const std::size_t n = queries.size();
+  std::vector<float> q(n * dim);
+  for (std::size_t i = 0; i < n; ++i) {
+    if (queries[i].size() != dim) throw std::invalid_argument("select_clusters: dimension mismatch");
+    std::copy(queries[i].begin(), queries[i].end(), q.begin() + i * dim);
+  }
+  std::vector<std::uint64_t> ids(n * k);
+  std::vector<double> d(n * k);
+  std::vector<std::uint32_t> cnt(n);
+  if (n)
+    check(hivf_search(index.raw(), q.data(), static_cast<std::uint32_t>(n),
+                      static_cast<std::uint32_t>(nprobe), static_cast<std::uint32_t>(k), ids.data(),
+                      d.data(), cnt.data()));
+  std::vector<TopKResult> out(n, TopKResult(k));
+  for (std::size_t i = 0; i < n; ++i) out[i].assign_sorted(ids.data() + i * k, d.data() + i * k, cnt[i]);
+  return out;
+}
+
+}  // namespace ivf
+
+// ---- cache::ClusterCacheState ------------------------------------------------------
+namespace cache {
+
+void ClusterCacheState::record_access(std::span<const ClusterId> cluster_ids) {
+  for (ClusterId c : std::set<ClusterId>(cluster_ids.begin(), cluster_ids.end())) freq_[c] += 1.0;
+  ++since_update_;
+}
+
+std::vector<SwapOp> ClusterCacheState::maybe_update(double now_ms, const ivf::IvfIndex& index) {
+  if (cfg_.capacity_gc == 0 || since_update_ < cfg_.update_interval || !in_flight_.empty()) return {};
+  since_update_ = 0;
+  std::vector<std::pair<double, ClusterId>> by_freq;
+  for (const auto& [c, f] : freq_) by_freq.emplace_back(f, c);
+  std::sort(by_freq.begin(), by_freq.end(), [](const auto& x, const auto& y) {
+    return x.first != y.first ? x.first > y.first : x.second < y.second;  // ties: lower id
+  });
+  std::set<ClusterId> want;
+  for (std::size_t i = 0; i < by_freq.size() && want.size() < cfg_.capacity_gc; ++i)
+    want.insert(by_freq[i].second);
+  const double bytes_per_ms = cfg_.transfer_bandwidth_gb_s * 1e6;
+  std::vector<SwapOp> plan;
+  auto enqueue = [&](ClusterId c, bool inbound) {
+    const double bytes = static_cast<double>(index.cluster_size(c)) * index.dim() * sizeof(float);
+    const double start = std::max(now_ms, link_free_at_ms_);
+    plan.push_back(SwapOp{c, inbound, start + bytes / bytes_per_ms});
+    link_free_at_ms_ = plan.back().completes_at_ms;
+    ++swaps_;
+  };
+  std::vector<ClusterId> out, in;
+  for (ClusterId c : resident_)
+    if (!want.count(c)) out.push_back(c);
+  for (ClusterId c : want)
+    if (!resident_.count(c)) in.push_back(c);
+  for (ClusterId c : out) {  // evictions leave residency at once
+    resident_.erase(c);
+    enqueue(c, false);
+    dirty_ = true;
+  }
+  for (ClusterId c : in) enqueue(c, true);
+  in_flight_ = plan;
+  for (auto& kv : freq_) kv.second *= cfg_.decay;
+  return plan;
+}
+
+void ClusterCacheState::complete_swaps(double now_ms) {
+  std::vector<SwapOp> keep;
+  for (const auto& op : in_flight_) {
+    if (op.completes_at_ms <= now_ms) {
+      if (op.inbound) {
+        resident_.insert(op.cluster);
+        dirty_ = true;
+      }
+    } else {
+      keep.push_back(op);
+    }
+  }
+  in_flight_.swap(keep);
+}
+
+LanePartition ClusterCacheState::partition_batch(std::span<const ClusterId> clusters) const {
+  LanePartition p;
+  std::set<ClusterId> hot;
+  if (cfg_.capacity_gc)
+    for (ClusterId c : clusters)
+      if (resident_.count(c)) hot.insert(c);
+  if (cfg_.capacity_gc == 0 || hot.size() < cfg_.min_fast_clusters) {
+    p.slow.assign(clusters.begin(), clusters.end());
+    return p;
+  }
+  for (ClusterId c : clusters) (hot.count(c) ? p.fast : p.slow).push_back(c);
+  return p;
+}
+
+void ClusterCacheState::count_access_hits(std::span<const ClusterId> clusters) {
+  for (ClusterId c : std::set<ClusterId>(clusters.begin(), clusters.end()))
+    (resident_.count(c) ? hits_ : misses_) += 1;
+}
+
+void ClusterCacheState::apply_to(const ivf::IvfIndex& index) {
+  if (!dirty_) return;
+  const std::vector<ClusterId> res(resident_.begin(), resident_.end());
+  check(hivf_residency_set(index.raw(), res.data(), static_cast<std::uint32_t>(res.size())));
+  dirty_ = false;
+}
+
+}  // namespace cache
+
+// ---- ret::RetrievalEngine ----------------------------------------------------------
+namespace ret {
+
+double cluster_variable_ms(const ivf::IvfIndex& index, ClusterId cluster, Lane lane,
+                           const RetrievalCostModel& model) {
+  if (cluster >= index.k_clusters()) throw std::invalid_argument("cluster_variable_ms: unknown cluster");
+  double ns = static_cast<double>(index.cluster_size(cluster)) * model.per_vector_ns;
+  if (lane == Lane::Fast) ns /= model.fast_speedup;
+  return ns / 1e6;
+}
+
+double estimate_cluster_cost_ms(const ivf::IvfIndex& index, ClusterId cluster, Lane lane,
+                                const RetrievalCostModel& model) {
+  return cluster_variable_ms(index, cluster, lane, model) + fixed_call_ms(model);
+}
+
+void RetrievalEngine::submit(RetrievalTask task) {
+  const auto key = std::make_pair(task.request_id, task.node_id);
+  if (tasks_.count(key)) throw std::invalid_argument("submit: duplicate live task for this stage");
+  tasks_.emplace(key, std::move(task));
+}
+
+bool RetrievalEngine::has_task(RequestId r, NodeId n) const { return tasks_.count({r, n}) > 0; }
+
+const RetrievalTask* RetrievalEngine::find(RequestId r, NodeId n) const {
+  const auto it = tasks_.find({r, n});
+  return it == tasks_.end() ? nullptr : &it->second;
+}
+
+RetrievalTask RetrievalEngine::extract(RequestId r, NodeId n) {
+  auto it = tasks_.find({r, n});
+  if (it == tasks_.end()) throw std::invalid_argument("extract: no live task for this stage");
+  RetrievalTask t = std::move(it->second);
+  tasks_.erase(it);
+  return t;
+}
+
+bool RetrievalEngine::cancel(RequestId r, NodeId n) { return tasks_.erase({r, n}) > 0; }
+
+RetStepReport RetrievalEngine::execute(SubStageBatch& batch, double now_ms, bool /*live_math*/) {
+  RetStepReport rep;
+  if (batch.items.empty()) return rep;
+  cache_.complete_swaps(now_ms);
+  cache_.apply_to(*index_);
+  std::vector<ClusterId> all;
+  for (const auto& it : batch.items) all.insert(all.end(), it.clusters.begin(), it.clusters.end());
+  const auto part = cache_.partition_batch(all);
+  const std::set<ClusterId> fast(part.fast.begin(), part.fast.end());
+  cache_.count_access_hits(all);
+  double slow_ns = 0.0, fast_ns = 0.0;  // modeled lane billing, as the reference bills it
+  for (auto& it : batch.items) {
+    it.fast.clear();
+    it.slow.clear();
+    for (ClusterId c : it.clusters) {
+      const double ns = static_cast<double>(index_->cluster_size(c)) * model_.per_vector_ns;
+      if (fast.count(c)) {
+        it.fast.push_back(c);
+        fast_ns += ns / model_.fast_speedup;
+        ++rep.fast_clusters;
+      } else {
+        it.slow.push_back(c);
+        slow_ns += ns;
+        ++rep.slow_clusters;
+      }
+    }
+  }
+  rep.slow_lane_ms = slow_ns / 1e6;
+  rep.fast_lane_ms = fast_ns / 1e6;
+  rep.modeled_ms = std::max(rep.slow_lane_ms, rep.fast_lane_ms) + fixed_call_ms(model_);
+  std::vector<ivf::SearchCursor*> cursors;
+  std::vector<std::span<const ClusterId>> spans;
+  for (const auto& it : batch.items) {
+    auto t = tasks_.find({it.request_id, it.node_id});
+    if (t == tasks_.end()) throw std::runtime_error("execute: batch references unknown task");
+    cursors.push_back(&t->second.cursor);
+    spans.emplace_back(it.clusters.data(), it.clusters.size());
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto steps = ivf::search_clusters_batch(*index_, cursors, spans);  // one GPU sub-stage
+  rep.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::set<ClusterId> accessed;
+  for (std::size_t i = 0; i < batch.items.size(); ++i) {
+    const auto& it = batch.items[i];
+    rep.deltas.push_back(TaskDelta{it.request_id, it.node_id, it.clusters.size(),
+                                   steps[i].heap_changed, cursors[i]->done()});
+    accessed.insert(it.clusters.begin(), it.clusters.end());
+  }
+  const std::vector<ClusterId> acc(accessed.begin(), accessed.end());
+  cache_.record_access(acc);
+  rep.swaps_started = cache_.maybe_update(now_ms, *index_);
+  cache_.apply_to(*index_);
+  return rep;
+}
+
+}  // namespace ret
+}  // namespace hedra_gpu
