@@ -33,8 +33,11 @@ __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32
   const uint32_t b = blockIdx.x;
   if (b >= n) return;
   __shared__ double s_norm;
+  __shared__ double s_part[4];
   const float* q = qin + (uint64_t)b * dim;
-  if (threadIdx.x == 0) {
+  const bool do_norm_metric = metric == 1 && normalize;
+  if (do_norm_metric && threadIdx.x == 0) {
+    // cosine: the reference's sequential double norm (embedding.hpp:36-43), exactly
     double nrm = 0.0;
     for (uint32_t d = 0; d < dim; ++d) {
       const double x = (double)q[d];
@@ -43,21 +46,22 @@ __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32
     s_norm = __dsqrt_rn(nrm);
   }
   __syncthreads();
-  const double nrm = s_norm;
-  const bool do_norm = metric == 1 && normalize && nrm != 0.0;
+  const double nrm = do_norm_metric ? s_norm : 0.0;
+  const bool do_norm = do_norm_metric && nrm != 0.0;
+  double part = 0.0;  // |q|^2 for the filter bound only: any summation order is fine
   for (uint32_t d = threadIdx.x; d < dpad; d += blockDim.x) {
     float v = d < dim ? q[d] : 0.f;
     if (d < dim && !isfinite(v)) *err = 1;
     if (do_norm) v = __double2float_rn(__ddiv_rn((double)v, nrm));
     qs[(uint64_t)b * dpad + d] = v;
+    part += (double)v * (double)v;
   }
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
     double acc = 0.0;
-    for (uint32_t d = 0; d < dim; ++d) {
-      const double x = (double)qs[(uint64_t)b * dpad + d];
-      acc = __dadd_rn(acc, __dmul_rn(x, x));
-    }
+    for (uint32_t w = 0; w < (blockDim.x + 31) / 32; ++w) acc += s_part[w];
     qn2[b] = __double2float_rn(acc);
     qnorm[b] = __double2float_ru(sqrt(acc) * (1.0 + 1e-6));
   }
@@ -81,31 +85,45 @@ __global__ void __launch_bounds__(256) k_coarse_dist(IndexView ix, QueryView qv,
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // register-prefetched k-tiles: tile k0+CT_K is loaded from global while tile
+  // k0 is multiplied out of shared memory
+  float4 pa[2], pb = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto fetch = [&](uint32_t k0) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int f = tid + t * 256;
+      const uint32_t c = c0 + (f >> 2);
+      pa[t] = (c < ix.K && k0 < ix.dpad)
+                  ? __ldg(reinterpret_cast<const float4*>(ix.cent + (uint64_t)c * ix.dpad + k0 + (f & 3) * 4))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid < 128) {
+      const uint32_t q = q0 + (tid >> 2);
+      pb = (q < qv.n && k0 < ix.dpad)
+               ? __ldg(reinterpret_cast<const float4*>(qv.qs + (uint64_t)q * ix.dpad + k0 + (tid & 3) * 4))
+               : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  fetch(0);
   for (uint32_t k0 = 0; k0 < ix.dpad; k0 += CT_K) {
-    // centroids: 128 rows x 16 dims = 512 float4, 2 per thread
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const int f = tid + t * 256;
       const int row = f >> 2, g = f & 3;
-      const uint32_t c = c0 + row;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c < ix.K) v = *reinterpret_cast<const float4*>(ix.cent + (uint64_t)c * ix.dpad + k0 + g * 4);
-      As[g * 4 + 0][row] = v.x;
-      As[g * 4 + 1][row] = v.y;
-      As[g * 4 + 2][row] = v.z;
-      As[g * 4 + 3][row] = v.w;
+      As[g * 4 + 0][row] = pa[t].x;
+      As[g * 4 + 1][row] = pa[t].y;
+      As[g * 4 + 2][row] = pa[t].z;
+      As[g * 4 + 3][row] = pa[t].w;
     }
     if (tid < 128) {
       const int row = tid >> 2, g = tid & 3;
-      const uint32_t q = q0 + row;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (q < qv.n) v = *reinterpret_cast<const float4*>(qv.qs + (uint64_t)q * ix.dpad + k0 + g * 4);
-      Bs[g * 4 + 0][row] = v.x;
-      Bs[g * 4 + 1][row] = v.y;
-      Bs[g * 4 + 2][row] = v.z;
-      Bs[g * 4 + 3][row] = v.w;
+      Bs[g * 4 + 0][row] = pb.x;
+      Bs[g * 4 + 1][row] = pb.y;
+      Bs[g * 4 + 2][row] = pb.z;
+      Bs[g * 4 + 3][row] = pb.w;
     }
     __syncthreads();
+    fetch(k0 + CT_K);
 #pragma unroll
     for (int kk = 0; kk < CT_K; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&As[kk][tc * 4]);
@@ -152,17 +170,36 @@ __device__ uint32_t block_radix_select(uint32_t n, uint32_t want, KeyOf key_of, 
     }
     __syncthreads();
     __shared__ uint32_t s_digit, s_before;
-    if (threadIdx.x == 0) {
-      uint32_t cum = 0, dig = 255;
-      for (uint32_t dg = 0; dg < 256; ++dg) {
-        if (cum + hist[dg] >= want) {
-          dig = dg;
-          break;
-        }
-        cum += hist[dg];
+    if (threadIdx.x < 32) {  // warp 0: 8 bins per lane, warp prefix sum, first bin reaching `want`
+      const uint32_t lane = threadIdx.x;
+      uint32_t h[8], local = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        h[j] = hist[lane * 8 + j];
+        local += h[j];
       }
-      s_digit = dig;
-      s_before = cum;
+      uint32_t incl = local;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      const uint32_t excl = incl - local;
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= want && excl < want);
+      const uint32_t src = hit ? __ffs(hit) - 1 : 31;
+      if (lane == src) {
+        uint32_t cum = excl, dig = lane * 8 + 7;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (cum + h[j] >= want) {
+            dig = lane * 8 + j;
+            break;
+          }
+          cum += h[j];
+        }
+        s_digit = dig;
+        s_before = cum;
+      }
     }
     __syncthreads();
     prefix |= s_digit << shift;
@@ -235,10 +272,8 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
   // exact fp64 distances in the reference's order (select_clusters uses
   // squared_l2(centroid, query), :272)
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const float* crow = ix.cent + (uint64_t)cid[i] * ix.dpad;
-    double acc = 0.0;
-    for (uint32_t d = 0; d < ix.dim; ++d) acc = exact_step(acc, crow[d], qsh[d]);
-    cd[i] = acc;
+    const float4* crow = reinterpret_cast<const float4*>(ix.cent + (uint64_t)cid[i] * ix.dpad);
+    cd[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) { return __ldg(crow + g); });
   }
   uint32_t mp = 1;
   while (mp < m) mp <<= 1;
@@ -282,8 +317,8 @@ __global__ void __launch_bounds__(512) k_coarse_fallback(IndexView ix, QueryView
     double acc = DBL_MAX;
     if (c < ix.K) {
       acc = 0.0;
-      const float* crow = ix.cent + (uint64_t)c * ix.dpad;
-      for (uint32_t d = 0; d < ix.dim; ++d) acc = exact_step(acc, crow[d], qsh[d]);
+      const float4* crow = reinterpret_cast<const float4*>(ix.cent + (uint64_t)c * ix.dpad);
+      acc = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) { return __ldg(crow + g); });
     }
     const uint32_t cnt_now = s_cnt;
     __syncthreads();  // every thread has read s_cnt before any append
@@ -339,7 +374,7 @@ void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float*
   const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 4;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_coarse_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_coarse_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_coarse_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_set = true;

@@ -62,6 +62,34 @@ __device__ __forceinline__ double exact_step(double acc, float a, float b) {
   return __dadd_rn(acc, __dmul_rn(d, d));
 }
 
+// Exact distance of one row to the query in smem, loads double-buffered 32
+// dims (8 x 16 B) ahead so the memory latency overlaps the sequential fp64
+// chain.  load(g) returns dims 4g..4g+3 of the row (zero past dim).
+template <typename Load>
+__device__ __forceinline__ double exact_row_pipelined(uint32_t dim, const float* qsh, Load load) {
+  const uint32_t ng = (dim + 3) / 4;
+  double acc = 0.0;
+  float4 cur[8], nxt[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) cur[e] = (uint32_t)e < ng ? load(e) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t g0 = 0; g0 < ng; g0 += 8) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      nxt[e] = g0 + 8 + e < ng ? load(g0 + 8 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t d = (g0 + e) * 4;
+      if (d + 0 < dim) acc = exact_step(acc, qsh[d + 0], cur[e].x);
+      if (d + 1 < dim) acc = exact_step(acc, qsh[d + 1], cur[e].y);
+      if (d + 2 < dim) acc = exact_step(acc, qsh[d + 2], cur[e].z);
+      if (d + 3 < dim) acc = exact_step(acc, qsh[d + 3], cur[e].w);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) cur[e] = nxt[e];
+  }
+  return acc;
+}
+
 // ---- orderable float keys ----------------------------------------------------
 __device__ __forceinline__ uint32_t f2key(float f) {
   uint32_t u = __float_as_uint(f);

@@ -22,43 +22,10 @@ namespace hivf {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kFinThreads = 128;
-constexpr int kCandMax = 1024;
+constexpr int kFinThreads = 256;
+constexpr int kCandMax = 512;
+constexpr uint32_t kSlotCap = 320;  // staged (plan position, segment) slots per query
 constexpr float kInf = __builtin_inff();
-
-__device__ __forceinline__ float list_E(double eps, double ab, float qn, float xn) {
-  const double m = (double)qn + (double)xn;
-  return __double2float_ru(eps * m * m + ab);
-}
-
-__device__ __forceinline__ uint32_t list_of_row(const IndexView& ix, uint64_t r) {
-  uint32_t lo = 0, hi = ix.K;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (ix.list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// Exact reference distance between the (search-space) query in smem and the
-// row `r` of list `c` (squared_l2(query, vec), vector_index.cpp:303).
-__device__ double exact_row_dist(const IndexView& ix, const float* qsh, uint32_t c, uint64_t r) {
-  const uint64_t lbeg = ix.list_off[c];
-  const uint64_t n_c = ix.list_off[c + 1] - lbeg;
-  const uint64_t base = lbeg * ix.dpad;
-  const uint64_t lr = r - lbeg;
-  double acc = 0.0;
-  const uint32_t ng = (ix.dim + 3) / 4;
-  for (uint32_t g = 0; g < ng; ++g) {
-    const float4 x = *reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4));
-    const uint32_t d = g * 4;
-    acc = exact_step(acc, qsh[d], x.x);
-    if (d + 1 < ix.dim) acc = exact_step(acc, qsh[d + 1], x.y);
-    if (d + 2 < ix.dim) acc = exact_step(acc, qsh[d + 2], x.z);
-    if (d + 3 < ix.dim) acc = exact_step(acc, qsh[d + 3], x.w);
-  }
-  return acc;
-}
 
 // Merge a sorted-ascending 32-lane list `v` into sorted-ascending `cur`
 // (keeps the 32 smallest).
@@ -132,50 +99,136 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     s_total = 0;
   }
   __syncthreads();
-  // 1. tau = k-th smallest upper bound
-  float cur = kInf;
-  unsigned long long total = 0;
-  for (uint32_t p = warp; p < nprobe; p += NW) {
-    const uint32_t c = plans[(uint64_t)b * nprobe + p];
-    const float E = seg_bound(ix, qn, ix.maxnorm[c]);
-    const uint32_t ns = nseg_of(ix, c);
-    total += ix.list_off[c + 1] - ix.list_off[c];
-    for (uint32_t s = 0; s < ns; ++s) {
-      const uint64_t slot = ((uint64_t)b * nprobe + p) * ix.s_max + s;
-      const uint32_t n = cand_n[slot];
-      const float v = lane < (int)n ? __fadd_ru(cand_d[slot * kKP + lane], E) : kInf;
-      cur = warp_merge32(cur, v);
+  // 0. per plan position metadata (list, segment count, bound) -> smem, in parallel
+  float* pE = reinterpret_cast<float*>(qsh + ix.dpad);   // nprobe
+  uint32_t* pc = reinterpret_cast<uint32_t*>(pE + nprobe);  // nprobe
+  uint32_t* pns = pc + nprobe;                            // nprobe
+  {
+    unsigned long long tot = 0;
+    for (uint32_t p = threadIdx.x; p < nprobe; p += blockDim.x) {
+      const uint32_t c = plans[(uint64_t)b * nprobe + p];
+      const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
+      pc[p] = c;
+      pns[p] = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+      pE[p] = seg_bound(ix, qn, ix.maxnorm[c]);
+      tot += rows;
+    }
+    atomicAdd(&s_total, tot);
+  }
+  __syncthreads();
+  // Compacted list of the query's valid (plan position, segment) slots, and
+  // their candidate lists staged into smem with all threads' loads in flight
+  // (the scan's outputs are read once, latency paid once).
+  uint32_t* soff = pns + nprobe;                              // nprobe + 1
+  uint32_t* sp = soff + nprobe + 1;                           // kSlotCap
+  uint32_t* sn = sp + kSlotCap;                               // kSlotCap
+  float* sthr = reinterpret_cast<float*>(sn + kSlotCap);      // kSlotCap
+  float* sdv = sthr + kSlotCap;                               // kSlotCap x 32
+  __shared__ uint32_t s_nslots;
+  if (warp == 0) {  // exclusive scan of pns (nprobe <= kNprobeMax) by one warp
+    const uint32_t per = (nprobe + 31) / 32;
+    const uint32_t p0 = min(nprobe, lane * per), p1 = min(nprobe, p0 + per);
+    uint32_t local = 0;
+    for (uint32_t p = p0; p < p1; ++p) local += pns[p];
+    uint32_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t run = incl - local;
+    for (uint32_t p = p0; p < p1; ++p) {
+      soff[p] = run;
+      run += pns[p];
+    }
+    if (lane == 31) {
+      soff[nprobe] = incl;
+      s_nslots = incl;
     }
   }
-  wl[warp][lane] = cur;
-  if (lane == 0) atomicAdd(&s_total, total);
   __syncthreads();
-  if (warp == 0) {
-    float x = wl[0][lane];
-    for (int w = 1; w < NW; ++w) x = warp_merge32(x, wl[w][lane]);
-    const float t = __shfl_sync(FULL, x, (int)min(k, 32u) - 1);
-    if (lane == 0) s_tau = t;
-  }
-  __syncthreads();
-  const float tau = s_tau;
-  // 2. candidates + completeness
-  for (uint32_t p = warp; p < nprobe; p += NW) {
-    const uint32_t c = plans[(uint64_t)b * nprobe + p];
-    const float E = seg_bound(ix, qn, ix.maxnorm[c]);
-    const uint32_t ns = nseg_of(ix, c);
-    for (uint32_t s = 0; s < ns; ++s) {
-      const uint64_t slot = ((uint64_t)b * nprobe + p) * ix.s_max + s;
-      const uint32_t n = cand_n[slot];
-      const bool take = lane < (int)n && __fsub_rd(cand_d[slot * kKP + lane], E) <= tau;
-      const unsigned m = __ballot_sync(FULL, take);
+  const uint32_t V = s_nslots;
+  const uint64_t slot0 = (uint64_t)b * nprobe * ix.s_max;
+  if (V <= kSlotCap) {
+    for (uint32_t p = threadIdx.x; p < nprobe; p += blockDim.x)
+      for (uint32_t t = 0; t < pns[p]; ++t) sp[soff[p] + t] = p * ix.s_max + t;  // p*s_max+s
+    __syncthreads();
+    for (uint32_t v = threadIdx.x; v < V; v += blockDim.x) {
+      sn[v] = cand_n[slot0 + sp[v]];
+      sthr[v] = cand_thr[slot0 + sp[v]];
+    }
+    for (uint32_t idx = threadIdx.x; idx < V * kKP; idx += blockDim.x)
+      sdv[idx] = cand_d[(slot0 + sp[idx / kKP]) * kKP + (idx % kKP)];
+    __syncthreads();
+    // 1. tau = k-th smallest upper bound
+    float cur = kInf;
+    for (uint32_t v = warp; v < V; v += NW) {
+      const float E = pE[sp[v] / ix.s_max];
+      cur = warp_merge32(cur, lane < (int)sn[v] ? __fadd_ru(sdv[v * kKP + lane], E) : kInf);
+    }
+    wl[warp][lane] = cur;
+    __syncthreads();
+    if (warp == 0) {
+      float x = wl[0][lane];
+      for (int w = 1; w < NW; ++w) x = warp_merge32(x, wl[w][lane]);
+      const float t = __shfl_sync(FULL, x, (int)min(k, 32u) - 1);
+      if (lane == 0) s_tau = t;
+    }
+    __syncthreads();
+    const float tau = s_tau;
+    // 2. candidates + completeness
+    for (uint32_t v = warp; v < V; v += NW) {
+      const uint32_t p = sp[v] / ix.s_max;
+      const float E = pE[p];
+      const bool take = lane < (int)sn[v] && __fsub_rd(sdv[v * kKP + lane], E) <= tau;
+      const unsigned msk = __ballot_sync(FULL, take);
       uint32_t base = 0;
-      if (lane == 0 && m) base = atomicAdd(&s_cnt, (uint32_t)__popc(m));
+      if (lane == 0 && msk) base = atomicAdd(&s_cnt, (uint32_t)__popc(msk));
       base = __shfl_sync(FULL, base, 0);
       if (take) {
-        const uint32_t pos = base + __popc(m & ((1u << lane) - 1));
+        const uint32_t pos = base + __popc(msk & ((1u << lane) - 1));
+        if (pos < kCandMax) {
+          crow[pos] = cand_row[(slot0 + sp[v]) * kKP + lane];
+          clist[pos] = pc[p];
+        }
+      }
+      if (lane == 0 && __fsub_rd(sthr[v], E) <= tau) s_bad = 1;
+    }
+  } else {
+    // more segments than fit in smem: read the scan's outputs from global
+    const uint32_t T = nprobe * ix.s_max;
+    float cur = kInf;
+    for (uint32_t t = warp; t < T; t += NW) {
+      if ((t % ix.s_max) >= pns[t / ix.s_max]) continue;
+      const uint32_t n = cand_n[slot0 + t];
+      const float v = lane < (int)n ? __fadd_ru(cand_d[(slot0 + t) * kKP + lane], pE[t / ix.s_max]) : kInf;
+      cur = warp_merge32(cur, v);
+    }
+    wl[warp][lane] = cur;
+    __syncthreads();
+    if (warp == 0) {
+      float x = wl[0][lane];
+      for (int w = 1; w < NW; ++w) x = warp_merge32(x, wl[w][lane]);
+      const float t = __shfl_sync(FULL, x, (int)min(k, 32u) - 1);
+      if (lane == 0) s_tau = t;
+    }
+    __syncthreads();
+    const float tau = s_tau;
+    for (uint32_t t = warp; t < T; t += NW) {
+      const uint32_t p = t / ix.s_max;
+      if ((t % ix.s_max) >= pns[p]) continue;
+      const float E = pE[p];
+      const uint64_t slot = slot0 + t;
+      const uint32_t n = cand_n[slot];
+      const bool take = lane < (int)n && __fsub_rd(cand_d[slot * kKP + lane], E) <= tau;
+      const unsigned msk = __ballot_sync(FULL, take);
+      uint32_t base = 0;
+      if (lane == 0 && msk) base = atomicAdd(&s_cnt, (uint32_t)__popc(msk));
+      base = __shfl_sync(FULL, base, 0);
+      if (take) {
+        const uint32_t pos = base + __popc(msk & ((1u << lane) - 1));
         if (pos < kCandMax) {
           crow[pos] = cand_row[slot * kKP + lane];
-          clist[pos] = c;
+          clist[pos] = pc[p];
         }
       }
       if (lane == 0 && __fsub_rd(cand_thr[slot], E) <= tau) s_bad = 1;
@@ -183,13 +236,20 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   }
   __syncthreads();
   const uint32_t m = s_cnt;
+  const float tau = s_tau;
   if (s_bad || m > kCandMax || !(tau < kInf && tau >= -FLT_MAX) && s_total >= k) {
     if (threadIdx.x == 0) flags[b] = 1;
     return;
   }
-  // 3. exact distances
+  // 3. exact distances: one candidate per thread, loads pipelined ahead of the chain
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    cdist[i] = exact_row_dist(ix, qsh, clist[i], crow[i]);
+    const uint32_t c = clist[i];
+    const uint64_t lbeg = ix.list_off[c];
+    const uint64_t n_c = ix.list_off[c + 1] - lbeg;
+    const uint64_t lr = crow[i] - lbeg, base = lbeg * ix.dpad;
+    cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
+      return __ldg(reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4)));
+    });
     cid[i] = ix.ids[crow[i]];
   }
   uint32_t mp = 1;
@@ -253,7 +313,10 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
       double dist = DBL_MAX;
       uint64_t id = ~0ull;
       if (r < end) {
-        dist = exact_row_dist(ix, qsh, c, r);
+        const uint64_t n_c = end - beg, lr = r - beg, base = beg * ix.dpad;
+        dist = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
+          return __ldg(reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4)));
+        });
         id = ix.ids[r];
       }
       const uint32_t cnt_now = s_cnt;
@@ -391,10 +454,11 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                             const uint32_t* cand_row, const float* cand_thr,
                             const uint32_t* cand_n, uint64_t* ids_out, double* d_out,
                             uint32_t* counts_out, int* flags, cudaStream_t s) {
-  const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 4;
+  const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 4 + (size_t)nprobe * 16 + 4 +
+                      (size_t)kSlotCap * (4 + 4 + 4 + kKP * 4);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_finalize_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_finalize_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_exact_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }

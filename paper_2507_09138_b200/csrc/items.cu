@@ -35,29 +35,6 @@ constexpr int kItThreads = 128;
 constexpr int kItCand = 2048;
 constexpr float kInf = __builtin_inff();
 
-__device__ __forceinline__ float it_E(double eps, double ab, float qn, float xn) {
-  const double m = (double)qn + (double)xn;
-  return __double2float_ru(eps * m * m + ab);
-}
-
-__device__ double it_exact_row(const IndexView& ix, const float* qsh, uint32_t c, uint64_t r) {
-  const uint64_t lbeg = ix.list_off[c];
-  const uint64_t n_c = ix.list_off[c + 1] - lbeg;
-  const uint64_t base = lbeg * ix.dpad;
-  const uint64_t lr = r - lbeg;
-  double acc = 0.0;
-  const uint32_t ng = (ix.dim + 3) / 4;
-  for (uint32_t g = 0; g < ng; ++g) {
-    const float4 x = *reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4));
-    const uint32_t d = g * 4;
-    acc = exact_step(acc, qsh[d], x.x);
-    if (d + 1 < ix.dim) acc = exact_step(acc, qsh[d + 1], x.y);
-    if (d + 2 < ix.dim) acc = exact_step(acc, qsh[d + 2], x.z);
-    if (d + 3 < ix.dim) acc = exact_step(acc, qsh[d + 3], x.w);
-  }
-  return acc;
-}
-
 __device__ __forceinline__ float it_merge32(float cur, float v) {
   const int lane = threadIdx.x & 31;
   const float o = __shfl_sync(FULL, v, 31 - lane);
@@ -185,9 +162,15 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     return;
   }
   const uint32_t m = cj_off[mcl];
-  // B. exact distances
+  // B. exact distances (loads pipelined ahead of each sequential chain)
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    cdist[i] = it_exact_row(ix, qsh, clist[i], crow[i]);
+    const uint32_t c = clist[i];
+    const uint64_t lbeg = ix.list_off[c];
+    const uint64_t n_c = ix.list_off[c + 1] - lbeg;
+    const uint64_t lr = crow[i] - lbeg, base = lbeg * ix.dpad;
+    cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
+      return __ldg(reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4)));
+    });
     cid[i] = ix.ids[crow[i]];
   }
   __syncthreads();
@@ -263,7 +246,10 @@ __global__ void __launch_bounds__(256) k_exact_items(IndexView ix, QueryView qv,
     for (uint64_t r0 = beg; r0 < end; r0 += blockDim.x) {
       const uint64_t r = r0 + threadIdx.x;
       if (r < end) {
-        td[threadIdx.x] = it_exact_row(ix, qsh, c, r);
+        const uint64_t n_c = end - beg, lr = r - beg, base = beg * ix.dpad;
+        td[threadIdx.x] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
+          return __ldg(reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4)));
+        });
         ti[threadIdx.x] = ix.ids[r];
       }
       __syncthreads();
@@ -335,7 +321,7 @@ void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_
   const size_t smem = (size_t)kItCand * (8 + 8 + 4 + 4) + (kNprobeMax + 1) * 4 + (size_t)ix.dpad * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_finalize_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    cudaFuncSetAttribute(k_finalize_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_exact_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
     attr = true;
   }
