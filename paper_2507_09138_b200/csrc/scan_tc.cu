@@ -51,6 +51,8 @@ constexpr int kTcTile = 128;       // rows per MMA tile (M)
 constexpr int kTcCps = 4;          // 16-dim chunks per pipeline stage (64 dims)
 constexpr int kTcMaxA = 8;         // max depth of the A landing ring
 constexpr int kTcLo = 4;           // depth of the A_lo ring (in TMEM, 64 columns per slot)
+constexpr int kMergeQ = 16;        // queries per round of the item-end cross-warp merge
+constexpr int kItemQ = 4;          // published work items in flight (producer runs ahead)
 constexpr int kTcChunkBytes = kTcTile * kChunk * 4;       // 8 KB
 constexpr int kTcStageBytes = kTcCps * kTcChunkBytes;     // 32 KB
 constexpr int kTcSplitWarps = 4;
@@ -180,20 +182,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   const uint32_t SA = P.sa;
   const bool split = P.split != 0;
   const uint32_t qblk = (split ? 2 : 1) * qmax * 64;                // per chunk: [raw rows | lo rows]
-  uint8_t* aring = smem;                                            // SA x 16 KB (raw A)
+  uint8_t* aring = smem;                                            // SA x 32 KB (raw A)
   uint8_t* qsm = smem + SA * kTcStageBytes;                         // nch x qblk
-  uint64_t* bars = reinterpret_cast<uint64_t*>(qsm + (size_t)nch * qblk);
-  uint64_t* full = bars;                        // [SA] TMA -> splitter
+  float* md = reinterpret_cast<float*>(qsm + (size_t)nch * qblk);   // merge scratch [4][kMergeQ][32]
+  uint32_t* mr = reinterpret_cast<uint32_t*>(md + kTcEpiWarps * kMergeQ * 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(mr + kTcEpiWarps * kMergeQ * 32);
+  uint64_t* full = bars;                        // [SA] TMA -> splitter / MMA
   uint64_t* empty = bars + kTcMaxA;             // [SA] MMA -> TMA
   uint64_t* lfull = bars + 2 * kTcMaxA;         // [kTcLo] splitter -> MMA
   uint64_t* lempty = lfull + kTcLo;             // [kTcLo] MMA -> splitter
   uint64_t* tfull = lempty + kTcLo;             // [2] MMA -> epilogue
   uint64_t* tempty = tfull + 2;                 // [2] epilogue -> MMA
-  __shared__ ScanItem s_item;
-  __shared__ int s_valid;
+  uint64_t* ifull = tempty + 2;                 // [kItemQ] producer -> all roles (item published)
+  uint64_t* iempty = ifull + kItemQ;            // [kItemQ] roles -> producer (slot consumed)
+  uint64_t* qfull = iempty + kItemQ;            // stagers -> MMA (query group staged)
+  uint64_t* qempty = qfull + 1;                 // MMA commit -> stagers (query group free)
+  __shared__ ScanItem s_item[kItemQ];
+  __shared__ int s_valid[kItemQ];
   __shared__ uint32_t s_tmem;
-  __shared__ float s_qn2[32];
-  __shared__ uint32_t s_slot[32];
+  float (*s_qn2)[32] = reinterpret_cast<float (*)[32]>(qempty + 1);            // [kItemQ][32]
+  uint32_t (*s_slot)[32] = reinterpret_cast<uint32_t (*)[32]>(s_qn2 + kItemQ);  // [kItemQ][32]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -209,6 +217,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kTcEpiWarps);
     }
+    for (int i = 0; i < kItemQ; ++i) {
+      mbar_init(&ifull[i], 1);
+      mbar_init(&iempty[i], 1 + kTcSplitWarps + kTcEpiWarps);
+    }
+    mbar_init(qfull, kTcSplitWarps);
+    mbar_init(qempty, 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -221,27 +235,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = s_tmem;
+  const uint32_t nstg = (nch + kTcCps - 1) / kTcCps;
 
-  // ring positions (each role keeps its own copy): A ring slot/phase, lo ring slot/phase
+  // Every role walks the same item sequence: the producer claims work items
+  // (atomic counter) into a kItemQ-deep queue of published items, so the bulk
+  // copies of item i+1 start while the MMA / epilogue still finish item i (no
+  // CTA-wide barrier between items).  ring positions are per role.
   uint32_t ra = 0, rpa = 0, rl = 0, rpl = 0;
   uint32_t tb = 0, tph = 0;   // TMEM accumulator ring
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const uint32_t it = atomicAdd(P.work_ctr, 1u);
-      s_valid = it < *P.n_items;
-      if (s_valid) s_item = P.items[it];
-    }
-    __syncthreads();
-    if (!s_valid) break;
-    const ScanItem item = s_item;
-    const uint32_t nq = item.nq;
-    const uint32_t npad = (nq + 7) & ~7u;
-    const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
-    const uint32_t nstg = (nch + kTcCps - 1) / kTcCps;
-    const uint64_t lbeg = P.ix.list_off[item.list];
-    if (warp == 0) {
-      // ---------------- producer: list slices -> A_hi ----------------
-      if (lane == 0) {
+  if (warp == 0) {
+    // ---------------- producer: claims items, list slices -> A ring ----------------
+    if (lane == 0) {
+      for (uint32_t i = 0;; ++i) {
+        const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+        mbar_wait(&iempty[slot], iph ^ 1);
+        const uint32_t it = atomicAdd(P.work_ctr, 1u);
+        const int valid = it < *P.n_items;
+        ScanItem item{};
+        if (valid) item = P.items[it];
+        s_item[slot] = item;
+        s_valid[slot] = valid;
+        mbar_arrive(&ifull[slot]);
+        if (!valid) break;
+        const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
+        const uint64_t lbeg = P.ix.list_off[item.list];
         const uint64_t n_c = P.ix.list_off[item.list + 1] - lbeg;
         const float* lbase = P.ix.vec + lbeg * dpad;
         for (uint32_t t = 0; t < ntiles; ++t) {
@@ -260,13 +277,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           }
         }
       }
-    } else if (warp == 1) {
-      // ---------------- MMA issuer: tf32, single pass or 3-pass split ----------------
-      named_bar_sync(1, (kTcEpiWarps + kTcSplitWarps + 1) * 32);  // queries staged
-      if (lane == 0) {
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: tf32, single pass or 3-pass split ----------------
+    if (lane == 0) {
+      for (uint32_t i = 0;; ++i) {
+        const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+        mbar_wait(&ifull[slot], iph);
+        if (!s_valid[slot]) break;
+        const ScanItem item = s_item[slot];
+        mbar_arrive(&iempty[slot]);
+        const uint32_t npad = (item.nq + 7) & ~7u;
+        const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
         const uint32_t idesc2 = tf32_idesc(split ? 2 * npad : npad);
         const uint32_t idesc1 = tf32_idesc(npad);
         const uint32_t q_base = smem_u32(qsm);
+        mbar_wait(qfull, i & 1);  // this item's query group is staged
+        tc_fence_after();
         for (uint32_t t = 0; t < ntiles; ++t) {
           mbar_wait(&tempty[tb], tph ^ 1);
           tc_fence_after();
@@ -306,15 +333,83 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
             tph ^= 1;
           }
         }
+        mma_commit(qempty);  // query group free once this item's MMAs retire
       }
+    }
+    __syncwarp();
+  } else if (warp < 2 + kTcSplitWarps) {
+    // -------- stagers (query group of each item) + splitters (lo(A) rows -> TMEM) --------
+    const uint32_t sw = warp - 2;                // 0..3
+    const uint32_t quad = warp & 3;              // TMEM lane quadrant of this warp
+    const uint32_t row = quad * 32 + lane;       // tile row owned by this thread
+    const uint32_t swz = (row >> 1) & 3;
+    const int cm = P.conv;
+    const uint32_t ng = dpad / 4;                // float4 groups per query row
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+      mbar_wait(&ifull[slot], iph);
+      if (!s_valid[slot]) break;
+      const ScanItem item = s_item[slot];
+      const uint32_t nq = item.nq;
+      const uint32_t npad = (nq + 7) & ~7u;
+      // rows n = sw + 4m of the query group belong to this warp; lane m < 8 resolves
+      // row m's query id / output slot / |q|^2 (two dependent L2 loads, once)
+      uint32_t my_qi = 0;
+      {
+        const uint32_t n = sw + 4 * lane;
+        if (lane < 8 && n < nq) {
+          const uint32_t pair = P.sorted_pairs[item.pair0 + n];
+          my_qi = P.pair_query[pair];
+          s_qn2[slot][n] = P.qv.qn2[my_qi];
+          s_slot[slot][n] = pair * P.ix.s_max + item.seg;
+        }
+      }
+      if (i > 0) mbar_wait(qempty, (i - 1) & 1);  // previous item's MMAs retired
+      const uint32_t nmine = npad > sw ? (npad - sw + 3) / 4 : 0;
+      for (uint32_t m0 = 0; m0 < nmine; m0 += 2) {
+        for (uint32_t e0 = 0; e0 * 32 < ng; e0 += 8) {
+          float4 v[2][8];
+#pragma unroll
+          for (uint32_t r = 0; r < 2; ++r) {
+            const uint32_t m = m0 + r, n = sw + 4 * m;
+            const uint32_t qi = __shfl_sync(FULL, my_qi, m & 7);
+            const float* qrow = P.qv.qs + (uint64_t)qi * dpad;
+#pragma unroll
+            for (uint32_t e = 0; e < 8; ++e) {
+              const uint32_t g4 = lane + 32 * (e0 + e);
+              v[r][e] = (m < nmine && n < nq && g4 < ng) ? *reinterpret_cast<const float4*>(qrow + g4 * 4)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+#pragma unroll
+          for (uint32_t r = 0; r < 2; ++r) {
+            const uint32_t m = m0 + r, n = sw + 4 * m;
+            if (m >= nmine) break;
+#pragma unroll
+            for (uint32_t e = 0; e < 8; ++e) {
+              const uint32_t g4 = lane + 32 * (e0 + e);
+              if (g4 >= ng) break;
+              const uint32_t ch = g4 >> 2, g = g4 & 3;
+              uint8_t* blk = qsm + ch * qblk;
+              const float4 x = v[r][e];
+              *reinterpret_cast<float4*>(blk + n * 64 + ((g ^ ((n >> 1) & 3)) << 4)) = x;
+              if (split) {
+                const float4 lo = make_float4(x.x - tf32_conv(x.x, cm), x.y - tf32_conv(x.y, cm),
+                                              x.z - tf32_conv(x.z, cm), x.w - tf32_conv(x.w, cm));
+                const uint32_t nl = npad + n;  // lo rows follow the npad raw rows
+                *reinterpret_cast<float4*>(blk + nl * 64 + ((g ^ ((nl >> 1) & 3)) << 4)) = lo;
+              }
+            }
+          }
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
       __syncwarp();
-    } else if (warp < 2 + kTcSplitWarps) {
-      // ---------------- splitters: lo(A) rows -> TMEM ----------------
-      named_bar_sync(1, (kTcEpiWarps + kTcSplitWarps + 1) * 32);  // queries staged
-      const uint32_t quad = warp & 3;              // TMEM lane quadrant of this warp
-      const uint32_t row = quad * 32 + lane;       // tile row owned by this thread
-      const uint32_t swz = (row >> 1) & 3;
-      const int cm = P.conv;
+      if (lane == 0) {
+        mbar_arrive(qfull);
+        mbar_arrive(&iempty[slot]);
+      }
+      const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
       for (uint32_t t = 0; split && t < ntiles; ++t) {
         for (uint32_t sg = 0; sg < nstg; ++sg) {
           const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
@@ -350,39 +445,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           if (++rl == kTcLo) { rl = 0; rpl ^= 1; }
         }
       }
-    } else {
-      // ---------------- epilogue warps ----------------
-      const int et = threadIdx.x - (2 + kTcSplitWarps) * 32;  // 0..127
-      const uint32_t ng = dpad / 4;
-      for (uint32_t idx = et; idx < qmax * ng; idx += kTcEpiWarps * 32) {
-        const uint32_t n = idx / ng, g4 = idx % ng;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (n < nq) {
-          const uint32_t qi = P.pair_query[P.sorted_pairs[item.pair0 + n]];
-          v = *reinterpret_cast<const float4*>(P.qv.qs + (uint64_t)qi * dpad + g4 * 4);
-        }
-        const uint32_t ch = g4 >> 2, g = g4 & 3;
-        if (n < npad && !split) {
-          uint8_t* blk = qsm + ch * qblk;
-          *reinterpret_cast<float4*>(blk + n * 64 + ((g ^ ((n >> 1) & 3)) << 4)) = v;
-        } else if (n < npad) {
-          const int cm = P.conv;
-          const float4 lo = make_float4(v.x - tf32_conv(v.x, cm), v.y - tf32_conv(v.y, cm),
-                                        v.z - tf32_conv(v.z, cm), v.w - tf32_conv(v.w, cm));
-          uint8_t* blk = qsm + ch * qblk;
-          *reinterpret_cast<float4*>(blk + n * 64 + ((g ^ ((n >> 1) & 3)) << 4)) = v;
-          const uint32_t nl = npad + n;  // lo rows follow the npad raw rows
-          *reinterpret_cast<float4*>(blk + nl * 64 + ((g ^ ((nl >> 1) & 3)) << 4)) = lo;
-        }
-      }
-      fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-      if (et < (int)nq) {
-        const uint32_t pair = P.sorted_pairs[item.pair0 + et];
-        s_qn2[et] = P.qv.qn2[P.pair_query[pair]];
-        s_slot[et] = pair * P.ix.s_max + item.seg;
-      }
-      named_bar_sync(1, (kTcEpiWarps + kTcSplitWarps + 1) * 32);
-      const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+    }
+  } else {
+    // ---------------- epilogue warps ----------------
+    const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint32_t ew = warp - (2 + kTcSplitWarps);
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+      mbar_wait(&ifull[slot], iph);
+      if (!s_valid[slot]) break;
+      const ScanItem item = s_item[slot];
+      const uint32_t nq = item.nq;
+      const uint32_t npad = (nq + 7) & ~7u;
+      const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
+      const uint64_t lbeg = P.ix.list_off[item.list];
       float ld[32];
       uint32_t lr[32];
 #pragma unroll
@@ -424,7 +500,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           if (j >= (int)nq) break;
           const float dot = split ? __fadd_rn(__uint_as_float(acc[j]), __uint_as_float(acc2[j]))
                                   : __uint_as_float(acc[j]);
-          const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, s_qn2[j]))
+          const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, s_qn2[slot][j]))
                                 : __int_as_float(0x7f800000);
           float th = __shfl_sync(FULL, ld[j], 31);
           unsigned m = __ballot_sync(FULL, v < th);
@@ -492,53 +568,56 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           }
         }
       }
-      // cross-warp merge (the smem stages are idle: every MMA of this item retired)
-      named_bar_sync(2, kTcEpiWarps * 32);
-      float* md = reinterpret_cast<float*>(aring);
-      uint32_t* mr = reinterpret_cast<uint32_t*>(aring + kTcEpiWarps * 32 * 32 * 4);
-      const uint32_t ew = warp - (2 + kTcSplitWarps);
+      // cross-warp merge through the dedicated scratch (the MMA / producer are
+      // already on the next item), kMergeQ queries per round
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j >= (int)nq) break;
-        md[(ew * 32 + j) * 32 + lane] = ld[j];
-        mr[(ew * 32 + j) * 32 + lane] = lr[j];
-      }
-      named_bar_sync(2, kTcEpiWarps * 32);
-      for (uint32_t j = ew; j < nq; j += kTcEpiWarps) {
-        float v = md[j * 32 + lane];
-        uint32_t r = mr[j * 32 + lane];
-        for (uint32_t w2 = 1; w2 < kTcEpiWarps; ++w2) {
-          const float o = md[(w2 * 32 + j) * 32 + 31 - lane];
-          const uint32_t orr = mr[(w2 * 32 + j) * 32 + 31 - lane];
-          if (o < v || (o == v && orr < r)) {
-            v = o;
-            r = orr;
-          }
+      for (int h0 = 0; h0 < 32; h0 += kMergeQ) {
+        if (h0 >= (int)nq) break;
+        named_bar_sync(2, kTcEpiWarps * 32);  // previous round's reads are done
 #pragma unroll
-          for (int s = 16; s > 0; s >>= 1) {
-            const float pv = __shfl_xor_sync(FULL, v, s);
-            const uint32_t pr = __shfl_xor_sync(FULL, r, s);
-            const bool keep_min = (lane & s) == 0;
-            const bool p_less = (pv < v) || (pv == v && pr < r);
-            if (keep_min == p_less) {
-              v = pv;
-              r = pr;
+        for (int jj = 0; jj < kMergeQ; ++jj) {
+          if (h0 + jj >= (int)nq) break;
+          md[(ew * kMergeQ + jj) * 32 + lane] = ld[h0 + jj];
+          mr[(ew * kMergeQ + jj) * 32 + lane] = lr[h0 + jj];
+        }
+        named_bar_sync(2, kTcEpiWarps * 32);
+        for (uint32_t jj = ew; jj < kMergeQ && h0 + jj < nq; jj += kTcEpiWarps) {
+          const uint32_t j = h0 + jj;
+          float v = md[jj * 32 + lane];
+          uint32_t r = mr[jj * 32 + lane];
+          for (uint32_t w2 = 1; w2 < kTcEpiWarps; ++w2) {
+            const float o = md[(w2 * kMergeQ + jj) * 32 + 31 - lane];
+            const uint32_t orr = mr[(w2 * kMergeQ + jj) * 32 + 31 - lane];
+            if (o < v || (o == v && orr < r)) {
+              v = o;
+              r = orr;
+            }
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+              const float pv = __shfl_xor_sync(FULL, v, s);
+              const uint32_t pr = __shfl_xor_sync(FULL, r, s);
+              const bool keep_min = (lane & s) == 0;
+              const bool p_less = (pv < v) || (pv == v && pr < r);
+              if (keep_min == p_less) {
+                v = pv;
+                r = pr;
+              }
             }
           }
-        }
-        const uint32_t slot = s_slot[j];
-        P.out_d[(uint64_t)slot * kKP + lane] = v;
-        P.out_row[(uint64_t)slot * kKP + lane] = r;
-        const uint32_t n_valid = __popc(__ballot_sync(FULL, r != kNoRow));
-        const float last = __shfl_sync(FULL, v, 31);
-        if (lane == 0) {
-          P.out_thr[slot] = n_valid == kKP ? last : __int_as_float(0x7f800000);
-          P.out_n[slot] = n_valid;
+          const uint32_t oslot = s_slot[slot][j];
+          P.out_d[(uint64_t)oslot * kKP + lane] = v;
+          P.out_row[(uint64_t)oslot * kKP + lane] = r;
+          const uint32_t n_valid = __popc(__ballot_sync(FULL, r != kNoRow));
+          const float last = __shfl_sync(FULL, v, 31);
+          if (lane == 0) {
+            P.out_thr[oslot] = n_valid == kKP ? last : __int_as_float(0x7f800000);
+            P.out_n[oslot] = n_valid;
+          }
         }
       }
-      fence_proxy_async_smem();  // generic writes (merge buffers) before the next bulk copies
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&iempty[slot]);
     }
-    __syncthreads();
   }
   tc_fence_before();
   __syncthreads();
@@ -553,13 +632,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
 
 // Shared-memory plan: the unsplit query group stays resident for the whole
 // item; what is left feeds the A landing ring (bytes in flight per SM).
-static constexpr int kTcBudget = 225 * 1024;
+// Dynamic smem budget = the device's opt-in per-block maximum (227 KB on B200)
+// minus the kernel's static __shared__ variables, queried once.
+static int tc_budget() {
+  static int budget = -1;
+  if (budget < 0) {
+    int dev = 0, optin = 232448;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      optin = 232448;
+    cudaFuncAttributes fa{};
+    size_t st = 1024;
+    if (cudaFuncGetAttributes(&fa, k_scan_tc) == cudaSuccess) st = fa.sharedSizeBytes;
+    budget = optin - (int)st;
+  }
+  return budget;
+}
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
   return 1024 + (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64 +
-         8 * (2 * kTcMaxA + 2 * kTcLo + 4);
+         kTcEpiWarps * kMergeQ * 32 * 8 +                         // merge scratch
+         8 * (2 * kTcMaxA + 2 * kTcLo + 4 + 2 * kItemQ + 2) + kItemQ * 32 * 8;
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
-  const int left = kTcBudget - tc_fixed_bytes(dpad, qmax, split);
+  const int left = tc_budget() - tc_fixed_bytes(dpad, qmax, split);
   return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / kTcStageBytes);
 }
 static uint32_t g_tc_qmax_override = 0;
