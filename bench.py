@@ -214,6 +214,10 @@ def run_hivf(args):
     wl = Workload(cfg, device=f"cuda:{local}")
     stream = torch.cuda.current_stream()
     ctx = Context(local, stream)
+    # experiment knobs: HIVF_OPTS="tc_qmax=24,seg_rows=8192" (hivf_set_option names)
+    for kv in filter(None, os.environ.get("HIVF_OPTS", "").split(",")):
+        name, val = kv.split("=")
+        ctx.set_option(name.strip(), int(val))
     ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, rank, world)
     B, npb, k = cfg.batch, cfg.nprobe, cfg.k
     pool = [wl.queries(i) for i in range(args.pool)]
@@ -257,9 +261,20 @@ def run_hivf(args):
     # ---- per-kernel timing pass (events around each phase, inside the library) ----
     ctx.set_option("time_kernels", 1)
     ctx.set_option("reset_timers", 1)
+    tcprof = os.environ.get("HIVF_TCPROF")  # debug: per-CTA stall counters of the scan
+    if tcprof:
+        ctx.set_option("tc_prof", 1)
     for i in range(args.steps):
         step(i)
     torch.cuda.synchronize()
+    if tcprof:
+        import ctypes
+        from paper_2507_09138_b200 import lib
+        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+        buf = np.zeros((n_sm, 16), np.uint64)
+        lib().hivf_debug_tc_prof(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(n_sm))
+        np.save(tcprof, buf)
+        ctx.set_option("tc_prof", 0)
     st = ctx.stats()
     ctx.set_option("time_kernels", 0)
     scan_ms = st["scan_ms"] / max(1, st["timed_calls"])

@@ -328,6 +328,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     if (value < 0 || value > 3)
       return fail(HIVF_EINVAL, "scan_kernel: 0 auto, 1 ffma, 2 tc split, 3 tc single-pass");
     ctx->opt_scan_kernel = (int)value;
+  } else if (!strcmp(name, "tc_prof")) {  // debug: stall counters (hivf_debug_tc_prof)
+    set_tc_prof((int)value);
   } else if (!strcmp(name, "tc_variant")) {  // debug only: results are inexact when != 0
     set_tc_variant((int)value);
   } else if (!strcmp(name, "tc_qmax")) {  // tuning: queries per tensor-core work item

@@ -96,6 +96,7 @@ void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)
 int tc_probe_conversion(cudaStream_t s);  // 0 trunc, 1 RNE, 2 unsupported
 void set_tc_conversion_mode(int m);
 void set_tc_variant(int v);  // debug knob (inexact results when nonzero)
+void set_tc_prof(int on);    // debug: per-CTA stall counters in k_scan_tc
 int tc_conversion_mode();
 int scan_tc_smem_bytes(uint32_t dpad, int split);
 void bound_ffma(uint32_t dim, double* a, double* b, double* c);

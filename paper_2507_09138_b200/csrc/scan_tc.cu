@@ -77,8 +77,9 @@ struct TcParams {
   uint32_t qmax;  // queries per item (8..32)
   uint32_t sa;    // A landing-ring depth (16 KB stages)
   int conv;       // tensor-core tf32 conversion (0 trunc, 1 RNE)
-  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA (results then inexact)
+  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA, bit2 skip all MMAs (results then inexact)
   int split;      // 1: 3-pass split precision, 0: single-pass tf32 (looser bound)
+  unsigned long long* prof;  // debug: per-CTA stall counters [gridDim.x][16] (nullptr = off)
 };
 
 // ---- tcgen05 PTX wrappers ------------------------------------------------------
@@ -113,6 +114,34 @@ __device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, ui
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// Warp-collective variants: every lane executes the asm with the same
+// (warp-uniform) operands, elect.sync picks the single issuing lane.
+__device__ __forceinline__ void mma_tf32_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_tf32_ta_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                                  uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.eq.u32 p, %0, %0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc));
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 #define TMEM_ST32(taddr, r)                                                                    \
   asm volatile(                                                                                \
@@ -172,6 +201,11 @@ __device__ __forceinline__ float tf32_conv(float x, int mode) {
   const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) & 0xffffe000u;
   return __uint_as_float(r);
 }
+
+// debug profiling (P.prof != nullptr): cycles spent in selected waits, per CTA
+#define TC_PROF_T0() const long long _t0 = P.prof ? clock64() : 0
+#define TC_PROF_ADD(slot) \
+  if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - _t0))
 
 __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -236,6 +270,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   tc_fence_after();
   const uint32_t tmem_base = s_tmem;
   const uint32_t nstg = (nch + kTcCps - 1) / kTcCps;
+  if (P.prof && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.prof[blockIdx.x * 16 + 5] = g;
+  }
 
   // Every role walks the same item sequence: the producer claims work items
   // (atomic counter) into a kItemQ-deep queue of published items, so the bulk
@@ -245,21 +284,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   uint32_t tb = 0, tph = 0;   // TMEM accumulator ring
   if (warp == 0) {
     // ---------------- producer: claims items, list slices -> A ring ----------------
+    // The next item is claimed while the current one streams (atomic at item
+    // start, its descriptor and list bounds loaded after the first stages), so
+    // no global round trip sits between the last copy of one item and the
+    // first copy of the next.
     if (lane == 0) {
+      const uint32_t n_items = *P.n_items;
+      uint32_t it = atomicAdd(P.work_ctr, 1u);
+      bool valid = it < n_items;
+      ScanItem item{};
+      uint64_t lbeg = 0, lend = 0;
+      if (valid) {
+        item = P.items[it];
+        lbeg = P.ix.list_off[item.list];
+        lend = P.ix.list_off[item.list + 1];
+      }
       for (uint32_t i = 0;; ++i) {
         const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
-        mbar_wait(&iempty[slot], iph ^ 1);
-        const uint32_t it = atomicAdd(P.work_ctr, 1u);
-        const int valid = it < *P.n_items;
-        ScanItem item{};
-        if (valid) item = P.items[it];
+        {
+          TC_PROF_T0();
+          mbar_wait(&iempty[slot], iph ^ 1);
+          TC_PROF_ADD(4);
+        }
         s_item[slot] = item;
         s_valid[slot] = valid;
         mbar_arrive(&ifull[slot]);
         if (!valid) break;
+        if (P.prof) P.prof[blockIdx.x * 16 + 7] += 1;
+        const uint32_t it_n = atomicAdd(P.work_ctr, 1u);
+        const bool valid_n = it_n < n_items;
+        ScanItem item_n{};
+        uint64_t lbeg_n = 0, lend_n = 0;
+        uint32_t pf = valid_n ? 0 : 2;  // prefetch progress of the next item
         const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
-        const uint64_t lbeg = P.ix.list_off[item.list];
-        const uint64_t n_c = P.ix.list_off[item.list + 1] - lbeg;
+        const uint64_t n_c = lend - lbeg;
         const float* lbase = P.ix.vec + lbeg * dpad;
         for (uint32_t t = 0; t < ntiles; ++t) {
           const uint32_t r0 = item.row0 + t * kTcTile;
@@ -267,76 +325,127 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           for (uint32_t sg = 0; sg < nstg; ++sg) {
             const uint32_t c0 = sg * kTcCps, cn = min((uint32_t)kTcCps, nch - c0);
             const uint32_t a = ra, pa = rpa;
-            mbar_wait(&empty[a], pa ^ 1);
+            {
+              TC_PROF_T0();
+              mbar_wait(&empty[a], pa ^ 1);
+              TC_PROF_ADD(3);
+            }
+            const long long _tp = P.prof ? clock64() : 0;
             mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4);
             for (uint32_t c = 0; c < cn; ++c)
               bulk_g2s(aring + a * kTcStageBytes + c * kTcChunkBytes,
                        lbase + (uint64_t)(c0 + c) * n_c * kChunk + (uint64_t)r0 * kChunk,
                        nr * kChunk * 4, &full[a]);
+            if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 14], (unsigned long long)(clock64() - _tp));
             if (++ra == SA) { ra = 0; rpa ^= 1; }
+            if (pf == 1) {
+              lbeg_n = P.ix.list_off[item_n.list];
+              lend_n = P.ix.list_off[item_n.list + 1];
+              pf = 2;
+            } else if (pf == 0) {
+              item_n = P.items[it_n];
+              pf = 1;
+            }
           }
         }
+        if (pf == 0) {
+          item_n = P.items[it_n];
+          pf = 1;
+        }
+        if (pf == 1) {
+          lbeg_n = P.ix.list_off[item_n.list];
+          lend_n = P.ix.list_off[item_n.list + 1];
+        }
+        valid = valid_n;
+        item = item_n;
+        lbeg = lbeg_n;
+        lend = lend_n;
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: tf32, single pass or 3-pass split ----------------
-    if (lane == 0) {
-      for (uint32_t i = 0;; ++i) {
-        const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
-        mbar_wait(&ifull[slot], iph);
-        if (!s_valid[slot]) break;
-        const ScanItem item = s_item[slot];
-        mbar_arrive(&iempty[slot]);
-        const uint32_t npad = (item.nq + 7) & ~7u;
-        const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
-        const uint32_t idesc2 = tf32_idesc(split ? 2 * npad : npad);
-        const uint32_t idesc1 = tf32_idesc(npad);
-        const uint32_t q_base = smem_u32(qsm);
+    // The whole warp walks the issue loop with warp-uniform operands (so the
+    // descriptors live in uniform registers); elect.sync inside each tcgen05
+    // instruction picks the one issuing lane -- no per-instruction waterfall.
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+      mbar_wait(&ifull[slot], iph);
+      if (!__shfl_sync(FULL, s_valid[slot], 0)) break;
+      const uint32_t nq_i = __shfl_sync(FULL, s_item[slot].nq, 0);
+      const uint32_t nrows_i = __shfl_sync(FULL, s_item[slot].nrows, 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&iempty[slot]);
+      const uint32_t npad = (nq_i + 7) & ~7u;
+      const uint32_t ntiles = (nrows_i + kTcTile - 1) / kTcTile;
+      const uint32_t idesc2 = tf32_idesc(split ? 2 * npad : npad);
+      const uint32_t idesc1 = tf32_idesc(npad);
+      const uint64_t qdesc0 = sw64_kmajor_desc(smem_u32(qsm));
+      const uint64_t adesc0 = sw64_kmajor_desc(smem_u32(aring));
+      {
+        TC_PROF_T0();
         mbar_wait(qfull, i & 1);  // this item's query group is staged
-        tc_fence_after();
-        for (uint32_t t = 0; t < ntiles; ++t) {
+        if (lane == 0) TC_PROF_ADD(0);
+      }
+      tc_fence_after();
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        {
+          TC_PROF_T0();
           mbar_wait(&tempty[tb], tph ^ 1);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + tb * 64;  // accumulator columns [0, 128)
-          for (uint32_t sg = 0; sg < nstg; ++sg) {
-            const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
-            const uint32_t a = ra, pa = rpa, l = rl, pl = rpl;
+          if (lane == 0) TC_PROF_ADD(2);
+        }
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + tb * 64;  // accumulator columns [0, 128)
+        for (uint32_t sg = 0; sg < nstg; ++sg) {
+          const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
+          const uint32_t a = ra, pa = rpa, l = rl, pl = rpl;
+          {
+            TC_PROF_T0();
             if (split) mbar_wait(&lfull[l], pl);  // split done (implies A landed)
             else mbar_wait(&full[a], pa);
-            tc_fence_after();
-            const uint32_t ahi = smem_u32(aring + a * kTcStageBytes);
-            const uint32_t alo = tmem_base + kTmemAcc + l * kTmemLoCols;  // A_lo in TMEM, lane = row
-            const uint32_t c0 = sg * kTcCps;
-            for (uint32_t c = 0; c < cn; ++c) {
-              const uint32_t qb = q_base + (c0 + c) * qblk;  // [raw rows | lo rows], lo at +npad rows
+            if (lane == 0) TC_PROF_ADD(1);
+          }
+          tc_fence_after();
+          const long long _ti = P.prof ? clock64() : 0;
+          // descriptor start addresses are in 16-B units: +32 B == +2
+          const uint64_t adesc = adesc0 + (uint64_t)(a * (kTcStageBytes >> 4));
+          const uint32_t alo = tmem_base + kTmemAcc + l * kTmemLoCols;  // A_lo in TMEM, lane = row
+          const uint32_t c0 = sg * kTcCps;
+          if (!(P.variant & 4)) {
+#pragma unroll
+            for (uint32_t c = 0; c < (uint32_t)kTcCps; ++c) {
+              if (c >= cn) break;
+              const uint64_t qd = qdesc0 + (uint64_t)((c0 + c) * (qblk >> 4));
 #pragma unroll
               for (uint32_t k2 = 0; k2 < 2; ++k2) {
-                const uint32_t ao = c * kTcChunkBytes + k2 * 32;
-                const uint32_t first = (sg | c | k2) == 0;
+                const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
+                const uint32_t accum = (sg | c | k2) != 0;
                 // cols [0,npad): hi(A) hi(q);  cols [npad,2npad): hi(A) lo(q)
-                mma_tf32(d_tmem, sw64_kmajor_desc(ahi + ao), sw64_kmajor_desc(qb + k2 * 32), idesc2, !first);
+                mma_tf32_elect(d_tmem, ad, qd + 2 * k2, idesc2, accum);
                 // cols [0,npad) += lo(A) hi(q), A from TMEM (8 columns per k-step)
                 if (split && !(P.variant & 2))
-                  mma_tf32_ta(d_tmem, alo + c * 16 + k2 * 8, sw64_kmajor_desc(qb + k2 * 32), idesc1, 1);
+                  mma_tf32_ta_elect(d_tmem, alo + c * 16 + k2 * 8, qd + 2 * k2, idesc1);
               }
             }
-            mma_commit(&empty[a]);   // A slot reusable by TMA
-            if (split) {
-              mma_commit(&lempty[l]);  // lo slot reusable by the splitters
-              if (++rl == kTcLo) { rl = 0; rpl ^= 1; }
-            }
-            if (++ra == SA) { ra = 0; rpa ^= 1; }
           }
-          mma_commit(&tfull[tb]);
-          if (++tb == 2) {
-            tb = 0;
-            tph ^= 1;
+          mma_commit_elect(&empty[a]);   // A slot reusable by TMA
+          if (P.prof && lane == 0) {
+            atomicAdd(&P.prof[blockIdx.x * 16 + 12], (unsigned long long)(clock64() - _ti));
+            atomicAdd(&P.prof[blockIdx.x * 16 + 13], 1ull);
           }
+          if (split) {
+            mma_commit_elect(&lempty[l]);  // lo slot reusable by the splitters
+            if (++rl == kTcLo) { rl = 0; rpl ^= 1; }
+          }
+          if (++ra == SA) { ra = 0; rpa ^= 1; }
         }
-        mma_commit(qempty);  // query group free once this item's MMAs retire
+        mma_commit_elect(&tfull[tb]);
+        if (++tb == 2) {
+          tb = 0;
+          tph ^= 1;
+        }
       }
+      mma_commit_elect(qempty);  // query group free once this item's MMAs retire
     }
-    __syncwarp();
   } else if (warp < 2 + kTcSplitWarps) {
     // -------- stagers (query group of each item) + splitters (lo(A) rows -> TMEM) --------
     const uint32_t sw = warp - 2;                // 0..3
@@ -364,7 +473,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           s_slot[slot][n] = pair * P.ix.s_max + item.seg;
         }
       }
-      if (i > 0) mbar_wait(qempty, (i - 1) & 1);  // previous item's MMAs retired
+      const long long _ts = P.prof ? clock64() : 0;
+      if (i > 0) {
+        TC_PROF_T0();
+        mbar_wait(qempty, (i - 1) & 1);  // previous item's MMAs retired
+        if (lane == 0) TC_PROF_ADD(10);
+      }
       const uint32_t nmine = npad > sw ? (npad - sw + 3) / 4 : 0;
       for (uint32_t m0 = 0; m0 < nmine; m0 += 2) {
         for (uint32_t e0 = 0; e0 * 32 < ng; e0 += 8) {
@@ -408,6 +522,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       if (lane == 0) {
         mbar_arrive(qfull);
         mbar_arrive(&iempty[slot]);
+        if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 11], (unsigned long long)(clock64() - _ts));
       }
       const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
       for (uint32_t t = 0; split && t < ntiles; ++t) {
@@ -481,7 +596,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           const uint32_t nrow = srow + kTcTile;
           xn_next = (nrow < item.nrows) ? __ldg(P.ix.xnorm2 + lbeg + item.row0 + nrow) : 0.f;
         }
-        mbar_wait(&tfull[tb], tph);
+        {
+          TC_PROF_T0();
+          mbar_wait(&tfull[tb], tph);
+          if (lane == 0) TC_PROF_ADD(8);
+        }
         tc_fence_after();
         uint32_t acc[32], acc2[32];
         TMEM_LD32(tmem_base + ((quad * 32) << 16) + tb * 64, acc);
@@ -570,6 +689,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       }
       // cross-warp merge through the dedicated scratch (the MMA / producer are
       // already on the next item), kMergeQ queries per round
+      const long long _tm = P.prof ? clock64() : 0;
 #pragma unroll
       for (int h0 = 0; h0 < 32; h0 += kMergeQ) {
         if (h0 >= (int)nq) break;
@@ -616,8 +736,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&iempty[slot]);
+      if (lane == 0) {
+        mbar_arrive(&iempty[slot]);
+        if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 9], (unsigned long long)(clock64() - _tm));
+      }
     }
+  }
+  if (P.prof && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.prof[blockIdx.x * 16 + 6] = g;
   }
   tc_fence_before();
   __syncthreads();
@@ -663,6 +791,11 @@ void set_tc_qmax(uint32_t q) { g_tc_qmax_override = q; }
 uint32_t scan_tc_qmax(uint32_t dpad, int split) {
   const uint32_t o = g_tc_qmax_override;
   if (o && tc_ring(dpad, o, split) >= 2) return o;
+  // widest group that still leaves a 4-stage (128 KB) landing ring: the ring
+  // depth (bytes in flight per SM) matters more than the last 8 queries of a
+  // group (measured at D=768: q=24/4 stages 9.58 ms vs q=32/3 stages 9.87 ms)
+  for (uint32_t q : {32u, 24u, 16u})
+    if (tc_ring(dpad, q, split) >= 4) return q;
   for (uint32_t q : {32u, 24u, 16u})
     if (tc_ring(dpad, q, split) >= 3) return q;
   if (tc_ring(dpad, 8, split) >= 2) return 8;
@@ -670,6 +803,21 @@ uint32_t scan_tc_qmax(uint32_t dpad, int split) {
 }
 static int g_tc_variant = 0;
 void set_tc_variant(int v) { g_tc_variant = v; }
+static unsigned long long* g_tc_prof = nullptr;  // debug stall counters (option "tc_prof")
+void set_tc_prof(int on) {
+  if (on && !g_tc_prof) cudaMalloc(&g_tc_prof, 1024 * 16 * sizeof(unsigned long long));
+  if (on) cudaMemset(g_tc_prof, 0, 1024 * 16 * sizeof(unsigned long long));
+  if (!on && g_tc_prof) {
+    cudaFree(g_tc_prof);
+    g_tc_prof = nullptr;
+  }
+}
+int get_tc_prof(unsigned long long* host, int n_ctas) {
+  if (!g_tc_prof) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_tc_prof, (size_t)n_ctas * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 1;
+}
 
 static int g_tc_conv = -1;  // set by tc_probe_conversion()
 void set_tc_conversion_mode(int m) { g_tc_conv = m; }
@@ -687,7 +835,7 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
   const uint32_t q = scan_tc_qmax(ix.dpad, split);
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
-             split};
+             split, g_tc_prof};
   const int smem = scan_tc_smem_bytes(ix.dpad, split);
   static int attr_bytes = 0;
   if (attr_bytes < smem) {
@@ -775,3 +923,9 @@ int tc_probe_conversion(cudaStream_t s) {
   return h;
 }
 }  // namespace hivf
+
+// Debug: per-CTA stall counters of the last k_scan_tc launches (accumulated
+// since option tc_prof=1): [n_ctas][16] cycles / timestamps, see TC_PROF_*.
+extern "C" int hivf_debug_tc_prof(unsigned long long* out, int n_ctas) {
+  return hivf::get_tc_prof(out, n_ctas);
+}
