@@ -118,6 +118,12 @@ class ClockSampler:
 # distributed plumbing (torch.distributed over NCCL; one process per GPU)
 # ---------------------------------------------------------------------------
 
+# HIVF_DIST_BACKEND=gloo: functional simulation of the N-rank path on fewer GPUs
+# (ranks share devices, collectives staged through host memory).  Never used
+# for a reported number; the default and the driver's runs use NCCL.
+DIST_BACKEND = os.environ.get("HIVF_DIST_BACKEND", "nccl")
+
+
 def dist_setup(n_gpus: int):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -125,8 +131,13 @@ def dist_setup(n_gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group(DIST_BACKEND)
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -143,9 +154,21 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if DIST_BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def all_gather_parts(out, t):
+    """out[world, ...] <- every rank's t (NCCL over NVLink; host-staged for gloo)."""
+    import torch.distributed as dist
+    if DIST_BACKEND == "nccl":
+        dist.all_gather_into_tensor(out, t)
+        return
+    parts = [p.cpu() for p in out.unbind(0)]
+    dist.all_gather(parts, t.cpu())
+    for dst, src in zip(out.unbind(0), parts):
+        dst.copy_(src)
 
 
 # ---------------------------------------------------------------------------
@@ -234,9 +257,9 @@ def run_hivf(args):
     def step(i):
         ix.search_device(pool[i % len(pool)], npb, k, ids, dd, cnt)
         if world > 1:
-            dist.all_gather_into_tensor(g_ids, ids)
-            dist.all_gather_into_tensor(g_d, dd)
-            dist.all_gather_into_tensor(g_cnt, cnt)
+            all_gather_parts(g_ids, ids)
+            all_gather_parts(g_d, dd)
+            all_gather_parts(g_cnt, cnt)
             ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
 
     for i in range(args.warmup):
@@ -297,10 +320,11 @@ def run_hivf(args):
     step_gbs = float(np.mean(steps_ab)) / (ms_per_step / 1e3) / 1e9
     # ---- e2e: host buffers through the C-ABI ------------------------------------
     e2e = None
+    qh = [torch.empty(B, cfg.dim, dtype=torch.float32, pin_memory=True) for _ in pool]
+    for a, b in zip(qh, pool):
+        a.copy_(b.cpu())
     if world == 1:
-        qh = [torch.empty(B, cfg.dim, dtype=torch.float32, pin_memory=True) for _ in pool]
-        for a, b in zip(qh, pool):
-            a.copy_(b.cpu())
+        # the reference-facing C-ABI call with host buffers (hivf_search)
         qn = [a.numpy() for a in qh]
         for i in range(args.warmup):
             ix.search(qn[i % len(qn)], npb, k)
@@ -313,15 +337,51 @@ def run_hivf(args):
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         e2e_ms = max(e0.elapsed_time(e1), wall * 1e3)
-        e2e = {"value": B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": B * cfg.dim * 4,
-               "d2h_bytes_per_step": B * k * (8 + 8) + B * 4,
-               "api": "hivf_search (host buffers, pinned)"}
+        api = "hivf_search (host buffers, pinned)"
+    else:
+        # pinned host queries -> HBM, sharded search + all-gather + device merge,
+        # merged results -> host, every step inside the timed region
+        qd = torch.empty(B, cfg.dim, dtype=torch.float32, device=wl.device)
+        h_ids = torch.empty(B, k, dtype=torch.int64, pin_memory=True)
+        h_d = torch.empty(B, k, dtype=torch.float64, pin_memory=True)
+        h_c = torch.empty(B, dtype=torch.int32, pin_memory=True)
+
+        def e2e_step(i):
+            qd.copy_(qh[i % len(qh)], non_blocking=True)
+            ix.search_device(qd, npb, k, ids, dd, cnt)
+            all_gather_parts(g_ids, ids)
+            all_gather_parts(g_d, dd)
+            all_gather_parts(g_cnt, cnt)
+            ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
+            h_ids.copy_(m_ids, non_blocking=True)
+            h_d.copy_(m_d, non_blocking=True)
+            h_c.copy_(m_cnt, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for i in range(args.warmup):
+            e2e_step(i)
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for i in range(args.steps):
+            e2e_step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        wall = time.perf_counter() - t0
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3), world)
+        api = "hivf_search_device + all-gather + hivf_merge_parts_device (pinned host in/out)"
+    e2e = {"value": B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": B * cfg.dim * 4,
+           "d2h_bytes_per_step": B * k * (8 + 8) + B * 4, "api": api}
     # ---- CPU baseline + full-scale parity sample (rank 0, N=1) -------------------
     cpu = None
     parity = None
     if world == 1 and rank == 0 and not args.no_cpu:
         cpu, parity = cpu_baseline_and_parity(ix, wl, cents, pool[0], cfg, args)
+    if world > 1:
+        parity = sharded_parity(ix, wl, cents, pool[0], cfg, step, (m_ids, m_d, m_cnt), rank, world)
     if rank != 0:
         return
     clocks = clk.summary()
@@ -369,6 +429,46 @@ def _ref_restricted_index(rows_by_list, cents, k_clusters):
     # index_from_assignments keeps corpus order inside a list: order rows by doc id
     o = np.argsort(ids, kind="stable")
     return oracle.RefIndex.from_assignments(corpus[o], ids[o], cents, assign[o], 0)
+
+
+def sharded_parity(ix, wl, cents, q0, cfg, step, merged, rank, world, S=4):
+    """N>1: every rank runs the reference (oracle/_ref) on its own shard for S
+    sample queries (exact local top-k), rank 0 folds the parts with the
+    reference's merge_topk and compares with the GPU result of the full
+    sharded step (local scan -> all-gather -> device merge)."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    if not oracle.ref_available():
+        return None
+    Q = q0[:S].cpu().numpy()
+    plans = ix.select_clusters(Q, cfg.nprobe)
+    sizes = ix.cluster_sizes()
+    off = np.zeros(len(sizes) + 1, np.uint64)
+    off[1:] = np.cumsum(sizes)
+    rows_by_list = {}
+    for c in np.unique(plans):
+        if sizes[c]:
+            rows_by_list[int(c)] = ix.get_rows(int(off[c]), int(sizes[c]))
+    ri = _ref_restricted_index(rows_by_list, cents.cpu().numpy(), cfg.k_clusters)
+    oi, od, oc = ri.search(Q, cfg.nprobe, cfg.k)
+    local = [[(int(oi[b, j]), float(od[b, j])) for j in range(int(oc[b]))] for b in range(S)]
+    parts = [None] * world
+    dist.all_gather_object(parts, local)
+    step(0)  # pool[0] through the sharded GPU path
+    torch.cuda.synchronize()
+    gi, gd, gc = (t[:S].cpu().numpy() for t in merged)
+    exact = True
+    for b in range(S):
+        ref = []
+        for r in range(world):
+            ref = oracle.merge_topk(ref, parts[r][b], cfg.k)
+        got = [(int(gi[b, j]), float(gd[b, j])) for j in range(int(gc[b]))]
+        exact &= [(i, np.float64(d).view(np.uint64)) for i, d in ref] == \
+                 [(i, np.float64(d).view(np.uint64)) for i, d in got]
+    return {"queries": S, "bit_exact_vs_reference": bool(exact), "nprobe": cfg.nprobe, "k": cfg.k,
+            "method": f"reference search per shard ({world} shards) + merge_topk vs GPU "
+                      "all-gather + device merge"}
 
 
 def cpu_baseline_and_parity(ix, wl, cents, q0, cfg, args):
@@ -515,7 +615,10 @@ def main():
         run_reference(args)
     else:
         import torch
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if DIST_BACKEND != "nccl":
+            local %= torch.cuda.device_count()
+        torch.cuda.set_device(local)
         with torch.cuda.stream(torch.cuda.Stream()):  # one explicit stream for torch + hivf
             run_hivf(args)
 
