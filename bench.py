@@ -244,29 +244,51 @@ def run_hivf(args):
     ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, rank, world)
     B, npb, k = cfg.batch, cfg.nprobe, cfg.k
     pool = [wl.queries(i) for i in range(args.pool)]
-    ids = torch.empty(B, k, dtype=torch.int64, device=wl.device)
-    dd = torch.empty(B, k, dtype=torch.float64, device=wl.device)
-    cnt = torch.empty(B, dtype=torch.int32, device=wl.device)
+    # one packed result buffer per rank (ids | dists | counts) so the shard
+    # exchange is a single all-gather
+    Bk = B * k
+    packed = torch.empty(2 * Bk + (B + 1) // 2, dtype=torch.int64, device=wl.device)
+    ids = packed[:Bk].view(B, k)
+    dd = packed[Bk:2 * Bk].view(torch.float64).view(B, k)
+    cnt = packed[2 * Bk:].view(torch.int32)[:B]
+    split_assign = world > 1 and B % world == 0
     if world > 1:
+        g_packed = torch.empty(world, packed.numel(), dtype=torch.int64, device=wl.device)
         g_ids = torch.empty(world, B, k, dtype=torch.int64, device=wl.device)
         g_d = torch.empty(world, B, k, dtype=torch.float64, device=wl.device)
         g_cnt = torch.empty(world, B, dtype=torch.int32, device=wl.device)
         m_ids, m_d, m_cnt = torch.empty_like(ids), torch.empty_like(dd), torch.empty_like(cnt)
+        bs = B // world
+        plans_loc = torch.empty(bs, npb, dtype=torch.int32, device=wl.device)
+        plans_all = torch.empty(world, bs, npb, dtype=torch.int32, device=wl.device)
     import torch.distributed as dist
 
     def step(i):
-        ix.search_device(pool[i % len(pool)], npb, k, ids, dd, cnt)
-        if world > 1:
-            all_gather_parts(g_ids, ids)
-            all_gather_parts(g_d, dd)
-            all_gather_parts(g_cnt, cnt)
-            ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
+        q = pool[i % len(pool)]
+        if world == 1:
+            ix.search_device(q, npb, k, ids, dd, cnt)
+            return
+        if split_assign:
+            # coarse assign split across ranks (each assigns B/N queries, the plans
+            # are identical to a full assign), plans all-gathered
+            ix.assign_device(q[rank * bs:(rank + 1) * bs], npb, plans_loc)
+            all_gather_parts(plans_all, plans_loc)
+            ix.search_planned_device(q, npb, k, plans_all.view(B, npb), ids, dd, cnt)
+        else:
+            ix.search_device(q, npb, k, ids, dd, cnt)
+        all_gather_parts(g_packed, packed)
+        g_ids.copy_(g_packed[:, :Bk].view(world, B, k))
+        g_d.copy_(g_packed[:, Bk:2 * Bk].view(torch.float64).view(world, B, k))
+        g_cnt.copy_(g_packed[:, 2 * Bk:].view(torch.int32)[:, :B])
+        ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
     st = ctx.stats()
-    kernels_per_step = st["kernels_launched"] + (1 if world > 1 else 0)
+    # our kernels per step: the search call's (stats of the last call) plus, at
+    # N>1, the merge and (split assign) the hivf_assign_device kernels
+    kernels_per_step = st["kernels_launched"] + (1 if world > 1 else 0) + (4 if split_assign else 0)
     # ---- timed region (value) ----------------------------------------------------
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -348,11 +370,12 @@ def run_hivf(args):
 
         def e2e_step(i):
             qd.copy_(qh[i % len(qh)], non_blocking=True)
-            ix.search_device(qd, npb, k, ids, dd, cnt)
-            all_gather_parts(g_ids, ids)
-            all_gather_parts(g_d, dd)
-            all_gather_parts(g_cnt, cnt)
-            ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
+            saved = pool[0]
+            pool[0] = qd
+            try:
+                step(0)
+            finally:
+                pool[0] = saved
             h_ids.copy_(m_ids, non_blocking=True)
             h_d.copy_(m_d, non_blocking=True)
             h_c.copy_(m_cnt, non_blocking=True)
@@ -371,7 +394,8 @@ def run_hivf(args):
         barrier(world)
         wall = time.perf_counter() - t0
         e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3), world)
-        api = "hivf_search_device + all-gather + hivf_merge_parts_device (pinned host in/out)"
+        api = ("hivf_assign_device (B/N per rank) + plan all-gather + hivf_search_planned_device"
+               " + result all-gather + hivf_merge_parts_device (pinned host in/out)")
     e2e = {"value": B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": B * cfg.dim * 4,
            "d2h_bytes_per_step": B * k * (8 + 8) + B * 4, "api": api}

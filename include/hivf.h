@@ -140,6 +140,20 @@ hivf_status hivf_search_device(hivf_index* idx, const float* d_queries, uint32_t
                                uint32_t nprobe, uint32_t k, uint64_t* d_ids_out,
                                double* d_dists_out, uint32_t* d_counts_out);
 
+/* Split form of the same call for multi-GPU list sharding:
+ * hivf_assign_device is ivf::select_clusters for a batch (plans in HBM, the
+ * same exact order as hivf_assign; each rank may assign a slice of the batch
+ * and all-gather the plans), and hivf_search_planned_device runs the search
+ * with those plans -- make_cursor with a given plan + search_step over it
+ * (proj/src/vector_index.cpp:280-289,319-328).  Plan ids >= n_clusters are
+ * replaced by 0 and reported as EINVAL by the host-buffer calls. */
+hivf_status hivf_assign_device(hivf_index* idx, const float* d_queries, uint32_t n_queries,
+                               uint32_t nprobe, uint32_t* d_plans_out, double* d_dists_out);
+hivf_status hivf_search_planned_device(hivf_index* idx, const float* d_queries, uint32_t n_queries,
+                                       uint32_t nprobe, uint32_t k, const uint32_t* d_plans,
+                                       uint64_t* d_ids_out, double* d_dists_out,
+                                       uint32_t* d_counts_out);
+
 /* ---- node-split sub-search --------------------------------------------------
  * Many cursors advanced by one sub-stage: ivf::search_clusters
  * (proj/src/vector_index.cpp:291-317) for every item of a SubStageBatch, as

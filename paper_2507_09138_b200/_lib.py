@@ -21,7 +21,8 @@ SYMBOLS = [
     "hivf_index_upload_device", "hivf_index_begin", "hivf_index_add_rows_device",
     "hivf_index_add_rows_at_device", "hivf_index_finish", "hivf_index_get_rows",
     "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
-    "hivf_assign", "hivf_search", "hivf_search_device", "hivf_scan_items",
+    "hivf_assign", "hivf_search", "hivf_search_device", "hivf_assign_device",
+    "hivf_search_planned_device", "hivf_scan_items",
     "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get", "hivf_last_stats",
     "hivf_set_option",
 ]
@@ -83,6 +84,8 @@ def lib():
         "hivf_assign": (i32, [vp, vp, u32, u32, vp, vp]),
         "hivf_search": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
         "hivf_search_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
+        "hivf_assign_device": (i32, [vp, vp, u32, u32, vp, vp]),
+        "hivf_search_planned_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp, vp]),
         "hivf_scan_items": (i32, [vp, vp, u32, vp, vp, vp, vp, vp, vp, u32, vp]),
         "hivf_merge_parts_device": (i32, [vp, u32, u32, u32, vp, vp, vp, vp, vp, vp]),
         "hivf_residency_set": (i32, [vp, vp, u32]),

@@ -673,6 +673,7 @@ static hivf_status prep_queries(hivf_index* ix, const float* d_q, uint32_t n, bo
   launch_prep_queries(d_q, n, ix->dim, ix->dpad, ix->metric, normalize, c->qs.as<float>(),
                       c->qn2.as<float>(), c->qnorm.as<float>(), c->err.as<int>(), c->stream);
   CKL();
+  c->stats.kernels_launched += 1;
   qv->qs = c->qs.as<float>();
   qv->qn2 = c->qn2.as<float>();
   qv->qnorm = c->qnorm.as<float>();
@@ -754,8 +755,10 @@ static hivf_status check_search_args(hivf_index* ix, uint32_t n, uint32_t nprobe
   return HIVF_OK;
 }
 
-hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t n,
-                               uint32_t nprobe, uint32_t k, uint64_t* d_ids_out,
+// Batched search; d_plans == nullptr runs the coarse assign, otherwise the
+// caller's select_clusters plans are used (validated on device).
+static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t n, uint32_t nprobe,
+                               uint32_t k, const uint32_t* d_plans, uint64_t* d_ids_out,
                                double* d_dists_out, uint32_t* d_counts_out) {
   hivf_status st = check_search_args(ix, n, nprobe, k);
   if (st != HIVF_OK) return st;
@@ -771,8 +774,14 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
   QueryView qv;
   c->mark(0);
   if ((st = prep_queries(ix, d_queries, n, true, &qv)) != HIVF_OK) return st;
-  if ((st = run_assign(ix, qv, nprobe, nullptr)) != HIVF_OK) return st;
   const uint32_t np = n * nprobe;
+  if (!d_plans) {
+    if ((st = run_assign(ix, qv, nprobe, nullptr)) != HIVF_OK) return st;
+  } else {
+    CK(c->plans.ensure((size_t)np * 4));
+    CK(c->flags_c.ensure((size_t)n * 4));  // no coarse fallback in a planned search
+    CK(cudaMemsetAsync(c->flags_c.p, 0, (size_t)n * 4, c->stream));
+  }
   CK(c->pq.ensure((size_t)np * 4));
   CK(c->pl.ensure((size_t)np * 4));
   CK(c->flags_f.ensure((size_t)n * 4));
@@ -785,9 +794,13 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
     CK(c->x_cnt.ensure(parts * 4));
     CK(c->x_tot.ensure(parts * 8));
   }
-  if (!exact_only) {
-    launch_plans_to_pairs(c->plans.as<uint32_t>(), n, nprobe, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), c->stream);
+  if (d_plans || !exact_only) {
+    launch_plans_to_pairs(d_plans ? d_plans : c->plans.as<uint32_t>(), n, nprobe, ix->K, c->pq.as<uint32_t>(),
+                          c->pl.as<uint32_t>(), d_plans ? c->plans.as<uint32_t>() : nullptr,
+                          c->err.as<int>(), c->stream);
     CKL();
+  }
+  if (!exact_only) {
     if ((st = run_scan(ix, qv, np, true)) != HIVF_OK) return st;
     c->mark(2);
     launch_finalize_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(),
@@ -811,6 +824,37 @@ hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t 
     c->stats.kernels_launched += 1;
     c->mark(3);
   }
+  return HIVF_OK;
+}
+
+hivf_status hivf_search_device(hivf_index* ix, const float* d_queries, uint32_t n,
+                               uint32_t nprobe, uint32_t k, uint64_t* d_ids_out,
+                               double* d_dists_out, uint32_t* d_counts_out) {
+  return search_impl(ix, d_queries, n, nprobe, k, nullptr, d_ids_out, d_dists_out, d_counts_out);
+}
+
+hivf_status hivf_search_planned_device(hivf_index* ix, const float* d_queries, uint32_t n,
+                                       uint32_t nprobe, uint32_t k, const uint32_t* d_plans,
+                                       uint64_t* d_ids_out, double* d_dists_out,
+                                       uint32_t* d_counts_out) {
+  if (!d_plans) return fail(HIVF_EINVAL, "hivf_search_planned_device: plans NULL");
+  return search_impl(ix, d_queries, n, nprobe, k, d_plans, d_ids_out, d_dists_out, d_counts_out);
+}
+
+hivf_status hivf_assign_device(hivf_index* ix, const float* d_queries, uint32_t n, uint32_t nprobe,
+                               uint32_t* d_plans_out, double* d_dists_out) {
+  hivf_status st = check_search_args(ix, n, nprobe, 1);
+  if (st != HIVF_OK) return st;
+  if (n == 0) return HIVF_OK;
+  if (!d_queries || !d_plans_out) return fail(HIVF_EINVAL, "hivf_assign_device: NULL buffer");
+  hivf_ctx* c = ix->ctx;
+  CK(cudaSetDevice(c->device));
+  c->stats = hivf_stats{};
+  c->last_nq = 0;
+  QueryView qv;
+  if ((st = prep_queries(ix, d_queries, n, true, &qv)) != HIVF_OK) return st;
+  if ((st = run_assign(ix, qv, nprobe, d_dists_out)) != HIVF_OK) return st;
+  CK(cudaMemcpyAsync(d_plans_out, c->plans.p, (size_t)n * nprobe * 4, cudaMemcpyDeviceToDevice, c->stream));
   return HIVF_OK;
 }
 

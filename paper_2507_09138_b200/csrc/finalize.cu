@@ -393,12 +393,20 @@ __global__ void __launch_bounds__(256) k_exact_merge(uint32_t nsplit, uint32_t k
   if (threadIdx.x == 0) counts_out[b] = cnt;
 }
 
-__global__ void k_plans_to_pairs(const uint32_t* plans, uint32_t n, uint32_t nprobe, uint32_t* pq,
-                                 uint32_t* pl) {
+// (query, list) pairs of the plans.  Caller-supplied plans (planned search)
+// are validated: an id >= K is replaced by 0 in the working copy and flags err.
+__global__ void k_plans_to_pairs(const uint32_t* plans, uint32_t n, uint32_t nprobe, uint32_t K,
+                                 uint32_t* pq, uint32_t* pl, uint32_t* plans_out, int* err) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n * nprobe) return;
+  uint32_t c = plans[p];
+  if (c >= K) {
+    c = 0;
+    if (err) atomicOr(err, 2);
+  }
   pq[p] = p / nprobe;
-  pl[p] = plans[p];
+  pl[p] = c;
+  if (plans_out) plans_out[p] = c;
 }
 
 // merge_topk (vector_index.cpp:71-91) over n_parts exact per-shard lists.
@@ -442,11 +450,13 @@ __global__ void k_merge_parts(uint32_t n_parts, uint32_t nq, uint32_t k, const u
 
 }  // namespace
 
-void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe,
-                           uint32_t* pair_query, uint32_t* pair_list, cudaStream_t s) {
+void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe, uint32_t K,
+                           uint32_t* pair_query, uint32_t* pair_list, uint32_t* plans_out, int* err,
+                           cudaStream_t s) {
   const uint32_t n = n_queries * nprobe;
   if (!n) return;
-  k_plans_to_pairs<<<(n + 255) / 256, 256, 0, s>>>(plans, n_queries, nprobe, pair_query, pair_list);
+  k_plans_to_pairs<<<(n + 255) / 256, 256, 0, s>>>(plans, n_queries, nprobe, K, pair_query, pair_list,
+                                                    plans_out, err);
 }
 
 void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,

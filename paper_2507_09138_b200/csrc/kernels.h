@@ -104,8 +104,9 @@ void bound_tc(uint32_t dim, double* a, double* b, double* c);   // 3-pass split
 void bound_tc1(uint32_t dim, double* a, double* b, double* c);  // single pass
 
 // ---- finalize.cu
-void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe,
-                           uint32_t* pair_query, uint32_t* pair_list, cudaStream_t s);
+void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe, uint32_t K,
+                           uint32_t* pair_query, uint32_t* pair_list, uint32_t* plans_out, int* err,
+                           cudaStream_t s);
 void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
                             uint32_t nprobe, uint32_t k, const float* cand_d,
                             const uint32_t* cand_row, const float* cand_thr,

@@ -237,6 +237,21 @@ class IvfIndex:
                                        ids_out.data_ptr(), dists_out.data_ptr(),
                                        counts_out.data_ptr()))
 
+    def assign_device(self, d_queries, nprobe, plans_out, dists_out=None):
+        """select_clusters for a batch of HBM-resident queries (plans_out: int32
+        [B, nprobe] tensor on the device), async on the context stream."""
+        B = d_queries.shape[0]
+        check(lib().hivf_assign_device(self.h, d_queries.data_ptr(), B, nprobe, plans_out.data_ptr(),
+                                       dists_out.data_ptr() if dists_out is not None else None))
+
+    def search_planned_device(self, d_queries, nprobe, k, plans, ids_out, dists_out, counts_out):
+        """search_device with caller-supplied plans (e.g. all-gathered from the
+        ranks that assigned slices of the batch)."""
+        B = d_queries.shape[0]
+        check(lib().hivf_search_planned_device(self.h, d_queries.data_ptr(), B, nprobe, k,
+                                               plans.data_ptr(), ids_out.data_ptr(),
+                                               dists_out.data_ptr(), counts_out.data_ptr()))
+
     def scan_items(self, queries, cluster_off, clusters, k, heap_ids, heap_dists, heap_counts):
         """search_clusters for many cursors (vector_index.cpp:291-317); heaps
         updated in place; returns per-cluster changed flags."""
