@@ -545,6 +545,70 @@ def cpu_baseline_and_parity(ix, wl, cents, q0, cfg, args):
 # reference arm
 # ---------------------------------------------------------------------------
 
+def run_c5(args):
+    """BASELINE.json configs[4]: heterogeneous node-split retrieval stream,
+    p50/p99 latency per concurrency level, both arms on the same batches
+    (bench_c5.py).  Single GPU; rank 0 only."""
+    import torch
+    import oracle
+    import bench_c5 as c5
+    from bench_workload import CONFIGS, Workload
+    from paper_2507_09138_b200 import Context
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    cfg = CONFIGS["c2"]  # the stream runs on the C2 index (1M x 768, IVF-1024, nprobe 32)
+    torch.cuda.set_device(0)
+    wl = Workload(cfg, device="cuda:0")
+    ctx = Context(0, torch.cuda.current_stream())  # same stream as the torch-built inputs
+    ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, 0, 1)
+    k = max(cfg.k, c5.K_CACHE)
+    Qpool = torch.cat([wl.queries(1000 + i) for i in range(8)]).cpu().numpy()
+    budget = int(64 * sizes.mean())  # ~64 lists of rows per sub-stage
+    levels = [int(x) for x in os.environ.get("HIVF_C5_LEVELS", "1,8,64,256,512").split(",")]
+    ref_ix = None
+    if oracle.ref_available() and not args.no_cpu:
+        t0 = time.time()
+        loff = np.zeros(len(sizes) + 1, np.uint64)
+        loff[1:] = np.cumsum(ix.cluster_sizes())
+        rows_by_list = {int(c): ix.get_rows(int(loff[c]), int(loff[c + 1] - loff[c]))
+                        for c in range(cfg.k_clusters) if loff[c + 1] > loff[c]}
+        ref_ix = _ref_restricted_index(rows_by_list, cents.cpu().numpy(), cfg.k_clusters)
+        del rows_by_list
+        log(f"c5: reference index in {time.time() - t0:.1f}s")
+    table = []
+    exact_all = True
+    for C in levels:
+        n_req = max(16, 2 * C)
+        gpu = c5.run_stream(c5.GpuArm(ix, cfg.nprobe, k), Qpool, sizes, C, min(8, n_req), budget)
+        gpu = c5.run_stream(c5.GpuArm(ix, cfg.nprobe, k), Qpool, sizes, C, n_req, budget)
+        row = {"concurrency": C, "requests": n_req, "hivf": c5.summarize(gpu)}
+        if ref_ix is not None:
+            ref = c5.run_stream(c5.RefArm(ref_ix, cfg.nprobe, k), Qpool, sizes, C, n_req, budget)
+            row["reference"] = c5.summarize(ref)
+            row["bit_exact"] = c5.same_results(gpu, ref)
+            exact_all &= row["bit_exact"]
+        table.append(row)
+        log(f"c5: C={C}: {json.dumps(row)}")
+    head = max(table, key=lambda r: r["concurrency"])
+    line = {
+        "metric": "node-split retrieval stream: p99 stage search latency (configs[4])",
+        "value": head["hivf"]["stage_ms"]["p99"], "unit": "ms", "higher_is_better": False,
+        "n_gpus": 1, "dtype": "f32+f64",
+        "data": "synthetic gaussian mixture (bench_workload.py c2 index), closed-loop "
+                "workflow stream (bench_c5.py)",
+        "config": {"workload": "C5 node-split stream on 1Mx768 IVF-1024 nprobe=32, "
+                               f"heap k={k}, sub-stage budget {budget} rows, "
+                               f"concurrency {levels}",
+                   "mix": "one-shot 0.4 / HyDE 0.2 / iterative(3 stages) 0.4"},
+        "levels": table,
+        "parity": {"bit_exact_vs_reference_all_stages": exact_all if ref_ix is not None else None},
+        "api": "hivf_select_clusters (make_cursor) + hivf_scan_items per sub-stage, host buffers",
+        "reference_arm": "oracle/_ref RetrievalEngine::execute(live_math=true), "
+                         f"{os.cpu_count()} host threads" if ref_ix is not None else None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """The reference's own CPU implementation (oracle/_ref), rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
@@ -635,7 +699,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.config == "c5":
+        run_c5(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         import torch

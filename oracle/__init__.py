@@ -382,3 +382,62 @@ def ref_train_kmeans(corpus, k_clusters, iters, seed):
                               out) != 0:
         raise ValueError("train_kmeans: invalid argument")
     return out
+
+
+class RefEngine:
+    """ret::RetrievalEngine (retrieval_engine.hpp:80-110) built by the reference's
+    own code over a RefIndex; used as the CPU arm of the node-split stream bench
+    (config 5) and its parity check."""
+
+    def __init__(self, index: "RefIndex", per_vector_ns=1.0, fast_speedup=8.0, fixed_call_us=0.0,
+                 capacity_gc=0, update_interval=50, bw_gb_s=16.0, decay=0.5, min_fast=2):
+        self.index = index  # keeps the IvfIndex alive (the engine borrows it)
+        self.h = ref().ref_engine_new(index.h, per_vector_ns, fast_speedup, fixed_call_us,
+                                      capacity_gc, update_interval, bw_gb_s, decay, min_fast)
+
+    def __del__(self):
+        try:
+            if self.h:
+                ref().ref_engine_free(self.h)
+        except Exception:
+            pass
+
+    def submit(self, req, node, query, nprobe, k):
+        """make_cursor + submit (scheduler.cpp:920-944); returns the plan."""
+        if ref().ref_engine_submit(self.h, req, node, _f32(query), nprobe, k, None, None, 0,
+                                   None) != 0:
+            raise ValueError("submit failed")
+        plan = np.zeros(nprobe, np.uint32)
+        n = C.c_uint32()
+        ref().ref_engine_plan(self.h, req, node, plan, C.byref(n))
+        return plan[: n.value]
+
+    def execute(self, reqs, nodes, item_off, clusters, live=True):
+        """One SubStageBatch; returns (heap_changed, completed) per item."""
+        n = len(reqs)
+        hc = np.zeros(max(1, n), np.uint8)
+        done = np.zeros(max(1, n), np.uint8)
+        wall, mod = C.c_double(), C.c_double()
+        fa, sl = C.c_uint64(), C.c_uint64()
+        rc = ref().ref_engine_execute(self.h, n, np.ascontiguousarray(reqs, np.int64),
+                                      np.ascontiguousarray(nodes, np.int32),
+                                      np.ascontiguousarray(item_off, np.uint32),
+                                      np.ascontiguousarray(clusters, np.uint32), 0.0,
+                                      1 if live else 0, hc, done, C.byref(wall), C.byref(mod),
+                                      C.byref(fa), C.byref(sl))
+        if rc != 0:
+            raise RuntimeError("execute failed")
+        return hc[:n].astype(bool), done[:n].astype(bool)
+
+    def heap(self, req, node, cap=64):
+        ids = np.zeros(cap, np.uint64)
+        d = np.zeros(cap, np.float64)
+        n = C.c_uint32()
+        st, npos, srch = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        if ref().ref_engine_heap(self.h, req, node, ids, d, cap, C.byref(n), C.byref(st),
+                                 C.byref(npos), C.byref(srch)) != 0:
+            raise KeyError((req, node))
+        return ids[: n.value], d[: n.value], int(st.value)
+
+    def extract(self, req, node):
+        ref().ref_engine_extract(self.h, req, node)

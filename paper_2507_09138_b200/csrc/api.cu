@@ -1018,8 +1018,16 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
   if (n_pairs) CK(cudaMemcpyAsync(changed_out, c->changed.p, n_pairs, cudaMemcpyDeviceToHost, s));
   int err = 0;
   CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, s));
+  // auto policy (adapt_scan): items whose filter proof failed took the exact path
+  std::vector<int> fb(!exact_only && n_pairs && c->opt_scan_kernel == 0 && !ix->auto_split ? n_items : 0);
+  if (!fb.empty()) CK(cudaMemcpyAsync(fb.data(), c->flags_f.p, 4ull * n_items, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (err) return fail(HIVF_EINVAL, "hivf_scan_items: non-finite query value");
+  if (!fb.empty()) {
+    uint32_t nf = 0;
+    for (int v : fb) nf += v != 0;
+    adapt_scan(ix, n_items, nf);
+  }
   return HIVF_OK;
 }
 

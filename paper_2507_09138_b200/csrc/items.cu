@@ -252,14 +252,25 @@ __global__ void __launch_bounds__(256) k_exact_items(IndexView ix, QueryView qv,
         });
         ti[threadIdx.x] = ix.ids[r];
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
+      // Only rows that beat the heap's current worst can change it (the worst
+      // only improves while this round is replayed, and a duplicate id already
+      // in a full heap has distance <= worst): a block-wide prefilter against
+      // the worst at the start of the round leaves the serial replay a handful
+      // of rows instead of 256.
+      const uint32_t lim = (uint32_t)min((uint64_t)blockDim.x, end - r0);
+      bool cand = false;
+      if (threadIdx.x < lim) {
+        const uint32_t n0 = s_n;
+        cand = n0 < k || pair_less(td[threadIdx.x], ti[threadIdx.x], hd[n0 - 1], hi[n0 - 1]);
+      }
+      const int any = __syncthreads_or(cand);
+      if (any && threadIdx.x == 0) {
         uint32_t n = s_n;
-        const uint32_t lim = (uint32_t)min((uint64_t)blockDim.x, end - r0);
         for (uint32_t t = 0; t < lim; ++t) {
           const double d = td[t];
           const uint64_t id = ti[t];
           if (k == 0) break;
+          if (n >= k && !pair_less(d, id, hd[n - 1], hi[n - 1])) continue;
           // TopKResult::insert
           bool skip = false;
           for (uint32_t i = 0; i < n; ++i) {
