@@ -216,6 +216,7 @@ def build_shard(wl, ctx, rank, world):
                 yield p, rows, ids
 
     t1 = time.time()
+    torch.cuda.empty_cache()  # k-means / assignment temporaries -> back to the driver for the lists
     ix = IvfIndex.build_scatter(ctx, cents, my_off.cpu().numpy().astype(np.uint64), 0,
                                 int(my_off[-1].item()), chunks())
     log(f"rank {rank}: packed {int(my_off[-1].item())} rows into HBM in {time.time() - t1:.1f}s")
@@ -241,7 +242,10 @@ def run_hivf(args):
     for kv in filter(None, os.environ.get("HIVF_OPTS", "").split(",")):
         name, val = kv.split("=")
         ctx.set_option(name.strip(), int(val))
-    ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, rank, world)
+    # --shard R/N: single-GPU measurement of rank R's shard of an N-GPU job (the
+    # local search only; the all-gather + merge of the real N-GPU step is not run)
+    shard_r, shard_n = (int(x) for x in args.shard.split("/")) if args.shard else (rank, world)
+    ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, shard_r, shard_n)
     B, npb, k = cfg.batch, cfg.nprobe, cfg.k
     pool = [wl.queries(i) for i in range(args.pool)]
     # one packed result buffer per rank (ids | dists | counts) so the shard
@@ -327,7 +331,7 @@ def run_hivf(args):
     fin_ms = st["finalize_ms"] / max(1, st["timed_calls"])
     # algorithmic bytes of the steps (distinct lists per batch)
     plans = [ix.select_clusters(q.cpu().numpy(), npb) for q in pool]
-    my_sizes = np.where(owner == rank, sizes, 0)
+    my_sizes = np.where(owner == shard_r, sizes, 0)
     lb = [list_bytes(p, my_sizes, cfg.dim) for p in plans]
     ab = [algorithmic_bytes(p, my_sizes, cfg.dim, cfg.k_clusters) for p in plans]
     steps_lb = [lb[i % len(pool)] for i in range(args.steps)]
@@ -416,7 +420,11 @@ def run_hivf(args):
         "data": "synthetic gaussian mixture (bench_workload.py), generated on device",
         "config": {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
                    "k_clusters": cfg.k_clusters, "nprobe": npb, "k": k, "batch": B,
-                   "query_pool_batches": len(pool), "parallelism": f"list-sharded x{world}",
+                   "query_pool_batches": len(pool),
+                   "parallelism": (f"list-sharded x{world}" if not args.shard else
+                                   f"one GPU running list shard {shard_r} of {shard_n} (local search "
+                                   f"only: value = this shard's queries/s)"),
+                   "zipf": cfg.zipf,
                    "probes_per_probed_list": probes_per_list,
                    "l2": "index (%.1f GB) >> 126 MB L2: no flush needed" % (
                        cfg.n * cfg.dim * 4 / 1e9)},
@@ -696,6 +704,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", default="", help="R/N: measure rank R's list shard of an N-GPU job on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -138,6 +138,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same, for waiters off the critical path: the suspend-time hint lets the
+// hardware park the warp until the phase completes (or ~the hint elapses)
+// instead of re-issuing try_wait, so spinning consumers do not steal issue
+// slots from the producer / MMA warps sharing their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITP_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITP_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
 // 1-D bulk async copy global -> shared, completion reported as tx bytes on bar.
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                          uint64_t* bar) {

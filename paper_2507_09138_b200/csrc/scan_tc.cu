@@ -77,7 +77,7 @@ struct TcParams {
   uint32_t qmax;  // queries per item (8..32)
   uint32_t sa;    // A landing-ring depth (16 KB stages)
   int conv;       // tensor-core tf32 conversion (0 trunc, 1 RNE)
-  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA, bit2 skip all MMAs (results then inexact)
+  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA, bit2 skip all MMAs, bit3 skip odd k-steps (results then inexact), bit4 spin-wait epilogue
   int split;      // 1: 3-pass split precision, 0: single-pass tf32 (looser bound)
   unsigned long long* prof;  // debug: per-CTA stall counters [gridDim.x][16] (nullptr = off)
 };
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
                 const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
                 const uint32_t accum = (sg | c | k2) != 0;
                 // cols [0,npad): hi(A) hi(q);  cols [npad,2npad): hi(A) lo(q)
-                mma_tf32_elect(d_tmem, ad, qd + 2 * k2, idesc2, accum);
+                if (!(P.variant & 8) || k2 == 0) mma_tf32_elect(d_tmem, ad, qd + 2 * k2, idesc2, accum);
                 // cols [0,npad) += lo(A) hi(q), A from TMEM (8 columns per k-step)
                 if (split && !(P.variant & 2))
                   mma_tf32_ta_elect(d_tmem, alo + c * 16 + k2 * 8, qd + 2 * k2, idesc1);
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
     const uint32_t ng = dpad / 4;                // float4 groups per query row
     for (uint32_t i = 0;; ++i) {
       const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
-      mbar_wait(&ifull[slot], iph);
+      mbar_wait_parked(&ifull[slot], iph);
       if (!s_valid[slot]) break;
       const ScanItem item = s_item[slot];
       const uint32_t nq = item.nq;
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       const long long _ts = P.prof ? clock64() : 0;
       if (i > 0) {
         TC_PROF_T0();
-        mbar_wait(qempty, (i - 1) & 1);  // previous item's MMAs retired
+        mbar_wait_parked(qempty, (i - 1) & 1);  // previous item's MMAs retired
         if (lane == 0) TC_PROF_ADD(10);
       }
       const uint32_t nmine = npad > sw ? (npad - sw + 3) / 4 : 0;
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
     const uint32_t ew = warp - (2 + kTcSplitWarps);
     for (uint32_t i = 0;; ++i) {
       const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
-      mbar_wait(&ifull[slot], iph);
+      mbar_wait_parked(&ifull[slot], iph);
       if (!s_valid[slot]) break;
       const ScanItem item = s_item[slot];
       const uint32_t nq = item.nq;
@@ -598,7 +598,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         }
         {
           TC_PROF_T0();
-          mbar_wait(&tfull[tb], tph);
+          if (P.variant & 16) mbar_wait(&tfull[tb], tph);
+          else mbar_wait_parked(&tfull[tb], tph);
           if (lane == 0) TC_PROF_ADD(8);
         }
         tc_fence_after();
