@@ -114,6 +114,25 @@ hivf_status hivf_index_info(const hivf_index* idx, uint32_t* dim, uint32_t* n_cl
                             double* mean_assigned_distance);
 hivf_status hivf_index_cluster_sizes(const hivf_index* idx, uint64_t* sizes_out);
 
+/* ---- index build -------------------------------------------------------------
+ * Replaces ivf::compute_assignments and ivf::train_kmeans
+ * (proj/src/vector_index.cpp:202-208, 99-200) with the reference's exact
+ * arithmetic (nearest centroid in double, ties -> lowest id; k-means++ seeding
+ * with the reference's Rng stream and sequential running sums; Lloyd means
+ * summed in point order in double; empty clusters re-seeded to the farthest
+ * point), so the centroids / assignments are bit-identical to the reference's.
+ * All arrays in device memory, row-major [n][dim] / [K][dim]; rows already in
+ * search space (normalized for cosine, as build_index does at :245-252).
+ * train_kmeans: EINVAL for n < K, K == 0, max_iters == 0 (:101-105).  Its
+ * k-means++ seeding walks the n running sums once per seed (sequential by
+ * definition), so it costs O(K n) serial adds on one thread. */
+hivf_status hivf_compute_assignments(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim,
+                                     const float* d_centroids, uint32_t n_clusters,
+                                     uint32_t* d_assign_out);
+hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim,
+                              uint32_t n_clusters, uint32_t max_iters, uint64_t seed,
+                              float* d_centroids_out);
+
 /* ---- coarse assign --------------------------------------------------------
  * Batched ivf::select_clusters (proj/src/vector_index.cpp:261-278): for each
  * query, the nprobe nearest centroids in exact (double distance, cluster id)

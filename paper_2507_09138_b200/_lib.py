@@ -22,7 +22,8 @@ SYMBOLS = [
     "hivf_index_add_rows_at_device", "hivf_index_finish", "hivf_index_get_rows",
     "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
     "hivf_assign", "hivf_search", "hivf_search_device", "hivf_assign_device",
-    "hivf_search_planned_device", "hivf_scan_items",
+    "hivf_search_planned_device", "hivf_scan_items", "hivf_compute_assignments",
+    "hivf_train_kmeans",
     "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get", "hivf_last_stats",
     "hivf_set_option",
 ]
@@ -85,6 +86,8 @@ def lib():
         "hivf_search": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
         "hivf_search_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
         "hivf_assign_device": (i32, [vp, vp, u32, u32, vp, vp]),
+        "hivf_compute_assignments": (i32, [vp, vp, u64, u32, vp, u32, vp]),
+        "hivf_train_kmeans": (i32, [vp, vp, u64, u32, u32, u32, u64, vp]),
         "hivf_search_planned_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp, vp]),
         "hivf_scan_items": (i32, [vp, vp, u32, vp, vp, vp, vp, vp, vp, u32, vp]),
         "hivf_merge_parts_device": (i32, [vp, u32, u32, u32, vp, vp, vp, vp, vp, vp]),

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -921,6 +922,162 @@ hivf_status hivf_assign(hivf_index* ix, const float* queries, uint32_t n, uint32
   CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (err) return fail(HIVF_EINVAL, "select_clusters: non-finite query value");
+  return HIVF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// index build: compute_assignments / train_kmeans (vector_index.cpp:99-208)
+// ---------------------------------------------------------------------------
+
+// nearest_centroid for every row (ties -> lowest id): the exact coarse assign
+// with nprobe = 1 against a centroid-only L2 index (rows already in search
+// space, so no query normalization).
+static hivf_status assign_rows(hivf_ctx* c, const float* X, uint64_t n, uint32_t dim, const float* dcent,
+                               uint32_t K, uint32_t* out) {
+  std::vector<uint64_t> offs(K + 1, 0);
+  hivf_index* ix = nullptr;
+  hivf_status st = hivf_index_begin(c, dim, HIVF_METRIC_L2, K, dcent, 1, offs.data(), &ix);
+  if (st != HIVF_OK) return st;
+  if ((st = hivf_index_finish(ix)) != HIVF_OK) {
+    hivf_index_destroy(ix);
+    return st;
+  }
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65536, (256ull << 20) / (4ull * K)));
+  for (uint64_t b = 0; b < n && st == HIVF_OK; b += chunk) {
+    const uint32_t m = (uint32_t)std::min(chunk, n - b);
+    QueryView qv;
+    if ((st = prep_queries(ix, X + b * dim, m, false, &qv)) != HIVF_OK) break;
+    if ((st = run_assign(ix, qv, 1, nullptr)) != HIVF_OK) break;
+    if (cudaMemcpyAsync(out + b, c->plans.p, m * 4ull, cudaMemcpyDeviceToDevice, c->stream) != cudaSuccess)
+      st = fail(HIVF_ECUDA, "assign copy");
+  }
+  std::string keep = g_err;
+  hivf_index_destroy(ix);
+  g_err = keep;
+  return st;
+}
+
+hivf_status hivf_compute_assignments(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim,
+                                     const float* d_centroids, uint32_t K, uint32_t* d_assign_out) {
+  if (!ctx || (!d_corpus && n) || !d_centroids || (!d_assign_out && n))
+    return fail(HIVF_EINVAL, "compute_assignments: NULL argument");
+  if (dim == 0 || K == 0) return fail(HIVF_EINVAL, "compute_assignments: dim and K must be >= 1");
+  if (n == 0) return HIVF_OK;
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->err.ensure(4));
+  CK(cudaMemsetAsync(ctx->err.p, 0, 4, ctx->stream));
+  hivf_status st = assign_rows(ctx, d_corpus, n, dim, d_centroids, K, d_assign_out);
+  if (st != HIVF_OK) return st;
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, ctx->err.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (err) return fail(HIVF_EINVAL, "compute_assignments: non-finite corpus value");
+  return HIVF_OK;
+}
+
+namespace {
+struct DevScratch {  // RAII cudaMalloc set for the k-means run
+  std::vector<void*> p;
+  cudaError_t alloc(void** out, size_t bytes) {
+    cudaError_t e = cudaMalloc(out, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) p.push_back(*out);
+    return e;
+  }
+  ~DevScratch() {
+    for (void* q : p) cudaFree(q);
+  }
+};
+}  // namespace
+
+hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim, uint32_t K,
+                              uint32_t max_iters, uint64_t seed, float* d_centroids_out) {
+  if (!ctx || !d_corpus || !d_centroids_out) return fail(HIVF_EINVAL, "train_kmeans: NULL argument");
+  if (n < K) return fail(HIVF_EINVAL, "train_kmeans: corpus smaller than k_clusters");
+  if (K == 0) return fail(HIVF_EINVAL, "train_kmeans: k_clusters must be >= 1");
+  if (max_iters == 0) return fail(HIVF_EINVAL, "train_kmeans: max_iters must be >= 1");
+  if (dim == 0) return fail(HIVF_EINVAL, "train_kmeans: dim must be >= 1");
+  if (n >= 0xffffffffull) return fail(HIVF_EUNSUPPORTED, "train_kmeans: n >= 2^32");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  // the reference's Rng (common.hpp:18-76): mt19937_64, uniform_index by
+  // rejection, uniform = (x >> 11) * 2^-53; the k-means++ draws are taken in
+  // stream order (one per seed whose total > 0, consumed on the device)
+  std::mt19937_64 gen(seed);
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+  uint64_t x;
+  do {
+    x = gen();
+  } while (x >= limit);
+  const uint64_t first = x % n;
+  std::vector<double> us(std::max<uint32_t>(1, K));
+  for (uint32_t i = 0; i + 1 < K; ++i) us[i] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+  DevScratch S;
+  double *dist2, *prefix, *total, *d_us, *dd;
+  int *draw, *zero, *differs;
+  uint64_t *pick, *off;
+  uint32_t *assign, *prev, *idx, *idx_s, *keys_s;
+  uint8_t* used;
+  float* new_c;
+  unsigned long long* sc2;
+  cudaError_t e = cudaSuccess;
+  for (auto [ptr, bytes] : std::initializer_list<std::pair<void**, size_t>>{
+           {(void**)&dist2, n * 8}, {(void**)&prefix, n * 8}, {(void**)&total, 8},
+           {(void**)&d_us, us.size() * 8}, {(void**)&dd, n * 8}, {(void**)&draw, 4}, {(void**)&zero, 4},
+           {(void**)&differs, 4}, {(void**)&pick, 8}, {(void**)&off, (K + 1) * 8ull},
+           {(void**)&assign, n * 4}, {(void**)&prev, n * 4}, {(void**)&idx, n * 4},
+           {(void**)&idx_s, n * 4}, {(void**)&keys_s, n * 4}, {(void**)&used, n},
+           {(void**)&new_c, (size_t)K * dim * 4}, {(void**)&sc2, 16}})
+    if ((e = S.alloc(ptr, bytes)) != cudaSuccess)
+      return fail(e == cudaErrorMemoryAllocation ? HIVF_ENOMEM : HIVF_ECUDA, "train_kmeans alloc: %s",
+                  cudaGetErrorString(e));
+  float* cents = d_centroids_out;
+  CK(cudaMemcpyAsync(d_us, us.data(), us.size() * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(draw, 0, 4, s));
+  // k-means++ seeding (vector_index.cpp:114-154)
+  CK(cudaMemcpyAsync(cents, d_corpus + first * dim, dim * 4ull, cudaMemcpyDeviceToDevice, s));
+  launch_kmeans_dist2(d_corpus, n, dim, cents, dist2, 0, s);
+  CKL();
+  for (uint32_t m = 1; m < K; ++m) {
+    launch_kmeans_prefix(dist2, n, prefix, total, s);
+    launch_kmeans_pick(prefix, n, total, d_us, draw, pick, zero, d_corpus, dim, cents, m, s);
+    launch_kmeans_dist2(d_corpus, n, dim, cents + (uint64_t)m * dim, dist2, 1, s);
+    CKL();
+  }
+  // Lloyd iterations (vector_index.cpp:156-197)
+  CK(cudaMemsetAsync(prev, 0xff, n * 4, s));
+  size_t sort_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, assign, keys_s, idx, idx_s, (int64_t)n, 0, 32, s));
+  void* sort_tmp = nullptr;
+  if ((e = S.alloc(&sort_tmp, sort_bytes)) != cudaSuccess) return fail(HIVF_ENOMEM, "train_kmeans sort scratch");
+  std::vector<uint64_t> hoff(K + 1);
+  for (uint32_t it = 0; it < max_iters; ++it) {
+    hivf_status st = assign_rows(ctx, d_corpus, n, dim, cents, K, assign);
+    if (st != HIVF_OK) return st;
+    int h_diff = 0;
+    CK(cudaMemsetAsync(differs, 0, 4, s));
+    launch_same_assign(assign, prev, n, differs, s);
+    CKL();
+    CK(cudaMemcpyAsync(&h_diff, differs, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!h_diff) break;
+    launch_iota(idx, n, s);
+    CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, assign, keys_s, idx, idx_s, (int64_t)n, 0, 32, s));
+    CK(cudaMemcpyAsync(new_c, cents, (size_t)K * dim * 4, cudaMemcpyDeviceToDevice, s));
+    launch_cluster_means(d_corpus, dim, K, keys_s, idx_s, n, off, new_c, s);
+    CKL();
+    CK(cudaMemcpyAsync(hoff.data(), off, (K + 1) * 8ull, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    bool any_empty = false;
+    for (uint32_t c = 0; c < K; ++c) {
+      if (hoff[c + 1] != hoff[c]) continue;
+      if (!any_empty) CK(cudaMemsetAsync(used, 0, n, s));
+      any_empty = true;
+      launch_far_point(d_corpus, n, dim, assign, new_c, cents, c, used, dd, sc2, s);
+      CKL();
+    }
+    CK(cudaMemcpyAsync(cents, new_c, (size_t)K * dim * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
   return HIVF_OK;
 }
 

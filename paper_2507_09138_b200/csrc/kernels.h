@@ -103,6 +103,22 @@ void bound_ffma(uint32_t dim, double* a, double* b, double* c);
 void bound_tc(uint32_t dim, double* a, double* b, double* c);   // 3-pass split
 void bound_tc1(uint32_t dim, double* a, double* b, double* c);  // single pass
 
+// ---- kmeans.cu (index build: train_kmeans / Lloyd, vector_index.cpp:99-200)
+void launch_kmeans_dist2(const float* X, uint64_t n, uint32_t dim, const float* c, double* dist2, int mode,
+                         cudaStream_t s);
+void launch_kmeans_prefix(const double* dist2, uint64_t n, double* prefix, double* total, cudaStream_t s);
+void launch_kmeans_pick(const double* prefix, uint64_t n, const double* total, const double* us, int* draw,
+                        uint64_t* pick, int* zero, const float* X, uint32_t dim, float* cents, uint32_t m,
+                        cudaStream_t s);
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t s);
+void launch_same_assign(const uint32_t* a, uint32_t* prev, uint64_t n, int* differs, cudaStream_t s);
+void launch_cluster_means(const float* X, uint32_t dim, uint32_t K, const uint32_t* sorted_keys,
+                          const uint32_t* sorted_idx, uint64_t n, uint64_t* off, float* cents,
+                          cudaStream_t s);
+void launch_far_point(const float* X, uint64_t n, uint32_t dim, const uint32_t* assign, const float* new_c,
+                      const float* old_c, uint32_t c, uint8_t* used, double* dd, unsigned long long* scratch2,
+                      cudaStream_t s);
+
 // ---- finalize.cu
 void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe, uint32_t K,
                            uint32_t* pair_query, uint32_t* pair_list, uint32_t* plans_out, int* err,
