@@ -51,27 +51,57 @@ __global__ void k_dist2(const float* __restrict__ X, uint64_t n, uint32_t dim, c
 }
 
 // running sum in index order (total += d, :123-124) with every prefix kept;
-// the walk is the reference's own left-to-right chain of rounded adds
-__global__ void k_prefix_seq(const double* __restrict__ dist2, uint64_t n, double* __restrict__ prefix,
-                             double* __restrict__ total) {
-  if (threadIdx.x || blockIdx.x) return;
+// the walk is the reference's own left-to-right chain of rounded adds.  One
+// thread owns the chain; the other warps of the block stream dist2 tiles into
+// shared memory ahead of it and write the finished prefixes back, so the
+// serial thread only sees shared-memory latency.
+constexpr int kScanTile = 2048;  // doubles per tile (16 KB), double-buffered
+__global__ void __launch_bounds__(512, 1) k_prefix_seq(const double* __restrict__ dist2, uint64_t n,
+                                                       double* __restrict__ prefix,
+                                                       double* __restrict__ total) {
+  __shared__ double buf[2][kScanTile];
+  const uint64_t ntile = (n + kScanTile - 1) / kScanTile;
   double acc = 0.0;
-  uint64_t i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double v[8];
+  // prologue: tile 0
+  for (uint32_t e = threadIdx.x; e < kScanTile; e += blockDim.x) {
+    const uint64_t i = e;
+    buf[0][e] = i < n ? dist2[i] : 0.0;
+  }
+  __syncthreads();
+  for (uint64_t t = 0; t < ntile; ++t) {
+    const int cur = (int)(t & 1), nxt = cur ^ 1;
+    const uint64_t base = t * kScanTile;
+    const uint32_t len = (uint32_t)min((uint64_t)kScanTile, n - base);
+    if (threadIdx.x == 0) {
+      double* b = buf[cur];
+      uint32_t e = 0;
+      for (; e + 8 <= len; e += 8) {
+        double v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = dist2[i + e];
+        for (int u = 0; u < 8; ++u) v[u] = b[e + u];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      acc = __dadd_rn(acc, v[e]);
-      prefix[i + e] = acc;
+        for (int u = 0; u < 8; ++u) {
+          acc = __dadd_rn(acc, v[u]);
+          b[e + u] = acc;
+        }
+      }
+      for (; e < len; ++e) {
+        acc = __dadd_rn(acc, b[e]);
+        b[e] = acc;
+      }
+    } else if (t + 1 < ntile) {
+      // helpers (threads 32..): stage the next tile while the chain runs
+      const uint64_t nb = base + kScanTile;
+      for (uint32_t e = threadIdx.x - 32; threadIdx.x >= 32 && e < kScanTile; e += blockDim.x - 32) {
+        const uint64_t i = nb + e;
+        buf[nxt][e] = i < n ? dist2[i] : 0.0;
+      }
     }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) prefix[base + e] = buf[cur][e];
+    __syncthreads();
   }
-  for (; i < n; ++i) {
-    acc = __dadd_rn(acc, dist2[i]);
-    prefix[i] = acc;
-  }
-  *total = acc;
+  if (threadIdx.x == 0) *total = acc;
 }
 
 // k-means++ pick (vector_index.cpp:125-135): target = u * total, first i with
@@ -215,7 +245,7 @@ void launch_kmeans_dist2(const float* X, uint64_t n, uint32_t dim, const float* 
   k_dist2<<<grid(n, 128), 128, 0, s>>>(X, n, dim, c, dist2, mode);
 }
 void launch_kmeans_prefix(const double* dist2, uint64_t n, double* prefix, double* total, cudaStream_t s) {
-  k_prefix_seq<<<1, 1, 0, s>>>(dist2, n, prefix, total);
+  k_prefix_seq<<<1, 512, 0, s>>>(dist2, n, prefix, total);
 }
 void launch_kmeans_pick(const double* prefix, uint64_t n, const double* total, const double* us, int* draw,
                         uint64_t* pick, int* zero, const float* X, uint32_t dim, float* cents, uint32_t m,
