@@ -207,11 +207,24 @@ hivf_status hivf_merge_parts_device(hivf_ctx* ctx, uint32_t n_parts, uint32_t n_
 
 /* ---- hot-cluster residency set ---------------------------------------------
  * Device side of cache::ClusterCacheState (proj/include/hedra/tiered_cache.hpp
- * :37-78): the host adapter keeps the reference's bookkeeping; these calls
- * apply a residency set to the device (hot lists are scheduled first and kept
- * L2-persistent while resident). */
+ * :37-78; the host adapter keeps the reference's counters and target choice).
+ * With option "hbm_list_budget" (bytes, set on the context before the index
+ * is built) smaller than the index, lists live in a pinned host backing store
+ * read by the kernels over PCIe, and only the resident set occupies HBM:
+ *   hivf_residency_set  -- make exactly `clusters` resident: evictions take
+ *       effect for every later launch (tiered_cache.cpp:23-36), admissions in
+ *       the given order while they fit the budget start asynchronous H2D
+ *       copies on the index's copy stream; a list stays non-resident (read
+ *       from the backing store) until its copy completes -- mid-swap =
+ *       non-resident, as complete_swaps (:70-80) models it.
+ *   hivf_residency_get  -- resident flags [n_clusters] (completed swaps).
+ *   hivf_residency_sync -- wait for the swaps in flight and complete them.
+ * Results never depend on residency (lane transparency,
+ * proj/tests/test_retrieval_engine.cpp:158-199).  Without a budget every list
+ * is in HBM and the set is bookkeeping only. */
 hivf_status hivf_residency_set(hivf_index* idx, const uint32_t* clusters, uint32_t n);
 hivf_status hivf_residency_get(const hivf_index* idx, uint8_t* resident_out);
+hivf_status hivf_residency_sync(hivf_index* idx);
 
 /* ---- introspection (bench / tests) ----------------------------------------- */
 typedef struct {
@@ -228,6 +241,8 @@ typedef struct {
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
+ * "hbm_list_budget" (bytes of list storage an index may keep in HBM; the
+ * rest stays in pinned host memory, see residency),
  * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
  * 3 tcgen05 single-pass), "tc_qmax", "time_kernels" (record events around each
  * phase and accumulate into hivf_stats), "reset_timers". */

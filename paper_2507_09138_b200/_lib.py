@@ -24,7 +24,8 @@ SYMBOLS = [
     "hivf_assign", "hivf_search", "hivf_search_device", "hivf_assign_device",
     "hivf_search_planned_device", "hivf_scan_items", "hivf_compute_assignments",
     "hivf_train_kmeans",
-    "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get", "hivf_last_stats",
+    "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get",
+    "hivf_residency_sync", "hivf_last_stats",
     "hivf_set_option",
 ]
 
@@ -93,6 +94,7 @@ def lib():
         "hivf_merge_parts_device": (i32, [vp, u32, u32, u32, vp, vp, vp, vp, vp, vp]),
         "hivf_residency_set": (i32, [vp, vp, u32]),
         "hivf_residency_get": (i32, [vp, vp]),
+        "hivf_residency_sync": (i32, [vp]),
         "hivf_last_stats": (i32, [vp, P(Stats)]),
         "hivf_set_option": (i32, [vp, C.c_char_p, C.c_int64]),
     }

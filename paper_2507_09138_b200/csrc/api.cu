@@ -114,6 +114,9 @@ struct hivf_ctx {
   // split-precision, 3 tcgen05 single-pass
   int opt_scan_kernel = 0;
   int opt_scan_ctas = 0;
+  // tiered residency: list bytes an index may keep in HBM (0 = all lists in HBM);
+  // the rest stays in a pinned host backing store read over PCIe
+  uint64_t opt_hbm_list_budget = 0;
   // scratch
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
@@ -193,6 +196,22 @@ struct hivf_index {
   double mean_assigned = -1.0;
   uint32_t seg_rows = 4096, s_max = 1;
   std::vector<uint8_t> resident;
+  // ---- tiered residency (hivf_residency_set) ----
+  bool tiered = false;           // vec is pinned host memory, hot lists copied into pool
+  float* pool = nullptr;         // HBM slots for resident lists
+  uint64_t pool_bytes = 0;
+  const float** d_list_ptr = nullptr;  // device table read by the kernels
+  std::vector<uint64_t> slot_off;      // per list: byte offset in pool, or ~0
+  std::vector<std::pair<uint64_t, uint64_t>> free_ext;  // free (offset, size) extents
+  std::vector<uint8_t> swap_in;        // per list: copy in flight
+  struct Swap {
+    cudaEvent_t done;
+    std::vector<uint32_t> lists;
+  };
+  std::vector<Swap> swaps;             // in flight, oldest first
+  cudaStream_t copy_stream = nullptr;
+  uint64_t swapped_in_bytes = 0;
+  uint64_t list_bytes(uint32_t c) const { return (list_off[c + 1] - list_off[c]) * dpad * 4; }
   int auto_split = 0;  // auto policy: 0 single-pass tf32, 1 split-precision
   uint32_t adapt_seen = 0, adapt_fallback = 0;
   // scan kernel for the next call: 1 FFMA, 2 tensor-core split, 3 tensor-core single pass
@@ -204,6 +223,7 @@ struct hivf_index {
     else if (kind == 3) bound_tc1(dim, &v.e_a, &v.e_b, &v.e_c);
     else bound_ffma(dim, &v.e_a, &v.e_b, &v.e_c);
     v.vec = vec;
+    v.list_ptr = tiered ? d_list_ptr : nullptr;
     v.ids = ids;
     v.xnorm2 = xnorm2;
     v.list_off = d_list_off;
@@ -222,8 +242,14 @@ struct hivf_index {
     return v;
   }
   ~hivf_index() {
-    for (void* p : {(void*)vec, (void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits,
-                    (void*)cent, (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err})
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
+    for (auto& w : swaps) cudaEventDestroy(w.done);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (tiered && vec) cudaFreeHost(vec);
+    else if (vec) cudaFree(vec);
+    for (void* p : {(void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
+                    (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err, (void*)pool,
+                    (void*)d_list_ptr})
       if (p) cudaFree(p);
   }
 };
@@ -246,6 +272,72 @@ static void adapt_scan(hivf_index* ix, uint32_t n_queries, uint32_t n_fallback) 
   ix->adapt_seen += n_queries;
   ix->adapt_fallback += n_fallback;
   if (ix->adapt_fallback * 50 > ix->adapt_seen && ix->adapt_fallback >= 2) ix->auto_split = 1;
+}
+
+// ---- tiered residency helpers ------------------------------------------------
+namespace {
+// first-fit allocator over the pool's free extents (host bookkeeping)
+uint64_t pool_alloc(hivf_index* ix, uint64_t bytes) {
+  bytes = (bytes + 255) & ~uint64_t(255);
+  for (size_t i = 0; i < ix->free_ext.size(); ++i) {
+    auto& f = ix->free_ext[i];
+    if (f.second >= bytes) {
+      const uint64_t off = f.first;
+      f.first += bytes;
+      f.second -= bytes;
+      if (!f.second) ix->free_ext.erase(ix->free_ext.begin() + (long)i);
+      return off;
+    }
+  }
+  return ~0ull;
+}
+void pool_free(hivf_index* ix, uint64_t off, uint64_t bytes) {
+  if (off == ~0ull) return;
+  bytes = (bytes + 255) & ~uint64_t(255);
+  auto& v = ix->free_ext;
+  v.push_back({off, bytes});
+  std::sort(v.begin(), v.end());
+  std::vector<std::pair<uint64_t, uint64_t>> m;
+  for (auto& e : v) {
+    if (!m.empty() && m.back().first + m.back().second == e.first) m.back().second += e.second;
+    else m.push_back(e);
+  }
+  v.swap(m);
+}
+}  // namespace
+
+// pointer-table updates ride in kernel arguments (no host buffer lifetime):
+// ordered on the context stream, so launches before keep the old address
+static hivf_status apply_flips(hivf_index* ix, const std::vector<std::pair<uint32_t, const float*>>& f) {
+  for (size_t b = 0; b < f.size(); b += kPtrFlipBatch) {
+    PtrFlips pf{};
+    pf.n = (uint32_t)std::min<size_t>(kPtrFlipBatch, f.size() - b);
+    for (uint32_t i = 0; i < pf.n; ++i) {
+      pf.list[i] = f[b + i].first;
+      pf.ptr[i] = f[b + i].second;
+    }
+    launch_ptr_flips(ix->d_list_ptr, pf, ix->ctx->stream);
+    CKL();
+  }
+  return HIVF_OK;
+}
+
+// complete_swaps (tiered_cache.cpp:70-80) on real copies: lists whose H2D
+// copy finished become resident (their table entry points at the HBM slot
+// for every launch issued from now on)
+static void complete_swaps(hivf_index* ix) {
+  std::vector<std::pair<uint32_t, const float*>> flips;
+  while (!ix->swaps.empty() && cudaEventQuery(ix->swaps.front().done) == cudaSuccess) {
+    for (uint32_t c : ix->swaps.front().lists) {
+      if (!ix->swap_in[c]) continue;
+      ix->swap_in[c] = 0;
+      ix->resident[c] = 1;
+      flips.push_back({c, reinterpret_cast<const float*>(reinterpret_cast<uint8_t*>(ix->pool) + ix->slot_off[c])});
+    }
+    cudaEventDestroy(ix->swaps.front().done);
+    ix->swaps.erase(ix->swaps.begin());
+  }
+  if (!flips.empty()) apply_flips(ix, flips);
 }
 
 extern "C" {
@@ -323,6 +415,9 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->opt_seg_rows = (uint32_t)value;
   } else if (!strcmp(name, "force_exact")) {
     ctx->opt_force_exact = value != 0;
+  } else if (!strcmp(name, "hbm_list_budget")) {  // bytes; applies to indexes created later
+    if (value < 0) return fail(HIVF_EINVAL, "hbm_list_budget must be >= 0");
+    ctx->opt_hbm_list_budget = (uint64_t)value;
   } else if (!strcmp(name, "scan_ctas")) {
     ctx->opt_scan_ctas = (int)value;
   } else if (!strcmp(name, "scan_kernel")) {
@@ -429,7 +524,30 @@ hivf_status hivf_index_begin(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n
     return fail(e == cudaErrorMemoryAllocation ? HIVF_ENOMEM : HIVF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&ix->vec, std::max<uint64_t>(16, N * ix->dpad * 4))) != cudaSuccess) return bail(e, "alloc lists");
+  const uint64_t vec_bytes = std::max<uint64_t>(16, N * ix->dpad * 4);
+  if (ctx->opt_hbm_list_budget && ctx->opt_hbm_list_budget < vec_bytes) {
+    // tiered: backing store in pinned, device-mapped host memory (UVA: the same
+    // address on both sides; the build kernels write it over PCIe), plus an
+    // HBM pool of `budget` bytes for the resident (hot) lists
+    ix->tiered = true;
+    ix->pool_bytes = ctx->opt_hbm_list_budget & ~uint64_t(255);
+    if ((e = cudaHostAlloc(&ix->vec, vec_bytes, cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess) {
+      ix->vec = nullptr;
+      return bail(e, "alloc host backing store");
+    }
+    if ((e = cudaMalloc(&ix->pool, std::max<uint64_t>(256, ix->pool_bytes))) != cudaSuccess) return bail(e, "alloc list pool");
+    if ((e = cudaMalloc(&ix->d_list_ptr, n_clusters * 8ull)) != cudaSuccess) return bail(e, "alloc list table");
+    std::vector<uint64_t> ptr(n_clusters);
+    for (uint32_t c = 0; c < n_clusters; ++c)
+      ptr[c] = reinterpret_cast<uint64_t>(ix->vec + list_offsets[c] * ix->dpad);
+    cudaMemcpy(ix->d_list_ptr, ptr.data(), n_clusters * 8ull, cudaMemcpyHostToDevice);
+    ix->slot_off.assign(n_clusters, ~0ull);
+    ix->swap_in.assign(n_clusters, 0);
+    ix->free_ext.push_back({0, ix->pool_bytes});
+    if ((e = cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "copy stream");
+  } else if ((e = cudaMalloc(&ix->vec, vec_bytes)) != cudaSuccess) {
+    return bail(e, "alloc lists");
+  }
   if ((e = cudaMalloc(&ix->ids, std::max<uint64_t>(8, N * 8))) != cudaSuccess) return bail(e, "alloc ids");
   if ((e = cudaMalloc(&ix->xnorm2, std::max<uint64_t>(4, N * 4))) != cudaSuccess) return bail(e, "alloc norms");
   if ((e = cudaMalloc(&ix->d_list_off, (n_clusters + 1) * 8ull)) != cudaSuccess) return bail(e, "alloc offsets");
@@ -766,6 +884,7 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
   if (n == 0) return HIVF_OK;
   hivf_ctx* c = ix->ctx;
   CK(cudaSetDevice(c->device));
+  if (ix->tiered) complete_swaps(ix);
   c->stats = hivf_stats{};
   c->last_nq = n;
   c->last_index = ix;
@@ -1110,6 +1229,7 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
     if (clusters[p] >= ix->K) return fail(HIVF_EINVAL, "cluster id %u out of range", clusters[p]);
   hivf_ctx* c = ix->ctx;
   CK(cudaSetDevice(c->device));
+  if (ix->tiered) complete_swaps(ix);
   c->stats = hivf_stats{};
   c->last_nq = 0;
   c->last_index = ix;
@@ -1210,18 +1330,82 @@ hivf_status hivf_merge_parts_device(hivf_ctx* ctx, uint32_t n_parts, uint32_t n_
 hivf_status hivf_residency_set(hivf_index* ix, const uint32_t* clusters, uint32_t n) {
   if (!ix) return fail(HIVF_EINVAL, "index is NULL");
   if (n && !clusters) return fail(HIVF_EINVAL, "clusters NULL");
-  std::vector<uint8_t> res(ix->K, 0);
-  for (uint32_t i = 0; i < n; ++i) {
+  for (uint32_t i = 0; i < n; ++i)
     if (clusters[i] >= ix->K) return fail(HIVF_EINVAL, "cluster %u out of range", clusters[i]);
-    res[clusters[i]] = 1;
+  if (!ix->tiered) {  // every list already lives in HBM: the set is bookkeeping only
+    std::vector<uint8_t> res(ix->K, 0);
+    for (uint32_t i = 0; i < n; ++i) res[clusters[i]] = 1;
+    ix->resident.swap(res);
+    return HIVF_OK;
   }
-  ix->resident.swap(res);
+  CK(cudaSetDevice(ix->ctx->device));
+  complete_swaps(ix);
+  std::vector<uint8_t> want(ix->K, 0);
+  for (uint32_t i = 0; i < n; ++i) want[clusters[i]] = 1;
+  // evictions take effect immediately (tiered_cache.cpp:23-36): the list reads
+  // from the backing store from the next launch on; its slot is reused only by
+  // copies ordered after every launch issued so far
+  std::vector<std::pair<uint32_t, const float*>> flips;
+  for (uint32_t c = 0; c < ix->K; ++c)
+    if (!want[c] && (ix->resident[c] || ix->swap_in[c])) {
+      if (ix->swap_in[c]) {  // cancel an in-flight swap: forget it on completion
+        for (auto& w : ix->swaps)
+          w.lists.erase(std::remove(w.lists.begin(), w.lists.end(), c), w.lists.end());
+        ix->swap_in[c] = 0;
+      }
+      if (ix->resident[c]) flips.push_back({c, ix->vec + ix->list_off[c] * ix->dpad});
+      ix->resident[c] = 0;
+      pool_free(ix, ix->slot_off[c], ix->list_bytes(c));
+      ix->slot_off[c] = ~0ull;
+    }
+  hivf_status st = apply_flips(ix, flips);
+  if (st != HIVF_OK) return st;
+  cudaEvent_t after_evict;
+  CK(cudaEventCreateWithFlags(&after_evict, cudaEventDisableTiming));
+  CK(cudaEventRecord(after_evict, ix->ctx->stream));
+  CK(cudaStreamWaitEvent(ix->copy_stream, after_evict, 0));
+  cudaEventDestroy(after_evict);
+  // admissions in the caller's order while they fit the pool: H2D copies on
+  // the copy stream; the list stays non-resident until its copy completes
+  hivf_index::Swap w{};
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t c = clusters[i];
+    if (ix->resident[c] || ix->swap_in[c]) continue;
+    const uint64_t bytes = ix->list_bytes(c);
+    if (bytes == 0) {
+      ix->resident[c] = 1;  // an empty list is trivially resident
+      continue;
+    }
+    const uint64_t off = pool_alloc(ix, bytes);
+    if (off == ~0ull) continue;  // does not fit the HBM budget
+    ix->slot_off[c] = off;
+    ix->swap_in[c] = 1;
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ix->pool) + off, ix->vec + ix->list_off[c] * ix->dpad, bytes,
+                       cudaMemcpyHostToDevice, ix->copy_stream));
+    ix->swapped_in_bytes += bytes;
+    w.lists.push_back(c);
+  }
+  if (!w.lists.empty()) {
+    CK(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
+    CK(cudaEventRecord(w.done, ix->copy_stream));
+    ix->swaps.push_back(std::move(w));
+  }
   return HIVF_OK;
 }
 
-hivf_status hivf_residency_get(const hivf_index* ix, uint8_t* out) {
-  if (!ix || !out) return fail(HIVF_EINVAL, "NULL argument");
+hivf_status hivf_residency_get(const hivf_index* cix, uint8_t* out) {
+  if (!cix || !out) return fail(HIVF_EINVAL, "NULL argument");
+  hivf_index* ix = const_cast<hivf_index*>(cix);
+  if (ix->tiered) complete_swaps(ix);
   std::memcpy(out, ix->resident.data(), ix->K);
+  return HIVF_OK;
+}
+
+hivf_status hivf_residency_sync(hivf_index* ix) {
+  if (!ix) return fail(HIVF_EINVAL, "index is NULL");
+  if (!ix->tiered) return HIVF_OK;
+  CK(cudaStreamSynchronize(ix->copy_stream));
+  complete_swaps(ix);
   return HIVF_OK;
 }
 

@@ -246,9 +246,10 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     const uint32_t c = clist[i];
     const uint64_t lbeg = ix.list_off[c];
     const uint64_t n_c = ix.list_off[c + 1] - lbeg;
-    const uint64_t lr = crow[i] - lbeg, base = lbeg * ix.dpad;
+    const uint64_t lr = crow[i] - lbeg;
+    const float* lb = list_base(ix, c, lbeg);
     cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-      return __ldg(reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4)));
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
     });
     cid[i] = ix.ids[crow[i]];
   }
@@ -313,9 +314,10 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
       double dist = DBL_MAX;
       uint64_t id = ~0ull;
       if (r < end) {
-        const uint64_t n_c = end - beg, lr = r - beg, base = beg * ix.dpad;
+        const uint64_t n_c = end - beg, lr = r - beg;
+        const float* lb = list_base(ix, c, beg);
         dist = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-          return __ldg(reinterpret_cast<const float4*>(ix.vec + swz_offset(base, n_c, lr, g * 4)));
+          return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
         });
         id = ix.ids[r];
       }

@@ -20,7 +20,11 @@ struct ScanItem {
 
 // Device view of an uploaded index.
 struct IndexView {
-  const float* vec;         // chunk-major swizzled lists
+  const float* vec;         // chunk-major swizzled lists (the backing store)
+  // tiered index (option hbm_list_budget): per-list base address -- an HBM
+  // pool slot for resident lists, the pinned host backing store otherwise;
+  // nullptr when every list lives in HBM at vec + list_off[c] * dpad
+  const float* const* list_ptr;
   const uint64_t* ids;      // [N] doc ids, list order
   const float* xnorm2;      // [N] fp32(|x|^2)
   const uint64_t* list_off; // [K+1] row offsets
@@ -39,6 +43,13 @@ struct IndexView {
   double e_a, e_b, e_c;
 };
 
+#ifdef __CUDACC__
+// base of list c's chunk-major block (swz_offset(0, n_c, row, d) indexes into it)
+__device__ __forceinline__ const float* list_base(const IndexView& ix, uint32_t c, uint64_t lbeg) {
+  return ix.list_ptr ? ix.list_ptr[c] : ix.vec + lbeg * ix.dpad;
+}
+#endif
+
 // Per-batch query state (search space).
 struct QueryView {
   const float* qs;      // [nq][dpad] search-space queries, zero padded
@@ -48,6 +59,14 @@ struct QueryView {
 };
 
 // ---- layout.cu
+// tiered residency: list-table entries updated by value through kernel args
+constexpr int kPtrFlipBatch = 64;
+struct PtrFlips {
+  uint32_t n;
+  uint32_t list[kPtrFlipBatch];
+  const float* ptr[kPtrFlipBatch];
+};
+void launch_ptr_flips(const float** table, const PtrFlips& f, cudaStream_t s);
 void launch_pack_lists(const float* src_rows, uint64_t r_first, const uint64_t* pos,
                        uint64_t n_rows, uint32_t dim, uint32_t dpad, const uint64_t* d_list_off,
                        uint32_t K, float* dst, float* xnorm2, uint32_t* maxnorm_bits, int* err,

@@ -180,4 +180,14 @@ void launch_scatter_ids(const uint64_t* ids, const uint64_t* pos, uint64_t n, ui
                         cudaStream_t s) {
   if (n) k_scatter_ids<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ids, pos, n, out);
 }
+namespace {
+__global__ void k_ptr_flips(const float** table, PtrFlips f) {
+  if (threadIdx.x < f.n) table[f.list[threadIdx.x]] = f.ptr[threadIdx.x];
+}
+}  // namespace
+
+void launch_ptr_flips(const float** table, const PtrFlips& f, cudaStream_t s) {
+  if (f.n) k_ptr_flips<<<1, kPtrFlipBatch, 0, s>>>(table, f);
+}
+
 }  // namespace hivf

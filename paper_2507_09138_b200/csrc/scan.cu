@@ -229,7 +229,7 @@ __global__ void __launch_bounds__((kScanWarps + 1) * 32, 1) k_scan(ScanParams P)
       if (lane == 0) {
         const uint64_t lbeg = P.ix.list_off[item.list];
         const uint64_t n_c = P.ix.list_off[item.list + 1] - lbeg;
-        const float* lbase = P.ix.vec + lbeg * dpad;
+        const float* lbase = list_base(P.ix, item.list, lbeg);
         for (uint32_t r0 = 0; r0 < item.nrows; r0 += kRowBlock) {
           const uint32_t nr = min((uint32_t)kRowBlock, item.nrows - r0);
           const uint32_t bytes = nr * kChunk * 4;

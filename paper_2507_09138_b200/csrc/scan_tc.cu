@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         uint32_t pf = valid_n ? 0 : 2;  // prefetch progress of the next item
         const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
         const uint64_t n_c = lend - lbeg;
-        const float* lbase = P.ix.vec + lbeg * dpad;
+        const float* lbase = list_base(P.ix, item.list, lbeg);
         for (uint32_t t = 0; t < ntiles; ++t) {
           const uint32_t r0 = item.row0 + t * kTcTile;
           const uint32_t nr = min((uint32_t)kTcTile, item.nrows - t * kTcTile);

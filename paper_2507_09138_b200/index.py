@@ -300,6 +300,9 @@ class IvfIndex:
         cl = np.ascontiguousarray(clusters, np.uint32)
         check(lib().hivf_residency_set(self.h, cl.ctypes.data if len(cl) else None, len(cl)))
 
+    def residency_sync(self):
+        check(lib().hivf_residency_sync(self.h))
+
     def residency(self) -> np.ndarray:
         out = np.zeros(self.k_clusters, np.uint8)
         check(lib().hivf_residency_get(self.h, out.ctypes.data))

@@ -308,3 +308,40 @@ def test_unit_norm_data_split_no_fallback(ctx):
         assert ctx.stats()["scan_kernel"] == 3
     finally:
         ctx.set_option("scan_kernel", 0)
+
+
+def test_assign_device_and_planned_search(ctx):
+    """hivf_assign_device == hivf_assign, and hivf_search_planned_device with
+    those plans (or with the plans of split batches, all-gather style) ==
+    hivf_search_device, bit for bit."""
+    import torch
+    from paper_2507_09138_b200 import Context
+    rng = np.random.default_rng(5)
+    c2 = Context(0, torch.cuda.current_stream())
+    ix, csr, X, centers = _random_index(c2, rng, 20000, 64, 48)
+    Q = (centers[rng.integers(0, len(centers), 96)] +
+         rng.standard_normal((96, 64)).astype(np.float32) * 0.3).astype(np.float32)
+    npb, k = 12, 10
+    dq = torch.from_numpy(Q).cuda()
+    plans = torch.empty(len(Q), npb, dtype=torch.int32, device="cuda")
+    ix.assign_device(dq, npb, plans)
+    # split assign: two halves, as two ranks would
+    half = len(Q) // 2
+    p2 = torch.empty_like(plans)
+    ix.assign_device(dq[:half].contiguous(), npb, p2[:half])
+    ix.assign_device(dq[half:].contiguous(), npb, p2[half:])
+    torch.cuda.synchronize()
+    want = ix.select_clusters(Q, npb)
+    assert np.array_equal(plans.cpu().numpy().astype(np.uint32), want)
+    assert np.array_equal(p2.cpu().numpy().astype(np.uint32), want)
+    outs = [(torch.empty(len(Q), k, dtype=torch.int64, device="cuda"),
+             torch.empty(len(Q), k, dtype=torch.float64, device="cuda"),
+             torch.empty(len(Q), dtype=torch.int32, device="cuda")) for _ in range(2)]
+    ix.search_device(dq, npb, k, *outs[0])
+    ix.search_planned_device(dq, npb, k, p2, *outs[1])
+    torch.cuda.synchronize()
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    oi, od, oc = csr.search(Q, npb, k)
+    assert np.array_equal(outs[1][0].cpu().numpy().astype(np.uint64), oi)
+    assert np.array_equal(outs[1][1].cpu().numpy().view(np.uint64), od.view(np.uint64))
