@@ -245,9 +245,39 @@ def run_hivf(args):
     # --shard R/N: single-GPU measurement of rank R's shard of an N-GPU job (the
     # local search only; the all-gather + merge of the real N-GPU step is not run)
     shard_r, shard_n = (int(x) for x in args.shard.split("/")) if args.shard else (rank, world)
+    if args.hbm_budget_gb > 0:  # tiered residency: lists in pinned host memory, hot set in HBM
+        ctx.set_option("hbm_list_budget", int(args.hbm_budget_gb * 1e9))
     ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, shard_r, shard_n)
     B, npb, k = cfg.batch, cfg.nprobe, cfg.k
     pool = [wl.queries(i) for i in range(args.pool)]
+    residency = None
+    if args.hbm_budget_gb > 0:
+        # the ClusterCacheState target (tiered_cache.cpp:23-36): lists by access
+        # frequency over the stream (distinct lists per batch), desc, ties by id
+        t0 = time.time()
+        freq = np.zeros(cfg.k_clusters, np.int64)
+        plan_np = [ix.select_clusters(q.cpu().numpy(), npb) for q in pool]
+        for p in plan_np:
+            freq[np.unique(p)] += 1
+        hot = np.lexsort((np.arange(cfg.k_clusters), -freq)).astype(np.uint32)
+        hot = hot[freq[hot] > 0]
+        ix.set_residency(hot)
+        ix.residency_sync()
+        res = ix.residency()
+        lb = sizes.astype(np.float64) * ((cfg.dim + 15) // 16 * 16) * 4
+        scanned = np.zeros(cfg.k_clusters, bool)
+        hit = tot = 0.0
+        for p in plan_np:
+            u = np.unique(p)
+            tot += lb[u].sum()
+            hit += lb[u][res[u]].sum()
+        residency = {"hbm_list_budget_gb": args.hbm_budget_gb,
+                     "index_list_gb": round(float(lb.sum()) / 1e9, 2),
+                     "resident_lists": int(res.sum()), "resident_gb": round(float(lb[res].sum()) / 1e9, 2),
+                     "scanned_bytes_from_hbm": round(hit / max(tot, 1.0), 4),
+                     "policy": "top lists by access frequency over the query stream (freq desc, id asc)",
+                     "swap_in_s": round(time.time() - t0, 2)}
+        log(f"residency: {residency}")
     # one packed result buffer per rank (ids | dists | counts) so the shard
     # exchange is a single all-gather
     Bk = B * k
@@ -440,6 +470,7 @@ def run_hivf(args):
                                   "finalize": round(fin_ms, 4)}},
         "cpu_baseline": cpu,
         "parity_sample": parity,
+        "residency": residency,
         "scan_stats": {"work_items": st["n_work_items"], "fallback_queries": st["n_fallback"],
                        "unique_lists": st["n_unique_lists"]},
         "clocks": clocks,
@@ -704,6 +735,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
+                    help="tiered residency: HBM bytes for list storage (rest in pinned host memory)")
     ap.add_argument("--shard", default="", help="R/N: measure rank R's list shard of an N-GPU job on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -48,6 +48,8 @@ CONFIGS = {
     "c1": Config("c1", 100_000, 128, 256, 8, 10, 64, 0.25),
     "c2": Config("c2", 1_000_000, 768, 1024, 32, 10, 256, 0.03),
     "c3": Config("c3", 21_000_000, 768, 4096, 128, 10, 256, 0.03),
+    # C3 index with a Zipf(1.0) topic-skewed query stream (residency experiments)
+    "c3z": Config("c3z", 21_000_000, 768, 4096, 128, 10, 256, 0.03, zipf=1.0),
     # configs[3]: 100M x 768 (307 GB) IVF-16384 over 8 GPUs, Zipf(1.0) topic-skewed
     # queries (workload.cpp:168-183); nprobe unspecified in BASELINE -> 128
     "c4": Config("c4", 100_000_000, 768, 16384, 128, 10, 256, 0.03, zipf=1.0),
