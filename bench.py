@@ -373,6 +373,16 @@ def run_hivf(args):
                        "p90": int(np.percentile(pp, 90)), "max": int(pp.max())}
     peak, peak_kind = measured_peaks()
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
+    # DRAM traffic per scan launch from the committed ncu --set full capture of
+    # this workload (profiles/ncu_traffic_<config>.json), when one exists
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")) as f:
+            tj = json.load(f)
+        if world == 1 and not args.shard and not args.hbm_budget_gb:
+            traffic = int(tj["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        pass
     step_gbs = float(np.mean(steps_ab)) / (ms_per_step / 1e3) / 1e9
     # ---- e2e: host buffers through the C-ABI ------------------------------------
     e2e = None
@@ -463,7 +473,7 @@ def run_hivf(args):
         "roofline": {"bound": "hbm", "kernel": "k_scan (grouped list scan)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "traffic": None,
+                     "traffic": traffic,
                      "bytes_per_launch": int(scan_bytes), "launch_ms": round(scan_ms, 4),
                      "step_hbm_frac": round(step_gbs / peak, 4),
                      "phase_ms": {"assign": round(assign_ms, 4), "scan": round(scan_ms, 4),
