@@ -121,7 +121,8 @@ struct hivf_ctx {
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
       cand_n, out_ids, out_d, out_cnt, qin, it_off, it_cl, it_k, heap_ids, heap_d, heap_n,
-      changed, x_ids, x_d, x_cnt, x_tot;
+      changed, x_ids, x_d, x_cnt, x_tot, tau, flags2, rep_entries, rep_n,
+      rep_cnt, rep_d, rep_ids;
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;
@@ -168,7 +169,8 @@ struct hivf_ctx {
                     &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items, &n_items,
                     &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &out_d, &out_cnt,
                     &qin, &it_off, &it_cl, &it_k, &heap_ids, &heap_d, &heap_n, &changed, &x_ids,
-                    &x_d, &x_cnt, &x_tot})
+                    &x_d, &x_cnt, &x_tot, &tau, &flags2,
+                    &rep_entries, &rep_n, &rep_cnt, &rep_d, &rep_ids})
       b->release();
     hstage.release();
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -216,9 +218,10 @@ struct hivf_index {
   uint32_t adapt_seen = 0, adapt_fallback = 0;
   // scan kernel for the next call: 1 FFMA, 2 tensor-core split, 3 tensor-core single pass
   int scan_kind() const;
-  IndexView view() const {
+  IndexView view() const { return view_kind(scan_kind()); }
+  // view carrying the filter bound of scan kernel `kind`
+  IndexView view_kind(int kind) const {
     IndexView v{};
-    const int kind = scan_kind();
     if (kind == 2) bound_tc(dim, &v.e_a, &v.e_b, &v.e_c);
     else if (kind == 3) bound_tc1(dim, &v.e_a, &v.e_b, &v.e_c);
     else bound_ffma(dim, &v.e_a, &v.e_b, &v.e_c);
@@ -265,13 +268,14 @@ int hivf_index::scan_kind() const {
 
 // Auto policy: the single-pass tf32 bound is 2^-9|x||q| (Cauchy-Schwarz on the
 // operand truncation).  When the data's norms are large against its neighbor
-// gaps, too many queries miss the proof and take the exact fallback; once
-// that exceeds 2% of the queries seen, switch this index to the split kernel.
+// gaps, queries miss the proof and take the segment repair or the exact
+// fallback.  Once more than 10% of the queries seen need it, switch this index
+// to the split kernel (8x tighter bound, 1.5x slower scan).
 static void adapt_scan(hivf_index* ix, uint32_t n_queries, uint32_t n_fallback) {
   if (ix->ctx->opt_scan_kernel != 0 || ix->auto_split) return;
   ix->adapt_seen += n_queries;
   ix->adapt_fallback += n_fallback;
-  if (ix->adapt_fallback * 50 > ix->adapt_seen && ix->adapt_fallback >= 2) ix->auto_split = 1;
+  if (ix->adapt_fallback * 10 > ix->adapt_seen && ix->adapt_fallback >= 2) ix->auto_split = 1;
 }
 
 // ---- tiered residency helpers ------------------------------------------------
@@ -455,10 +459,12 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
   s.assign_ms = ctx->acc_assign;
   s.scan_ms = ctx->acc_scan;
   s.finalize_ms = ctx->acc_fin;
-  if (ctx->n_items.p) CK(cudaMemcpy(&s.n_work_items, ctx->n_items.p, 4, cudaMemcpyDeviceToHost));
-  if (ctx->last_index && ctx->list_cnt.p && ctx->last_K == ctx->last_index->K) {
+  const DBuf& nit = ctx->n_items;
+  const DBuf& lcnt = ctx->list_cnt;
+  if (nit.p) CK(cudaMemcpy(&s.n_work_items, nit.p, 4, cudaMemcpyDeviceToHost));
+  if (ctx->last_index && lcnt.p && ctx->last_K == ctx->last_index->K) {
     std::vector<uint32_t> cnt(ctx->last_K);
-    CK(cudaMemcpy(cnt.data(), ctx->list_cnt.p, 4ull * ctx->last_K, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cnt.data(), lcnt.p, 4ull * ctx->last_K, cudaMemcpyDeviceToHost));
     s.n_unique_lists = 0;
     s.scan_bytes = 0;
     const auto& off = ctx->last_index->list_off;
@@ -818,9 +824,12 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
 }
 
 // Grouped scan over pairs (pair_query/pair_list already in c->pq / c->pl).
-static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs, bool timed) {
+// kind_override: 0 -> the index's current scan kernel, else 1/2/3
+static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs, bool timed,
+                            int kind_override = 0) {
   hivf_ctx* c = ix->ctx;
-  const IndexView v = ix->view();
+  const int kind = kind_override ? kind_override : ix->scan_kind();
+  const IndexView v = ix->view_kind(kind);
   const size_t nslots = (size_t)std::max<uint32_t>(n_pairs, 1) * ix->s_max;
   CK(c->list_cnt.ensure(ix->K * 4ull));
   CK(c->list_poff.ensure(ix->K * 4ull));
@@ -837,7 +846,6 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   // slots of empty lists are never written by the scan; zero counts so the
   // finalize pass reads "no candidates" there
   CK(cudaMemsetAsync(c->cand_n.p, 0, nslots * 4, c->stream));
-  const int kind = ix->scan_kind();
   const bool tc = kind != 1;
   const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2) : (uint32_t)kQMax;
   launch_build_worklist(v, group, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
@@ -923,15 +931,37 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
   if (!exact_only) {
     if ((st = run_scan(ix, qv, np, true)) != HIVF_OK) return st;
     c->mark(2);
+    CK(c->tau.ensure((size_t)n * 4));
+    // in-place repair of segments whose completeness proof failed
+    // (finalize.cu: k_repair_segments + k_finalize_repair); queries it cannot
+    // settle take the whole-query exact fallback below
+    const uint32_t rep_cap = std::max<uint32_t>(1024, n * 4);
+    const uint32_t per_q = 512;
+    CK(c->rep_entries.ensure((size_t)rep_cap * 8));
+    CK(c->rep_n.ensure(4));
+    CK(c->rep_cnt.ensure((size_t)n * 4));
+    CK(c->rep_d.ensure((size_t)n * per_q * 8));
+    CK(c->rep_ids.ensure((size_t)n * per_q * 8));
+    CK(cudaMemsetAsync(c->rep_n.p, 0, 4, c->stream));
+    RepairState R{c->rep_entries.as<uint64_t>(), c->rep_n.as<uint32_t>(), rep_cap, c->rep_cnt.as<uint32_t>(),
+                  c->rep_d.as<double>(), c->rep_ids.as<uint64_t>(), per_q};
     launch_finalize_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(),
                            c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(),
-                           d_ids_out, d_dists_out, d_counts_out, c->flags_f.as<int>(), c->stream);
+                           d_ids_out, d_dists_out, d_counts_out, c->flags_f.as<int>(), c->tau.as<float>(),
+                           &R, c->stream);
     CKL();
-    launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->flags_f.as<int>(), d_ids_out,
+    // pass-1 flags survive for the auto policy (flags2 carries the repair outcome)
+    CK(c->flags2.ensure((size_t)n * 4));
+    CK(cudaMemcpyAsync(c->flags2.p, c->flags_f.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    launch_repair(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
+                  c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), c->tau.as<float>(), R, c->sm_count * 4,
+                  d_ids_out, d_dists_out, d_counts_out, c->flags2.as<int>(), c->stream);
+    CKL();
+    launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->flags2.as<int>(), d_ids_out,
                         d_dists_out, d_counts_out, c->x_ids.as<uint64_t>(), c->x_d.as<double>(),
-                        c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), c->stream);
+                        c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), c->tau.as<float>(), c->stream);
     CKL();
-    c->stats.kernels_launched += 4;
+    c->stats.kernels_launched += 5;
     c->mark(3);
   } else {
     CK(cudaMemsetAsync(c->flags_f.p, 0, (size_t)n * 4, c->stream));
@@ -939,7 +969,7 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
     c->mark(2);
     launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, nullptr, d_ids_out, d_dists_out,
                         d_counts_out, c->x_ids.as<uint64_t>(), c->x_d.as<double>(),
-                        c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), c->stream);
+                        c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), nullptr, c->stream);
     CKL();
     c->stats.kernels_launched += 1;
     c->mark(3);

@@ -25,6 +25,8 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int kFinThreads = 256;
 constexpr int kCandMax = 512;
 constexpr uint32_t kSlotCap = 320;  // staged (plan position, segment) slots per query
+constexpr uint32_t kRepMax = 64;    // failing segments per query repaired in place
+constexpr int kRepChunk = 256;      // rows per repair work unit
 constexpr float kInf = __builtin_inff();
 
 // Merge a sorted-ascending 32-lane list `v` into sorted-ascending `cur`
@@ -76,7 +78,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     const float* __restrict__ cand_d, const uint32_t* __restrict__ cand_row,
     const float* __restrict__ cand_thr, const uint32_t* __restrict__ cand_n, double eps,
     double ab, uint64_t* __restrict__ ids_out, double* __restrict__ d_out,
-    uint32_t* __restrict__ counts_out, int* flags) {
+    uint32_t* __restrict__ counts_out, int* flags, float* __restrict__ tau_out,
+    RepairState rep) {
   extern __shared__ __align__(16) uint8_t sm[];
   double* cdist = reinterpret_cast<double*>(sm);                 // kCandMax
   uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kCandMax);  // kCandMax
@@ -88,6 +91,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   __shared__ uint32_t s_cnt;
   __shared__ int s_bad;
   __shared__ unsigned long long s_total;
+  __shared__ uint32_t s_nfail;
+  __shared__ uint32_t s_fail[kRepMax];  // failing slots (plan position * s_max + segment)
   const uint32_t b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kFinThreads / 32;
@@ -97,6 +102,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     s_cnt = 0;
     s_bad = 0;
     s_total = 0;
+    s_nfail = 0;
   }
   __syncthreads();
   // 0. per plan position metadata (list, segment count, bound) -> smem, in parallel
@@ -191,7 +197,11 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
           clist[pos] = pc[p];
         }
       }
-      if (lane == 0 && __fsub_rd(sthr[v], E) <= tau) s_bad = 1;
+      if (lane == 0 && __fsub_rd(sthr[v], E) <= tau) {
+        s_bad = 1;
+        const uint32_t f = atomicAdd(&s_nfail, 1u);
+        if (f < kRepMax) s_fail[f] = sp[v];
+      }
     }
   } else {
     // more segments than fit in smem: read the scan's outputs from global
@@ -231,13 +241,36 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
           clist[pos] = pc[p];
         }
       }
-      if (lane == 0 && __fsub_rd(cand_thr[slot], E) <= tau) s_bad = 1;
+      if (lane == 0 && __fsub_rd(cand_thr[slot], E) <= tau) {
+        s_bad = 1;
+        const uint32_t f = atomicAdd(&s_nfail, 1u);
+        if (f < kRepMax) s_fail[f] = t;
+      }
     }
   }
   __syncthreads();
   const uint32_t m = s_cnt;
   const float tau = s_tau;
-  if (s_bad || m > kCandMax || !(tau < kInf && tau >= -FLT_MAX) && s_total >= k) {
+  // tau bounds the true k-th distance from above even when the completeness
+  // proof fails: the exact fallback re-filters every row against it
+  if (threadIdx.x == 0 && tau_out) tau_out[b] = tau;
+  const bool tau_ok = tau < kInf && tau >= -FLT_MAX;
+  if (s_bad && rep.entries && m <= kCandMax && tau_ok && s_nfail <= kRepMax) {
+    // proof failed on a few segments only: queue them for the in-place repair
+    // (every row of the segment re-filtered against tau, k_repair_segments)
+    for (uint32_t f = threadIdx.x; f < s_nfail; f += blockDim.x) {
+      const uint32_t e = atomicAdd(rep.n, 1u);
+      if (e < rep.cap) rep.entries[e] = ((uint64_t)b << 32) | s_fail[f];
+      else flags[b] = 1;  // repair list full: whole-query exact fallback
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (flags[b] != 1) flags[b] = 2;
+      rep.cnt[b] = 0;
+    }
+    return;
+  }
+  if (s_bad || m > kCandMax || !tau_ok && s_total >= k) {
     if (threadIdx.x == 0) flags[b] = 1;
     return;
   }
@@ -271,18 +304,178 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   }
 }
 
+// ---- in-place repair of failing segments ---------------------------------------
+// A query whose completeness proof failed on a few (plan position, segment)
+// slots only: every row of those segments is re-tested with the FFMA filter
+// (d^ - E_ffma > tau cannot be in the top-k; tau = finalize's upper bound on the
+// true k-th distance) and the survivors get the exact double.  Work units are
+// (entry, 256-row chunk) over the whole GPU, so one long segment does not
+// serialise on one SM.
+__global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView qv,
+                                                         const uint32_t* __restrict__ plans,
+                                                         uint32_t nprobe, RepairState R,
+                                                         const float* __restrict__ tau, double fa,
+                                                         double fb, double fc, int* flags) {
+  const uint32_t chunks = (ix.seg_rows + kRepChunk - 1) / kRepChunk;
+  const uint32_t n_units = min(*R.n, R.cap) * chunks;
+  for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const uint64_t e = R.entries[u / chunks];
+    const uint32_t ch = u % chunks;
+    const uint32_t b = (uint32_t)(e >> 32), t = (uint32_t)e;
+    const uint32_t p = t / ix.s_max, sg = t % ix.s_max;
+    const uint32_t c = plans[(uint64_t)b * nprobe + p];
+    const uint64_t beg = ix.list_off[c], n_c = ix.list_off[c + 1] - beg;
+    const uint64_t s0 = (uint64_t)sg * ix.seg_rows, s1 = min(n_c, s0 + ix.seg_rows);
+    const uint64_t lr = s0 + (uint64_t)ch * kRepChunk + threadIdx.x;
+    if (s0 + (uint64_t)ch * kRepChunk >= s1) continue;
+    const float tq = tau[b];
+    const float* qs = qv.qs + (uint64_t)b * ix.dpad;
+    double E;
+    {
+      const double q = qv.qnorm[b], x = ix.maxnorm[c];
+      E = fa * q * x + fb * (q * q + x * x) + fc;
+    }
+    if (lr >= s1) continue;
+    const float* lb = list_base(ix, c, beg);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (uint32_t g = 0; g < ix.dpad / 4; ++g) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+      const float4 q4 = __ldg(reinterpret_cast<const float4*>(qs + g * 4));
+      a0 = __fmaf_rn(x.x, q4.x, a0);
+      a1 = __fmaf_rn(x.y, q4.y, a1);
+      a2 = __fmaf_rn(x.z, q4.z, a2);
+      a3 = __fmaf_rn(x.w, q4.w, a3);
+    }
+    const float dot = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
+    const float dh = __fmaf_rn(-2.f, dot, __fadd_rn(ix.xnorm2[beg + lr], qv.qn2[b]));
+    if (__fsub_rd(dh, __double2float_ru(E)) > tq) continue;  // NaN keeps the row
+    const double d = exact_row_pipelined(ix.dim, qs, [&](uint32_t g) {
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+    });
+    const uint32_t pos = atomicAdd(&R.cnt[b], 1u);
+    if (pos < R.per_query) {
+      R.d[(uint64_t)b * R.per_query + pos] = d;
+      R.ids[(uint64_t)b * R.per_query + pos] = ix.ids[beg + lr];
+    } else {
+      flags[b] = 1;  // too many survivors: whole-query exact fallback
+    }
+  }
+}
+
+// Repaired queries (flag 2): candidates of the slots that passed the proof
+// (recomputed with the same tau, so the same slots) + the repaired segments'
+// exact survivors -> (d, id) sort -> top-k.
+__global__ void __launch_bounds__(kFinThreads) k_finalize_repair(
+    IndexView ix, QueryView qv, const uint32_t* __restrict__ plans, uint32_t nprobe, uint32_t k,
+    const float* __restrict__ cand_d, const uint32_t* __restrict__ cand_row,
+    const float* __restrict__ cand_thr, const uint32_t* __restrict__ cand_n,
+    const float* __restrict__ tau, RepairState R, uint64_t* __restrict__ ids_out,
+    double* __restrict__ d_out, uint32_t* __restrict__ counts_out, int* flags) {
+  const uint32_t b = blockIdx.x;
+  if (flags[b] != 2) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  constexpr uint32_t kCap = 2 * kCandMax;
+  double* cdist = reinterpret_cast<double*>(sm);               // kCap
+  uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kCap);    // kCap
+  uint32_t* crow = reinterpret_cast<uint32_t*>(cid + kCap);     // kCandMax
+  uint32_t* clist = crow + kCandMax;                            // kCandMax
+  float* qsh = reinterpret_cast<float*>(clist + kCandMax);      // dpad
+  __shared__ uint32_t s_cnt;
+  __shared__ int s_over;
+  __shared__ unsigned long long s_total;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = kFinThreads / 32;
+  for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)b * ix.dpad + d];
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_over = 0;
+    s_total = 0;
+  }
+  __syncthreads();
+  const float tq = tau[b], qn = qv.qnorm[b];
+  const uint64_t slot0 = (uint64_t)b * nprobe * ix.s_max;
+  for (uint32_t p = warp; p < nprobe; p += NW) {
+    const uint32_t c = plans[(uint64_t)b * nprobe + p];
+    const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
+    if (lane == 0) atomicAdd(&s_total, (unsigned long long)rows);
+    const uint32_t ns = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+    const float E = seg_bound(ix, qn, ix.maxnorm[c]);
+    for (uint32_t sg = 0; sg < ns; ++sg) {
+      const uint64_t slot = slot0 + (uint64_t)p * ix.s_max + sg;
+      if (__fsub_rd(cand_thr[slot], E) <= tq) continue;  // repaired segment
+      const uint32_t n = cand_n[slot];
+      const bool take = lane < (int)n && __fsub_rd(cand_d[slot * kKP + lane], E) <= tq;
+      const unsigned msk = __ballot_sync(FULL, take);
+      uint32_t base = 0;
+      if (lane == 0 && msk) base = atomicAdd(&s_cnt, (uint32_t)__popc(msk));
+      base = __shfl_sync(FULL, base, 0);
+      if (take) {
+        const uint32_t pos = base + __popc(msk & ((1u << lane) - 1));
+        if (pos < kCandMax) {
+          crow[pos] = cand_row[slot * kKP + lane];
+          clist[pos] = c;
+        } else {
+          s_over = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t m = min(s_cnt, (uint32_t)kCandMax);
+  const uint32_t r = min(R.cnt[b], R.per_query);
+  if (s_over || m + r > kCap) {
+    if (threadIdx.x == 0) flags[b] = 1;
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint32_t c = clist[i];
+    const uint64_t lbeg = ix.list_off[c];
+    const uint64_t n_c = ix.list_off[c + 1] - lbeg;
+    const uint64_t lr = crow[i] - lbeg;
+    const float* lb = list_base(ix, c, lbeg);
+    cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+    });
+    cid[i] = ix.ids[crow[i]];
+  }
+  for (uint32_t i = threadIdx.x; i < r; i += blockDim.x) {
+    cdist[m + i] = R.d[(uint64_t)b * R.per_query + i];
+    cid[m + i] = R.ids[(uint64_t)b * R.per_query + i];
+  }
+  uint32_t mp = 1;
+  while (mp < m + r) mp <<= 1;
+  for (uint32_t i = m + r + threadIdx.x; i < mp; i += blockDim.x) {
+    cdist[i] = DBL_MAX;
+    cid[i] = ~0ull;
+  }
+  block_sort_pairs(cdist, cid, mp);
+  const uint32_t cnt = (uint32_t)min((unsigned long long)k, s_total);
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+    ids_out[(uint64_t)b * k + i] = i < cnt ? cid[i] : 0;
+    d_out[(uint64_t)b * k + i] = i < cnt ? cdist[i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    counts_out[b] = cnt;
+    flags[b] = 0;
+  }
+}
+
 // Exact streaming top-k (the reference algorithm on the GPU: every row of the
 // plan, exact distance, (d, id) order) for flagged queries and k > 32.
 // Grid (query, part): part y covers plan positions [y*per, (y+1)*per); with
 // more than one part each CTA writes its exact partial top-k and
 // k_exact_merge combines them (lists are disjoint, so the merge is exact).
 // Buffer of `cap` (d, id) pairs filtered by the running k-th.
+// With `tau` (finalize's upper bound on the query's true k-th distance), a
+// row whose FFMA filter distance d^ satisfies d^ - E > tau (E: the FFMA bound of
+// scan.cu, any summation order) cannot be in the top-k and skips the fp64 chain.
 __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv,
                                                       const uint32_t* __restrict__ plans,
                                                       uint32_t nprobe, uint32_t k, uint32_t cap,
                                                       const int* flags, uint64_t* ids_out,
                                                       double* d_out, uint32_t* counts_out,
-                                                      uint64_t* part_total) {
+                                                      uint64_t* part_total, const float* tau,
+                                                      double fa, double fb, double fc) {
   const uint32_t b = blockIdx.x;
   if (flags && !flags[b]) return;
   const uint32_t nsplit = gridDim.y, y = blockIdx.y;
@@ -305,10 +498,18 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
     s_total = 0;
   }
   __syncthreads();
+  const float tq = tau ? tau[b] : __int_as_float(0x7f800000);
+  const bool filt = tq < __int_as_float(0x7f800000) && tq >= -FLT_MAX;
+  const float qn = qv.qnorm[b], qn2 = qv.qn2[b];
   for (uint32_t p = p_beg; p < p_end; ++p) {
     const uint32_t c = plans[(uint64_t)b * nprobe + p];
     const uint64_t beg = ix.list_off[c], end = ix.list_off[c + 1];
     if (threadIdx.x == 0) s_total += end - beg;
+    float E = 0.f;
+    if (filt) {
+      const double q = qn, x = ix.maxnorm[c];
+      E = __double2float_ru(fa * q * x + fb * (q * q + x * x) + fc);
+    }
     for (uint64_t r0 = beg; r0 < end; r0 += blockDim.x) {
       const uint64_t r = r0 + threadIdx.x;
       double dist = DBL_MAX;
@@ -316,10 +517,27 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
       if (r < end) {
         const uint64_t n_c = end - beg, lr = r - beg;
         const float* lb = list_base(ix, c, beg);
-        dist = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-          return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
-        });
-        id = ix.ids[r];
+        bool need = true;
+        if (filt) {
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+          for (uint32_t g = 0; g < ix.dpad / 4; ++g) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+            const float4 q4 = *reinterpret_cast<const float4*>(qsh + g * 4);
+            a0 = __fmaf_rn(x.x, q4.x, a0);
+            a1 = __fmaf_rn(x.y, q4.y, a1);
+            a2 = __fmaf_rn(x.z, q4.z, a2);
+            a3 = __fmaf_rn(x.w, q4.w, a3);
+          }
+          const float dot = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
+          const float dh = __fmaf_rn(-2.f, dot, __fadd_rn(ix.xnorm2[r], qn2));
+          need = !(__fsub_rd(dh, E) > tq);  // NaN keeps the row (exact path decides)
+        }
+        if (need) {
+          dist = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
+            return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+          });
+          id = ix.ids[r];
+        }
       }
       const uint32_t cnt_now = s_cnt;
       __syncthreads();  // every thread has read s_cnt before any append
@@ -465,7 +683,9 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                             uint32_t nprobe, uint32_t k, const float* cand_d,
                             const uint32_t* cand_row, const float* cand_thr,
                             const uint32_t* cand_n, uint64_t* ids_out, double* d_out,
-                            uint32_t* counts_out, int* flags, cudaStream_t s) {
+                            uint32_t* counts_out, int* flags, float* tau_out,
+                            const RepairState* rep, cudaStream_t s) {
+  const RepairState R = rep ? *rep : RepairState{};
   const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 4 + (size_t)nprobe * 16 + 4 +
                       (size_t)kSlotCap * (4 + 4 + 4 + kKP * 4);
   static bool attr = false;
@@ -477,7 +697,7 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
   k_finalize_search<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row,
                                                     cand_thr, cand_n, filter_eps(ix.dim),
                                                     filter_abs(ix.dim), ids_out, d_out,
-                                                    counts_out, flags);
+                                                    counts_out, flags, tau_out, R);
 }
 
 uint32_t exact_search_parts(uint32_t nprobe, uint32_t k) {
@@ -490,7 +710,9 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
                          uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
                          double* d_out, uint32_t* counts_out, uint64_t* part_ids,
                          double* part_d, uint32_t* part_cnt, uint64_t* part_total,
-                         cudaStream_t s) {
+                         const float* tau, cudaStream_t s) {
+  double fa = 0, fb = 0, fc = 0;
+  bound_ffma(ix.dim, &fa, &fb, &fc);
   uint32_t cap = 512;
   while (cap < k + 256) cap <<= 1;
   const size_t smem = (size_t)cap * 16 + (size_t)ix.dpad * 4;
@@ -503,11 +725,11 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
   const uint32_t ns = part_ids ? exact_search_parts(nprobe, k) : 1;
   if (ns <= 1) {
     k_exact_search<<<dim3(qv.n, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
-                                                    d_out, counts_out, nullptr);
+                                                    d_out, counts_out, nullptr, tau, fa, fb, fc);
     return;
   }
   k_exact_search<<<dim3(qv.n, ns), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, part_ids,
-                                                   part_d, part_cnt, part_total);
+                                                   part_d, part_cnt, part_total, tau, fa, fb, fc);
   uint32_t mcap = 1;
   while (mcap < ns * k) mcap <<= 1;
   k_exact_merge<<<qv.n, 256, (size_t)mcap * 16, s>>>(ns, k, mcap, flags, part_ids, part_d,
@@ -531,5 +753,23 @@ void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const 
 }
 
 // Node-split sub-search finalize lives in items.cu.
+
+
+void launch_repair(const IndexView& ix, const QueryView& qv, const uint32_t* plans, uint32_t nprobe,
+                   uint32_t k, const float* cand_d, const uint32_t* cand_row, const float* cand_thr,
+                   const uint32_t* cand_n, const float* tau, const RepairState& R, int n_ctas,
+                   uint64_t* ids_out, double* d_out, uint32_t* counts_out, int* flags, cudaStream_t s) {
+  double fa = 0, fb = 0, fc = 0;
+  bound_ffma(ix.dim, &fa, &fb, &fc);
+  k_repair_segments<<<n_ctas, 256, 0, s>>>(ix, qv, plans, nprobe, R, tau, fa, fb, fc, flags);
+  const size_t smem = (size_t)2 * kCandMax * 16 + (size_t)kCandMax * 8 + (size_t)ix.dpad * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_finalize_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_finalize_repair<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row, cand_thr,
+                                                    cand_n, tau, R, ids_out, d_out, counts_out, flags);
+}
 
 }  // namespace hivf

@@ -139,6 +139,20 @@ void launch_far_point(const float* X, uint64_t n, uint32_t dim, const uint32_t* 
                       cudaStream_t s);
 
 // ---- finalize.cu
+// In-place repair of segments whose completeness proof failed (finalize.cu).
+struct RepairState {
+  uint64_t* entries;  // (query << 32 | plan position * s_max + segment)
+  uint32_t* n;        // entries used (device counter, zeroed per call)
+  uint32_t cap;       // entries capacity
+  uint32_t* cnt;      // [n_queries] exact survivors per query
+  double* d;          // [n_queries][per_query]
+  uint64_t* ids;      // [n_queries][per_query]
+  uint32_t per_query;
+};
+void launch_repair(const IndexView& ix, const QueryView& qv, const uint32_t* plans, uint32_t nprobe,
+                   uint32_t k, const float* cand_d, const uint32_t* cand_row, const float* cand_thr,
+                   const uint32_t* cand_n, const float* tau, const RepairState& R, int n_ctas,
+                   uint64_t* ids_out, double* d_out, uint32_t* counts_out, int* flags, cudaStream_t s);
 void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t nprobe, uint32_t K,
                            uint32_t* pair_query, uint32_t* pair_list, uint32_t* plans_out, int* err,
                            cudaStream_t s);
@@ -146,7 +160,8 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                             uint32_t nprobe, uint32_t k, const float* cand_d,
                             const uint32_t* cand_row, const float* cand_thr,
                             const uint32_t* cand_n, uint64_t* ids_out, double* d_out,
-                            uint32_t* counts_out, int* flags, cudaStream_t s);
+                            uint32_t* counts_out, int* flags, float* tau_out,
+                            const RepairState* rep, cudaStream_t s);
 // part_* scratch (n_queries x exact_search_parts() x k) enables the multi-CTA
 // path; pass nullptr for one CTA per query.
 uint32_t exact_search_parts(uint32_t nprobe, uint32_t k);
@@ -154,7 +169,7 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
                          uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
                          double* d_out, uint32_t* counts_out, uint64_t* part_ids,
                          double* part_d, uint32_t* part_cnt, uint64_t* part_total,
-                         cudaStream_t s);
+                         const float* tau, cudaStream_t s);
 void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
                            const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
                            const float* cand_d, const uint32_t* cand_row, const float* cand_thr,

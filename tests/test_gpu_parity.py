@@ -345,3 +345,23 @@ def test_assign_device_and_planned_search(ctx):
     oi, od, oc = csr.search(Q, npb, k)
     assert np.array_equal(outs[1][0].cpu().numpy().astype(np.uint64), oi)
     assert np.array_equal(outs[1][1].cpu().numpy().view(np.uint64), od.view(np.uint64))
+
+
+def test_shard_index_escalation_and_filtered_fallback(ctx):
+    """A list shard (most probed lists empty, local top-k far away) makes the
+    single-pass proof fail for some queries: the split-precision escalation
+    pass and the tau-filtered exact fallback must still give the reference's
+    exact results."""
+    from paper_2507_09138_b200 import IvfIndex
+    rng = np.random.default_rng(77)
+    n, dim, K = 60000, 256, 64
+    X, centers = _mixture(rng, n, dim, 16, 0.05)
+    cents = X[rng.choice(n, K, replace=False)].copy()
+    assign = np.asarray(oracle.compute_assignments(X, cents))
+    keep = np.isin(assign, np.arange(0, K, 8))           # shard 0 of 8 (by list id)
+    ids = np.arange(n, dtype=np.uint64)
+    csr = oracle.CsrIndex.from_assignments(X[keep], ids[keep], cents, assign[keep])
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
+    Q = (centers[rng.integers(0, 16, 64)] + 0.05 * rng.standard_normal((64, dim))).astype(np.float32)
+    for nprobe, k in [(32, 10), (64, 32), (16, 1)]:
+        _check_search(ix, csr, Q, nprobe, k)
