@@ -132,6 +132,13 @@ hivf_status hivf_compute_assignments(hivf_ctx* ctx, const float* d_corpus, uint6
 hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim,
                               uint32_t n_clusters, uint32_t max_iters, uint64_t seed,
                               float* d_centroids_out);
+/* Same with host buffers (staged through HBM), as the C++ adapter calls them. */
+hivf_status hivf_compute_assignments_host(hivf_ctx* ctx, const float* corpus, uint64_t n, uint32_t dim,
+                                          const float* centroids, uint32_t n_clusters,
+                                          uint32_t* assign_out);
+hivf_status hivf_train_kmeans_host(hivf_ctx* ctx, const float* corpus, uint64_t n, uint32_t dim,
+                                   uint32_t n_clusters, uint32_t max_iters, uint64_t seed,
+                                   float* centroids_out);
 
 /* ---- coarse assign --------------------------------------------------------
  * Batched ivf::select_clusters (proj/src/vector_index.cpp:261-278): for each

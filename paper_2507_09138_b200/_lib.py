@@ -23,7 +23,7 @@ SYMBOLS = [
     "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
     "hivf_assign", "hivf_search", "hivf_search_device", "hivf_assign_device",
     "hivf_search_planned_device", "hivf_scan_items", "hivf_compute_assignments",
-    "hivf_train_kmeans",
+    "hivf_train_kmeans", "hivf_compute_assignments_host", "hivf_train_kmeans_host",
     "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get",
     "hivf_residency_sync", "hivf_last_stats",
     "hivf_set_option",
@@ -89,6 +89,8 @@ def lib():
         "hivf_assign_device": (i32, [vp, vp, u32, u32, vp, vp]),
         "hivf_compute_assignments": (i32, [vp, vp, u64, u32, vp, u32, vp]),
         "hivf_train_kmeans": (i32, [vp, vp, u64, u32, u32, u32, u64, vp]),
+        "hivf_compute_assignments_host": (i32, [vp, vp, u64, u32, vp, u32, vp]),
+        "hivf_train_kmeans_host": (i32, [vp, vp, u64, u32, u32, u32, u64, vp]),
         "hivf_search_planned_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp, vp]),
         "hivf_scan_items": (i32, [vp, vp, u32, vp, vp, vp, vp, vp, vp, u32, vp]),
         "hivf_merge_parts_device": (i32, [vp, u32, u32, u32, vp, vp, vp, vp, vp, vp]),

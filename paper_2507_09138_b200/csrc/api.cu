@@ -1230,6 +1230,47 @@ hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, 
   return HIVF_OK;
 }
 
+// host-buffer forms (the C++ adapter's ivf::train_kmeans / compute_assignments)
+hivf_status hivf_train_kmeans_host(hivf_ctx* ctx, const float* corpus, uint64_t n, uint32_t dim, uint32_t K,
+                                   uint32_t max_iters, uint64_t seed, float* centroids_out) {
+  if (!ctx || !corpus || !centroids_out) return fail(HIVF_EINVAL, "train_kmeans: NULL argument");
+  if (n < K) return fail(HIVF_EINVAL, "train_kmeans: corpus smaller than k_clusters");
+  CK(cudaSetDevice(ctx->device));
+  DevScratch S;
+  float *dx = nullptr, *dc = nullptr;
+  cudaError_t e;
+  if ((e = S.alloc((void**)&dx, n * dim * 4ull)) != cudaSuccess || (e = S.alloc((void**)&dc, (uint64_t)K * dim * 4)) != cudaSuccess)
+    return fail(HIVF_ENOMEM, "train_kmeans staging: %s", cudaGetErrorString(e));
+  CK(cudaMemcpyAsync(dx, corpus, n * dim * 4ull, cudaMemcpyHostToDevice, ctx->stream));
+  hivf_status st = hivf_train_kmeans(ctx, dx, n, dim, K, max_iters, seed, dc);
+  if (st != HIVF_OK) return st;
+  CK(cudaMemcpyAsync(centroids_out, dc, (uint64_t)K * dim * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HIVF_OK;
+}
+
+hivf_status hivf_compute_assignments_host(hivf_ctx* ctx, const float* corpus, uint64_t n, uint32_t dim,
+                                          const float* centroids, uint32_t K, uint32_t* assign_out) {
+  if (!ctx || (!corpus && n) || !centroids || (!assign_out && n))
+    return fail(HIVF_EINVAL, "compute_assignments: NULL argument");
+  if (n == 0) return HIVF_OK;
+  CK(cudaSetDevice(ctx->device));
+  DevScratch S;
+  float *dx = nullptr, *dc = nullptr;
+  uint32_t* da = nullptr;
+  cudaError_t e;
+  if ((e = S.alloc((void**)&dx, n * dim * 4ull)) != cudaSuccess ||
+      (e = S.alloc((void**)&dc, (uint64_t)K * dim * 4)) != cudaSuccess || (e = S.alloc((void**)&da, n * 4ull)) != cudaSuccess)
+    return fail(HIVF_ENOMEM, "compute_assignments staging: %s", cudaGetErrorString(e));
+  CK(cudaMemcpyAsync(dx, corpus, n * dim * 4ull, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dc, centroids, (uint64_t)K * dim * 4, cudaMemcpyHostToDevice, ctx->stream));
+  hivf_status st = hivf_compute_assignments(ctx, dx, n, dim, dc, K, da);
+  if (st != HIVF_OK) return st;
+  CK(cudaMemcpyAsync(assign_out, da, n * 4ull, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HIVF_OK;
+}
+
 // ---------------------------------------------------------------------------
 // node-split sub-search
 // ---------------------------------------------------------------------------

@@ -144,6 +144,52 @@ double IvfIndex::mean_assigned_distance() const {
   return m;
 }
 
+// ---- index build ------------------------------------------------------------------
+Centroids train_kmeans(Context& ctx, const Corpus& corpus, std::size_t k_clusters, std::size_t max_iters,
+                       std::uint64_t seed) {
+  if (corpus.size() < k_clusters) throw std::invalid_argument("train_kmeans: corpus smaller than k_clusters");
+  if (k_clusters == 0) throw std::invalid_argument("train_kmeans: k_clusters must be >= 1");
+  if (max_iters == 0) throw std::invalid_argument("train_kmeans: max_iters must be >= 1");
+  std::vector<float> out(k_clusters * corpus.dim);
+  check(hivf_train_kmeans_host(ctx.raw(), corpus.data.data(), corpus.size(), corpus.dim,
+                               static_cast<std::uint32_t>(k_clusters), static_cast<std::uint32_t>(max_iters),
+                               seed, out.data()));
+  Centroids c;
+  c.dim = corpus.dim;
+  for (std::size_t r = 0; r < k_clusters; ++r)
+    c.rows.emplace_back(out.begin() + r * corpus.dim, out.begin() + (r + 1) * corpus.dim);
+  return c;
+}
+
+std::vector<ClusterId> compute_assignments(Context& ctx, const Corpus& corpus, const Centroids& centroids) {
+  std::vector<float> cents;
+  for (const auto& r : centroids.rows) {
+    if (r.size() != corpus.dim) throw std::invalid_argument("build_index: dimension mismatch");
+    cents.insert(cents.end(), r.begin(), r.end());
+  }
+  std::vector<ClusterId> a(corpus.size());
+  check(hivf_compute_assignments_host(ctx.raw(), corpus.data.data(), corpus.size(), corpus.dim, cents.data(),
+                                      static_cast<std::uint32_t>(centroids.k_clusters()), a.data()));
+  return a;
+}
+
+std::shared_ptr<IvfIndex> build_index(Context& ctx, const Corpus& corpus, const Centroids& centroids,
+                                      Metric metric) {
+  if (corpus.dim != centroids.dim) throw std::invalid_argument("build_index: dimension mismatch");
+  if (metric == Metric::Cosine) {  // vector_index.cpp:245-252
+    Corpus nc = corpus;
+    for (std::size_t i = 0; i < corpus.size(); ++i) {
+      Embedding e = normalized(corpus.embedding(i));
+      std::copy(e.begin(), e.end(), nc.data.begin() + i * corpus.dim);
+    }
+    return IvfIndex::from_assignments(ctx, nc.data, nc.doc_ids, nc.dim, metric, centroids.rows,
+                                      compute_assignments(ctx, nc, centroids));
+  }
+  // duplicate doc ids -> invalid_argument (vector_index.cpp:240-244) in hivf_index_finish
+  return IvfIndex::from_assignments(ctx, corpus.data, corpus.doc_ids, corpus.dim, metric, centroids.rows,
+                                    compute_assignments(ctx, corpus, centroids));
+}
+
 // ---- search API ---------------------------------------------------------------
 std::vector<ClusterId> select_clusters(const IvfIndex& index, const Embedding& query,
                                        std::size_t nprobe) {

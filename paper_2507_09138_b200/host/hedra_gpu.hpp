@@ -89,6 +89,23 @@ class Context {
   hivf_ctx* ctx_ = nullptr;
 };
 
+// vector_index.hpp:14-34
+struct Corpus {
+  std::uint32_t dim = 0;
+  Metric metric = Metric::L2;
+  std::vector<float> data;     // count * dim, row-major
+  std::vector<DocId> doc_ids;  // count
+  std::size_t size() const { return doc_ids.size(); }
+  const float* row(std::size_t i) const { return data.data() + i * dim; }
+  Embedding embedding(std::size_t i) const { return Embedding(row(i), row(i) + dim); }
+};
+
+struct Centroids {
+  std::uint32_t dim = 0;
+  std::vector<std::vector<float>> rows;
+  std::size_t k_clusters() const { return rows.size(); }
+};
+
 // The HBM-resident index (vector_index.hpp:83-113 without the host copies).
 class IvfIndex {
  public:
@@ -121,6 +138,16 @@ class IvfIndex {
   std::uint32_t dim_ = 0;
   Metric metric_ = Metric::L2;
 };
+
+// Index build on the GPU, bit-identical to the reference
+// (vector_index.cpp:99-259): train_kmeans, compute_assignments, build_index
+// (duplicate-id check, cosine normalization, assignment, index_from_assignments).
+Centroids train_kmeans(Context& ctx, const Corpus& corpus, std::size_t k_clusters,
+                       std::size_t max_iters, std::uint64_t seed);
+std::vector<ClusterId> compute_assignments(Context& ctx, const Corpus& corpus,
+                                           const Centroids& centroids);
+std::shared_ptr<IvfIndex> build_index(Context& ctx, const Corpus& corpus, const Centroids& centroids,
+                                      Metric metric);
 
 struct SearchCursor {
   Embedding query;

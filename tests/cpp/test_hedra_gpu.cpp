@@ -456,6 +456,50 @@ TEST_GPU(cache_update_swaps_ties_midswap_capacity) {  // test_tiered_cache.cpp:5
   }
 }
 
+// ---- index build (vector_index.cpp:99-259) ----------------------------------------
+TEST_GPU(build_index_equals_from_assignments_and_brute_force) {
+  // build_index = compute_assignments + index_from_assignments; with nprobe = K
+  // the IVF search equals brute force exactly (test_vector_index.cpp:196-208)
+  ivf::Context ctx(0);
+  const Data d = random_data(91, 3000, 12, 24);
+  ivf::Corpus corpus;
+  corpus.dim = d.dim;
+  corpus.data = d.x;
+  corpus.doc_ids = d.ids;
+  ivf::Centroids cents;
+  cents.dim = d.dim;
+  cents.rows = d.cents;
+  const auto asg = ivf::compute_assignments(ctx, corpus, cents);
+  CHECK(asg == d.assign);  // the C restatement's nearest_centroid, ties -> lowest id
+  auto ix = ivf::build_index(ctx, corpus, cents, Metric::L2);
+  std::mt19937_64 g(5);
+  for (int t = 0; t < 10; ++t) {
+    const Embedding q = rand_query(g, d.dim);
+    auto cur = ivf::make_cursor(*ix, q, cents.rows.size(), 10);
+    while (!cur.done()) ivf::search_step(*ix, cur, 7);
+    CHECK(cur.heap == brute(d, q, 10));
+  }
+}
+
+TEST_GPU(train_kmeans_contract) {
+  ivf::Context ctx(0);
+  const Data d = random_data(17, 2000, 8, 4);
+  ivf::Corpus corpus;
+  corpus.dim = d.dim;
+  corpus.data = d.x;
+  corpus.doc_ids = d.ids;
+  const auto a = ivf::train_kmeans(ctx, corpus, 16, 5, 3);
+  const auto b = ivf::train_kmeans(ctx, corpus, 16, 5, 3);
+  CHECK(a.k_clusters() == 16 && a.dim == 8);
+  CHECK(a.rows == b.rows);  // deterministic for a seed
+  // every centroid is a mean of data or a data point: finite
+  for (const auto& r : a.rows)
+    for (float v : r) CHECK(std::isfinite(v));
+  CHECK_THROWS_AS(ivf::train_kmeans(ctx, corpus, 3000, 5, 3), std::invalid_argument);  // n < K
+  CHECK_THROWS_AS(ivf::train_kmeans(ctx, corpus, 0, 5, 3), std::invalid_argument);
+  CHECK_THROWS_AS(ivf::train_kmeans(ctx, corpus, 4, 0, 3), std::invalid_argument);
+}
+
 int main(int argc, char** argv) {
   const bool cpu_only = argc > 1 && std::strcmp(argv[1], "--cpu-only") == 0;
   int ran = 0;
