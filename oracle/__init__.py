@@ -110,6 +110,13 @@ def ref():
         R.ref_compute_assignments.restype = C.c_int
         R.ref_compute_assignments.argtypes = [_f32p, C.c_uint64, C.c_uint32, _f32p,
                                               C.c_uint32, _u32p]
+        for nm in ("ref_save_corpus", "ref_save_centroids", "ref_save_assignments", "ref_load_corpus"):
+            getattr(R, nm).restype = C.c_int
+        R.ref_save_corpus.argtypes = [C.c_char_p, _f32p, _u64p, C.c_uint64, C.c_uint32, C.c_int]
+        R.ref_save_centroids.argtypes = [C.c_char_p, _f32p, C.c_uint32, C.c_uint32, C.c_int]
+        R.ref_save_assignments.argtypes = [C.c_char_p, _u32p, C.c_uint64]
+        R.ref_load_corpus.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_int), C.c_void_p, C.c_void_p]
         R.ref_select_clusters.restype = C.c_int
         R.ref_select_clusters.argtypes = [vp, _f32p, C.c_uint32, _u32p]
         R.ref_search.restype = C.c_int

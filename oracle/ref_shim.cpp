@@ -121,6 +121,34 @@ int ref_train_kmeans(const float* corpus, uint64_t n, uint32_t dim, uint32_t k_c
   });
 }
 
+// --- persistence (vector_index.cpp:344-473), for byte-level parity tests ------
+int ref_save_corpus(const char* path, const float* data, const uint64_t* ids, uint64_t n, uint32_t dim,
+                    int metric) {
+  return guarded([&] { ivf::save_corpus(path, make_corpus(data, ids, n, dim, metric)); });
+}
+int ref_save_centroids(const char* path, const float* rows, uint32_t k, uint32_t dim, int metric) {
+  return guarded([&] {
+    ivf::Centroids c;
+    c.dim = dim;
+    for (uint32_t i = 0; i < k; ++i) c.rows.emplace_back(rows + uint64_t(i) * dim, rows + uint64_t(i + 1) * dim);
+    ivf::save_centroids(path, c, static_cast<Metric>(metric));
+  });
+}
+int ref_save_assignments(const char* path, const uint32_t* a, uint64_t n) {
+  return guarded([&] { ivf::save_assignments(path, std::vector<ClusterId>(a, a + n)); });
+}
+// load_corpus into caller buffers sized by a first call with data == nullptr
+int ref_load_corpus(const char* path, uint32_t* dim, uint64_t* n, int* metric, float* data, uint64_t* ids) {
+  return guarded([&] {
+    auto c = ivf::load_corpus(path);
+    *dim = c.dim;
+    *n = c.size();
+    *metric = static_cast<int>(c.metric);
+    if (data) std::memcpy(data, c.data.data(), c.data.size() * sizeof(float));
+    if (ids) std::memcpy(ids, c.doc_ids.data(), c.doc_ids.size() * sizeof(uint64_t));
+  });
+}
+
 int ref_compute_assignments(const float* corpus, uint64_t n, uint32_t dim,
                             const float* centroids, uint32_t k_clusters, uint32_t* out) {
   return guarded([&] {

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstring>
 #include <numeric>
 
 namespace hedra_gpu {
@@ -142,6 +144,102 @@ double IvfIndex::mean_assigned_distance() const {
   double m = 0.0;
   check(hivf_index_info(ix_, nullptr, nullptr, nullptr, nullptr, &m));
   return m;
+}
+
+// ---- persistence (HVEC / u32, vector_index.cpp:344-473 formats) -----------------------
+namespace {
+struct File {
+  std::FILE* f = nullptr;
+  std::string path;
+  File(const std::string& p, const char* mode) : path(p) {
+    f = std::fopen(p.c_str(), mode);
+    if (!f) throw std::runtime_error(p + (mode[0] == 'w' ? ": cannot open for writing" : ": cannot open for reading"));
+  }
+  ~File() {
+    if (f) std::fclose(f);
+  }
+  void put(const void* p, std::size_t bytes) {
+    if (bytes && std::fwrite(p, 1, bytes, f) != bytes) throw std::runtime_error(path + ": write failed");
+  }
+  void get(void* p, std::size_t bytes, const char* what) {
+    if (bytes && std::fread(p, 1, bytes, f) != bytes) throw std::runtime_error(path + what);
+  }
+};
+constexpr char kHvec[4] = {'H', 'V', 'E', 'C'};
+void put_header(File& o, std::uint32_t dim, std::uint64_t count, Metric m) {
+  const std::uint32_t version = 1;
+  const std::uint8_t metric = static_cast<std::uint8_t>(m);
+  o.put(kHvec, 4);
+  o.put(&version, 4);
+  o.put(&dim, 4);
+  o.put(&count, 8);
+  o.put(&metric, 1);
+}
+void get_header(File& in, std::uint32_t* dim, std::uint64_t* count, Metric* m) {
+  char magic[4];
+  if (std::fread(magic, 1, 4, in.f) != 4 || std::memcmp(magic, kHvec, 4) != 0)
+    throw std::runtime_error(in.path + ": not a HVEC file");
+  std::uint32_t version = 0;
+  std::uint8_t metric = 0;
+  in.get(&version, 4, ": truncated read");
+  if (version != 1) throw std::runtime_error(in.path + ": unsupported HVEC version");
+  in.get(dim, 4, ": truncated read");
+  in.get(count, 8, ": truncated read");
+  in.get(&metric, 1, ": truncated read");
+  *m = static_cast<Metric>(metric);
+}
+}  // namespace
+
+void save_corpus(const std::string& path, const Corpus& corpus) {
+  File o(path, "wb");
+  put_header(o, corpus.dim, corpus.size(), corpus.metric);
+  o.put(corpus.data.data(), corpus.data.size() * sizeof(float));
+  o.put(corpus.doc_ids.data(), corpus.doc_ids.size() * sizeof(DocId));
+}
+
+Corpus load_corpus(const std::string& path) {
+  File in(path, "rb");
+  Corpus c;
+  std::uint64_t n = 0;
+  get_header(in, &c.dim, &n, &c.metric);
+  c.data.resize(n * c.dim);
+  c.doc_ids.resize(n);
+  in.get(c.data.data(), c.data.size() * sizeof(float), ": truncated corpus file");
+  in.get(c.doc_ids.data(), c.doc_ids.size() * sizeof(DocId), ": truncated corpus file");
+  return c;
+}
+
+void save_centroids(const std::string& path, const Centroids& centroids, Metric metric) {
+  File o(path, "wb");
+  put_header(o, centroids.dim, centroids.k_clusters(), metric);
+  for (const auto& r : centroids.rows) o.put(r.data(), r.size() * sizeof(float));
+}
+
+Centroids load_centroids(const std::string& path) {
+  File in(path, "rb");
+  Centroids c;
+  std::uint64_t k = 0;
+  Metric m;
+  get_header(in, &c.dim, &k, &m);
+  c.rows.assign(k, std::vector<float>(c.dim));
+  for (auto& r : c.rows) in.get(r.data(), r.size() * sizeof(float), ": truncated centroid file");
+  return c;
+}
+
+void save_assignments(const std::string& path, const std::vector<ClusterId>& assign) {
+  File o(path, "wb");
+  const std::uint64_t n = assign.size();
+  o.put(&n, 8);
+  o.put(assign.data(), assign.size() * sizeof(ClusterId));
+}
+
+std::vector<ClusterId> load_assignments(const std::string& path) {
+  File in(path, "rb");
+  std::uint64_t n = 0;
+  in.get(&n, 8, ": truncated read");
+  std::vector<ClusterId> a(n);
+  in.get(a.data(), a.size() * sizeof(ClusterId), ": truncated assignment file");
+  return a;
 }
 
 // ---- index build ------------------------------------------------------------------
@@ -491,3 +589,78 @@ RetStepReport RetrievalEngine::execute(SubStageBatch& batch, double now_ms, bool
 
 }  // namespace ret
 }  // namespace hedra_gpu
+
+// ---- C entry points over the persistence functions (ctypes parity tests) -----------
+extern "C" {
+int hg_save_corpus(const char* path, const float* data, const std::uint64_t* ids, std::uint64_t n,
+                   std::uint32_t dim, int metric) {
+  try {
+    hedra_gpu::ivf::Corpus c;
+    c.dim = dim;
+    c.metric = static_cast<hedra_gpu::Metric>(metric);
+    c.data.assign(data, data + n * dim);
+    c.doc_ids.assign(ids, ids + n);
+    hedra_gpu::ivf::save_corpus(path, c);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+int hg_save_centroids(const char* path, const float* rows, std::uint32_t k, std::uint32_t dim, int metric) {
+  try {
+    hedra_gpu::ivf::Centroids c;
+    c.dim = dim;
+    for (std::uint32_t i = 0; i < k; ++i) c.rows.emplace_back(rows + std::uint64_t(i) * dim, rows + std::uint64_t(i + 1) * dim);
+    hedra_gpu::ivf::save_centroids(path, c, static_cast<hedra_gpu::Metric>(metric));
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+int hg_save_assignments(const char* path, const std::uint32_t* a, std::uint64_t n) {
+  try {
+    hedra_gpu::ivf::save_assignments(path, std::vector<hedra_gpu::ClusterId>(a, a + n));
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+// load_corpus / load_centroids / load_assignments: sizes first (data == nullptr)
+int hg_load_corpus(const char* path, std::uint32_t* dim, std::uint64_t* n, int* metric, float* data,
+                   std::uint64_t* ids) {
+  try {
+    auto c = hedra_gpu::ivf::load_corpus(path);
+    *dim = c.dim;
+    *n = c.size();
+    *metric = static_cast<int>(c.metric);
+    if (data) std::memcpy(data, c.data.data(), c.data.size() * sizeof(float));
+    if (ids) std::memcpy(ids, c.doc_ids.data(), c.doc_ids.size() * sizeof(std::uint64_t));
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+int hg_load_centroids(const char* path, std::uint32_t* dim, std::uint64_t* k, float* rows) {
+  try {
+    auto c = hedra_gpu::ivf::load_centroids(path);
+    *dim = c.dim;
+    *k = c.k_clusters();
+    if (rows)
+      for (std::size_t i = 0; i < c.rows.size(); ++i)
+        std::memcpy(rows + i * c.dim, c.rows[i].data(), c.dim * sizeof(float));
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+int hg_load_assignments(const char* path, std::uint64_t* n, std::uint32_t* a) {
+  try {
+    auto v = hedra_gpu::ivf::load_assignments(path);
+    *n = v.size();
+    if (a) std::memcpy(a, v.data(), v.size() * sizeof(std::uint32_t));
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+}

@@ -139,6 +139,17 @@ class IvfIndex {
   Metric metric_ = Metric::L2;
 };
 
+// Persistence in the reference's HVEC / u32 formats (vector_index.hpp:162-175),
+// byte-identical files: "HVEC", u32 version 1, u32 dim, u64 count, u8 metric,
+// then the rows (+ doc ids for a corpus); assignments: u64 count + u32 ids.
+// Errors: std::runtime_error (cannot open, bad magic/version, truncated).
+void save_corpus(const std::string& path, const Corpus& corpus);
+Corpus load_corpus(const std::string& path);
+void save_centroids(const std::string& path, const Centroids& centroids, Metric metric);
+Centroids load_centroids(const std::string& path);
+void save_assignments(const std::string& path, const std::vector<ClusterId>& assign);
+std::vector<ClusterId> load_assignments(const std::string& path);
+
 // Index build on the GPU, bit-identical to the reference
 // (vector_index.cpp:99-259): train_kmeans, compute_assignments, build_index
 // (duplicate-id check, cosine normalization, assignment, index_from_assignments).
