@@ -106,6 +106,15 @@ hivf_status hivf_index_finish(hivf_index* idx);
  * floats + doc ids); the IvfIndex::doc_embedding of vector_index.hpp:105-108. */
 hivf_status hivf_index_get_rows(hivf_index* idx, uint64_t first_row, uint64_t n_rows,
                                 float* rows_out, uint64_t* ids_out);
+/* IvfIndex::locate / doc_embedding (vector_index.hpp:98-111; the locator map of
+ * vector_index.cpp:226-227): list and list-order row of each doc id
+ * (clusters_out = UINT32_MAX, rows_out = UINT64_MAX when unknown), and the
+ * rows' vectors (row-major host floats).  Used by the locality helpers
+ * (make_locality_record, similarity.cpp:18-33). */
+hivf_status hivf_index_locate(hivf_index* idx, const uint64_t* doc_ids, uint32_t n,
+                              uint32_t* clusters_out, uint64_t* rows_out);
+hivf_status hivf_index_gather_rows(hivf_index* idx, const uint64_t* rows, uint32_t n,
+                                   float* rows_out);
 hivf_status hivf_index_destroy(hivf_index* idx);
 /* k_clusters / cluster_size / total_vectors / mean_assigned_distance
  * (vector_index.hpp:92-98).  Any output pointer may be NULL. */

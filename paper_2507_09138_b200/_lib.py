@@ -20,7 +20,7 @@ SYMBOLS = [
     "hivf_ctx_set_stream", "hivf_ctx_synchronize", "hivf_device_info", "hivf_index_upload",
     "hivf_index_upload_device", "hivf_index_begin", "hivf_index_add_rows_device",
     "hivf_index_add_rows_at_device", "hivf_index_finish", "hivf_index_get_rows",
-    "hivf_index_destroy", "hivf_index_info", "hivf_index_cluster_sizes",
+    "hivf_index_destroy", "hivf_index_locate", "hivf_index_gather_rows", "hivf_index_info", "hivf_index_cluster_sizes",
     "hivf_assign", "hivf_search", "hivf_search_device", "hivf_assign_device",
     "hivf_search_planned_device", "hivf_scan_items", "hivf_compute_assignments",
     "hivf_train_kmeans", "hivf_compute_assignments_host", "hivf_train_kmeans_host",
@@ -81,6 +81,8 @@ def lib():
         "hivf_index_finish": (i32, [vp]),
         "hivf_index_get_rows": (i32, [vp, u64, u64, vp, vp]),
         "hivf_index_destroy": (i32, [vp]),
+        "hivf_index_locate": (i32, [vp, vp, u32, vp, vp]),
+        "hivf_index_gather_rows": (i32, [vp, vp, u32, vp]),
         "hivf_index_info": (i32, [vp, P(u32), P(u32), P(u64), P(u64), P(f64)]),
         "hivf_index_cluster_sizes": (i32, [vp, vp]),
         "hivf_assign": (i32, [vp, vp, u32, u32, vp, vp]),

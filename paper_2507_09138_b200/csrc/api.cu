@@ -198,6 +198,9 @@ struct hivf_index {
   double mean_assigned = -1.0;
   uint32_t seg_rows = 4096, s_max = 1;
   std::vector<uint8_t> resident;
+  // locator (doc id -> row), built on the first hivf_index_locate
+  uint64_t* loc_ids = nullptr;
+  uint64_t* loc_rows = nullptr;
   // ---- tiered residency (hivf_residency_set) ----
   bool tiered = false;           // vec is pinned host memory, hot lists copied into pool
   float* pool = nullptr;         // HBM slots for resident lists
@@ -252,7 +255,7 @@ struct hivf_index {
     else if (vec) cudaFree(vec);
     for (void* p : {(void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
                     (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err, (void*)pool,
-                    (void*)d_list_ptr})
+                    (void*)d_list_ptr, (void*)loc_ids, (void*)loc_rows})
       if (p) cudaFree(p);
   }
 };
@@ -746,6 +749,67 @@ hivf_status hivf_index_destroy(hivf_index* ix) {
   cudaSetDevice(ix->ctx->device);
   cudaStreamSynchronize(ix->ctx->stream);
   delete ix;
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_locate(hivf_index* ix, const uint64_t* doc_ids, uint32_t n, uint32_t* clusters_out,
+                              uint64_t* rows_out) {
+  if (!ix || (n && (!doc_ids || !clusters_out || !rows_out))) return fail(HIVF_EINVAL, "hivf_index_locate: NULL argument");
+  if (!ix->finished) return fail(HIVF_EINVAL, "index not finished");
+  if (!n) return HIVF_OK;
+  CK(cudaSetDevice(ix->ctx->device));
+  cudaStream_t s = ix->ctx->stream;
+  if (!ix->loc_ids && ix->N) {  // sorted (id, row) table, once
+    uint64_t* rows = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    CK(cudaMalloc(&ix->loc_ids, ix->N * 8));
+    CK(cudaMalloc(&ix->loc_rows, ix->N * 8));
+    CK(cudaMalloc(&rows, ix->N * 8));
+    launch_iota64(rows, ix->N, s);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ix->ids, ix->loc_ids, rows, ix->loc_rows, (int64_t)ix->N, 0, 64, s));
+    CK(cudaMalloc(&tmp, tb));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ix->ids, ix->loc_ids, rows, ix->loc_rows, (int64_t)ix->N, 0, 64, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    cudaFree(rows);
+  }
+  hivf_ctx* c = ix->ctx;
+  CK(c->x_ids.ensure((size_t)n * 8 * 2));
+  CK(c->x_cnt.ensure((size_t)n * 4));
+  uint64_t* dq = c->x_ids.as<uint64_t>();
+  CK(cudaMemcpyAsync(dq, doc_ids, n * 8ull, cudaMemcpyHostToDevice, s));
+  if (ix->N) {
+    launch_locate(ix->loc_ids, ix->loc_rows, ix->N, ix->d_list_off, ix->K, dq, n, c->x_cnt.as<uint32_t>(), dq + n, s);
+    CKL();
+    CK(cudaMemcpyAsync(clusters_out, c->x_cnt.p, n * 4ull, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(rows_out, dq + n, n * 8ull, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    for (uint32_t i = 0; i < n; ++i) {
+      clusters_out[i] = 0xffffffffu;
+      rows_out[i] = ~0ull;
+    }
+  }
+  return HIVF_OK;
+}
+
+hivf_status hivf_index_gather_rows(hivf_index* ix, const uint64_t* rows, uint32_t n, float* rows_out) {
+  if (!ix || (n && (!rows || !rows_out))) return fail(HIVF_EINVAL, "hivf_index_gather_rows: NULL argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (rows[i] >= ix->N) return fail(HIVF_EINVAL, "hivf_index_gather_rows: row %llu out of range", (unsigned long long)rows[i]);
+  if (!n) return HIVF_OK;
+  CK(cudaSetDevice(ix->ctx->device));
+  cudaStream_t s = ix->ctx->stream;
+  hivf_ctx* c = ix->ctx;
+  if (ix->tiered) complete_swaps(ix);
+  CK(c->x_ids.ensure((size_t)n * 8));
+  CK(c->x_d.ensure((size_t)n * ix->dim * 4));
+  CK(cudaMemcpyAsync(c->x_ids.p, rows, n * 8ull, cudaMemcpyHostToDevice, s));
+  launch_gather_rows(ix->view(), c->x_ids.as<uint64_t>(), n, c->x_d.as<float>(), s);
+  CKL();
+  CK(cudaMemcpyAsync(rows_out, c->x_d.p, (size_t)n * ix->dim * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return HIVF_OK;
 }
 

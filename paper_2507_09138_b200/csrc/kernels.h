@@ -67,6 +67,10 @@ struct PtrFlips {
   const float* ptr[kPtrFlipBatch];
 };
 void launch_ptr_flips(const float** table, const PtrFlips& f, cudaStream_t s);
+void launch_locate(const uint64_t* sorted_ids, const uint64_t* sorted_rows, uint64_t N, const uint64_t* list_off,
+                   uint32_t K, const uint64_t* q, uint32_t n, uint32_t* cl_out, uint64_t* row_out, cudaStream_t s);
+void launch_gather_rows(const IndexView& ix, const uint64_t* rows, uint32_t n, float* out, cudaStream_t s);
+void launch_iota64(uint64_t* v, uint64_t n, cudaStream_t s);
 void launch_pack_lists(const float* src_rows, uint64_t r_first, const uint64_t* pos,
                        uint64_t n_rows, uint32_t dim, uint32_t dpad, const uint64_t* d_list_off,
                        uint32_t K, float* dst, float* xnorm2, uint32_t* maxnorm_bits, int* err,

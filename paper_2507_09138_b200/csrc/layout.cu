@@ -190,4 +190,66 @@ void launch_ptr_flips(const float** table, const PtrFlips& f, cudaStream_t s) {
   if (f.n) k_ptr_flips<<<1, kPtrFlipBatch, 0, s>>>(table, f);
 }
 
+namespace {
+// locator (vector_index.cpp:226-227): binary search of doc ids in the sorted
+// (id, row) table built on first use
+__global__ void k_locate(const uint64_t* __restrict__ sid, const uint64_t* __restrict__ srow, uint64_t N,
+                         const uint64_t* __restrict__ list_off, uint32_t K, const uint64_t* __restrict__ q,
+                         uint32_t n, uint32_t* __restrict__ cl_out, uint64_t* __restrict__ row_out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t id = q[i];
+  uint64_t lo = 0, hi = N;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (sid[mid] < id) lo = mid + 1; else hi = mid;
+  }
+  if (lo >= N || sid[lo] != id) {
+    cl_out[i] = 0xffffffffu;
+    row_out[i] = ~0ull;
+    return;
+  }
+  const uint64_t r = srow[lo];
+  uint32_t a = 0, b = K;
+  while (a < b) {
+    const uint32_t mid = (a + b) >> 1;
+    if (list_off[mid + 1] <= r) a = mid + 1; else b = mid;
+  }
+  cl_out[i] = a;
+  row_out[i] = r;
+}
+
+// doc_embedding for arbitrary rows (list order): out[i][d]
+__global__ void k_gather_rows(IndexView ix, const uint64_t* __restrict__ rows, uint32_t n, float* __restrict__ out) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (uint64_t)n * ix.dim) return;
+  const uint32_t i = (uint32_t)(gid / ix.dim), d = (uint32_t)(gid % ix.dim);
+  const uint64_t r = rows[i];
+  uint32_t a = 0, b = ix.K;
+  while (a < b) {
+    const uint32_t mid = (a + b) >> 1;
+    if (ix.list_off[mid + 1] <= r) a = mid + 1; else b = mid;
+  }
+  const uint64_t beg = ix.list_off[a], n_c = ix.list_off[a + 1] - beg;
+  out[gid] = list_base(ix, a, beg)[swz_offset(0, n_c, r - beg, d)];
+}
+
+__global__ void k_iota64(uint64_t* v, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+}  // namespace
+
+void launch_locate(const uint64_t* sid, const uint64_t* srow, uint64_t N, const uint64_t* list_off, uint32_t K,
+                   const uint64_t* q, uint32_t n, uint32_t* cl_out, uint64_t* row_out, cudaStream_t s) {
+  if (n) k_locate<<<(n + 127) / 128, 128, 0, s>>>(sid, srow, N, list_off, K, q, n, cl_out, row_out);
+}
+void launch_gather_rows(const IndexView& ix, const uint64_t* rows, uint32_t n, float* out, cudaStream_t s) {
+  const uint64_t t = (uint64_t)n * ix.dim;
+  if (t) k_gather_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(ix, rows, n, out);
+}
+void launch_iota64(uint64_t* v, uint64_t n, cudaStream_t s) {
+  if (n) k_iota64<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v, n);
+}
+
 }  // namespace hivf

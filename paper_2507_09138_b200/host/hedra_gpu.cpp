@@ -11,6 +11,20 @@
 
 namespace hedra_gpu {
 
+double squared_l2(const float* a, const float* b, std::size_t dim) {
+  double acc = 0.0;
+  for (std::size_t i = 0; i < dim; ++i) {
+    const double d = static_cast<double>(a[i]) - static_cast<double>(b[i]);
+    acc += d * d;
+  }
+  return acc;
+}
+
+double embedding_distance(const Embedding& a, const Embedding& b) {
+  if (a.size() != b.size()) throw std::invalid_argument("squared_l2: dimension mismatch");
+  return squared_l2(a.data(), b.data(), a.size());
+}
+
 Embedding normalized(Embedding v) {
   double norm = 0.0;
   for (float x : v) norm += static_cast<double>(x) * static_cast<double>(x);
@@ -133,12 +147,30 @@ std::shared_ptr<IvfIndex> IvfIndex::from_assignments(Context& ctx, const std::ve
   ix->total_ = ids.size();
   ix->sizes_.resize(K);
   for (std::size_t c = 0; c < K; ++c) ix->sizes_[c] = off[c + 1] - off[c];
+  ix->offsets_.assign(off.begin(), off.end());
   check(hivf_index_upload(ctx.raw(), dim, static_cast<int>(metric), static_cast<std::uint32_t>(K),
                           cents.data(), off.data(), rows.data(), lids.data(), &ix->ix_));
   return ix;
 }
 
 IvfIndex::~IvfIndex() { hivf_index_destroy(ix_); }
+
+std::optional<IvfIndex::DocLocation> IvfIndex::locate(DocId id) const {
+  std::uint32_t c = 0;
+  std::uint64_t row = 0;
+  check(hivf_index_locate(ix_, &id, 1, &c, &row));
+  if (c == 0xffffffffu) return std::nullopt;
+  return DocLocation{c, static_cast<std::uint32_t>(row - offsets_[c])};
+}
+
+Embedding IvfIndex::doc_embedding(DocLocation loc) const {
+  if (loc.cluster >= sizes_.size() || loc.offset >= sizes_[loc.cluster])
+    throw std::out_of_range("doc_embedding: location out of range");
+  const std::uint64_t row = offsets_[loc.cluster] + loc.offset;
+  Embedding e(dim_);
+  check(hivf_index_gather_rows(ix_, &row, 1, e.data()));
+  return e;
+}
 
 double IvfIndex::mean_assigned_distance() const {
   double m = 0.0;
@@ -588,6 +620,91 @@ RetStepReport RetrievalEngine::execute(SubStageBatch& batch, double now_ms, bool
 }
 
 }  // namespace ret
+}  // namespace hedra_gpu
+
+// ---- sim (similarity.cpp) -----------------------------------------------------------
+namespace hedra_gpu {
+namespace sim {
+
+void LocalityCache::record_search(RequestId request_id, LocalityRecord record) {
+  records_[request_id] = std::move(record);
+}
+const LocalityRecord* LocalityCache::find(RequestId request_id) const {
+  auto it = records_.find(request_id);
+  return it == records_.end() ? nullptr : &it->second;
+}
+void LocalityCache::evict(RequestId request_id) { records_.erase(request_id); }
+
+LocalityRecord make_locality_record(const ivf::IvfIndex& index, const Embedding& query,
+                                    const ivf::TopKResult& extended_topk,
+                                    std::span<const ClusterId> searched_plan) {
+  LocalityRecord record;
+  record.query = query;
+  record.searched.insert(searched_plan.begin(), searched_plan.end());
+  const auto& en = extended_topk.entries();
+  const std::uint32_t n = static_cast<std::uint32_t>(en.size());
+  if (!n) return record;
+  std::vector<std::uint64_t> ids(n), rows(n);
+  std::vector<std::uint32_t> cl(n);
+  for (std::uint32_t i = 0; i < n; ++i) ids[i] = en[i].doc_id;
+  check(hivf_index_locate(index.raw(), ids.data(), n, cl.data(), rows.data()));
+  for (std::uint32_t i = 0; i < n; ++i)
+    if (cl[i] == 0xffffffffu) throw std::invalid_argument("make_locality_record: unknown doc id");
+  std::vector<float> vec(static_cast<std::size_t>(n) * index.dim());
+  check(hivf_index_gather_rows(index.raw(), rows.data(), n, vec.data()));
+  for (std::uint32_t i = 0; i < n; ++i) {
+    record.candidates.push_back(CachedCandidate{
+        ids[i], cl[i], Embedding(vec.begin() + i * index.dim(), vec.begin() + (i + 1) * index.dim())});
+    record.result_clusters.insert(cl[i]);
+  }
+  return record;
+}
+
+std::optional<ProbeResult> probe_cache(const LocalityCache& cache, RequestId request_id,
+                                       const Embedding& v_prime, std::size_t k, double delta,
+                                       std::span<const ClusterId> plan) {
+  const LocalityRecord* record = cache.find(request_id);
+  if (!record) return std::nullopt;
+  if (record->query.size() != v_prime.size()) return std::nullopt;
+  if (embedding_distance(record->query, v_prime) > delta) return std::nullopt;
+  const std::set<ClusterId> in_plan(plan.begin(), plan.end());
+  ProbeResult out;
+  out.seed.set_k(k);
+  for (const auto& cand : record->candidates)
+    if (in_plan.count(cand.cluster))  // seeds stay result-neutral
+      out.seed.insert(cand.doc_id, embedding_distance(v_prime, cand.vec));
+  out.result_clusters = record->result_clusters;
+  out.searched = record->searched;
+  return out;
+}
+
+std::vector<ClusterId> reorder_clusters(std::span<const ClusterId> c_prime, const std::set<ClusterId>& h_v,
+                                        const std::set<ClusterId>& c_v) {
+  std::vector<ClusterId> hot, seen, rest;
+  for (ClusterId c : c_prime) (h_v.count(c) ? hot : c_v.count(c) ? seen : rest).push_back(c);
+  hot.insert(hot.end(), seen.begin(), seen.end());
+  hot.insert(hot.end(), rest.begin(), rest.end());
+  return hot;
+}
+
+bool should_terminate(const ivf::SearchCursor& cursor, std::size_t streak_threshold) {
+  return cursor.unchanged_streak >= streak_threshold;
+}
+
+SpeculationOutcome validate_speculation(const ivf::TopKResult& partial, const ivf::TopKResult& final_result,
+                                        std::size_t k) {
+  SpeculationOutcome o;
+  o.compared_k = k;
+  o.kind = partial.truncated(k).doc_ids() == final_result.truncated(k).doc_ids() ? SpecKind::Valid
+                                                                                 : SpecKind::Mismatch;
+  return o;
+}
+
+double semantic_drift(const Embedding& prev_partial, const Embedding& curr_partial) {
+  return embedding_distance(prev_partial, curr_partial);
+}
+
+}  // namespace sim
 }  // namespace hedra_gpu
 
 // ---- C entry points over the persistence functions (ctypes parity tests) -----------

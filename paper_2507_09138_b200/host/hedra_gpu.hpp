@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <optional>
 #include <set>
 #include <span>
 #include <stdexcept>
@@ -36,6 +37,10 @@ enum class Metric : std::uint8_t { L2 = 0, Cosine = 1 };
 
 // embedding.hpp:36-43 (double norm, sequential, divide, cast back to float)
 Embedding normalized(Embedding v);
+// embedding.hpp:27-34 / :53-55 (sequential double chain, no contraction:
+// the adapter is built with -ffp-contract=off)
+double squared_l2(const float* a, const float* b, std::size_t dim);
+double embedding_distance(const Embedding& a, const Embedding& b);
 
 // Throws the reference's exception type for a failed hivf call.
 void check(hivf_status st);
@@ -126,6 +131,14 @@ class IvfIndex {
   std::uint32_t dim() const { return dim_; }
   Metric metric() const { return metric_; }
   double mean_assigned_distance() const;
+  // IvfIndex::locate / doc_embedding (vector_index.hpp:98-111), served by the
+  // device locator (hivf_index_locate / hivf_index_gather_rows)
+  struct DocLocation {
+    ClusterId cluster = 0;
+    std::uint32_t offset = 0;
+  };
+  std::optional<DocLocation> locate(DocId id) const;
+  Embedding doc_embedding(DocLocation loc) const;
   hivf_index* raw() const { return ix_; }
   Context& context() const { return *ctx_; }
 
@@ -134,6 +147,7 @@ class IvfIndex {
   Context* ctx_ = nullptr;
   hivf_index* ix_ = nullptr;
   std::vector<std::size_t> sizes_;
+  std::vector<std::uint64_t> offsets_;  // list start rows (list order)
   std::size_t total_ = 0;
   std::uint32_t dim_ = 0;
   Metric metric_ = Metric::L2;
@@ -337,4 +351,66 @@ class RetrievalEngine {
 };
 
 }  // namespace ret
+
+// hedra::sim (proj/include/hedra/similarity.hpp): the locality helpers of the
+// Hedra mode -- host bookkeeping plus exact re-scoring of <= 20 cached docs;
+// the doc lookups go through the device locator.
+namespace sim {
+
+inline constexpr std::size_t kExtendedTopK = 20;  // K_cache
+
+struct CachedCandidate {
+  DocId doc_id = 0;
+  ClusterId cluster = 0;
+  Embedding vec;
+};
+
+struct LocalityRecord {
+  Embedding query;
+  std::vector<CachedCandidate> candidates;
+  std::set<ClusterId> result_clusters;  // H_v
+  std::set<ClusterId> searched;         // C_v
+};
+
+class LocalityCache {
+ public:
+  void record_search(RequestId request_id, LocalityRecord record);
+  const LocalityRecord* find(RequestId request_id) const;
+  void evict(RequestId request_id);
+  std::size_t size() const { return records_.size(); }
+
+ private:
+  std::map<RequestId, LocalityRecord> records_;
+};
+
+// similarity.cpp:18-33 (one batched locate + gather for all candidates)
+LocalityRecord make_locality_record(const ivf::IvfIndex& index, const Embedding& query,
+                                    const ivf::TopKResult& extended_topk,
+                                    std::span<const ClusterId> searched_plan);
+
+struct ProbeResult {
+  ivf::TopKResult seed;
+  std::set<ClusterId> result_clusters;
+  std::set<ClusterId> searched;
+};
+
+// similarity.cpp:35-55
+std::optional<ProbeResult> probe_cache(const LocalityCache& cache, RequestId request_id,
+                                       const Embedding& v_prime, std::size_t k, double delta,
+                                       std::span<const ClusterId> plan);
+// similarity.cpp:57-72
+std::vector<ClusterId> reorder_clusters(std::span<const ClusterId> c_prime, const std::set<ClusterId>& h_v,
+                                        const std::set<ClusterId>& c_v);
+bool should_terminate(const ivf::SearchCursor& cursor, std::size_t streak_threshold);
+
+enum class SpecKind { Valid, Mismatch };
+struct SpeculationOutcome {
+  SpecKind kind = SpecKind::Mismatch;
+  std::size_t compared_k = 0;
+};
+SpeculationOutcome validate_speculation(const ivf::TopKResult& partial, const ivf::TopKResult& final_result,
+                                        std::size_t k);
+double semantic_drift(const Embedding& prev_partial, const Embedding& curr_partial);
+
+}  // namespace sim
 }  // namespace hedra_gpu

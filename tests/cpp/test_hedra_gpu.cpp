@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <limits>
+#include <set>
 #include <random>
 #include <string>
 #include <vector>
@@ -498,6 +500,150 @@ TEST_GPU(train_kmeans_contract) {
   CHECK_THROWS_AS(ivf::train_kmeans(ctx, corpus, 3000, 5, 3), std::invalid_argument);  // n < K
   CHECK_THROWS_AS(ivf::train_kmeans(ctx, corpus, 0, 5, 3), std::invalid_argument);
   CHECK_THROWS_AS(ivf::train_kmeans(ctx, corpus, 4, 0, 3), std::invalid_argument);
+}
+
+// ---- sim (ported from proj/tests/test_similarity.cpp) ------------------------------
+static ivf::SearchCursor full_search(const ivf::IvfIndex& ix, const Embedding& q, std::size_t nprobe,
+                                     std::size_t k) {
+  auto cur = ivf::make_cursor(ix, q, nprobe, k);
+  while (!cur.done()) ivf::search_step(ix, cur, 3);
+  return cur;
+}
+
+TEST_GPU(sim_probe_identical_query_rescores_cached_topk) {  // test_similarity.cpp:60-72
+  ivf::Context ctx(0);
+  const Data d = random_data(33, 400, 8, 8);
+  auto ix = build(ctx, d);
+  sim::LocalityCache cache;
+  std::mt19937_64 g(3);
+  const auto q = rand_query(g, 8);
+  auto cur = full_search(*ix, q, 8, sim::kExtendedTopK);
+  cache.record_search(1, sim::make_locality_record(*ix, cur.query, cur.heap, cur.plan));
+  const auto probe = sim::probe_cache(cache, 1, cur.query, 5, 1e-12, cur.plan);
+  CHECK(probe.has_value());
+  if (probe) CHECK(probe->seed == cur.heap.truncated(5));
+  // the record holds the docs' own vectors and clusters (locate + doc_embedding)
+  const auto* rec = cache.find(1);
+  CHECK(rec && rec->candidates.size() == cur.heap.size());
+  for (const auto& c : rec->candidates) {
+    const auto loc = ix->locate(c.doc_id);
+    CHECK(loc.has_value() && loc->cluster == c.cluster);
+    if (loc) CHECK(ix->doc_embedding(*loc) == c.vec);
+    const float* row = d.x.data() + c.doc_id * d.dim;
+    CHECK(c.vec == Embedding(row, row + d.dim));
+  }
+  CHECK(!ix->locate(987654321ull).has_value());
+}
+
+TEST_GPU(sim_probe_misses_on_drift_or_no_record) {  // :74-88
+  ivf::Context ctx(0);
+  const Data d = random_data(34, 400, 8, 8);
+  auto ix = build(ctx, d);
+  sim::LocalityCache cache;
+  std::mt19937_64 g(4);
+  const auto q = rand_query(g, 8);
+  auto cur = full_search(*ix, q, 8, sim::kExtendedTopK);
+  cache.record_search(1, sim::make_locality_record(*ix, cur.query, cur.heap, cur.plan));
+  Embedding far = cur.query;
+  far[0] += 100.0f;
+  CHECK(!sim::probe_cache(cache, 1, far, 5, 0.5, cur.plan).has_value());
+  CHECK(!sim::probe_cache(cache, 2, cur.query, 5, 0.5, cur.plan).has_value());
+}
+
+TEST_GPU(sim_seeding_never_changes_the_result) {  // :90-112
+  ivf::Context ctx(0);
+  const Data d = random_data(35, 600, 8, 8);
+  auto ix = build(ctx, d);
+  sim::LocalityCache cache;
+  std::mt19937_64 g(6);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (int trial = 0; trial < 20; ++trial) {
+    const auto q = rand_query(g, 8);
+    auto base = full_search(*ix, q, 6, sim::kExtendedTopK);
+    cache.record_search(9, sim::make_locality_record(*ix, base.query, base.heap, base.plan));
+    Embedding q2 = q;
+    for (auto& x : q2) x += static_cast<float>(nd(g) * 0.05);
+    auto unseeded = ivf::make_cursor(*ix, q2, 6, 5);
+    auto seeded = ivf::make_cursor(*ix, q2, 6, 5);
+    const auto probe = sim::probe_cache(cache, 9, seeded.query, 5,
+                                        std::numeric_limits<double>::infinity(), seeded.plan);
+    CHECK(probe.has_value());
+    if (probe) seeded.heap = ivf::merge_topk(seeded.heap, probe->seed, 5);
+    while (!unseeded.done()) ivf::search_step(*ix, unseeded, 2);
+    while (!seeded.done()) ivf::search_step(*ix, seeded, 2);
+    CHECK(seeded.heap == unseeded.heap);
+  }
+}
+
+TEST_CPU(sim_reorder_three_group_rule) {  // :114-122 (+ permutation property :124-150)
+  const std::vector<ClusterId> c_prime = {5, 3, 8, 1};
+  CHECK(sim::reorder_clusters(c_prime, {3}, {3, 8}) == (std::vector<ClusterId>{3, 8, 5, 1}));
+  CHECK(sim::reorder_clusters(c_prime, {}, {}) == c_prime);
+  std::mt19937_64 g(7);
+  for (int t = 0; t < 50; ++t) {
+    std::vector<ClusterId> cp;
+    for (int i = 0; i < 20; ++i) cp.push_back(static_cast<ClusterId>(g() % 1000));
+    std::sort(cp.begin(), cp.end());
+    cp.erase(std::unique(cp.begin(), cp.end()), cp.end());
+    std::set<ClusterId> h, c;
+    for (ClusterId x : cp) {
+      const double u = (g() >> 11) * 0x1.0p-53;
+      if (u < 0.2) {
+        h.insert(x);
+        c.insert(x);
+      } else if (u < 0.5) {
+        c.insert(x);
+      }
+    }
+    auto out = sim::reorder_clusters(cp, h, c);
+    auto a = cp, b = out;
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    CHECK(a == b);
+    int phase = 0;
+    for (ClusterId x : out) {
+      const int grp = h.count(x) ? 0 : (c.count(x) ? 1 : 2);
+      CHECK(grp >= phase);
+      phase = std::max(phase, grp);
+    }
+  }
+}
+
+TEST_GPU(sim_reordered_plan_same_result) {  // :152-170
+  ivf::Context ctx(0);
+  const Data d = random_data(36, 600, 8, 8);
+  auto ix = build(ctx, d);
+  std::mt19937_64 g(8);
+  for (int t = 0; t < 15; ++t) {
+    const auto q = rand_query(g, 8);
+    auto plain = ivf::make_cursor(*ix, q, 8, 5);
+    auto re = plain;
+    std::set<ClusterId> h, c;
+    for (ClusterId x : plain.plan) {
+      if ((g() >> 11) * 0x1.0p-53 < 0.3) h.insert(x);
+      if ((g() >> 11) * 0x1.0p-53 < 0.5) c.insert(x);
+    }
+    re.plan = sim::reorder_clusters(re.plan, h, c);
+    while (!plain.done()) ivf::search_step(*ix, plain, 3);
+    while (!re.done()) ivf::search_step(*ix, re, 3);
+    CHECK(plain.heap == re.heap);
+  }
+}
+
+TEST_CPU(sim_should_terminate_and_validate_speculation) {  // :172-196
+  ivf::SearchCursor cur;
+  cur.unchanged_streak = 3;
+  CHECK(!sim::should_terminate(cur, 4));
+  cur.unchanged_streak = 4;
+  CHECK(sim::should_terminate(cur, 4));
+  ivf::TopKResult a(3), b(3);
+  a.insert(1, 0.5);
+  a.insert(2, 0.7);
+  b.insert(1, 0.5);
+  b.insert(2, 0.7);
+  CHECK(sim::validate_speculation(a, b, 2).kind == sim::SpecKind::Valid);
+  b.insert(3, 0.1);
+  CHECK(sim::validate_speculation(a, b, 2).kind == sim::SpecKind::Mismatch);
 }
 
 int main(int argc, char** argv) {
