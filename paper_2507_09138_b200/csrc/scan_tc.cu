@@ -58,7 +58,8 @@ constexpr int kTcStageBytes = kTcCps * kTcChunkBytes;     // 32 KB
 constexpr int kTcSplitWarps = 4;
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = (2 + kTcSplitWarps + kTcEpiWarps) * 32;
-constexpr uint32_t kTmemAcc = 128;  // 2 accumulator buffers x 64 columns ([hi*hi|hi*lo])
+constexpr uint32_t kTmemAcc = 128;  // split mode: 2 accumulator buffers x 64 columns ([hi*hi|hi*lo]), A_lo after
+constexpr int kAccMax = 8;          // single mode: up to 8 x 64 accumulator columns (the A_lo ring is unused)
 constexpr uint32_t kTmemLoCols = kTcCps * kChunk;            // 64 columns of A_lo per slot
 constexpr uint32_t kTmemCols = 512;  // 128 accumulator + kTcLo x 64 lo columns (pow2)
 
@@ -215,6 +216,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   const uint32_t qmax = P.qmax;
   const uint32_t SA = P.sa;
   const bool split = P.split != 0;
+  // TMEM accumulator ring: split mode shares TMEM with the A_lo ring; single
+  // mode spreads over the whole 512 columns to absorb epilogue jitter
+  const uint32_t nacc = split ? 2u : (uint32_t)kAccMax;
   const uint32_t qblk = (split ? 2 : 1) * qmax * 64;                // per chunk: [raw rows | lo rows]
   uint8_t* aring = smem;                                            // SA x 32 KB (raw A)
   uint8_t* qsm = smem + SA * kTcStageBytes;                         // nch x qblk
@@ -225,9 +229,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   uint64_t* empty = bars + kTcMaxA;             // [SA] MMA -> TMA
   uint64_t* lfull = bars + 2 * kTcMaxA;         // [kTcLo] splitter -> MMA
   uint64_t* lempty = lfull + kTcLo;             // [kTcLo] MMA -> splitter
-  uint64_t* tfull = lempty + kTcLo;             // [2] MMA -> epilogue
-  uint64_t* tempty = tfull + 2;                 // [2] epilogue -> MMA
-  uint64_t* ifull = tempty + 2;                 // [kItemQ] producer -> all roles (item published)
+  uint64_t* tfull = lempty + kTcLo;             // [nacc] MMA -> epilogue
+  uint64_t* tempty = tfull + kAccMax;           // [nacc] epilogue -> MMA
+  uint64_t* ifull = tempty + kAccMax;                 // [kItemQ] producer -> all roles (item published)
   uint64_t* iempty = ifull + kItemQ;            // [kItemQ] roles -> producer (slot consumed)
   uint64_t* qfull = iempty + kItemQ;            // stagers -> MMA (query group staged)
   uint64_t* qempty = qfull + 1;                 // MMA commit -> stagers (query group free)
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       mbar_init(&lfull[i], kTcSplitWarps);
       mbar_init(&lempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kAccMax; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kTcEpiWarps);
     }
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           if (++ra == SA) { ra = 0; rpa ^= 1; }
         }
         mma_commit_elect(&tfull[tb]);
-        if (++tb == 2) {
+        if (++tb == nacc) {
           tb = 0;
           tph ^= 1;
         }
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[tb]);
-        if (++tb == 2) {
+        if (++tb == nacc) {
           tb = 0;
           tph ^= 1;
         }
@@ -780,7 +784,7 @@ static int tc_budget() {
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
   return 1024 + (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64 +
          kTcEpiWarps * kMergeQ * 32 * 8 +                         // merge scratch
-         8 * (2 * kTcMaxA + 2 * kTcLo + 4 + 2 * kItemQ + 2) + kItemQ * 32 * 8;
+         8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 8;
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int left = tc_budget() - tc_fixed_bytes(dpad, qmax, split);
