@@ -283,12 +283,14 @@ static void adapt_scan(hivf_index* ix, uint32_t n_queries, uint32_t n_fallback) 
 
 // Rows per scan segment: long segments amortise the per-item costs of the
 // grouped scan (query staging, pipeline refill), short ones balance the
-// persistent grid.  Keep >= 16 segments per SM when the index allows it:
-// C3 (21M rows) 4096, a C3 shard of an 8-GPU job (2.6M rows) 1024 -- measured
-// at --shard 0/8: 1.79 ms (4096) vs 1.68 ms (1024) per step.
+// persistent grid.  The longest of 8192/4096/2048/1024 that still gives >= 16
+// segments per SM.  Measured (scan ms per C3 batch): 8192 -> 9.19-9.31,
+// 4096 -> 9.57-9.85, 2048 -> 10.45, 16384 -> 13.6 (tail); a C3 shard of an
+// 8-GPU job (2.6M rows) gets 1024: 1.68 vs 1.79 ms per step at 4096.  Failed
+// proofs of long segments are repaired in place (k_repair_segments).
 static uint32_t auto_seg_rows(uint64_t n_rows, int sm_count) {
   const uint64_t want = 16ull * (uint64_t)std::max(1, sm_count);
-  for (uint32_t seg : {4096u, 2048u})
+  for (uint32_t seg : {8192u, 4096u, 2048u})
     if (n_rows / seg >= want) return seg;
   return 1024;
 }
