@@ -55,8 +55,12 @@ hivf_status fail(hivf_status st, const char* fmt, ...) {
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  // grows by >= 1.5x: a stream of varying batch shapes (node-split
+  // sub-stages) settles after a few calls instead of re-allocating (cudaFree
+  // synchronises the device) whenever a batch is a little larger than before
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
+    want = std::max(want, bytes + bytes / 2);
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -81,6 +85,7 @@ struct HBuf {  // grow-only pinned host buffer
   size_t bytes = 0;
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
+    want = std::max(want, bytes + bytes / 2);
     if (p) cudaFreeHost(p);
     p = nullptr;
     bytes = 0;
@@ -1384,74 +1389,87 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
   c->last_index = ix;
   c->last_K = ix->K;
   cudaStream_t s = c->stream;
-  // item -> query index per pair
-  std::vector<uint32_t> pq(n_pairs);
+  // All inputs go down in ONE pinned H2D copy and all outputs come back in ONE
+  // D2H copy (latency of a sub-stage, config 5): staging layout
+  //   in : queries | pair->item | clusters | cluster_off | k | heap ids | heap d | heap n
+  //   out: heap ids | heap d | heap n | changed | err | fallback flags
+  // (the heap segments are shared: updated in place on the device).
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t qb = (size_t)n_items * ix->dim * 4, pb = (size_t)std::max<uint32_t>(n_pairs, 1) * 4;
+  const size_t hb = (size_t)n_items * heap_stride * 8;
+  const size_t o_q = 0, o_pq = al(o_q + qb), o_cl = al(o_pq + pb), o_off = al(o_cl + pb),
+               o_k = al(o_off + (n_items + 1) * 4ull), o_hi = al(o_k + n_items * 4ull), o_hd = al(o_hi + hb),
+               o_hn = al(o_hd + hb), o_ch = al(o_hn + n_items * 4ull), o_err = al(o_ch + std::max<uint32_t>(n_pairs, 1)),
+               o_fb = al(o_err + 4), total = al(o_fb + n_items * 4ull);
+  CK(c->hstage.ensure(total));
+  CK(c->qin.ensure(total));
+  uint8_t* h = c->hstage.as<uint8_t>();
+  uint8_t* d = c->qin.as<uint8_t>();
+  std::memcpy(h + o_q, queries, qb);
+  uint32_t* hpq = reinterpret_cast<uint32_t*>(h + o_pq);
   for (uint32_t i = 0; i < n_items; ++i)
-    for (uint32_t p = cluster_off[i]; p < cluster_off[i + 1]; ++p) pq[p] = i;
-  const size_t qb = (size_t)n_items * ix->dim * 4;
-  CK(c->qin.ensure(qb));
-  CK(c->pq.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
-  CK(c->pl.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
-  CK(c->it_off.ensure((n_items + 1) * 4ull));
-  CK(c->it_cl.ensure((size_t)std::max<uint32_t>(n_pairs, 1) * 4));
-  CK(c->it_k.ensure(n_items * 4ull));
-  CK(c->heap_ids.ensure((size_t)n_items * heap_stride * 8));
-  CK(c->heap_d.ensure((size_t)n_items * heap_stride * 8));
-  CK(c->heap_n.ensure(n_items * 4ull));
-  CK(c->changed.ensure((size_t)std::max<uint32_t>(n_pairs, 1)));
-  CK(c->flags_f.ensure(n_items * 4ull));
-  CK(c->err.ensure(4));
-  CK(cudaMemsetAsync(c->err.p, 0, 4, s));
-  CK(cudaMemcpyAsync(c->qin.p, queries, qb, cudaMemcpyHostToDevice, s));
+    for (uint32_t p = cluster_off[i]; p < cluster_off[i + 1]; ++p) hpq[p] = i;
+  if (n_pairs) std::memcpy(h + o_cl, clusters, n_pairs * 4ull);
+  std::memcpy(h + o_off, cluster_off, (n_items + 1) * 4ull);
+  std::memcpy(h + o_k, kv, n_items * 4ull);
+  std::memcpy(h + o_hi, heap_ids, hb);
+  std::memcpy(h + o_hd, heap_dists, hb);
+  std::memcpy(h + o_hn, heap_counts, n_items * 4ull);
+  std::memset(h + o_err, 0, 4);
+  CK(cudaMemcpyAsync(d, h, o_ch, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(d + o_err, 0, 4, s));
+  const uint32_t* d_pq = reinterpret_cast<const uint32_t*>(d + o_pq);
+  const uint32_t* d_cl = reinterpret_cast<const uint32_t*>(d + o_cl);
+  const uint32_t* d_off = reinterpret_cast<const uint32_t*>(d + o_off);
+  const uint32_t* d_k = reinterpret_cast<const uint32_t*>(d + o_k);
+  uint64_t* d_hi = reinterpret_cast<uint64_t*>(d + o_hi);
+  double* d_hd = reinterpret_cast<double*>(d + o_hd);
+  uint32_t* d_hn = reinterpret_cast<uint32_t*>(d + o_hn);
+  uint8_t* d_ch = d + o_ch;
+  int* d_fb = reinterpret_cast<int*>(d + o_fb);
+  // the scan's pair arrays (run_scan reads c->pq / c->pl)
+  CK(c->pq.ensure(pb));
+  CK(c->pl.ensure(pb));
   if (n_pairs) {
-    CK(cudaMemcpyAsync(c->pq.p, pq.data(), n_pairs * 4ull, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c->pl.p, clusters, n_pairs * 4ull, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c->it_cl.p, clusters, n_pairs * 4ull, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->pq.p, d_pq, n_pairs * 4ull, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->pl.p, d_cl, n_pairs * 4ull, cudaMemcpyDeviceToDevice, s));
   }
-  CK(cudaMemcpyAsync(c->it_off.p, cluster_off, (n_items + 1) * 4ull, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->it_k.p, kv, n_items * 4ull, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->heap_ids.p, heap_ids, (size_t)n_items * heap_stride * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->heap_d.p, heap_dists, (size_t)n_items * heap_stride * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->heap_n.p, heap_counts, n_items * 4ull, cudaMemcpyHostToDevice, s));
   hivf_status st;
   QueryView qv;
   // cursor queries are already in search space: no re-normalization
-  if ((st = prep_queries(ix, c->qin.as<float>(), n_items, false, &qv)) != HIVF_OK) return st;
+  CK(c->err.ensure(4));
+  CK(cudaMemsetAsync(c->err.p, 0, 4, s));
+  if ((st = prep_queries(ix, reinterpret_cast<const float*>(d + o_q), n_items, false, &qv)) != HIVF_OK) return st;
+  CK(cudaMemcpyAsync(d + o_err, c->err.p, 4, cudaMemcpyDeviceToDevice, s));
   const IndexView v = ix->view();
   const bool exact_only = c->opt_force_exact || kmax > (uint32_t)kKP;
+  CK(cudaMemsetAsync(d_fb, 0, n_items * 4ull, s));
   if (!exact_only && n_pairs) {
     if ((st = run_scan(ix, qv, n_pairs, false)) != HIVF_OK) return st;
-    launch_finalize_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
-                          c->it_k.as<uint32_t>(), c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
-                          c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), c->heap_ids.as<uint64_t>(),
-                          c->heap_d.as<double>(), c->heap_n.as<uint32_t>(), heap_stride,
-                          c->changed.as<uint8_t>(), c->flags_f.as<int>(), s);
+    launch_finalize_items(v, qv, n_items, d_off, d_cl, d_k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
+                          c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), d_hi, d_hd, d_hn, heap_stride, d_ch,
+                          d_fb, s);
     CKL();
-    launch_exact_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
-                       c->it_k.as<uint32_t>(), c->heap_ids.as<uint64_t>(), c->heap_d.as<double>(),
-                       c->heap_n.as<uint32_t>(), heap_stride, c->changed.as<uint8_t>(),
-                       c->flags_f.as<int>(), s);
+    launch_exact_items(v, qv, n_items, d_off, d_cl, d_k, d_hi, d_hd, d_hn, heap_stride, d_ch, d_fb, s);
     CKL();
   } else {
-    launch_exact_items(v, qv, n_items, c->it_off.as<uint32_t>(), c->it_cl.as<uint32_t>(),
-                       c->it_k.as<uint32_t>(), c->heap_ids.as<uint64_t>(), c->heap_d.as<double>(),
-                       c->heap_n.as<uint32_t>(), heap_stride, c->changed.as<uint8_t>(), nullptr, s);
+    launch_exact_items(v, qv, n_items, d_off, d_cl, d_k, d_hi, d_hd, d_hn, heap_stride, d_ch, nullptr, s);
     CKL();
   }
-  CK(cudaMemcpyAsync(heap_ids, c->heap_ids.p, (size_t)n_items * heap_stride * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(heap_dists, c->heap_d.p, (size_t)n_items * heap_stride * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(heap_counts, c->heap_n.p, n_items * 4ull, cudaMemcpyDeviceToHost, s));
-  if (n_pairs) CK(cudaMemcpyAsync(changed_out, c->changed.p, n_pairs, cudaMemcpyDeviceToHost, s));
-  int err = 0;
-  CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, s));
-  // auto policy (adapt_scan): items whose filter proof failed took the exact path
-  std::vector<int> fb(!exact_only && n_pairs && c->opt_scan_kernel == 0 && !ix->auto_split ? n_items : 0);
-  if (!fb.empty()) CK(cudaMemcpyAsync(fb.data(), c->flags_f.p, 4ull * n_items, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + o_hi, d + o_hi, total - o_hi, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  int err = 0;
+  std::memcpy(&err, h + o_err, 4);
   if (err) return fail(HIVF_EINVAL, "hivf_scan_items: non-finite query value");
-  if (!fb.empty()) {
+  std::memcpy(heap_ids, h + o_hi, hb);
+  std::memcpy(heap_dists, h + o_hd, hb);
+  std::memcpy(heap_counts, h + o_hn, n_items * 4ull);
+  if (n_pairs) std::memcpy(changed_out, h + o_ch, n_pairs);
+  // auto policy (adapt_scan): items whose filter proof failed took the exact path
+  if (!exact_only && n_pairs && c->opt_scan_kernel == 0 && !ix->auto_split) {
+    const int* fb = reinterpret_cast<const int*>(h + o_fb);
     uint32_t nf = 0;
-    for (int v : fb) nf += v != 0;
+    for (uint32_t i = 0; i < n_items; ++i) nf += fb[i] != 0;
     adapt_scan(ix, n_items, nf);
   }
   return HIVF_OK;
