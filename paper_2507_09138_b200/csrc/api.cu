@@ -1100,24 +1100,33 @@ hivf_status hivf_search(hivf_index* ix, const float* queries, uint32_t n, uint32
   hivf_ctx* c = ix->ctx;
   CK(cudaSetDevice(c->device));
   const size_t qb = (size_t)n * ix->dim * 4, ob = (size_t)n * k;
+  // results, error flag and fallback flags come back in ONE D2H copy:
+  //   ids | dists | counts | err | flags
+  const size_t o_d = ob * 8, o_c = 2 * ob * 8, o_e = o_c + (size_t)n * 4, o_f = o_e + 4,
+               total = o_f + (size_t)n * 4;
+  const bool want_fb = c->opt_scan_kernel == 0 && !ix->auto_split;
   CK(c->qin.ensure(qb));
-  CK(c->out_ids.ensure(ob * 8));
-  CK(c->out_d.ensure(ob * 8));
-  CK(c->out_cnt.ensure((size_t)n * 4));
+  CK(c->out_ids.ensure(total));
+  CK(c->hstage.ensure(total));
   CK(c->err.ensure(4));
   CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
   CK(cudaMemcpyAsync(c->qin.p, queries, qb, cudaMemcpyHostToDevice, c->stream));
-  if ((st = hivf_search_device(ix, c->qin.as<float>(), n, nprobe, k, c->out_ids.as<uint64_t>(),
-                               c->out_d.as<double>(), c->out_cnt.as<uint32_t>())) != HIVF_OK)
+  uint8_t* dpk = c->out_ids.as<uint8_t>();
+  if ((st = hivf_search_device(ix, c->qin.as<float>(), n, nprobe, k, reinterpret_cast<uint64_t*>(dpk),
+                               reinterpret_cast<double*>(dpk + o_d), reinterpret_cast<uint32_t*>(dpk + o_c))) != HIVF_OK)
     return st;
-  CK(cudaMemcpyAsync(ids_out, c->out_ids.p, ob * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(dists_out, c->out_d.p, ob * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(counts_out, c->out_cnt.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
-  int err = 0;
-  CK(cudaMemcpyAsync(&err, c->err.p, 4, cudaMemcpyDeviceToHost, c->stream));
-  std::vector<int> fb(c->opt_scan_kernel == 0 && !ix->auto_split ? n : 0);
-  if (!fb.empty()) CK(cudaMemcpyAsync(fb.data(), c->flags_f.p, 4ull * n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(dpk + o_e, c->err.p, 4, cudaMemcpyDeviceToDevice, c->stream));
+  if (want_fb) CK(cudaMemcpyAsync(dpk + o_f, c->flags_f.p, 4ull * n, cudaMemcpyDeviceToDevice, c->stream));
+  uint8_t* hpk = c->hstage.as<uint8_t>();
+  CK(cudaMemcpyAsync(hpk, dpk, want_fb ? total : o_f, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  int err = 0;
+  std::memcpy(&err, hpk + o_e, 4);
+  std::memcpy(ids_out, hpk, ob * 8);
+  std::memcpy(dists_out, hpk + o_d, ob * 8);
+  std::memcpy(counts_out, hpk + o_c, (size_t)n * 4);
+  std::vector<int> fb(want_fb ? n : 0);
+  if (want_fb) std::memcpy(fb.data(), hpk + o_f, 4ull * n);
   if (err) return fail(HIVF_EINVAL, "hivf_search: non-finite query value");
   if (!fb.empty()) {
     uint32_t nf = 0;
