@@ -12,12 +12,17 @@
 namespace hivf {
 
 // ---- layout constants ------------------------------------------------------
-// Lists live in HBM chunk-major: for list c (rows [R_c, R_c+n_c) in list order)
-// the 16-dim chunk `ch` of all its rows is one contiguous plane of n_c*64 B,
-// and inside a 64-B row slice the four 16-B groups are XOR-swizzled by
-// ((row>>1)&3) so a warp reading 8 consecutive rows at one group is
-// bank-conflict-free in shared memory (see DESIGN.md "HBM layout").
+// Lists live in HBM tile-major, chunk-major inside a tile: list c's rows
+// [R_c, R_c+n_c) (list order) form tiles of kTileRows rows (the last one may
+// be short, nt rows); a tile occupies nt*dpad floats, and inside it the 16-dim
+// chunk `ch` of its rows is one contiguous plane of nt*64 B.  Inside a 64-B
+// row slice the four 16-B groups are XOR-swizzled by ((row>>1)&3).  So a
+// (full tile x 64 dims) pipeline stage of the tensor-core scan is ONE
+// contiguous 32 KB span already in the canonical SWIZZLE_64B K-major UMMA
+// layout, and a warp reading 8 consecutive rows at one group is
+// bank-conflict-free in shared memory (see DESIGN.md "Data layout").
 constexpr int kChunk = 16;            // dims per chunk (64 B per row slice)
+constexpr uint32_t kTileRows = 128;   // rows per layout tile (= the MMA's M)
 constexpr int kQMax = 16;             // queries per scan work item
 constexpr int kKP = 32;               // candidates kept per (query, segment)
 constexpr int kScanWarps = 8;         // consumer warps per scan CTA
@@ -27,11 +32,23 @@ constexpr int kStages = 4;
 constexpr int kStageBytes = kRowBlock * kChunk * 4;  // 32 KB
 constexpr uint32_t kNoRow = 0xffffffffu;
 
-__host__ __device__ inline uint64_t swz_offset(uint64_t list_base_floats, uint64_t n_rows,
-                                               uint64_t r, uint32_t d) {
+// Rows in the tile that starts at (tile-aligned) list row r0.
+__host__ __device__ inline uint64_t tile_rows(uint64_t n_rows, uint64_t r0) {
+  const uint64_t left = n_rows - r0;
+  return left < kTileRows ? left : kTileRows;
+}
+// Float offset (from the list base) of chunk `ch` of the tile starting at row r0.
+__host__ __device__ inline uint64_t tile_chunk_offset(uint64_t n_rows, uint32_t dpad, uint64_t r0,
+                                                      uint32_t ch) {
+  return r0 * dpad + (uint64_t)ch * tile_rows(n_rows, r0) * kChunk;
+}
+// Float offset of element d of list row r.
+__host__ __device__ inline uint64_t swz_offset(uint64_t list_base_floats, uint64_t n_rows, uint64_t r,
+                                               uint32_t d, uint32_t dpad) {
   const uint32_t ch = d >> 4, e = d & 15;
   const uint32_t g = (e >> 2) ^ ((uint32_t)(r >> 1) & 3u);
-  return list_base_floats + (uint64_t)ch * n_rows * kChunk + r * kChunk + g * 4 + (e & 3);
+  const uint64_t r0 = r - r % kTileRows;
+  return list_base_floats + tile_chunk_offset(n_rows, dpad, r0, ch) + (r - r0) * kChunk + g * 4 + (e & 3);
 }
 
 // ---- error bound of the fp32 filter -------------------------------------------

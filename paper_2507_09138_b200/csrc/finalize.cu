@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     const uint64_t lr = crow[i] - lbeg;
     const float* lb = list_base(ix, c, lbeg);
     cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
     });
     cid[i] = ix.ids[crow[i]];
   }
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView
     const float* lb = list_base(ix, c, beg);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     for (uint32_t g = 0; g < ix.dpad / 4; ++g) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+      const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
       const float4 q4 = __ldg(reinterpret_cast<const float4*>(qs + g * 4));
       a0 = __fmaf_rn(x.x, q4.x, a0);
       a1 = __fmaf_rn(x.y, q4.y, a1);
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView
     const float dh = __fmaf_rn(-2.f, dot, __fadd_rn(ix.xnorm2[beg + lr], qv.qn2[b]));
     if (__fsub_rd(dh, __double2float_ru(E)) > tq) continue;  // NaN keeps the row
     const double d = exact_row_pipelined(ix.dim, qs, [&](uint32_t g) {
-      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
     });
     const uint32_t pos = atomicAdd(&R.cnt[b], 1u);
     if (pos < R.per_query) {
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_repair(
     const uint64_t lr = crow[i] - lbeg;
     const float* lb = list_base(ix, c, lbeg);
     cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
     });
     cid[i] = ix.ids[crow[i]];
   }
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
         if (filt) {
           float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
           for (uint32_t g = 0; g < ix.dpad / 4; ++g) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+            const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
             const float4 q4 = *reinterpret_cast<const float4*>(qsh + g * 4);
             a0 = __fmaf_rn(x.x, q4.x, a0);
             a1 = __fmaf_rn(x.y, q4.y, a1);
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
         }
         if (need) {
           dist = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-            return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+            return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
           });
           id = ix.ids[r];
         }

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     const uint64_t lr = crow[i] - lbeg;
     const float* lb = list_base(ix, c, lbeg);
     cdist[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+      return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
     });
     cid[i] = ix.ids[crow[i]];
   }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) k_exact_items(IndexView ix, QueryView qv,
         const uint64_t n_c = end - beg, lr = r - beg;
         const float* lb = list_base(ix, c, beg);
         td[threadIdx.x] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) {
-          return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4)));
+          return __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
         });
         ti[threadIdx.x] = ix.ids[r];
       }

@@ -44,7 +44,7 @@ __global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first,
     v[e] = d < dim ? src[lrow * dim + d] : 0.f;
     if (!isfinite(v[e])) *err = 1;
   }
-  const uint64_t o = swz_offset(base, n_c, lr, g * 4);
+  const uint64_t o = swz_offset(base, n_c, lr, g * 4, dpad);
   *reinterpret_cast<float4*>(dst + o) = make_float4(v[0], v[1], v[2], v[3]);
   if (g == 0) {
     double acc = 0.0;
@@ -73,7 +73,7 @@ __global__ void k_unpack_rows(const float* __restrict__ vec, const uint64_t* __r
     if (list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
   }
   const uint64_t n_c = list_off[lo + 1] - list_off[lo];
-  out[gid] = vec[swz_offset(list_off[lo] * (uint64_t)dpad, n_c, r - list_off[lo], d)];
+  out[gid] = vec[swz_offset(list_off[lo] * (uint64_t)dpad, n_c, r - list_off[lo], d, dpad)];
 }
 
 __global__ void k_pack_centroids(const float* __restrict__ src, uint32_t K, uint32_t dim,
@@ -114,7 +114,7 @@ __global__ void k_mean_assigned(IndexView ix, double* partial) {
     const uint64_t lr = r - ix.list_off[lo];
     double d = 0.0;
     for (uint32_t k = 0; k < ix.dim; ++k)
-      d = exact_step(d, ix.vec[swz_offset(base, n_c, lr, k)], ix.cent[(uint64_t)lo * ix.dpad + k]);
+      d = exact_step(d, ix.vec[swz_offset(base, n_c, lr, k, ix.dpad)], ix.cent[(uint64_t)lo * ix.dpad + k]);
     acc += d;
   }
   red[threadIdx.x] = acc;
@@ -231,7 +231,7 @@ __global__ void k_gather_rows(IndexView ix, const uint64_t* __restrict__ rows, u
     if (ix.list_off[mid + 1] <= r) a = mid + 1; else b = mid;
   }
   const uint64_t beg = ix.list_off[a], n_c = ix.list_off[a + 1] - beg;
-  out[gid] = list_base(ix, a, beg)[swz_offset(0, n_c, r - beg, d)];
+  out[gid] = list_base(ix, a, beg)[swz_offset(0, n_c, r - beg, d, ix.dpad)];
 }
 
 __global__ void k_iota64(uint64_t* v, uint64_t n) {

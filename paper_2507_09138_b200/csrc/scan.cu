@@ -236,9 +236,14 @@ __global__ void __launch_bounds__((kScanWarps + 1) * 32, 1) k_scan(ScanParams P)
           for (uint32_t ch = 0; ch < nch; ++ch) {
             mbar_wait(&empty[st], ph ^ 1);
             mbar_arrive_expect_tx(&full[st], bytes);
-            bulk_g2s(stage + st * (kStageBytes / 4),
-                     lbase + (uint64_t)ch * n_c * kChunk + (uint64_t)(item.row0 + r0) * kChunk, bytes,
-                     &full[st]);
+            // the row block spans up to 4 layout tiles: one copy per tile piece,
+            // landing back to back (row order) in the stage
+            for (uint32_t t0 = 0; t0 < nr; t0 += kTileRows) {
+              const uint64_t rt = (uint64_t)item.row0 + r0 + t0;
+              const uint32_t tn = (uint32_t)tile_rows(n_c, rt);
+              bulk_g2s(stage + st * (kStageBytes / 4) + t0 * kChunk, lbase + tile_chunk_offset(n_c, dpad, rt, ch),
+                       tn * kChunk * 4, &full[st]);
+            }
             if (++st == kStages) {
               st = 0;
               ph ^= 1;

@@ -24,8 +24,8 @@
 // (IndexView::e_*), so every id/distance is still the reference's exact double.
 //
 // CTA (1 per SM, persistent) = 6 warps:
-//   warp 0   producer: 1-D bulk copies of (<=128 rows x 16 dims) list slices --
-//            contiguous in the chunk-major HBM layout, whose 16-B XOR swizzle
+//   warp 0   producer: ONE 1-D bulk copy per (128-row tile x 64 dims) stage --
+//            contiguous in the tile-major HBM layout, whose 16-B XOR swizzle
 //            IS the canonical SWIZZLE_64B K-major UMMA layout -- into a deep
 //            ring (3-8 stages of 4 chunks = 64 dims) sized from the smem left
 //            after the resident query group
@@ -336,10 +336,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
             }
             const long long _tp = P.prof ? clock64() : 0;
             mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4);
-            for (uint32_t c = 0; c < cn; ++c)
-              bulk_g2s(aring + a * kTcStageBytes + c * kTcChunkBytes,
-                       lbase + (uint64_t)(c0 + c) * n_c * kChunk + (uint64_t)r0 * kChunk,
-                       nr * kChunk * 4, &full[a]);
+            if (nr == kTcTile) {  // full tile: the stage is one contiguous span
+              bulk_g2s(aring + a * kTcStageBytes, lbase + tile_chunk_offset(n_c, dpad, r0, c0),
+                       cn * kTcChunkBytes, &full[a]);
+            } else {  // short last tile: its chunk planes are nr rows apart
+              for (uint32_t c = 0; c < cn; ++c)
+                bulk_g2s(aring + a * kTcStageBytes + c * kTcChunkBytes,
+                         lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c), nr * kChunk * 4, &full[a]);
+            }
             if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 14], (unsigned long long)(clock64() - _tp));
             if (++ra == SA) { ra = 0; rpa ^= 1; }
             if (pf == 1) {
