@@ -125,9 +125,8 @@ struct hivf_ctx {
   // scratch
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
-      cand_n, out_ids, out_d, out_cnt, qin, it_off, it_cl, it_k, heap_ids, heap_d, heap_n,
-      changed, x_ids, x_d, x_cnt, x_tot, tau, flags2, rep_entries, rep_n,
-      rep_cnt, rep_d, rep_ids;
+      cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, rep_entries, rep_n, rep_cnt,
+      rep_d, rep_ids;
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;
@@ -170,12 +169,11 @@ struct hivf_ctx {
   }
   ~hivf_ctx() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-    for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq, &pl,
-                    &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items, &n_items,
-                    &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &out_d, &out_cnt,
-                    &qin, &it_off, &it_cl, &it_k, &heap_ids, &heap_d, &heap_n, &changed, &x_ids,
-                    &x_d, &x_cnt, &x_tot, &tau, &flags2,
-                    &rep_entries, &rep_n, &rep_cnt, &rep_d, &rep_ids})
+    for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq,
+                    &pl, &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items,
+                    &n_items, &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &qin,
+                    &x_ids, &x_d, &x_cnt, &x_tot, &tau, &flags2, &rep_entries, &rep_n, &rep_cnt,
+                    &rep_d, &rep_ids})
       b->release();
     hstage.release();
     if (own_stream && stream) cudaStreamDestroy(stream);

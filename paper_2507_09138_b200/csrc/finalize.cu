@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView
     if (lr >= s1) continue;
     const float* lb = list_base(ix, c, beg);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 16
     for (uint32_t g = 0; g < ix.dpad / 4; ++g) {
       const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
       const float4 q4 = __ldg(reinterpret_cast<const float4*>(qs + g * 4));
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
         bool need = true;
         if (filt) {
           float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 16
           for (uint32_t g = 0; g < ix.dpad / 4; ++g) {
             const float4 x = __ldg(reinterpret_cast<const float4*>(lb + swz_offset(0, n_c, lr, g * 4, ix.dpad)));
             const float4 q4 = *reinterpret_cast<const float4*>(qsh + g * 4);
