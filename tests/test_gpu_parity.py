@@ -365,3 +365,37 @@ def test_shard_index_escalation_and_filtered_fallback(ctx):
     Q = (centers[rng.integers(0, 16, 64)] + 0.05 * rng.standard_normal((64, dim))).astype(np.float32)
     for nprobe, k in [(32, 10), (64, 32), (16, 1)]:
         _check_search(ix, csr, Q, nprobe, k)
+
+
+def test_search_device_cuda_graph_capture(ctx):
+    """hivf_search_device is CUDA-graph capturable after one warm call with the
+    same shapes (include/hivf.h): a captured search replays to the same
+    results as direct calls, for new query contents in the same buffer."""
+    import torch
+    from paper_2507_09138_b200 import Context
+    rng = np.random.default_rng(21)
+    s = torch.cuda.Stream()
+    c2 = Context(0, s)
+    ix, csr, X, centers = _random_index(c2, rng, 30000, 64, 48)
+    B, npb, k = 64, 12, 10
+    qs = [(centers[rng.integers(0, len(centers), B)] + 0.3 * rng.standard_normal((B, 64))).astype(np.float32)
+          for _ in range(3)]
+    qbuf = torch.empty(B, 64, dtype=torch.float32, device="cuda")
+    ids = torch.empty(B, k, dtype=torch.int64, device="cuda")
+    dd = torch.empty(B, k, dtype=torch.float64, device="cuda")
+    cnt = torch.empty(B, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(s):
+        qbuf.copy_(torch.from_numpy(qs[0]))
+        ix.search_device(qbuf, npb, k, ids, dd, cnt)  # warm: sizes every scratch buffer
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ix.search_device(qbuf, npb, k, ids, dd, cnt)
+        for q in qs:
+            qbuf.copy_(torch.from_numpy(q))
+            g.replay()
+            s.synchronize()
+            oi, od, oc = csr.search(q, npb, k)
+            assert np.array_equal(cnt.cpu().numpy(), oc)
+            assert np.array_equal(ids.cpu().numpy().astype(np.uint64), oi)
+            assert np.array_equal(dd.cpu().numpy().view(np.uint64), od.view(np.uint64))
