@@ -22,10 +22,13 @@ buffers, one call per sub-stage), the reference's own RetrievalEngine::execute
 (oracle/_ref, live_math=true on all host cores).  Every completed stage's heap
 is compared bit-for-bit between the arms.
 
-Latencies: `substage` = one execute call (wall clock, synchronous, host in/out);
-`stage` = first sub-stage start -> completing sub-stage end of a retrieval
-stage (the search latency a request sees, generation time excluded);
-percentiles are nearest-rank as in proj/src/report.cpp:15-21.
+Latencies are engine time: each arm times its own API calls (wall clock,
+synchronous, host buffers in/out) -- `substage` = make_cursor of the stages
+admitted at that step + one SubStageBatch execute; `stage` = admission ->
+completing sub-stage of a retrieval stage on the clock that advances only by
+engine time (the search latency a request sees; generation time and this
+driver's own bookkeeping / plan_substages excluded).  Percentiles are
+nearest-rank as in proj/src/report.cpp:15-21.
 """
 from __future__ import annotations
 
@@ -117,9 +120,13 @@ class GpuArm:
     def __init__(self, ix, nprobe, k):
         self.ix, self.nprobe, self.k = ix, nprobe, k
         self.cur = {}
+        self.api_ms = []  # time inside hivf_scan_items (the C-ABI call) per sub-stage
 
     def submit(self, keys, queries):
-        plans = self.ix.select_clusters(np.stack(queries).astype(np.float32), self.nprobe)
+        Q = np.stack(queries).astype(np.float32)
+        t0 = time.perf_counter()
+        plans = self.ix.select_clusters(Q, self.nprobe)  # make_cursor's select_clusters, batched
+        self.last_ms = (time.perf_counter() - t0) * 1e3
         out = []
         for key, q, p in zip(keys, queries, plans):
             self.cur[key] = {"q": np.asarray(q, np.float32), "plan": p.astype(np.uint32), "pos": 0,
@@ -142,7 +149,10 @@ class GpuArm:
         hd = np.stack([self.cur[key]["d"] for key, _ in items])
         hn = np.array([self.cur[key]["n"] for key, _ in items], np.uint32)
         kv = np.full(n, self.k, np.uint32)
+        t0 = time.perf_counter()
         self.ix.scan_items(Q, off, clusters, kv, hi, hd, hn)
+        self.last_ms = (time.perf_counter() - t0) * 1e3
+        self.api_ms.append(self.last_ms)
         done = []
         for i, (key, m) in enumerate(items):
             c = self.cur[key]
@@ -174,11 +184,13 @@ class RefArm:
 
     def submit(self, keys, queries):
         out = []
+        t0 = time.perf_counter()
         for key, q in zip(keys, queries):
             p = self.eng.submit(key[0], key[1], q, self.nprobe, self.k)
             self.plans[key] = p
             self.pos[key] = 0
             out.append(p)
+        self.last_ms = (time.perf_counter() - t0) * 1e3
         return out
 
     def execute(self, items):
@@ -189,7 +201,10 @@ class RefArm:
         for i, (key, m) in enumerate(items):
             cl.append(self.plans[key][self.pos[key]:self.pos[key] + m])
             off[i + 1] = off[i] + m
-        _, completed = self.eng.execute(reqs, nodes, off, np.concatenate(cl), live=True)
+        cls = np.concatenate(cl)
+        t0 = time.perf_counter()
+        _, completed = self.eng.execute(reqs, nodes, off, cls, live=True)
+        self.last_ms = (time.perf_counter() - t0) * 1e3
         done = []
         for i, (key, m) in enumerate(items):
             self.pos[key] += m
@@ -218,6 +233,7 @@ def run_stream(arm, queries, sizes, concurrency, n_requests, budget_rows, seed=5
     t_start = {}
     results, plans = {}, {}
     sub_ms, stage_ms, batch = [], [], []
+    clock = 0.0  # ms of engine time
     started = finished = 0
     while finished < n_requests:
         # admit: ready follow-up stages first, then new requests
@@ -228,9 +244,14 @@ def run_stream(arm, queries, sizes, concurrency, n_requests, budget_rows, seed=5
             follow[req] = qs[1:]
         admit = pending[: max(0, concurrency - len(live))]
         pending = pending[len(admit):]
-        t0 = time.perf_counter()
+        # engine time only (the arms time their own API calls): make_cursor for the
+        # admitted stages + one SubStageBatch execute; the stream's bookkeeping and
+        # plan_substages (the scheduler's work) advance no clock
+        t0 = clock
+        eng = 0.0
         if admit:
             ps = arm.submit([k for k, _ in admit], [q for _, q in admit])
+            eng += arm.last_ms
             for (key, _), p in zip(admit, ps):
                 plans[key] = np.asarray(p, np.uint32)
                 t_start[key] = t0
@@ -239,12 +260,14 @@ def run_stream(arm, queries, sizes, concurrency, n_requests, budget_rows, seed=5
         taken = plan_substages(remaining, sizes, budget_rows)
         items = [(key, m) for key, m in zip(live, taken) if m > 0]
         done = arm.execute(items)
-        t1 = time.perf_counter()
-        sub_ms.append((t1 - t0) * 1e3)
+        eng += arm.last_ms
+        clock += eng
+        t1 = clock
+        sub_ms.append(eng)
         batch.append(len(items))
         for key in done:
             results[key] = arm.result(key)
-            stage_ms.append((t1 - t_start.pop(key)) * 1e3)
+            stage_ms.append(t1 - t_start.pop(key))
             live.remove(key)
             req, node = key
             if follow.get(req):
@@ -253,7 +276,7 @@ def run_stream(arm, queries, sizes, concurrency, n_requests, budget_rows, seed=5
                 follow.pop(req, None)
                 finished += 1
     return {"substage_ms": sub_ms, "stage_ms": stage_ms, "batch": batch, "results": results,
-            "plans": plans}
+            "plans": plans, "api_ms": list(getattr(arm, "api_ms", []))}
 
 
 def summarize(r):
@@ -264,7 +287,9 @@ def summarize(r):
             "substage_ms": {"p50": round(nearest_rank(r["substage_ms"], 50), 3),
                             "p99": round(nearest_rank(r["substage_ms"], 99), 3)},
             "stage_ms": {"p50": round(nearest_rank(r["stage_ms"], 50), 3),
-                         "p99": round(nearest_rank(r["stage_ms"], 99), 3)}}
+                         "p99": round(nearest_rank(r["stage_ms"], 99), 3)},
+            **({"api_call_ms": {"p50": round(nearest_rank(r["api_ms"], 50), 3),
+                                "p99": round(nearest_rank(r["api_ms"], 99), 3)}} if r.get("api_ms") else {})}
 
 
 def same_results(a, b):
