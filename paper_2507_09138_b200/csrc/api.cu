@@ -119,13 +119,14 @@ struct hivf_ctx {
   // split-precision, 3 tcgen05 single-pass
   int opt_scan_kernel = 0;
   int opt_scan_ctas = 0;
+  int opt_no_bound = 0;  // debug: disable the scan's shared per-query drop bound
   // tiered residency: list bytes an index may keep in HBM (0 = all lists in HBM);
   // the rest stays in a pinned host backing store read over PCIe
   uint64_t opt_hbm_list_budget = 0;
   // scratch
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
-      cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, rep_entries, rep_n, rep_cnt,
+      cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, qbound, rep_entries, rep_n, rep_cnt,
       rep_d, rep_ids;
   HBuf hstage;
   hivf_stats stats{};
@@ -172,7 +173,7 @@ struct hivf_ctx {
     for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq,
                     &pl, &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items,
                     &n_items, &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &qin,
-                    &x_ids, &x_d, &x_cnt, &x_tot, &tau, &flags2, &rep_entries, &rep_n, &rep_cnt,
+                    &x_ids, &x_d, &x_cnt, &x_tot, &tau, &flags2, &qbound, &rep_entries, &rep_n, &rep_cnt,
                     &rep_d, &rep_ids})
       b->release();
     hstage.release();
@@ -442,6 +443,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   } else if (!strcmp(name, "hbm_list_budget")) {  // bytes; applies to indexes created later
     if (value < 0) return fail(HIVF_EINVAL, "hbm_list_budget must be >= 0");
     ctx->opt_hbm_list_budget = (uint64_t)value;
+  } else if (!strcmp(name, "no_bound")) {
+    ctx->opt_no_bound = value != 0;
   } else if (!strcmp(name, "scan_ctas")) {
     ctx->opt_scan_ctas = (int)value;
   } else if (!strcmp(name, "scan_kernel")) {
@@ -906,8 +909,10 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
 
 // Grouped scan over pairs (pair_query/pair_list already in c->pq / c->pl).
 // kind_override: 0 -> the index's current scan kernel, else 1/2/3
+// topk > 0 (a search for the k nearest): the tensor-core scan shares a per-query
+// drop bound across items (scan_tc.cu); 0 (node-split items, seeded heaps) off.
 static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs, bool timed,
-                            int kind_override = 0) {
+                            int kind_override = 0, uint32_t topk = 0) {
   hivf_ctx* c = ix->ctx;
   const int kind = kind_override ? kind_override : ix->scan_kind();
   const IndexView v = ix->view_kind(kind);
@@ -936,12 +941,16 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
                         c->stream);
   CKL();
   const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;
+  if (tc && topk) {  // shared drop bounds start at "none" (0x7f7f7f7f ~ 3.4e38)
+    CK(c->qbound.ensure((size_t)qv.n * 4));
+    CK(cudaMemsetAsync(c->qbound.p, 0x7f, (size_t)qv.n * 4, c->stream));
+  }
   if (timed) c->mark(1);
   if (tc)
     launch_scan_tc(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                    c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
                    c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
-                   kind == 2, c->stream);
+                   kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, c->stream);
   else
     launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                 c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
@@ -1010,7 +1019,7 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
     CKL();
   }
   if (!exact_only) {
-    if ((st = run_scan(ix, qv, np, true)) != HIVF_OK) return st;
+    if ((st = run_scan(ix, qv, np, true, 0, c->opt_no_bound ? 0 : k)) != HIVF_OK) return st;
     c->mark(2);
     CK(c->tau.ensure((size_t)n * 4));
     // in-place repair of segments whose completeness proof failed

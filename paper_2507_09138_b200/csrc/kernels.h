@@ -113,7 +113,8 @@ int scan_smem_bytes(uint32_t dpad);
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
-                    uint32_t* out_n, int n_ctas, int split, cudaStream_t s);
+                    uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
+                    cudaStream_t s);
 uint32_t scan_tc_qmax(uint32_t dpad, int split);
 void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)
 int tc_probe_conversion(cudaStream_t s);  // 0 trunc, 1 RNE, 2 unsupported

@@ -81,6 +81,11 @@ struct TcParams {
   int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA, bit2 skip all MMAs, bit3 skip odd k-steps (results then inexact), bit4 spin-wait epilogue
   int split;      // 1: 3-pass split precision, 0: single-pass tf32 (looser bound)
   unsigned long long* prof;  // debug: per-CTA stall counters [gridDim.x][16] (nullptr = off)
+  // shared per-query drop bound: U_q = min over
+  // finished items of their k-th smallest (d^ + E); rows with d^ >= U_q + E
+  // cannot reach the top-k and are not kept.  topk == 0 disables it.
+  float* qbound;
+  uint32_t topk;
 };
 
 // ---- tcgen05 PTX wrappers ------------------------------------------------------
@@ -190,6 +195,14 @@ __device__ __forceinline__ void tmem_wait_ld() {
 // ---- the kernel ------------------------------------------------------------------
 // smem carve-out (1024-B aligned): per stage [A_hi 16K | A_lo 16K | B_hi | B_lo],
 // then the resident (unsplit) query group, then the mbarriers.
+constexpr float kInfF = __builtin_inff();
+// Drop bound for a query from its shared upper bound u on the true k-th
+// distance: rows with d^ >= u + E (rounded up, plus two ulps) satisfy
+// d^ - E > u >= tau, so they are neither top-k nor finalize candidates.
+__device__ __forceinline__ float drop_bound(float u, float E) {
+  const float g = __fadd_ru(u, E);
+  return nextafterf(nextafterf(g, kInfF), kInfF);
+}
 __device__ __forceinline__ float tf32_trunc(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
@@ -240,6 +253,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   __shared__ uint32_t s_tmem;
   float (*s_qn2)[32] = reinterpret_cast<float (*)[32]>(qempty + 1);            // [kItemQ][32]
   uint32_t (*s_slot)[32] = reinterpret_cast<uint32_t (*)[32]>(s_qn2 + kItemQ);  // [kItemQ][32]
+  float (*s_E)[32] = reinterpret_cast<float (*)[32]>(s_slot + kItemQ);            // [kItemQ][32]
+  uint32_t (*s_qi)[32] = reinterpret_cast<uint32_t (*)[32]>(s_E + kItemQ);        // [kItemQ][32]
+  float (*s_g)[32] = reinterpret_cast<float (*)[32]>(s_qi + kItemQ);              // [4][32]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -479,6 +495,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           my_qi = P.pair_query[pair];
           s_qn2[slot][n] = P.qv.qn2[my_qi];
           s_slot[slot][n] = pair * P.ix.s_max + item.seg;
+          s_E[slot][n] = seg_bound(P.ix, P.qv.qnorm[my_qi], P.ix.maxnorm[item.list]);
+          s_qi[slot][n] = my_qi;
         }
       }
       const long long _ts = P.prof ? clock64() : 0;
@@ -596,6 +614,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         const uint32_t srow0 = quad * 32 + lane;
         if (srow0 < item.nrows) xn_next = __ldg(P.ix.xnorm2 + lbeg + item.row0 + srow0);
       }
+      float gmin = kInfF;  // lane j: smallest drop bound used for query j in this item
       for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t srow = t * kTcTile + quad * 32 + lane;
         const bool valid = srow < item.nrows;
@@ -622,6 +641,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           tb = 0;
           tph ^= 1;
         }
+        // lane j: this tile's drop bound for query j (read through L2: other
+        // CTAs lower it as their items finish).  After the tfull wait: the
+        // stagers' per-item s_qi / s_E writes are ordered before it.
+        float gl = kInfF;
+        if (P.topk && lane < (int)nq) {
+          const float u = __ldcg(P.qbound + s_qi[slot][lane]);
+          if (u < 3.0e38f) gl = drop_bound(u, s_E[slot][lane]);
+        }
+        gmin = fminf(gmin, gl);
         const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -630,7 +658,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
                                   : __uint_as_float(acc[j]);
           const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, s_qn2[slot][j]))
                                 : __int_as_float(0x7f800000);
-          float th = __shfl_sync(FULL, ld[j], 31);
+          const float gj = __shfl_sync(FULL, gl, j);
+          float th = fminf(__shfl_sync(FULL, ld[j], 31), gj);
           unsigned m = __ballot_sync(FULL, v < th);
           if (__popc(m) > 2) {
             // many candidates (early tiles): bitonic-sort this tile's 32 values and
@@ -690,7 +719,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
               ld[j] = cv;
               lr[j] = crow;
             }
-            th = __shfl_sync(FULL, ld[j], 31);
+            th = fminf(__shfl_sync(FULL, ld[j], 31), gj);
             m &= ~(1u << src);
             m &= __ballot_sync(FULL, v < th);
           }
@@ -703,6 +732,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       for (int h0 = 0; h0 < 32; h0 += kMergeQ) {
         if (h0 >= (int)nq) break;
         named_bar_sync(2, kTcEpiWarps * 32);  // previous round's reads are done
+        if (h0 == 0) s_g[ew][lane] = gmin;
 #pragma unroll
         for (int jj = 0; jj < kMergeQ; ++jj) {
           if (h0 + jj >= (int)nq) break;
@@ -738,9 +768,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           P.out_row[(uint64_t)oslot * kKP + lane] = r;
           const uint32_t n_valid = __popc(__ballot_sync(FULL, r != kNoRow));
           const float last = __shfl_sync(FULL, v, 31);
+          // every row not kept has d^ >= the 32nd kept value (when 32 are kept)
+          // or >= a drop bound this item used (bounds only decrease)
+          const float gm = fminf(fminf(s_g[0][j], s_g[1][j]), fminf(s_g[2][j], s_g[3][j]));
+          const float vk = __shfl_sync(FULL, v, (int)(P.topk ? P.topk - 1 : 0));
           if (lane == 0) {
-            P.out_thr[oslot] = n_valid == kKP ? last : __int_as_float(0x7f800000);
+            P.out_thr[oslot] = fminf(n_valid == kKP ? last : kInfF, gm);
             P.out_n[oslot] = n_valid;
+            if (P.topk && n_valid >= P.topk) {  // this item's k-th upper bound
+              float u = __fadd_ru(vk, s_E[slot][j]);
+              if (!(u > 0.f)) u = 0.f;
+              atomicMin(reinterpret_cast<int*>(P.qbound + s_qi[slot][j]), __float_as_int(u));
+            }
           }
         }
       }
@@ -788,7 +827,7 @@ static int tc_budget() {
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
   return 1024 + (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64 +
          kTcEpiWarps * kMergeQ * 32 * 8 +                         // merge scratch
-         8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 8;
+         8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 16 + 4 * 32 * 4;
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int left = tc_budget() - tc_fixed_bytes(dpad, qmax, split);
@@ -840,11 +879,12 @@ int scan_tc_smem_bytes(uint32_t dpad, int split) {
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
-                    uint32_t* out_n, int n_ctas, int split, cudaStream_t s) {
+                    uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
+                    cudaStream_t s) {
   const uint32_t q = scan_tc_qmax(ix.dpad, split);
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
-             split, g_tc_prof};
+             split, g_tc_prof, qbound, qbound ? topk : 0u};
   const int smem = scan_tc_smem_bytes(ix.dpad, split);
   static int attr_bytes = 0;
   if (attr_bytes < smem) {
