@@ -911,8 +911,9 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
 // kind_override: 0 -> the index's current scan kernel, else 1/2/3
 // topk > 0 (a search for the k nearest): the tensor-core scan shares a per-query
 // drop bound across items (scan_tc.cu); 0 (node-split items, seeded heaps) off.
+// item_bounds: node-split path -- fixed per-item bounds already in c->qbound
 static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs, bool timed,
-                            int kind_override = 0, uint32_t topk = 0) {
+                            int kind_override = 0, uint32_t topk = 0, bool item_bounds = false) {
   hivf_ctx* c = ix->ctx;
   const int kind = kind_override ? kind_override : ix->scan_kind();
   const IndexView v = ix->view_kind(kind);
@@ -941,7 +942,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
                         c->stream);
   CKL();
   const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;
-  if (tc && topk) {  // shared drop bounds start at "none" (0x7f7f7f7f ~ 3.4e38)
+  if (tc && topk && !item_bounds) {  // shared drop bounds start at "none" (0x7f7f7f7f ~ 3.4e38)
     CK(c->qbound.ensure((size_t)qv.n * 4));
     CK(cudaMemsetAsync(c->qbound.p, 0x7f, (size_t)qv.n * 4, c->stream));
   }
@@ -950,7 +951,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
     launch_scan_tc(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                    c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
                    c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
-                   kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, c->stream);
+                   kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, item_bounds ? 0 : 1, c->stream);
   else
     launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                 c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
@@ -1461,7 +1462,14 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
   const bool exact_only = c->opt_force_exact || kmax > (uint32_t)kKP;
   CK(cudaMemsetAsync(d_fb, 0, n_items * 4ull, s));
   if (!exact_only && n_pairs) {
-    if ((st = run_scan(ix, qv, n_pairs, false)) != HIVF_OK) return st;
+    // drop bound per item: its heap's worst before the sub-stage (fixed)
+    const bool use_bounds = !c->opt_no_bound;
+    if (use_bounds) {
+      CK(c->qbound.ensure((size_t)n_items * 4));
+      launch_item_bounds(d_hd, d_hn, d_k, heap_stride, n_items, c->qbound.as<float>(), s);
+      CKL();
+    }
+    if ((st = run_scan(ix, qv, n_pairs, false, 0, use_bounds ? 1u : 0u, use_bounds)) != HIVF_OK) return st;
     launch_finalize_items(v, qv, n_items, d_off, d_cl, d_k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
                           c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), d_hi, d_hd, d_hn, heap_stride, d_ch,
                           d_fb, s);

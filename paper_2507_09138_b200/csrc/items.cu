@@ -360,4 +360,28 @@ void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_ite
                                            heap_n, heap_stride, changed, flags);
 }
 
+namespace {
+// Rows with d^ >= float_ru(worst) + E can never enter a full heap at any step
+// of the sub-stage (its worst only decreases), so the scan may drop them
+// without touching the per-cluster `changed` semantics.
+__global__ void k_item_bounds(const double* heap_d, const uint32_t* heap_n, const uint32_t* k, uint32_t stride,
+                              uint32_t n_items, float* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const uint32_t n = heap_n[i];
+  float u = 3.3e38f;  // "none" (the scan treats >= 3e38 as no bound)
+  if (n > 0 && n >= k[i]) {
+    const double w = heap_d[(uint64_t)i * stride + n - 1];
+    if (w < 3.0e38) u = __double2float_ru(w);
+    if (!(u > 0.f)) u = 0.f;
+  }
+  out[i] = u;
+}
+}  // namespace
+
+void launch_item_bounds(const double* heap_d, const uint32_t* heap_n, const uint32_t* k, uint32_t stride,
+                        uint32_t n_items, float* out, cudaStream_t s) {
+  if (n_items) k_item_bounds<<<(n_items + 255) / 256, 256, 0, s>>>(heap_d, heap_n, k, stride, n_items, out);
+}
+
 }  // namespace hivf

@@ -114,7 +114,7 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    cudaStream_t s);
+                    int bound_update, cudaStream_t s);
 uint32_t scan_tc_qmax(uint32_t dpad, int split);
 void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)
 int tc_probe_conversion(cudaStream_t s);  // 0 trunc, 1 RNE, 2 unsupported
@@ -175,6 +175,9 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
                          double* d_out, uint32_t* counts_out, uint64_t* part_ids,
                          double* part_d, uint32_t* part_cnt, uint64_t* part_total,
                          const float* tau, cudaStream_t s);
+// node-split drop bounds: float_ru(heap worst) for full heaps, "none" otherwise
+void launch_item_bounds(const double* heap_d, const uint32_t* heap_n, const uint32_t* k, uint32_t stride,
+                        uint32_t n_items, float* out, cudaStream_t s);
 void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_items,
                            const uint32_t* item_off, const uint32_t* clusters, const uint32_t* k,
                            const float* cand_d, const uint32_t* cand_row, const float* cand_thr,

@@ -86,6 +86,10 @@ struct TcParams {
   // cannot reach the top-k and are not kept.  topk == 0 disables it.
   float* qbound;
   uint32_t topk;
+  // 0: the bounds are fixed inputs (node-split items: the heap's worst before
+  // the sub-stage -- updating them from later clusters would change the
+  // reference's per-cluster `changed` flags), 1: items publish their k-th
+  uint32_t bound_update;
 };
 
 // ---- tcgen05 PTX wrappers ------------------------------------------------------
@@ -775,7 +779,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           if (lane == 0) {
             P.out_thr[oslot] = fminf(n_valid == kKP ? last : kInfF, gm);
             P.out_n[oslot] = n_valid;
-            if (P.topk && n_valid >= P.topk) {  // this item's k-th upper bound
+            if (P.bound_update && n_valid >= P.topk) {  // this item's k-th upper bound
               float u = __fadd_ru(vk, s_E[slot][j]);
               if (!(u > 0.f)) u = 0.f;
               atomicMin(reinterpret_cast<int*>(P.qbound + s_qi[slot][j]), __float_as_int(u));
@@ -880,11 +884,11 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    cudaStream_t s) {
+                    int bound_update, cudaStream_t s) {
   const uint32_t q = scan_tc_qmax(ix.dpad, split);
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
-             split, g_tc_prof, qbound, qbound ? topk : 0u};
+             split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u};
   const int smem = scan_tc_smem_bytes(ix.dpad, split);
   static int attr_bytes = 0;
   if (attr_bytes < smem) {
