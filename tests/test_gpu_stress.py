@@ -62,3 +62,57 @@ def test_random_configs(ctx, seed, kernel):
         assert np.array_equal(ix.select_clusters(Q, nprobe), csr.assign(Q, nprobe)[0])
     finally:
         ctx.set_option("scan_kernel", 0)
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("HIVF_STRESS_SEEDS", "12")) // 2 + 2)))
+def test_random_node_split(ctx, seed):
+    """hivf_scan_items over random sub-stage slices with seeded heaps (a full
+    seeded heap turns on the per-item drop bound from the first sub-stage) vs
+    search_clusters of the C restatement: heaps and per-cluster changed flags."""
+    from paper_2507_09138_b200 import IvfIndex
+    X, ids, cents, assign, metric, Q, nprobe, k = _case(5000 + seed)
+    rng = np.random.default_rng(seed)
+    csr = oracle.CsrIndex.from_assignments(X, ids, cents, assign, metric)
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids, metric)
+    Q = Q[:24]
+    B = len(Q)
+    plans = ix.select_clusters(Q, nprobe)
+    qs = np.stack([oracle.normalized(q) if metric == 1 else q for q in Q]).astype(np.float32)
+    kv = rng.integers(1, 33, B).astype(np.uint32)
+    stride = 32
+    hi = np.zeros((B, stride), np.uint64)
+    hd = np.zeros((B, stride), np.float64)
+    hn = np.zeros(B, np.uint32)
+    heaps = [oracle.TopK(int(kv[b])) for b in range(B)]
+    # seeds: exact distances to random docs (probe_cache-style), half the cursors
+    for b in range(B):
+        if rng.random() < 0.5:
+            for r in rng.choice(len(X), size=int(kv[b]) + 3, replace=False):
+                heaps[b].insert(int(ids[r]), oracle.squared_l2(qs[b], X[r]))
+            ent = heaps[b].entries()
+            hn[b] = len(ent)
+            for j, (i, d) in enumerate(ent):
+                hi[b, j], hd[b, j] = i, d
+    pos = np.zeros(B, np.int64)
+    while (pos < nprobe).any():
+        take = [int(min(nprobe - pos[b], rng.integers(1, 6))) if pos[b] < nprobe else 0 for b in range(B)]
+        items = [b for b in range(B) if take[b] > 0]
+        off = np.zeros(len(items) + 1, np.uint32)
+        cl = []
+        for i, b in enumerate(items):
+            cl.append(plans[b, pos[b]:pos[b] + take[b]])
+            off[i + 1] = off[i] + take[b]
+        cl = np.concatenate(cl).astype(np.uint32)
+        sub_hi, sub_hd, sub_hn = hi[items].copy(), hd[items].copy(), hn[items].copy()
+        changed = ix.scan_items(qs[items], off, cl, kv[items], sub_hi, sub_hd, sub_hn)
+        for i, b in enumerate(items):
+            npos, ch = oracle.search_clusters(csr, qs[b], plans[b], int(pos[b]), heaps[b],
+                                              cl[off[i]:off[i + 1]])
+            assert list(changed[off[i]:off[i + 1]]) == list(ch)
+            ent = heaps[b].entries()
+            assert int(sub_hn[i]) == len(ent)
+            assert [int(x) for x in sub_hi[i, :len(ent)]] == [e[0] for e in ent]
+            assert np.array_equal(sub_hd[i, :len(ent)].view(np.uint64),
+                                  np.array([e[1] for e in ent], np.float64).view(np.uint64))
+            pos[b] = npos
+        hi[items], hd[items], hn[items] = sub_hi, sub_hd, sub_hn
