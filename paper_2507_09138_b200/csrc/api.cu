@@ -287,14 +287,15 @@ static void adapt_scan(hivf_index* ix, uint32_t n_queries, uint32_t n_fallback) 
 
 // Rows per scan segment: long segments amortise the per-item costs of the
 // grouped scan (query staging, pipeline refill), short ones balance the
-// persistent grid.  The longest of 8192/4096/2048/1024 that still gives >= 16
-// segments per SM.  Measured (scan ms per C3 batch): 8192 -> 9.19-9.31,
-// 4096 -> 9.57-9.85, 2048 -> 10.45, 16384 -> 13.6 (tail); a C3 shard of an
-// 8-GPU job (2.6M rows) gets 1024: 1.68 vs 1.79 ms per step at 4096.  Failed
-// proofs of long segments are repaired in place (k_repair_segments).
+// persistent grid and keep the 32 candidates per (query, segment) enough for
+// the completeness proof (fewer in-place repairs).  The longest of
+// 4096/2048/1024 that still gives >= 16 segments per SM.  Measured with the
+// shared drop bound (C3, ms per batch): 4096 -> scan 8.91 + finalize 0.14,
+// 8192 -> 8.89 + 0.20; a C3 shard of an 8-GPU job (2.6M rows) gets 1024:
+// step 1.46 ms vs 1.81 ms at 4096 (before the bound).
 static uint32_t auto_seg_rows(uint64_t n_rows, int sm_count) {
   const uint64_t want = 16ull * (uint64_t)std::max(1, sm_count);
-  for (uint32_t seg : {8192u, 4096u, 2048u})
+  for (uint32_t seg : {4096u, 2048u})
     if (n_rows / seg >= want) return seg;
   return 1024;
 }
