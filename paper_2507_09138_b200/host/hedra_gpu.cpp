@@ -622,6 +622,40 @@ RetStepReport RetrievalEngine::execute(SubStageBatch& batch, double now_ms, bool
 }  // namespace ret
 }  // namespace hedra_gpu
 
+// ---- bench (bench.cpp:139-163) ------------------------------------------------------
+namespace hedra_gpu {
+namespace bench {
+
+double measure_per_vector_ns(const ivf::IvfIndex& index, std::size_t repeats) {
+  if (index.total_vectors() == 0) throw std::invalid_argument("measure_per_vector_ns: empty index");
+  if (repeats == 0) repeats = 1;
+  const std::uint32_t K = static_cast<std::uint32_t>(index.k_clusters());
+  const std::uint32_t per = 2048;
+  const std::uint32_t n_items = (K + per - 1) / per;
+  std::vector<float> q(static_cast<std::size_t>(n_items) * index.dim(), 0.25f);
+  std::vector<std::uint32_t> off(n_items + 1), cl(K), kv(n_items, 1);
+  for (std::uint32_t c = 0; c < K; ++c) cl[c] = c;
+  for (std::uint32_t i = 0; i <= n_items; ++i) off[i] = std::min(K, i * per);
+  std::vector<std::uint64_t> hid(n_items);
+  std::vector<double> hd(n_items);
+  std::vector<std::uint32_t> hn(n_items);
+  std::vector<std::uint8_t> changed(K);
+  std::vector<double> runs;
+  for (std::size_t r = 0; r <= repeats; ++r) {  // the first call is a warm-up
+    std::fill(hn.begin(), hn.end(), 0u);
+    const auto t0 = std::chrono::steady_clock::now();
+    check(hivf_scan_items(index.raw(), q.data(), n_items, off.data(), cl.data(), kv.data(), hid.data(),
+                          hd.data(), hn.data(), 1, changed.data()));
+    const double ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+    if (r) runs.push_back(ns / static_cast<double>(index.total_vectors()));
+  }
+  std::sort(runs.begin(), runs.end());
+  return runs[runs.size() / 2];
+}
+
+}  // namespace bench
+}  // namespace hedra_gpu
+
 // ---- sim (similarity.cpp) -----------------------------------------------------------
 namespace hedra_gpu {
 namespace sim {

@@ -352,6 +352,16 @@ class RetrievalEngine {
 
 }  // namespace ret
 
+// hedra::bench::measure_per_vector_ns (proj/src/bench.cpp:139-163) on the GPU:
+// the reference's calibration of RetrievalCostModel::per_vector_ns (a full
+// scan of every list for a constant 0.25 query, median of `repeats`), so the
+// unmodified scheduler plans sub-stage budgets (plan_substages) with the
+// device's real cost.  One hivf_scan_items call per repeat (items of <= 2048
+// lists, same query), wall clock around the synchronous call.
+namespace bench {
+double measure_per_vector_ns(const ivf::IvfIndex& index, std::size_t repeats = 3);
+}  // namespace bench
+
 // hedra::sim (proj/include/hedra/similarity.hpp): the locality helpers of the
 // Hedra mode -- host bookkeeping plus exact re-scoring of <= 20 cached docs;
 // the doc lookups go through the device locator.

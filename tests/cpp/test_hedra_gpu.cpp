@@ -646,6 +646,15 @@ TEST_CPU(sim_should_terminate_and_validate_speculation) {  // :172-196
   CHECK(sim::validate_speculation(a, b, 2).kind == sim::SpecKind::Mismatch);
 }
 
+TEST_GPU(bench_measure_per_vector_ns) {  // bench.cpp:139-163 contract on the GPU
+  ivf::Context ctx(0);
+  const Data d = random_data(77, 5000, 16, 32);
+  auto ix = build(ctx, d);
+  const double ns = bench::measure_per_vector_ns(*ix, 3);
+  CHECK(std::isfinite(ns) && ns > 0.0);
+  CHECK(ns < 1e6);  // a whole-index GPU scan costs far below a millisecond per vector
+}
+
 int main(int argc, char** argv) {
   const bool cpu_only = argc > 1 && std::strcmp(argv[1], "--cpu-only") == 0;
   int ran = 0;
