@@ -935,7 +935,9 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   // finalize pass reads "no candidates" there
   CK(cudaMemsetAsync(c->cand_n.p, 0, nslots * 4, c->stream));
   const bool tc = kind != 1;
-  const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2) : (uint32_t)kQMax;
+  // batch density estimate (host-side, no sync): pairs per list of the index
+  const float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
+  const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl) : (uint32_t)kQMax;
   launch_build_worklist(v, group, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
                         c->list_poff.as<uint32_t>(), c->list_cur.as<uint32_t>(),
                         c->list_ioff.as<uint32_t>(), c->sorted_pairs.as<uint32_t>(),
@@ -952,7 +954,8 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
     launch_scan_tc(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                    c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
                    c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
-                   kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, item_bounds ? 0 : 1, c->stream);
+                   kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, item_bounds ? 0 : 1, ppl,
+                   c->stream);
   else
     launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                 c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),

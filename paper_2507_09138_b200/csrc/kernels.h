@@ -114,15 +114,16 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    int bound_update, cudaStream_t s);
-uint32_t scan_tc_qmax(uint32_t dpad, int split);
+                    int bound_update, float probes_per_list, cudaStream_t s);
+// queries per tensor-core work item; probes_per_list = the batch's pairs / lists
+uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list = 0.f);
 void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)
 int tc_probe_conversion(cudaStream_t s);  // 0 trunc, 1 RNE, 2 unsupported
 void set_tc_conversion_mode(int m);
 void set_tc_variant(int v);  // debug knob (inexact results when nonzero)
 void set_tc_prof(int on);    // debug: per-CTA stall counters in k_scan_tc
 int tc_conversion_mode();
-int scan_tc_smem_bytes(uint32_t dpad, int split);
+int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list = 0.f);
 void bound_ffma(uint32_t dim, double* a, double* b, double* c);
 void bound_tc(uint32_t dim, double* a, double* b, double* c);   // 3-pass split
 void bound_tc1(uint32_t dim, double* a, double* b, double* c);  // single pass

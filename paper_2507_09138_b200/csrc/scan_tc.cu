@@ -840,14 +840,17 @@ static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
 static uint32_t g_tc_qmax_override = 0;
 void set_tc_qmax(uint32_t q) { g_tc_qmax_override = q; }
 
-uint32_t scan_tc_qmax(uint32_t dpad, int split) {
+uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list) {
   const uint32_t o = g_tc_qmax_override;
   if (o && tc_ring(dpad, o, split) >= 2) return o;
-  // widest group that still leaves a 4-stage (128 KB) landing ring: the ring
-  // depth (bytes in flight per SM) matters more than the last 8 queries of a
-  // group (measured at D=768: q=24/4 stages 9.58 ms vs q=32/3 stages 9.87 ms)
-  for (uint32_t q : {32u, 24u, 16u})
-    if (tc_ring(dpad, q, split) >= 4) return q;
+  // HBM-bound batches (few probes per list): the widest group that still
+  // leaves a 4-stage (128 KB) landing ring -- ring depth (bytes in flight per
+  // SM) wins (C3, B=256, ~8 probes/list: q=24/4 stages 8.81 ms vs q=32/3
+  // stages 9.03 ms).  Dense batches (> 12 probes per list): fewer groups per
+  // list win (B=512: q=32 9.74 ms vs q=24 10.85 ms; B=1024: 60.6k vs 53.7k q/s).
+  if (probes_per_list <= 12.f)
+    for (uint32_t q : {32u, 24u, 16u})
+      if (tc_ring(dpad, q, split) >= 4) return q;
   for (uint32_t q : {32u, 24u, 16u})
     if (tc_ring(dpad, q, split) >= 3) return q;
   if (tc_ring(dpad, 8, split) >= 2) return 8;
@@ -875,8 +878,8 @@ static int g_tc_conv = -1;  // set by tc_probe_conversion()
 void set_tc_conversion_mode(int m) { g_tc_conv = m; }
 int tc_conversion_mode() { return g_tc_conv; }
 
-int scan_tc_smem_bytes(uint32_t dpad, int split) {
-  const uint32_t q = scan_tc_qmax(dpad, split);
+int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list) {
+  const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list);
   return tc_fixed_bytes(dpad, q, split) + (int)tc_ring(dpad, q, split) * kTcStageBytes;
 }
 
@@ -884,12 +887,12 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    int bound_update, cudaStream_t s) {
-  const uint32_t q = scan_tc_qmax(ix.dpad, split);
+                    int bound_update, float probes_per_list, cudaStream_t s) {
+  const uint32_t q = scan_tc_qmax(ix.dpad, split, probes_per_list);
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
              split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u};
-  const int smem = scan_tc_smem_bytes(ix.dpad, split);
+  const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list);
   static int attr_bytes = 0;
   if (attr_bytes < smem) {
     cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
