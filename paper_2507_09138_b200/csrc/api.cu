@@ -127,7 +127,7 @@ struct hivf_ctx {
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
       cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, qbound, rep_entries, rep_n, rep_cnt,
-      rep_d, rep_ids;
+      rep_d, rep_ids, qshift, qwide;
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;
@@ -174,7 +174,7 @@ struct hivf_ctx {
                     &pl, &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items,
                     &n_items, &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &qin,
                     &x_ids, &x_d, &x_cnt, &x_tot, &tau, &flags2, &qbound, &rep_entries, &rep_n, &rep_cnt,
-                    &rep_d, &rep_ids})
+                    &rep_d, &rep_ids, &qshift, &qwide})
       b->release();
     hstage.release();
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -457,8 +457,11 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   } else if (!strcmp(name, "tc_variant")) {  // debug only: results are inexact when != 0
     set_tc_variant((int)value);
   } else if (!strcmp(name, "tc_qmax")) {  // tuning: queries per tensor-core work item
-    if (value < 0 || value > 32 || value % 8) return fail(HIVF_EINVAL, "tc_qmax: 0 or 8..32 step 8");
+    if (value < 0 || (value > 32 && value != (int64_t)kTcWideQ) || value % 8)
+      return fail(HIVF_EINVAL, "tc_qmax: 0, 8..32 step 8, or 64 (wide)");
     set_tc_qmax((uint32_t)value);
+  } else if (!strcmp(name, "tc_wide_ppl")) {  // tuning: probes/list above which dense batches use
+    set_tc_wide_ppl((float)value);             // the wide (64-query) scan; negative = never
   } else if (!strcmp(name, "time_kernels")) {
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->resolve_timers();
@@ -938,12 +941,25 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   // batch density estimate (host-side, no sync): pairs per list of the index
   const float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
   const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl) : (uint32_t)kQMax;
+  WideStage ws;
+  if (group == kTcWideQ) {
+    ws.qplane = wide_stage_rows(n_pairs, ix->K) * 64;
+    CK(c->qshift.ensure(ix->K * 4ull));
+    CK(c->qwide.ensure((size_t)(ix->dpad / kChunk) * ws.qplane));
+    ws.qshift = c->qshift.as<uint32_t>();
+    ws.qstage = c->qwide.as<uint8_t>();
+  }
   launch_build_worklist(v, group, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
                         c->list_poff.as<uint32_t>(), c->list_cur.as<uint32_t>(),
                         c->list_ioff.as<uint32_t>(), c->sorted_pairs.as<uint32_t>(),
                         c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
-                        c->stream);
+                        ws.qshift, c->stream);
   CKL();
+  if (ws.qstage) {
+    launch_stage_wide(v, qv, c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->pl.as<uint32_t>(),
+                      n_pairs, ws, c->stream);
+    CKL();
+  }
   const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;
   if (tc && topk && !item_bounds) {  // shared drop bounds start at "none" (0x7f7f7f7f ~ 3.4e38)
     CK(c->qbound.ensure((size_t)qv.n * 4));
@@ -955,7 +971,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
                    c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
                    c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
                    kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, item_bounds ? 0 : 1, ppl,
-                   c->stream);
+                   ws, c->stream);
   else
     launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                 c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),

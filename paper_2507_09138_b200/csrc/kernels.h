@@ -103,18 +103,32 @@ void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* 
                            const uint32_t* pair_list, uint32_t n_pairs, uint32_t* list_cnt,
                            uint32_t* list_pair_off, uint32_t* list_cursor,
                            uint32_t* list_item_off, uint32_t* sorted_pairs, ScanItem* items,
-                           uint32_t* n_items, uint32_t* work_ctr, cudaStream_t s);
+                           uint32_t* n_items, uint32_t* work_ctr, uint32_t* qshift, cudaStream_t s);
 void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                  const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                  const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                  uint32_t* out_n, int n_ctas, cudaStream_t s);
 int scan_smem_bytes(uint32_t dpad);
 // ---- scan_tc.cu (tcgen05 tensor-core scan)
+// Wide tensor-core scan (query groups of kTcWideQ, dense batches): the
+// restaged query rows (launch_stage_wide) and per-list staging shifts
+// (launch_build_worklist's qshift).  Unused (zeros) for the narrow scan.
+constexpr uint32_t kTcWideQ = 64;
+struct WideStage {
+  uint8_t* qstage = nullptr;
+  uint64_t qplane = 0;  // bytes per 16-dim plane = rows * 64
+  uint32_t* qshift = nullptr;
+};
+uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists);
+void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,
+                       const uint32_t* pair_query, const uint32_t* pair_list, uint32_t n_pairs,
+                       const WideStage& ws, cudaStream_t s);
+void set_tc_wide_ppl(float v);
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    int bound_update, float probes_per_list, cudaStream_t s);
+                    int bound_update, float probes_per_list, const WideStage& ws, cudaStream_t s);
 // queries per tensor-core work item; probes_per_list = the batch's pairs / lists
 uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list = 0.f);
 void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)

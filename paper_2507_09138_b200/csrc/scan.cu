@@ -292,11 +292,13 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
                                                        const uint32_t* cnt,
                                                        uint32_t* pair_off, uint32_t* cursor,
                                                        uint32_t* item_off, uint32_t* n_items,
-                                                       uint32_t* work_ctr) {
-  __shared__ uint32_t sp[1024], si[1024];
+                                                       uint32_t* work_ctr, uint32_t* qshift) {
+  // qshift (wide tensor-core scan, optional): each list's pair range restaged
+  // at an 8-row aligned offset, staged row = pair position + qshift[c]
+  __shared__ uint32_t sp[1024], si[1024], sq[1024];
   const uint32_t per = (ix.K + 1023) / 1024;
   const uint32_t b = threadIdx.x * per, e = min(ix.K, b + per);
-  uint32_t tp = 0, ti = 0;
+  uint32_t tp = 0, ti = 0, tq = 0;
   for (uint32_t t = b; t < e; ++t) {
     const uint32_t c = ix.list_order[t];
     const uint32_t n = cnt[c];
@@ -304,19 +306,23 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
     const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
     tp += n;
     ti += n ? nseg * ((n + group - 1) / group) : 0;
+    tq += (n + 7) & ~7u;
   }
   sp[threadIdx.x] = tp;
   si[threadIdx.x] = ti;
+  sq[threadIdx.x] = tq;
   __syncthreads();
   for (int s = 1; s < 1024; s <<= 1) {  // Hillis-Steele inclusive scan
     const uint32_t a = threadIdx.x >= s ? sp[threadIdx.x - s] : 0;
     const uint32_t c2 = threadIdx.x >= s ? si[threadIdx.x - s] : 0;
+    const uint32_t c3 = threadIdx.x >= s ? sq[threadIdx.x - s] : 0;
     __syncthreads();
     sp[threadIdx.x] += a;
     si[threadIdx.x] += c2;
+    sq[threadIdx.x] += c3;
     __syncthreads();
   }
-  uint32_t op = sp[threadIdx.x] - tp, oi = si[threadIdx.x] - ti;
+  uint32_t op = sp[threadIdx.x] - tp, oi = si[threadIdx.x] - ti, oq = sq[threadIdx.x] - tq;
   for (uint32_t t = b; t < e; ++t) {
     const uint32_t c = ix.list_order[t];
     const uint32_t n = cnt[c];
@@ -325,8 +331,10 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
     pair_off[c] = op;
     item_off[c] = oi;
     cursor[c] = 0;
+    if (qshift) qshift[c] = oq - op;
     op += n;
     oi += n ? nseg * ((n + group - 1) / group) : 0;
+    oq += (n + 7) & ~7u;
   }
   if (threadIdx.x == 1023) {
     *n_items = si[1023];
@@ -380,12 +388,12 @@ void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* 
                            const uint32_t* pair_list, uint32_t n_pairs, uint32_t* list_cnt,
                            uint32_t* list_pair_off, uint32_t* list_cursor,
                            uint32_t* list_item_off, uint32_t* sorted_pairs, ScanItem* items,
-                           uint32_t* n_items, uint32_t* work_ctr, cudaStream_t s) {
+                           uint32_t* n_items, uint32_t* work_ctr, uint32_t* qshift, cudaStream_t s) {
   (void)pair_query;
   cudaMemsetAsync(list_cnt, 0, sizeof(uint32_t) * ix.K, s);
   if (n_pairs) k_count_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_cnt);
   k_list_offsets<<<1, 1024, 0, s>>>(ix, group, list_cnt, list_pair_off, list_cursor, list_item_off,
-                                    n_items, work_ctr);
+                                    n_items, work_ctr, qshift);
   if (n_pairs)
     k_scatter_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_pair_off,
                                                           list_cursor, sorted_pairs);

@@ -37,6 +37,8 @@
 //   warps 6-9 epilogue: tcgen05.ld of the tile (one row per thread, one column
 //            per query), fp32 expansion distance, per-warp register top-32 per
 //            query; at item end a bitonic merge across the four warps.
+#include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 
 #include "common.cuh"
@@ -51,7 +53,9 @@ constexpr int kTcTile = 128;       // rows per MMA tile (M)
 constexpr int kTcCps = 4;          // 16-dim chunks per pipeline stage (64 dims)
 constexpr int kTcMaxA = 8;         // max depth of the A landing ring
 constexpr int kTcLo = 4;           // depth of the A_lo ring (in TMEM, 64 columns per slot)
-constexpr int kMergeQ = 16;        // queries per round of the item-end cross-warp merge
+constexpr int kMergeQ = 16;        // queries per round of the item-end cross-warp merge (wide: 8)
+constexpr int kWideQ = (int)kTcWideQ;  // wide mode: queries per group (two epilogue groups of 32)
+constexpr int kWideQBytes = kTcCps * kWideQ * 64;  // wide mode: query slice per stage (16 KB)
 constexpr int kItemQ = 4;          // published work items in flight (producer runs ahead)
 constexpr int kTcChunkBytes = kTcTile * kChunk * 4;       // 8 KB
 constexpr int kTcStageBytes = kTcCps * kTcChunkBytes;     // 32 KB
@@ -90,6 +94,13 @@ struct TcParams {
   // the sub-stage -- updating them from later clusters would change the
   // reference's per-cluster `changed` flags), 1: items publish their k-th
   uint32_t bound_update;
+  // wide mode (k_scan_tc<true>): query groups of up
+  // to 64 streamed with the list stages from a restaged copy -- plane ch holds
+  // 64 B (16 dims) per staged row, SWIZZLE_64B; staged row = pair position +
+  // qshift[list], 8-row aligned per list (launch_stage_wide)
+  const uint8_t* qstage;
+  uint64_t qplane;
+  const uint32_t* qshift;
 };
 
 // ---- tcgen05 PTX wrappers ------------------------------------------------------
@@ -225,23 +236,29 @@ __device__ __forceinline__ float tf32_conv(float x, int mode) {
 #define TC_PROF_ADD(slot) \
   if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - _t0))
 
+template <bool kWide>
 __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
+  // wide: warps 2-5 are a second epilogue group (queries 32..63 of the item)
+  // instead of stagers/splitters; single-pass tf32 only
+  constexpr int kMQ = kWide ? 8 : kMergeQ;
+  constexpr uint32_t kSB = kTcStageBytes + (kWide ? kWideQBytes : 0);  // ring stage bytes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t dpad = P.ix.dpad;
   const uint32_t nch = dpad / kChunk;
   const uint32_t qmax = P.qmax;
   const uint32_t SA = P.sa;
-  const bool split = P.split != 0;
+  const bool split = !kWide && P.split != 0;
   // TMEM accumulator ring: split mode shares TMEM with the A_lo ring; single
   // mode spreads over the whole 512 columns to absorb epilogue jitter
   const uint32_t nacc = split ? 2u : (uint32_t)kAccMax;
   const uint32_t qblk = (split ? 2 : 1) * qmax * 64;                // per chunk: [raw rows | lo rows]
-  uint8_t* aring = smem;                                            // SA x 32 KB (raw A)
-  uint8_t* qsm = smem + SA * kTcStageBytes;                         // nch x qblk
-  float* md = reinterpret_cast<float*>(qsm + (size_t)nch * qblk);   // merge scratch [4][kMergeQ][32]
-  uint32_t* mr = reinterpret_cast<uint32_t*>(md + kTcEpiWarps * kMergeQ * 32);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(mr + kTcEpiWarps * kMergeQ * 32);
+  uint8_t* aring = smem;                                            // SA x kSB (raw A [| query slice])
+  uint8_t* qsm = smem + SA * kSB;                                   // nch x qblk (narrow only)
+  float* md = reinterpret_cast<float*>(qsm + (kWide ? 0 : (size_t)nch * qblk));  // merge scratch [groups][4][kMQ][32]
+  constexpr int kGroups = kWide ? 2 : 1;
+  uint32_t* mr = reinterpret_cast<uint32_t*>(md + kGroups * kTcEpiWarps * kMQ * 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(mr + kGroups * kTcEpiWarps * kMQ * 32);
   uint64_t* full = bars;                        // [SA] TMA -> splitter / MMA
   uint64_t* empty = bars + kTcMaxA;             // [SA] MMA -> TMA
   uint64_t* lfull = bars + 2 * kTcMaxA;         // [kTcLo] splitter -> MMA
@@ -259,7 +276,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   uint32_t (*s_slot)[32] = reinterpret_cast<uint32_t (*)[32]>(s_qn2 + kItemQ);  // [kItemQ][32]
   float (*s_E)[32] = reinterpret_cast<float (*)[32]>(s_slot + kItemQ);            // [kItemQ][32]
   uint32_t (*s_qi)[32] = reinterpret_cast<uint32_t (*)[32]>(s_E + kItemQ);        // [kItemQ][32]
-  float (*s_g)[32] = reinterpret_cast<float (*)[32]>(s_qi + kItemQ);              // [4][32]
+  float (*s_g)[32] = reinterpret_cast<float (*)[32]>(s_qi + kItemQ);              // [groups*4][32]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -273,7 +290,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
     }
     for (int i = 0; i < kAccMax; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kTcEpiWarps);
+      mbar_init(&tempty[i], kGroups * kTcEpiWarps);
     }
     for (int i = 0; i < kItemQ; ++i) {
       mbar_init(&ifull[i], 1);
@@ -318,10 +335,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       bool valid = it < n_items;
       ScanItem item{};
       uint64_t lbeg = 0, lend = 0;
+      uint32_t qsh = 0;
       if (valid) {
         item = P.items[it];
         lbeg = P.ix.list_off[item.list];
         lend = P.ix.list_off[item.list + 1];
+        if (kWide) qsh = P.qshift[item.list];
       }
       for (uint32_t i = 0;; ++i) {
         const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
@@ -339,10 +358,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         const bool valid_n = it_n < n_items;
         ScanItem item_n{};
         uint64_t lbeg_n = 0, lend_n = 0;
+        uint32_t qsh_n = 0;
         uint32_t pf = valid_n ? 0 : 2;  // prefetch progress of the next item
         const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
         const uint64_t n_c = lend - lbeg;
         const float* lbase = list_base(P.ix, item.list, lbeg);
+        const uint32_t qbytes = kWide ? ((item.nq + 7) & ~7u) * 64 : 0;  // per chunk
+        const uint8_t* qsrc = kWide ? P.qstage + (uint64_t)(item.pair0 + qsh) * 64 : nullptr;
         for (uint32_t t = 0; t < ntiles; ++t) {
           const uint32_t r0 = item.row0 + t * kTcTile;
           const uint32_t nr = min((uint32_t)kTcTile, item.nrows - t * kTcTile);
@@ -355,20 +377,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
               TC_PROF_ADD(3);
             }
             const long long _tp = P.prof ? clock64() : 0;
-            mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4);
+            mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4 + cn * qbytes);
             if (nr == kTcTile) {  // full tile: the stage is one contiguous span
-              bulk_g2s(aring + a * kTcStageBytes, lbase + tile_chunk_offset(n_c, dpad, r0, c0),
+              bulk_g2s(aring + a * kSB, lbase + tile_chunk_offset(n_c, dpad, r0, c0),
                        cn * kTcChunkBytes, &full[a]);
             } else {  // short last tile: its chunk planes are nr rows apart
               for (uint32_t c = 0; c < cn; ++c)
-                bulk_g2s(aring + a * kTcStageBytes + c * kTcChunkBytes,
+                bulk_g2s(aring + a * kSB + c * kTcChunkBytes,
                          lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c), nr * kChunk * 4, &full[a]);
             }
+            if (kWide)  // the group's query rows of these chunks (L2-resident restaged copy)
+              for (uint32_t c = 0; c < cn; ++c)
+                bulk_g2s(aring + a * kSB + kTcStageBytes + c * (kWideQ * 64),
+                         qsrc + (uint64_t)(c0 + c) * P.qplane, qbytes, &full[a]);
             if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 14], (unsigned long long)(clock64() - _tp));
             if (++ra == SA) { ra = 0; rpa ^= 1; }
             if (pf == 1) {
               lbeg_n = P.ix.list_off[item_n.list];
               lend_n = P.ix.list_off[item_n.list + 1];
+              if (kWide) qsh_n = P.qshift[item_n.list];
               pf = 2;
             } else if (pf == 0) {
               item_n = P.items[it_n];
@@ -383,11 +410,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         if (pf == 1) {
           lbeg_n = P.ix.list_off[item_n.list];
           lend_n = P.ix.list_off[item_n.list + 1];
+          if (kWide) qsh_n = P.qshift[item_n.list];
         }
         valid = valid_n;
         item = item_n;
         lbeg = lbeg_n;
         lend = lend_n;
+        qsh = qsh_n;
       }
     }
   } else if (warp == 1) {
@@ -409,7 +438,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       const uint32_t idesc1 = tf32_idesc(npad);
       const uint64_t qdesc0 = sw64_kmajor_desc(smem_u32(qsm));
       const uint64_t adesc0 = sw64_kmajor_desc(smem_u32(aring));
-      {
+      if (!kWide) {
         TC_PROF_T0();
         mbar_wait(qfull, i & 1);  // this item's query group is staged
         if (lane == 0) TC_PROF_ADD(0);
@@ -435,14 +464,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           tc_fence_after();
           const long long _ti = P.prof ? clock64() : 0;
           // descriptor start addresses are in 16-B units: +32 B == +2
-          const uint64_t adesc = adesc0 + (uint64_t)(a * (kTcStageBytes >> 4));
+          const uint64_t adesc = adesc0 + (uint64_t)(a * (kSB >> 4));
+          // wide: this stage's query slice follows its A tile (64 rows per chunk)
+          const uint64_t qdw = adesc + (uint64_t)(kTcStageBytes >> 4);
           const uint32_t alo = tmem_base + kTmemAcc + l * kTmemLoCols;  // A_lo in TMEM, lane = row
           const uint32_t c0 = sg * kTcCps;
           if (!(P.variant & 4)) {
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kTcCps; ++c) {
               if (c >= cn) break;
-              const uint64_t qd = qdesc0 + (uint64_t)((c0 + c) * (qblk >> 4));
+              const uint64_t qd = kWide ? qdw + (uint64_t)(c * ((kWideQ * 64) >> 4))
+                                        : qdesc0 + (uint64_t)((c0 + c) * (qblk >> 4));
 #pragma unroll
               for (uint32_t k2 = 0; k2 < 2; ++k2) {
                 const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
@@ -472,9 +504,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           tph ^= 1;
         }
       }
-      mma_commit_elect(qempty);  // query group free once this item's MMAs retire
+      if (!kWide) mma_commit_elect(qempty);  // query group free once this item's MMAs retire
     }
-  } else if (warp < 2 + kTcSplitWarps) {
+  } else if (!kWide && warp < 2 + kTcSplitWarps) {
     // -------- stagers (query group of each item) + splitters (lo(A) rows -> TMEM) --------
     const uint32_t sw = warp - 2;                // 0..3
     const uint32_t quad = warp & 3;              // TMEM lane quadrant of this warp
@@ -593,15 +625,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
     }
   } else {
     // ---------------- epilogue warps ----------------
+    // narrow: warps 6-9, queries 0..31.  wide: group h = 0 (warps 6-9) takes
+    // queries 0..31, group h = 1 (warps 2-5) queries 32..63 -- TMEM columns
+    // 32h.., each warp its lane quadrant
     const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
-    const uint32_t ew = warp - (2 + kTcSplitWarps);
+    const uint32_t ew = (warp - 2) & 3;
+    const uint32_t h = (kWide && warp < 2 + kTcSplitWarps) ? 1u : 0u;
     for (uint32_t i = 0;; ++i) {
       const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
       mbar_wait_parked(&ifull[slot], iph);
       if (!s_valid[slot]) break;
       const ScanItem item = s_item[slot];
-      const uint32_t nq = item.nq;
+      const uint32_t nq = kWide ? (item.nq > 32 * h ? min(32u, item.nq - 32 * h) : 0u) : item.nq;
       const uint32_t npad = (nq + 7) & ~7u;
+      // wide: per-query metadata in registers (lane j = query 32h + j), loaded
+      // here instead of by stager warps
+      float w_qn2 = 0.f, w_E = 0.f;
+      uint32_t w_qi = 0, w_slot = 0;
+      if (kWide && lane < nq) {
+        const uint32_t pair = P.sorted_pairs[item.pair0 + 32 * h + lane];
+        w_qi = P.pair_query[pair];
+        w_qn2 = P.qv.qn2[w_qi];
+        w_slot = pair * P.ix.s_max + item.seg;
+        w_E = seg_bound(P.ix, P.qv.qnorm[w_qi], P.ix.maxnorm[item.list]);
+      }
       const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
       const uint64_t lbeg = P.ix.list_off[item.list];
       float ld[32];
@@ -635,7 +682,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         }
         tc_fence_after();
         uint32_t acc[32], acc2[32];
-        TMEM_LD32(tmem_base + ((quad * 32) << 16) + tb * 64, acc);
+        TMEM_LD32(tmem_base + ((quad * 32) << 16) + tb * 64 + 32 * h, acc);
         if (split) TMEM_LD32(tmem_base + ((quad * 32) << 16) + tb * 64 + npad, acc2);
         tmem_wait_ld();
         tc_fence_before();
@@ -650,8 +697,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         // stagers' per-item s_qi / s_E writes are ordered before it.
         float gl = kInfF;
         if (P.topk && lane < (int)nq) {
-          const float u = __ldcg(P.qbound + s_qi[slot][lane]);
-          if (u < 3.0e38f) gl = drop_bound(u, s_E[slot][lane]);
+          const float u = __ldcg(P.qbound + (kWide ? w_qi : s_qi[slot][lane]));
+          if (u < 3.0e38f) gl = drop_bound(u, kWide ? w_E : s_E[slot][lane]);
         }
         gmin = fminf(gmin, gl);
         const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
@@ -660,7 +707,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           if (j >= (int)nq) break;
           const float dot = split ? __fadd_rn(__uint_as_float(acc[j]), __uint_as_float(acc2[j]))
                                   : __uint_as_float(acc[j]);
-          const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, s_qn2[slot][j]))
+          const float qn2j = kWide ? __shfl_sync(FULL, w_qn2, j) : s_qn2[slot][j];
+          const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, qn2j))
                                 : __int_as_float(0x7f800000);
           const float gj = __shfl_sync(FULL, gl, j);
           float th = fminf(__shfl_sync(FULL, ld[j], 31), gj);
@@ -732,25 +780,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       // cross-warp merge through the dedicated scratch (the MMA / producer are
       // already on the next item), kMergeQ queries per round
       const long long _tm = P.prof ? clock64() : 0;
+      float* gmd = md + h * (kTcEpiWarps * kMQ * 32);  // this group's scratch
+      uint32_t* gmr = mr + h * (kTcEpiWarps * kMQ * 32);
+      float (*gs_g)[32] = s_g + 4 * h;
 #pragma unroll
-      for (int h0 = 0; h0 < 32; h0 += kMergeQ) {
+      for (int h0 = 0; h0 < 32; h0 += kMQ) {
         if (h0 >= (int)nq) break;
-        named_bar_sync(2, kTcEpiWarps * 32);  // previous round's reads are done
-        if (h0 == 0) s_g[ew][lane] = gmin;
+        named_bar_sync(2 + h, kTcEpiWarps * 32);  // previous round's reads are done
+        if (h0 == 0) gs_g[ew][lane] = gmin;
 #pragma unroll
-        for (int jj = 0; jj < kMergeQ; ++jj) {
+        for (int jj = 0; jj < kMQ; ++jj) {
           if (h0 + jj >= (int)nq) break;
-          md[(ew * kMergeQ + jj) * 32 + lane] = ld[h0 + jj];
-          mr[(ew * kMergeQ + jj) * 32 + lane] = lr[h0 + jj];
+          gmd[(ew * kMQ + jj) * 32 + lane] = ld[h0 + jj];
+          gmr[(ew * kMQ + jj) * 32 + lane] = lr[h0 + jj];
         }
-        named_bar_sync(2, kTcEpiWarps * 32);
-        for (uint32_t jj = ew; jj < kMergeQ && h0 + jj < nq; jj += kTcEpiWarps) {
+        named_bar_sync(2 + h, kTcEpiWarps * 32);
+        for (uint32_t jj = ew; jj < (uint32_t)kMQ && h0 + jj < nq; jj += kTcEpiWarps) {
           const uint32_t j = h0 + jj;
-          float v = md[jj * 32 + lane];
-          uint32_t r = mr[jj * 32 + lane];
+          float v = gmd[jj * 32 + lane];
+          uint32_t r = gmr[jj * 32 + lane];
           for (uint32_t w2 = 1; w2 < kTcEpiWarps; ++w2) {
-            const float o = md[(w2 * kMergeQ + jj) * 32 + 31 - lane];
-            const uint32_t orr = mr[(w2 * kMergeQ + jj) * 32 + 31 - lane];
+            const float o = gmd[(w2 * kMQ + jj) * 32 + 31 - lane];
+            const uint32_t orr = gmr[(w2 * kMQ + jj) * 32 + 31 - lane];
             if (o < v || (o == v && orr < r)) {
               v = o;
               r = orr;
@@ -767,22 +818,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
               }
             }
           }
-          const uint32_t oslot = s_slot[slot][j];
+          const uint32_t oslot = kWide ? __shfl_sync(FULL, w_slot, j) : s_slot[slot][j];
+          const float Ej = kWide ? __shfl_sync(FULL, w_E, j) : s_E[slot][j];
+          const uint32_t qij = kWide ? __shfl_sync(FULL, w_qi, j) : s_qi[slot][j];
           P.out_d[(uint64_t)oslot * kKP + lane] = v;
           P.out_row[(uint64_t)oslot * kKP + lane] = r;
           const uint32_t n_valid = __popc(__ballot_sync(FULL, r != kNoRow));
           const float last = __shfl_sync(FULL, v, 31);
           // every row not kept has d^ >= the 32nd kept value (when 32 are kept)
           // or >= a drop bound this item used (bounds only decrease)
-          const float gm = fminf(fminf(s_g[0][j], s_g[1][j]), fminf(s_g[2][j], s_g[3][j]));
+          const float gm = fminf(fminf(gs_g[0][j], gs_g[1][j]), fminf(gs_g[2][j], gs_g[3][j]));
           const float vk = __shfl_sync(FULL, v, (int)(P.topk ? P.topk - 1 : 0));
           if (lane == 0) {
             P.out_thr[oslot] = fminf(n_valid == kKP ? last : kInfF, gm);
             P.out_n[oslot] = n_valid;
             if (P.bound_update && n_valid >= P.topk) {  // this item's k-th upper bound
-              float u = __fadd_ru(vk, s_E[slot][j]);
+              float u = __fadd_ru(vk, Ej);
               if (!(u > 0.f)) u = 0.f;
-              atomicMin(reinterpret_cast<int*>(P.qbound + s_qi[slot][j]), __float_as_int(u));
+              atomicMin(reinterpret_cast<int*>(P.qbound + qij), __float_as_int(u));
             }
           }
         }
@@ -821,28 +874,46 @@ static int tc_budget() {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
       optin = 232448;
-    cudaFuncAttributes fa{};
     size_t st = 1024;
-    if (cudaFuncGetAttributes(&fa, k_scan_tc) == cudaSuccess) st = fa.sharedSizeBytes;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k_scan_tc<false>) == cudaSuccess) st = fa.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa, k_scan_tc<true>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
     budget = optin - (int)st;
   }
   return budget;
 }
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
-  return 1024 + (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64 +
-         kTcEpiWarps * kMergeQ * 32 * 8 +                         // merge scratch
-         8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 16 + 4 * 32 * 4;
+  const bool wide = qmax == kTcWideQ;  // no resident query group; two merge groups of 8
+  return 1024 + (wide ? 0 : (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64) +
+         (wide ? 2 * 8 : kMergeQ) * kTcEpiWarps * 32 * 8 +       // merge scratch
+         8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 16 +
+         (wide ? 8 : 4) * 32 * 4;
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int left = tc_budget() - tc_fixed_bytes(dpad, qmax, split);
-  return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / kTcStageBytes);
+  const int sb = kTcStageBytes + (qmax == kTcWideQ ? kWideQBytes : 0);
+  return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / sb);
 }
 static uint32_t g_tc_qmax_override = 0;
 void set_tc_qmax(uint32_t q) { g_tc_qmax_override = q; }
 
+// option "tc_wide_ppl" (env HIVF_TC_WIDE_PPL sets the process default): the
+// probes-per-list density above which single-pass batches use the wide scan
+// (< 0: never)
+static float env_wide_ppl() {
+  const char* e = getenv("HIVF_TC_WIDE_PPL");
+  return e ? (float)atof(e) : 12.f;
+}
+static float g_tc_wide_ppl = env_wide_ppl();
+void set_tc_wide_ppl(float v) { g_tc_wide_ppl = v; }
+
 uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list) {
   const uint32_t o = g_tc_qmax_override;
-  if (o && tc_ring(dpad, o, split) >= 2) return o;
+  if (o && (o != kTcWideQ || !split) && tc_ring(dpad, o, split) >= 2) return o;
+  // dense batches, single pass: 64-query groups streamed with the list stages
+  // (k_scan_tc<true>) -- each list tile crosses HBM->smem once per 64 probes
+  if (!split && g_tc_wide_ppl >= 0.f && probes_per_list > g_tc_wide_ppl && tc_ring(dpad, kTcWideQ, 0) >= 3)
+    return kTcWideQ;
   // HBM-bound batches (few probes per list): the widest group that still
   // leaves a 4-stage (128 KB) landing ring -- ring depth (bytes in flight per
   // SM) wins (C3, B=256, ~8 probes/list: q=24/4 stages 8.81 ms vs q=32/3
@@ -880,25 +951,65 @@ int tc_conversion_mode() { return g_tc_conv; }
 
 int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list) {
   const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list);
-  return tc_fixed_bytes(dpad, q, split) + (int)tc_ring(dpad, q, split) * kTcStageBytes;
+  return tc_fixed_bytes(dpad, q, split) +
+         (int)tc_ring(dpad, q, split) * (kTcStageBytes + (q == kTcWideQ ? kWideQBytes : 0));
 }
 
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    int bound_update, float probes_per_list, cudaStream_t s) {
+                    int bound_update, float probes_per_list, const WideStage& ws, cudaStream_t s) {
   const uint32_t q = scan_tc_qmax(ix.dpad, split, probes_per_list);
+  const bool wide = q == kTcWideQ;
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
-             split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u};
+             wide ? 0 : split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u,
+             ws.qstage, ws.qplane, ws.qshift};
   const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list);
-  static int attr_bytes = 0;
-  if (attr_bytes < smem) {
-    cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_bytes = smem;
+  static int attr_bytes[2] = {0, 0};
+  if (attr_bytes[wide] < smem) {
+    cudaFuncSetAttribute(wide ? k_scan_tc<true> : k_scan_tc<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_bytes[wide] = smem;
   }
-  k_scan_tc<<<n_ctas, kTcThreads, smem, s>>>(P);
+  if (wide) k_scan_tc<true><<<n_ctas, kTcThreads, smem, s>>>(P);
+  else k_scan_tc<false><<<n_ctas, kTcThreads, smem, s>>>(P);
+}
+
+namespace {
+// Restage the pairs' query rows for the wide scan: staged row r = sorted pair
+// position + qshift[list] (8-row aligned per list), plane ch = dims
+// [16ch, 16ch+16) as 64 B rows in the SWIZZLE_64B K-major pattern, so every
+// (group, chunk) slice is one contiguous bulk copy landing in UMMA layout.
+__global__ void __launch_bounds__(64) k_stage_wide(const float* __restrict__ qs, uint32_t dpad,
+                                                   const uint32_t* __restrict__ sorted_pairs,
+                                                   const uint32_t* __restrict__ pair_query,
+                                                   const uint32_t* __restrict__ pair_list,
+                                                   const uint32_t* __restrict__ qshift, uint8_t* qstage,
+                                                   uint64_t qplane) {
+  const uint32_t p = blockIdx.x;
+  const uint32_t pair = sorted_pairs[p];
+  const uint32_t r = p + qshift[pair_list[pair]];
+  const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)pair_query[pair] * dpad);
+  for (uint32_t g4 = threadIdx.x; g4 < dpad / 4; g4 += blockDim.x) {
+    const uint32_t ch = g4 >> 2, g = g4 & 3;
+    *reinterpret_cast<float4*>(qstage + ch * qplane + (uint64_t)r * 64 + ((g ^ ((r >> 1) & 3)) << 4)) =
+        src[g4];
+  }
+}
+}  // namespace
+
+uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists) {
+  return (uint64_t)n_pairs + 7ull * n_lists + 8;
+}
+
+void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,
+                       const uint32_t* pair_query, const uint32_t* pair_list, uint32_t n_pairs,
+                       const WideStage& ws, cudaStream_t s) {
+  if (n_pairs)
+    k_stage_wide<<<n_pairs, 64, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list, ws.qshift,
+                                        ws.qstage, ws.qplane);
 }
 
 }  // namespace hivf
