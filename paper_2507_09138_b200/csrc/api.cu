@@ -943,9 +943,8 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl) : (uint32_t)kQMax;
   WideStage ws;
   if (group == kTcWideQ) {
-    ws.qplane = wide_stage_rows(n_pairs, ix->K) * 64;
     CK(c->qshift.ensure(ix->K * 4ull));
-    CK(c->qwide.ensure((size_t)(ix->dpad / kChunk) * ws.qplane));
+    CK(c->qwide.ensure((size_t)wide_stage_rows(n_pairs, ix->K) * ix->dpad * 4));
     ws.qshift = c->qshift.as<uint32_t>();
     ws.qstage = c->qwide.as<uint8_t>();
   }
@@ -957,7 +956,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   CKL();
   if (ws.qstage) {
     launch_stage_wide(v, qv, c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->pl.as<uint32_t>(),
-                      n_pairs, ws, c->stream);
+                      c->list_poff.as<uint32_t>(), c->list_cnt.as<uint32_t>(), n_pairs, ws, c->stream);
     CKL();
   }
   const int ctas = c->opt_scan_ctas > 0 ? c->opt_scan_ctas : c->sm_count;

@@ -115,14 +115,13 @@ int scan_smem_bytes(uint32_t dpad);
 // (launch_build_worklist's qshift).  Unused (zeros) for the narrow scan.
 constexpr uint32_t kTcWideQ = 64;
 struct WideStage {
-  uint8_t* qstage = nullptr;
-  uint64_t qplane = 0;  // bytes per 16-dim plane = rows * 64
+  uint8_t* qstage = nullptr;  // wide_stage_rows() x dpad floats
   uint32_t* qshift = nullptr;
 };
 uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists);
 void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,
-                       const uint32_t* pair_query, const uint32_t* pair_list, uint32_t n_pairs,
-                       const WideStage& ws, cudaStream_t s);
+                       const uint32_t* pair_query, const uint32_t* pair_list, const uint32_t* pair_off,
+                       const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s);
 void set_tc_wide_ppl(float v);
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,

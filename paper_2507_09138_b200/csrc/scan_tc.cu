@@ -95,11 +95,10 @@ struct TcParams {
   // reference's per-cluster `changed` flags), 1: items publish their k-th
   uint32_t bound_update;
   // wide mode (k_scan_tc<true>): query groups of up
-  // to 64 streamed with the list stages from a restaged copy -- plane ch holds
-  // 64 B (16 dims) per staged row, SWIZZLE_64B; staged row = pair position +
-  // qshift[list], 8-row aligned per list (launch_stage_wide)
+  // to 64 streamed with the list stages from a restaged copy (launch_stage_wide):
+  // group block at staged row (pair0 + qshift[list]), chunk-major [ch][npad
+  // rows][64 B] in the SWIZZLE_64B pattern, so a stage's query slice is one copy
   const uint8_t* qstage;
-  uint64_t qplane;
   const uint32_t* qshift;
 };
 
@@ -364,7 +363,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         const uint64_t n_c = lend - lbeg;
         const float* lbase = list_base(P.ix, item.list, lbeg);
         const uint32_t qbytes = kWide ? ((item.nq + 7) & ~7u) * 64 : 0;  // per chunk
-        const uint8_t* qsrc = kWide ? P.qstage + (uint64_t)(item.pair0 + qsh) * 64 : nullptr;
+        const uint8_t* qsrc = kWide ? P.qstage + (uint64_t)(item.pair0 + qsh) * dpad * 4 : nullptr;
         for (uint32_t t = 0; t < ntiles; ++t) {
           const uint32_t r0 = item.row0 + t * kTcTile;
           const uint32_t nr = min((uint32_t)kTcTile, item.nrows - t * kTcTile);
@@ -387,9 +386,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
                          lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c), nr * kChunk * 4, &full[a]);
             }
             if (kWide)  // the group's query rows of these chunks (L2-resident restaged copy)
-              for (uint32_t c = 0; c < cn; ++c)
-                bulk_g2s(aring + a * kSB + kTcStageBytes + c * (kWideQ * 64),
-                         qsrc + (uint64_t)(c0 + c) * P.qplane, qbytes, &full[a]);
+              bulk_g2s(aring + a * kSB + kTcStageBytes, qsrc + (uint64_t)c0 * qbytes, cn * qbytes, &full[a]);
             if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 14], (unsigned long long)(clock64() - _tp));
             if (++ra == SA) { ra = 0; rpa ^= 1; }
             if (pf == 1) {
@@ -473,7 +470,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kTcCps; ++c) {
               if (c >= cn) break;
-              const uint64_t qd = kWide ? qdw + (uint64_t)(c * ((kWideQ * 64) >> 4))
+              const uint64_t qd = kWide ? qdw + (uint64_t)(c * (npad * 4))  // npad*64 B per chunk
                                         : qdesc0 + (uint64_t)((c0 + c) * (qblk >> 4));
 #pragma unroll
               for (uint32_t k2 = 0; k2 < 2; ++k2) {
@@ -902,7 +899,7 @@ void set_tc_qmax(uint32_t q) { g_tc_qmax_override = q; }
 // (< 0: never)
 static float env_wide_ppl() {
   const char* e = getenv("HIVF_TC_WIDE_PPL");
-  return e ? (float)atof(e) : 12.f;
+  return e ? (float)atof(e) : 10.f;
 }
 static float g_tc_wide_ppl = env_wide_ppl();
 void set_tc_wide_ppl(float v) { g_tc_wide_ppl = v; }
@@ -965,7 +962,7 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
              wide ? 0 : split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u,
-             ws.qstage, ws.qplane, ws.qshift};
+             ws.qstage, ws.qshift};
   const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list);
   static int attr_bytes[2] = {0, 0};
   if (attr_bytes[wide] < smem) {
@@ -978,23 +975,30 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
 }
 
 namespace {
-// Restage the pairs' query rows for the wide scan: staged row r = sorted pair
-// position + qshift[list] (8-row aligned per list), plane ch = dims
-// [16ch, 16ch+16) as 64 B rows in the SWIZZLE_64B K-major pattern, so every
-// (group, chunk) slice is one contiguous bulk copy landing in UMMA layout.
+// Restage the pairs' query rows for the wide scan.  List c's pairs occupy
+// staged rows [pair_off[c] + qshift[c], +ceil8(n_c)) (8-row aligned); its
+// query group g (64 pairs, the last one npad = ceil8(rest) rows) is one block
+// of dpad*4*npad bytes laid out chunk-major [ch][npad rows][64 B] with the
+// SWIZZLE_64B XOR, so a stage's 4-chunk slice is one contiguous bulk copy
+// that lands in UMMA K-major layout.
 __global__ void __launch_bounds__(64) k_stage_wide(const float* __restrict__ qs, uint32_t dpad,
                                                    const uint32_t* __restrict__ sorted_pairs,
                                                    const uint32_t* __restrict__ pair_query,
                                                    const uint32_t* __restrict__ pair_list,
-                                                   const uint32_t* __restrict__ qshift, uint8_t* qstage,
-                                                   uint64_t qplane) {
+                                                   const uint32_t* __restrict__ pair_off,
+                                                   const uint32_t* __restrict__ list_cnt,
+                                                   const uint32_t* __restrict__ qshift, uint8_t* qstage) {
   const uint32_t p = blockIdx.x;
   const uint32_t pair = sorted_pairs[p];
-  const uint32_t r = p + qshift[pair_list[pair]];
+  const uint32_t c = pair_list[pair];
+  const uint32_t local = p - pair_off[c], n = list_cnt[c];
+  const uint32_t g = local / kWideQ, row = local % kWideQ;
+  const uint32_t npad = min((uint32_t)kWideQ, ((n - g * kWideQ) + 7) & ~7u);
+  uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * kWideQ) * dpad * 4;
   const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)pair_query[pair] * dpad);
   for (uint32_t g4 = threadIdx.x; g4 < dpad / 4; g4 += blockDim.x) {
-    const uint32_t ch = g4 >> 2, g = g4 & 3;
-    *reinterpret_cast<float4*>(qstage + ch * qplane + (uint64_t)r * 64 + ((g ^ ((r >> 1) & 3)) << 4)) =
+    const uint32_t ch = g4 >> 2, q4 = g4 & 3;
+    *reinterpret_cast<float4*>(blk + (uint64_t)ch * npad * 64 + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4)) =
         src[g4];
   }
 }
@@ -1005,11 +1009,11 @@ uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists) {
 }
 
 void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,
-                       const uint32_t* pair_query, const uint32_t* pair_list, uint32_t n_pairs,
-                       const WideStage& ws, cudaStream_t s) {
+                       const uint32_t* pair_query, const uint32_t* pair_list, const uint32_t* pair_off,
+                       const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s) {
   if (n_pairs)
-    k_stage_wide<<<n_pairs, 64, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list, ws.qshift,
-                                        ws.qstage, ws.qplane);
+    k_stage_wide<<<n_pairs, 64, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list, pair_off,
+                                        list_cnt, ws.qshift, ws.qstage);
 }
 
 }  // namespace hivf
