@@ -939,14 +939,22 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   CK(cudaMemsetAsync(c->cand_n.p, 0, nslots * 4, c->stream));
   const bool tc = kind != 1;
   // batch density estimate (host-side, no sync): pairs per list of the index
-  const float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
-  const uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl) : (uint32_t)kQMax;
+  float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
+  uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl) : (uint32_t)kQMax;
   WideStage ws;
   if (group == kTcWideQ) {
-    CK(c->qshift.ensure(ix->K * 4ull));
-    CK(c->qwide.ensure((size_t)wide_stage_rows(n_pairs, ix->K) * ix->dpad * 4));
-    ws.qshift = c->qshift.as<uint32_t>();
-    ws.qstage = c->qwide.as<uint8_t>();
+    // the restaged queries need (pairs + 7K) x D floats; when HBM is short
+    // (index near the budget) the batch takes the narrow kernel instead
+    if (c->qshift.ensure(ix->K * 4ull) != cudaSuccess ||
+        c->qwide.ensure((size_t)wide_stage_rows(n_pairs, ix->K) * ix->dpad * 4) != cudaSuccess) {
+      (void)cudaGetLastError();
+      ppl = 0.f;
+      group = scan_tc_qmax(ix->dpad, kind == 2, ppl);
+      if (group == kTcWideQ) return fail(HIVF_ENOMEM, "wide scan: query staging buffer");
+    } else {
+      ws.qshift = c->qshift.as<uint32_t>();
+      ws.qstage = c->qwide.as<uint8_t>();
+    }
   }
   launch_build_worklist(v, group, c->pq.as<uint32_t>(), c->pl.as<uint32_t>(), n_pairs, c->list_cnt.as<uint32_t>(),
                         c->list_poff.as<uint32_t>(), c->list_cur.as<uint32_t>(),
