@@ -260,8 +260,11 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * "hbm_list_budget" (bytes of list storage an index may keep in HBM; the
  * rest stays in pinned host memory, see residency),
  * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
- * 3 tcgen05 single-pass), "tc_qmax", "time_kernels" (record events around each
- * phase and accumulate into hivf_stats), "reset_timers". */
+ * 3 tcgen05 single-pass), "tc_qmax" (queries per scan work item: 8..32 step 8,
+ * or 64 = the wide scan), "tc_wide_ppl" (probes per list above which a
+ * single-pass batch uses the wide 64-query scan; default 10, negative = never;
+ * process default from env HIVF_TC_WIDE_PPL), "time_kernels" (record events
+ * around each phase and accumulate into hivf_stats), "reset_timers". */
 hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
 
 #ifdef __cplusplus
