@@ -1,3 +1,6 @@
+"""Index-build timing (bench infrastructure): GPU hivf_train_kmeans / hivf_compute_assignments
+on the C1/C2 workloads vs the reference train_kmeans (oracle/_ref) on the host; writes
+gpurun_out/build_bench.json (committed copy: profiles/r1_index_build.json)."""
 import sys, os, time, json
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
