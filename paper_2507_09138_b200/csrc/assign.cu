@@ -69,17 +69,23 @@ __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32
 
 // dist32[b][c] = fma(-2, <q_b, c>, |c|^2 + |q_b|^2); the dot accumulates in
 // ascending dim order with one FMA per term (the order the error bound
-// assumes).  Tile: 128 centroids x 32 queries, 256 threads, 4x4 per thread.
-constexpr int CT_C = 128, CT_Q = 32, CT_K = 16;
+// assumes).  Tile: CTC centroids x 32 queries, 4x4 per thread (CTC*2 threads);
+// CTC shrinks (128 -> 64 -> 32) until the grid covers the SMs twice, so
+// small-K / small-B batches (C1, C2) are not run on a fraction of the GPU.
+constexpr int CT_Q = 32, CT_K = 16;
 
-__global__ void __launch_bounds__(256) k_coarse_dist(IndexView ix, QueryView qv,
-                                                     float* __restrict__ out) {
-  __shared__ __align__(16) float As[CT_K][CT_C + 4];
+template <int CTC>
+__global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView qv,
+                                                         float* __restrict__ out) {
+  constexpr int NT = CTC * 2;  // threads
+  constexpr int NA = CTC * CT_K / 4;  // float4 loads per A k-tile
+  constexpr int NB = CT_Q * CT_K / 4;  // float4 loads per B k-tile
+  __shared__ __align__(16) float As[CT_K][CTC + 4];
   __shared__ __align__(16) float Bs[CT_K][CT_Q + 4];
   const int tid = threadIdx.x;
-  const int tc = tid & 31;  // centroid group (4 centroids)
-  const int tq = tid >> 5;  // query group (4 queries)
-  const uint32_t c0 = blockIdx.x * CT_C, q0 = blockIdx.y * CT_Q;
+  const int tc = tid % (CTC / 4);  // centroid group (4 centroids)
+  const int tq = tid / (CTC / 4);  // query group (4 queries)
+  const uint32_t c0 = blockIdx.x * CTC, q0 = blockIdx.y * CT_Q;
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -87,40 +93,47 @@ __global__ void __launch_bounds__(256) k_coarse_dist(IndexView ix, QueryView qv,
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   // register-prefetched k-tiles: tile k0+CT_K is loaded from global while tile
   // k0 is multiplied out of shared memory
-  float4 pa[2], pb = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int PA = NA / NT, PB = (NB + NT - 1) / NT;
+  float4 pa[PA], pb[PB];
   auto fetch = [&](uint32_t k0) {
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int f = tid + t * 256;
+    for (int t = 0; t < PA; ++t) {
+      const int f = tid + t * NT;
       const uint32_t c = c0 + (f >> 2);
       pa[t] = (c < ix.K && k0 < ix.dpad)
                   ? __ldg(reinterpret_cast<const float4*>(ix.cent + (uint64_t)c * ix.dpad + k0 + (f & 3) * 4))
                   : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (tid < 128) {
-      const uint32_t q = q0 + (tid >> 2);
-      pb = (q < qv.n && k0 < ix.dpad)
-               ? __ldg(reinterpret_cast<const float4*>(qv.qs + (uint64_t)q * ix.dpad + k0 + (tid & 3) * 4))
-               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      const int f = tid + t * NT;
+      const uint32_t q = q0 + (f >> 2);
+      pb[t] = (f < NB && q < qv.n && k0 < ix.dpad)
+                  ? __ldg(reinterpret_cast<const float4*>(qv.qs + (uint64_t)q * ix.dpad + k0 + (f & 3) * 4))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   fetch(0);
   for (uint32_t k0 = 0; k0 < ix.dpad; k0 += CT_K) {
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int f = tid + t * 256;
+    for (int t = 0; t < PA; ++t) {
+      const int f = tid + t * NT;
       const int row = f >> 2, g = f & 3;
       As[g * 4 + 0][row] = pa[t].x;
       As[g * 4 + 1][row] = pa[t].y;
       As[g * 4 + 2][row] = pa[t].z;
       As[g * 4 + 3][row] = pa[t].w;
     }
-    if (tid < 128) {
-      const int row = tid >> 2, g = tid & 3;
-      Bs[g * 4 + 0][row] = pb.x;
-      Bs[g * 4 + 1][row] = pb.y;
-      Bs[g * 4 + 2][row] = pb.z;
-      Bs[g * 4 + 3][row] = pb.w;
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      const int f = tid + t * NT;
+      if (f < NB) {
+        const int row = f >> 2, g = f & 3;
+        Bs[g * 4 + 0][row] = pb[t].x;
+        Bs[g * 4 + 1][row] = pb[t].y;
+        Bs[g * 4 + 2][row] = pb[t].z;
+        Bs[g * 4 + 3][row] = pb[t].w;
+      }
     }
     __syncthreads();
     fetch(k0 + CT_K);
@@ -364,8 +377,21 @@ void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t d
 }
 
 void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s) {
-  dim3 grid((ix.K + CT_C - 1) / CT_C, (qv.n + CT_Q - 1) / CT_Q);
-  k_coarse_dist<<<grid, 256, 0, s>>>(ix, qv, dist32);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint32_t qt = (qv.n + CT_Q - 1) / CT_Q;
+  auto tiles = [&](uint32_t ctc) { return (uint64_t)((ix.K + ctc - 1) / ctc) * qt; };
+  if (tiles(128) >= 2ull * sms)
+    k_coarse_dist<128><<<dim3((ix.K + 127) / 128, qt), 256, 0, s>>>(ix, qv, dist32);
+  else if (tiles(64) >= 2ull * sms)
+    k_coarse_dist<64><<<dim3((ix.K + 63) / 64, qt), 128, 0, s>>>(ix, qv, dist32);
+  else
+    k_coarse_dist<32><<<dim3((ix.K + 31) / 32, qt), 64, 0, s>>>(ix, qv, dist32);
 }
 
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
@@ -379,6 +405,8 @@ void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float*
                          200 * 1024);
     attr_set = true;
   }
+  // 512 threads: fewer (64-256, sized to the candidate count) measured slower
+  // (C2 41 -> 61 us, C3 59 -> 75 us)
   k_coarse_select<<<qv.n, 512, smem, s>>>(ix, qv, dist32, nprobe, filter_eps(ix.dim),
                                           filter_abs(ix.dim), plans, dists, flags);
 }
