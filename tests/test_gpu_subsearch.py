@@ -99,10 +99,16 @@ def _rand_index(ctx, seed, n=6000, dim=32, K=24):
     return ix, csr, X, centers, rng
 
 
-@pytest.mark.parametrize("kernel", [0, 1, 2])
+@pytest.mark.parametrize("kernel", [0, 1, 2, "wide"])
 def test_seeded_reordered_subsearch_vs_oracle(ctx, kernel):
     """Seeded heaps (probe_cache, similarity.cpp:35-55) and reordered plans
-    (reorder_clusters, :57-72), mixed k and slice sizes, vs the restatement."""
+    (reorder_clusters, :57-72), mixed k and slice sizes, vs the restatement.
+    "wide": the single-pass tensor-core scan forced onto its 64-query variant
+    (fixed per-item bounds, bound_update = 0)."""
+    wide = kernel == "wide"
+    if wide:
+        kernel = 3
+        ctx.set_option("tc_wide_ppl", 0)
     ix, csr, X, centers, rng = _rand_index(ctx, 41)
     B = 40
     Q = (centers[rng.integers(0, 8, B)] + 0.4 * rng.standard_normal((B, 32))).astype(np.float32)
@@ -153,6 +159,7 @@ def test_seeded_reordered_subsearch_vs_oracle(ctx, kernel):
                 pos[b] = npos
     finally:
         ctx.set_option("scan_kernel", 0)
+        ctx.set_option("tc_wide_ppl", 10)
     for b in range(B):
         e = oheaps[b].entries()
         assert int(hn[b]) == len(e)
