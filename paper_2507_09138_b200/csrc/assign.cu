@@ -283,7 +283,12 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
     return;
   }
   // exact fp64 distances in the reference's order (select_clusters uses
-  // squared_l2(centroid, query), :272)
+  // squared_l2(centroid, query), :272); the candidates' rows are warmed into
+  // L1 by all threads first (every 128-B line in flight at once)
+  for (uint32_t idx = threadIdx.x; idx < m * (ix.dpad / 32); idx += blockDim.x) {
+    const uint32_t i = idx / (ix.dpad / 32), l = idx - i * (ix.dpad / 32);
+    prefetch_l1(ix.cent + (uint64_t)cid[i] * ix.dpad + l * 32);
+  }
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
     const float4* crow = reinterpret_cast<const float4*>(ix.cent + (uint64_t)cid[i] * ix.dpad);
     cd[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) { return __ldg(crow + g); });

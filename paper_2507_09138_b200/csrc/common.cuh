@@ -107,6 +107,12 @@ __device__ __forceinline__ double exact_row_pipelined(uint32_t dim, const float*
   return acc;
 }
 
+// Warm a line into L1 ahead of a latency-bound sequential consumer (the exact
+// fp64 chains read their rows 128 B at a time).
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // ---- orderable float keys ----------------------------------------------------
 __device__ __forceinline__ uint32_t f2key(float f) {
   uint32_t u = __float_as_uint(f);
