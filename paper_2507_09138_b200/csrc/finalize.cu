@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
       pE[p] = seg_bound(ix, qn, ix.maxnorm[c]);
       tot += rows;
     }
-    atomicAdd(&s_total, tot);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    if (lane == 0 && tot) atomicAdd(&s_total, tot);  // one 64-bit smem atomic (a CAS loop) per warp
   }
   __syncthreads();
   // Compacted list of the query's valid (plan position, segment) slots, and
