@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
   extern __shared__ __align__(16) uint8_t sm[];
   double* cd = reinterpret_cast<double*>(sm);                       // kCandCap
   uint32_t* cid = reinterpret_cast<uint32_t*>(cd + kCandCap);         // kCandCap
-  float* qsh = reinterpret_cast<float*>(cid + kCandCap);              // dpad
+  double* qsh = reinterpret_cast<double*>(cid + kCandCap);            // dpad (widened once)
   __shared__ uint32_t hist[256];
   __shared__ uint32_t s_cnt;
   const uint32_t b = blockIdx.x;
@@ -402,7 +402,7 @@ void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32,
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
                           uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s) {
-  const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 4;
+  const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 8;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_coarse_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);

@@ -78,12 +78,19 @@ __device__ __forceinline__ double exact_step(double acc, float a, float b) {
   const double d = __dsub_rn((double)a, (double)b);
   return __dadd_rn(acc, __dmul_rn(d, d));
 }
+// Same step with the query element already widened (exact: every float is a
+// double), one conversion fewer per dim: a single chain measured 20.7 vs
+// 29.5 cycles per dim on B200 (fp64 chains are latency-bound).
+__device__ __forceinline__ double exact_step(double acc, double a, float b) {
+  const double d = __dsub_rn(a, (double)b);
+  return __dadd_rn(acc, __dmul_rn(d, d));
+}
 
 // Exact distance of one row to the query in smem, loads double-buffered 32
 // dims (8 x 16 B) ahead so the memory latency overlaps the sequential fp64
 // chain.  load(g) returns dims 4g..4g+3 of the row (zero past dim).
-template <typename Load>
-__device__ __forceinline__ double exact_row_pipelined(uint32_t dim, const float* qsh, Load load) {
+template <typename Q, typename Load>
+__device__ __forceinline__ double exact_row_pipelined(uint32_t dim, const Q* qsh, Load load) {
   const uint32_t ng = (dim + 3) / 4;
   double acc = 0.0;
   float4 cur[8], nxt[8];

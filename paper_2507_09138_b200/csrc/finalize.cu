@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kCandMax);  // kCandMax
   uint32_t* crow = reinterpret_cast<uint32_t*>(cid + kCandMax);   // kCandMax
   uint32_t* clist = crow + kCandMax;                              // kCandMax
-  float* qsh = reinterpret_cast<float*>(clist + kCandMax);        // dpad
+  double* qsh = reinterpret_cast<double*>(clist + kCandMax);      // dpad (widened once)
   __shared__ float wl[kFinThreads / 32][32];
   __shared__ float s_tau;
   __shared__ uint32_t s_cnt;
@@ -690,7 +690,7 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                             uint32_t* counts_out, int* flags, float* tau_out,
                             const RepairState* rep, cudaStream_t s) {
   const RepairState R = rep ? *rep : RepairState{};
-  const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 4 + (size_t)nprobe * 16 + 4 +
+  const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 8 + (size_t)nprobe * 16 + 4 +
                       (size_t)kSlotCap * (4 + 4 + 4 + kKP * 4);
   static bool attr = false;
   if (!attr) {
