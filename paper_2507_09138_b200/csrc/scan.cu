@@ -378,6 +378,104 @@ __global__ void k_make_items(IndexView ix, uint32_t group, const uint32_t* cnt,
   }
 }
 
+// Small batches, K <= kFusedK: the whole work list in ONE single-CTA kernel
+// (count -> scans in list_order -> scatter -> items) with the per-list
+// counters in shared memory -- the same outputs as the four-kernel chain
+// above, four launches (and a memset) fewer on the latency-bound configs
+// (C1, node-split sub-stages).
+constexpr uint32_t kFusedK = 4096;
+
+__global__ void __launch_bounds__(1024) k_worklist_fused(IndexView ix, uint32_t group,
+                                                         const uint32_t* __restrict__ pair_list,
+                                                         uint32_t n_pairs, uint32_t* cnt_out,
+                                                         uint32_t* pair_off_out, uint32_t* item_off_out,
+                                                         uint32_t* sorted_pairs, ScanItem* items,
+                                                         uint32_t* n_items, uint32_t* work_ctr,
+                                                         uint32_t* qshift) {
+  extern __shared__ uint32_t wsm[];
+  uint32_t* cnt = wsm;            // [K]
+  uint32_t* poff = cnt + ix.K;    // [K]
+  uint32_t* cur = poff + ix.K;    // [K]
+  __shared__ uint32_t sp[1024], si[1024], sq[1024];
+  for (uint32_t c = threadIdx.x; c < ix.K; c += blockDim.x) {
+    cnt[c] = 0;
+    cur[c] = 0;
+  }
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < n_pairs; p += blockDim.x) atomicAdd(&cnt[pair_list[p]], 1u);
+  __syncthreads();
+  // exclusive scans in list_order (largest lists first), as k_list_offsets
+  const uint32_t per = (ix.K + 1023) / 1024;
+  const uint32_t b = threadIdx.x * per, e = min(ix.K, b + per);
+  uint32_t tp = 0, ti = 0, tq = 0;
+  for (uint32_t t = b; t < e; ++t) {
+    const uint32_t c = ix.list_order[t];
+    const uint32_t n = cnt[c];
+    const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
+    const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+    tp += n;
+    ti += n ? nseg * ((n + group - 1) / group) : 0;
+    tq += (n + 7) & ~7u;
+  }
+  sp[threadIdx.x] = tp;
+  si[threadIdx.x] = ti;
+  sq[threadIdx.x] = tq;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const uint32_t a = threadIdx.x >= o ? sp[threadIdx.x - o] : 0;
+    const uint32_t c2 = threadIdx.x >= o ? si[threadIdx.x - o] : 0;
+    const uint32_t c3 = threadIdx.x >= o ? sq[threadIdx.x - o] : 0;
+    __syncthreads();
+    sp[threadIdx.x] += a;
+    si[threadIdx.x] += c2;
+    sq[threadIdx.x] += c3;
+    __syncthreads();
+  }
+  uint32_t op = sp[threadIdx.x] - tp, oi = si[threadIdx.x] - ti, oq = sq[threadIdx.x] - tq;
+  for (uint32_t t = b; t < e; ++t) {
+    const uint32_t c = ix.list_order[t];
+    const uint32_t n = cnt[c];
+    const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
+    const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+    poff[c] = op;
+    cnt_out[c] = n;
+    pair_off_out[c] = op;
+    item_off_out[c] = oi;
+    if (qshift) qshift[c] = oq - op;
+    // this list's work items (segment-major, query groups inside), as k_make_items
+    if (n) {
+      const uint32_t ng = (n + group - 1) / group;
+      uint32_t o = oi;
+      for (uint32_t sgi = 0; sgi < nseg; ++sgi) {
+        const uint32_t row0 = sgi * ix.seg_rows;
+        const uint32_t nr = (uint32_t)min((uint64_t)ix.seg_rows, rows - row0);
+        for (uint32_t g = 0; g < ng; ++g) {
+          ScanItem it;
+          it.list = c;
+          it.seg = sgi;
+          it.row0 = row0;
+          it.nrows = nr;
+          it.pair0 = op + g * group;
+          it.nq = min(group, n - g * group);
+          items[o++] = it;
+        }
+      }
+    }
+    op += n;
+    oi += n ? nseg * ((n + group - 1) / group) : 0;
+    oq += (n + 7) & ~7u;
+  }
+  if (threadIdx.x == 1023) {
+    *n_items = si[1023];
+    *work_ctr = 0;
+  }
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < n_pairs; p += blockDim.x) {
+    const uint32_t c = pair_list[p];
+    sorted_pairs[poff[c] + atomicAdd(&cur[c], 1u)] = p;
+  }
+}
+
 }  // namespace
 
 int scan_smem_bytes(uint32_t dpad) {
@@ -390,6 +488,18 @@ void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* 
                            uint32_t* list_item_off, uint32_t* sorted_pairs, ScanItem* items,
                            uint32_t* n_items, uint32_t* work_ctr, uint32_t* qshift, cudaStream_t s) {
   (void)pair_query;
+  (void)list_cursor;
+  if (ix.K <= kFusedK && n_pairs <= 8192u) {  // C3 (32k pairs) is faster on the 4-kernel chain
+    const size_t smem = (size_t)ix.K * 12;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_worklist_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kFusedK * 12));
+      attr = true;
+    }
+    k_worklist_fused<<<1, 1024, smem, s>>>(ix, group, pair_list, n_pairs, list_cnt, list_pair_off,
+                                           list_item_off, sorted_pairs, items, n_items, work_ctr, qshift);
+    return;
+  }
   cudaMemsetAsync(list_cnt, 0, sizeof(uint32_t) * ix.K, s);
   if (n_pairs) k_count_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_cnt);
   k_list_offsets<<<1, 1024, 0, s>>>(ix, group, list_cnt, list_pair_off, list_cursor, list_item_off,
