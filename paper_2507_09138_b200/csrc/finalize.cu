@@ -12,6 +12,7 @@
 // no FMA) and are ordered by (distance, doc id) (vector_index.hpp:41-44), so
 // ids AND distances are bit-identical to TopKResult after the full plan
 // (vector_index.cpp:38-53,291-317).
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -479,8 +480,24 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
                                                       double* d_out, uint32_t* counts_out,
                                                       uint64_t* part_total, const float* tau,
                                                       double fa, double fb, double fc) {
-  const uint32_t b = blockIdx.x;
-  if (flags && !flags[b]) return;
+  // grid-stride over queries: the grid is sized for ~one wave, so a batch
+  // with no flagged query costs a few hundred idle CTAs, not B x nsplit; each
+  // CTA checks the flags of its next blockDim.x queries at once and works
+  // through the flagged ones
+  __shared__ uint32_t s_list[256];
+  __shared__ uint32_t s_nl;
+  for (uint64_t base = blockIdx.x; base < qv.n; base += (uint64_t)gridDim.x * blockDim.x) {
+  __syncthreads();  // the previous chunk's list is consumed
+  if (threadIdx.x == 0) s_nl = 0;
+  __syncthreads();
+  {
+    const uint64_t bb = base + (uint64_t)threadIdx.x * gridDim.x;
+    if (bb < qv.n && (!flags || flags[bb])) s_list[atomicAdd(&s_nl, 1u)] = (uint32_t)bb;
+  }
+  __syncthreads();
+  const uint32_t nl = s_nl;
+  for (uint32_t li = 0; li < nl; ++li) {
+  const uint32_t b = s_list[li];
   const uint32_t nsplit = gridDim.y, y = blockIdx.y;
   const uint32_t per = (nprobe + nsplit - 1) / nsplit;
   const uint32_t p_beg = min(nprobe, y * per), p_end = min(nprobe, p_beg + per);
@@ -579,6 +596,9 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
   if (threadIdx.x == 0) {
     counts_out[out_row] = cnt;
     if (part_total) part_total[out_row] = s_total;
+  }
+  __syncthreads();  // shared state is re-initialised by the next query
+  }
   }
 }
 
@@ -727,12 +747,20 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
     attr = true;
   }
   const uint32_t ns = part_ids ? exact_search_parts(nprobe, k) : 1;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint32_t gx = std::max(1u, std::min(qv.n, (uint32_t)(4 * sms) / ns));
   if (ns <= 1) {
-    k_exact_search<<<dim3(qv.n, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
+    k_exact_search<<<dim3(gx, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
                                                     d_out, counts_out, nullptr, tau, fa, fb, fc);
     return;
   }
-  k_exact_search<<<dim3(qv.n, ns), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, part_ids,
+  k_exact_search<<<dim3(gx, ns), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, part_ids,
                                                    part_d, part_cnt, part_total, tau, fa, fb, fc);
   uint32_t mcap = 1;
   while (mcap < ns * k) mcap <<= 1;
