@@ -399,3 +399,19 @@ def test_search_device_cuda_graph_capture(ctx):
             assert np.array_equal(cnt.cpu().numpy(), oc)
             assert np.array_equal(ids.cpu().numpy().astype(np.uint64), oi)
             assert np.array_equal(dd.cpu().numpy().view(np.uint64), od.view(np.uint64))
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_large_batch_multi_kernel_worklist(ctx, wide):
+    """> 8192 (query, list) pairs: the work list is built by the multi-CTA
+    kernel chain (k_count_pairs / k_list_offsets / k_scatter_pairs /
+    k_make_items) instead of the fused single-CTA kernel; narrow and wide scan."""
+    rng = np.random.default_rng(97)
+    ix, csr, X, centers = _random_index(ctx, rng, 20000, 32, 64)
+    Q = (centers[rng.integers(0, len(centers), 700)] +
+         rng.standard_normal((700, 32)).astype(np.float32) * 0.3).astype(np.float32)
+    ctx.set_option("tc_wide_ppl", 0 if wide else -1)
+    try:
+        _check_search(ix, csr, Q, 16, 10)
+    finally:
+        ctx.set_option("tc_wide_ppl", 10)
