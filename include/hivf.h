@@ -264,7 +264,11 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * or 64 = the wide scan), "tc_wide_ppl" (probes per list above which a
  * single-pass batch uses the wide 64-query scan; default 10, negative = never;
  * process default from env HIVF_TC_WIDE_PPL), "time_kernels" (record events
- * around each phase and accumulate into hivf_stats), "reset_timers". */
+ * around each phase and accumulate into hivf_stats), "reset_timers",
+ * "search_graph" (default 1: hivf_search captures a batch shape seen twice in
+ * a row into a CUDA graph and replays it; any option write, buffer growth or
+ * index upload/destroy invalidates it; tiered indexes and kernel timing
+ * bypass it). */
 hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
 
 #ifdef __cplusplus

@@ -7,6 +7,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -51,6 +52,11 @@ hivf_status fail(hivf_status st, const char* fmt, ...) {
                   __LINE__);                                                             \
   } while (0)
 
+// Bumped whenever something a captured search graph bakes in may have
+// changed: a scratch buffer reallocation, an option, an index upload/destroy
+// (see search_device_cached).
+static std::atomic<uint64_t> g_state_gen{1};
+
 // Grow-only device buffer.
 struct DBuf {
   void* p = nullptr;
@@ -64,6 +70,7 @@ struct DBuf {
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    g_state_gen.fetch_add(1);
     want = std::max<size_t>(want, 256);
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) bytes = want;
@@ -137,6 +144,21 @@ struct hivf_ctx {
   bool stats_adapted = false;
   // phase timing (option "time_kernels"): one event set per call, resolved lazily
   int opt_time = 0;
+  int opt_search_graph = 1;  // hivf_search replays a captured graph for a repeated batch shape
+  // the cached search graph (search_device_cached): key, exec, and the host
+  // state the captured call left behind
+  struct SearchGraph {
+    const void* ix = nullptr;
+    const float* q = nullptr;
+    const void* out = nullptr;
+    uint32_t n = 0, nprobe = 0, k = 0;
+    int kind = -1;
+    uint64_t gen = 0;
+    bool seen = false;
+    cudaGraphExec_t exec = nullptr;
+    hivf_stats stats{};
+    int last_kind = 0;
+  } sgraph;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   uint32_t timed_calls = 0;
@@ -177,6 +199,7 @@ struct hivf_ctx {
                     &rep_d, &rep_ids, &qshift, &qwide})
       b->release();
     hstage.release();
+    if (sgraph.exec) cudaGraphExecDestroy(sgraph.exec);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -339,6 +362,7 @@ void pool_free(hivf_index* ix, uint64_t off, uint64_t bytes) {
 // pointer-table updates ride in kernel arguments (no host buffer lifetime):
 // ordered on the context stream, so launches before keep the old address
 static hivf_status apply_flips(hivf_index* ix, const std::vector<std::pair<uint32_t, const float*>>& f) {
+  g_state_gen.fetch_add(1);
   for (size_t b = 0; b < f.size(); b += kPtrFlipBatch) {
     PtrFlips pf{};
     pf.n = (uint32_t)std::min<size_t>(kPtrFlipBatch, f.size() - b);
@@ -439,7 +463,10 @@ hivf_status hivf_ctx_synchronize(hivf_ctx* ctx) {
 
 hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   if (!ctx || !name) return fail(HIVF_EINVAL, "hivf_set_option: NULL argument");
-  if (!strcmp(name, "seg_rows")) {  // 0: automatic (auto_seg_rows)
+  g_state_gen.fetch_add(1);  // any option may change what a captured search graph launches
+  if (!strcmp(name, "search_graph")) {
+    ctx->opt_search_graph = value != 0;
+  } else if (!strcmp(name, "seg_rows")) {  // 0: automatic (auto_seg_rows)
     if (value != 0 && (value < kRowBlock || value % kRowBlock))
       return fail(HIVF_EINVAL, "seg_rows must be a multiple of %d", kRowBlock);
     ctx->opt_seg_rows = (uint32_t)value;
@@ -715,6 +742,7 @@ static hivf_status upload_common(hivf_ctx* ctx, uint32_t dim, int metric, uint32
                                  const float* centroids, int cent_dev, const uint64_t* list_offsets,
                                  const float* vectors, const uint64_t* ids, bool dev,
                                  hivf_index** out) {
+  g_state_gen.fetch_add(1);
   if (!out) return fail(HIVF_EINVAL, "out is NULL");
   hivf_index* ix = nullptr;
   hivf_status st = hivf_index_begin(ctx, dim, metric, n_clusters, centroids, cent_dev, list_offsets, &ix);
@@ -774,6 +802,7 @@ hivf_status hivf_index_upload_device(hivf_ctx* ctx, uint32_t dim, int metric,
 
 hivf_status hivf_index_destroy(hivf_index* ix) {
   if (!ix) return HIVF_OK;
+  g_state_gen.fetch_add(1);
   cudaSetDevice(ix->ctx->device);
   cudaStreamSynchronize(ix->ctx->stream);
   delete ix;
@@ -1130,6 +1159,75 @@ hivf_status hivf_assign_device(hivf_index* ix, const float* d_queries, uint32_t 
   return HIVF_OK;
 }
 
+// hivf_search's device part through a cached CUDA graph: a batch shape seen
+// twice in a row (same index, n, nprobe, k, scan kind, buffers, options) is
+// captured on its second call and replayed from then on, so the ~15
+// dependent launches of a search cost one graph launch (the host-buffer API
+// is launch-latency bound on small batches).  The search itself has no host
+// decisions that depend on device data (repair / exact fallbacks are
+// device-side), so the replay does exactly what the captured call did; the
+// host-side bookkeeping it left (stats, last-call fields) is restored.  Any
+// reallocation, option change or index upload/destroy bumps g_state_gen and
+// invalidates the graph; tiered indexes, kernel timing and profiling bypass it.
+static hivf_status search_device_cached(hivf_index* ix, const float* dq, uint32_t n, uint32_t nprobe,
+                                        uint32_t k, uint64_t* ids, double* dists, uint32_t* counts) {
+  hivf_ctx* c = ix->ctx;
+  if (!c->opt_search_graph || ix->tiered || c->opt_time)
+    return hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
+  const int kind = (c->opt_force_exact || k > (uint32_t)kKP) ? 0 : ix->scan_kind();
+  auto& g = c->sgraph;
+  const bool same = g.ix == ix && g.q == dq && g.out == ids && g.n == n && g.nprobe == nprobe && g.k == k &&
+                    g.kind == kind && g.gen == g_state_gen.load();
+  if (same && g.exec) {
+    c->stats = g.stats;
+    c->last_nq = n;
+    c->last_index = ix;
+    c->last_K = ix->K;
+    c->last_kind = g.last_kind;
+    c->stats_adapted = false;
+    CK(cudaGraphLaunch(g.exec, c->stream));
+    return HIVF_OK;
+  }
+  if (same && g.seen) {  // second call with this shape: capture it
+    const uint64_t gen0 = g_state_gen.load();
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    hivf_status st = ok ? hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts) : HIVF_ECUDA;
+    if (ok) ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && st == HIVF_OK &&
+                 g_state_gen.load() == gen0;
+    cudaGraphExec_t ex = nullptr;
+    if (ok) ok = cudaGraphInstantiate(&ex, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    if (ok) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = ex;
+      g.gen = gen0;
+      g.stats = c->stats;
+      g.last_kind = c->last_kind;
+      CK(cudaGraphLaunch(g.exec, c->stream));
+      return HIVF_OK;
+    }
+    g.seen = false;  // not capturable this time: plain launches
+    return hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
+  }
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g = {};
+  hivf_status st = hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
+  if (st == HIVF_OK) {
+    g.ix = ix;
+    g.q = dq;
+    g.out = ids;
+    g.n = n;
+    g.nprobe = nprobe;
+    g.k = k;
+    g.kind = kind;
+    g.gen = g_state_gen.load();
+    g.seen = true;
+  }
+  return st;
+}
+
 hivf_status hivf_search(hivf_index* ix, const float* queries, uint32_t n, uint32_t nprobe,
                         uint32_t k, uint64_t* ids_out, double* dists_out, uint32_t* counts_out) {
   hivf_status st = check_search_args(ix, n, nprobe, k);
@@ -1151,8 +1249,9 @@ hivf_status hivf_search(hivf_index* ix, const float* queries, uint32_t n, uint32
   CK(cudaMemsetAsync(c->err.p, 0, 4, c->stream));
   CK(cudaMemcpyAsync(c->qin.p, queries, qb, cudaMemcpyHostToDevice, c->stream));
   uint8_t* dpk = c->out_ids.as<uint8_t>();
-  if ((st = hivf_search_device(ix, c->qin.as<float>(), n, nprobe, k, reinterpret_cast<uint64_t*>(dpk),
-                               reinterpret_cast<double*>(dpk + o_d), reinterpret_cast<uint32_t*>(dpk + o_c))) != HIVF_OK)
+  if ((st = search_device_cached(ix, c->qin.as<float>(), n, nprobe, k, reinterpret_cast<uint64_t*>(dpk),
+                                 reinterpret_cast<double*>(dpk + o_d), reinterpret_cast<uint32_t*>(dpk + o_c))) !=
+      HIVF_OK)
     return st;
   CK(cudaMemcpyAsync(dpk + o_e, c->err.p, 4, cudaMemcpyDeviceToDevice, c->stream));
   if (want_fb) CK(cudaMemcpyAsync(dpk + o_f, c->flags_f.p, 4ull * n, cudaMemcpyDeviceToDevice, c->stream));

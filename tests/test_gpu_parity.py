@@ -415,3 +415,29 @@ def test_large_batch_multi_kernel_worklist(ctx, wide):
         _check_search(ix, csr, Q, 16, 10)
     finally:
         ctx.set_option("tc_wide_ppl", 10)
+
+
+def test_repeated_search_graph_replay(ctx):
+    """hivf_search replays a captured graph from the third call of a batch
+    shape on: every call (new queries each time) must still equal the
+    reference, across an option change (invalidation) and a shape change."""
+    rng = np.random.default_rng(123)
+    ix, csr, X, centers = _random_index(ctx, rng, 12000, 48, 32)
+    def batch(B):
+        return (centers[rng.integers(0, len(centers), B)] +
+                rng.standard_normal((B, 48)).astype(np.float32) * 0.3).astype(np.float32)
+    for it in range(5):
+        _check_search(ix, csr, batch(40), 8, 10)
+        if it == 2:
+            st = ctx.stats()
+            assert st["kernels_launched"] > 0 and st["n_work_items"] > 0, st
+    ctx.set_option("search_graph", 1)  # option write: invalidates the cached graph
+    for _ in range(3):
+        _check_search(ix, csr, batch(40), 8, 10)
+    for _ in range(3):
+        _check_search(ix, csr, batch(17), 5, 7)
+    ctx.set_option("search_graph", 0)
+    try:
+        _check_search(ix, csr, batch(40), 8, 10)
+    finally:
+        ctx.set_option("search_graph", 1)
