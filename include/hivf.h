@@ -262,7 +262,8 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
  * 3 tcgen05 single-pass), "tc_qmax" (queries per scan work item: 8..32 step 8,
  * or 64 = the wide scan), "tc_wide_ppl" (probes per list above which a
- * single-pass batch uses the wide 64-query scan; default 10, negative = never;
+ * single-pass batch uses the wide 64-query scan; default 0 = every single-pass
+ * batch (measured faster at all densities), negative = never;
  * process default from env HIVF_TC_WIDE_PPL), "time_kernels" (record events
  * around each phase and accumulate into hivf_stats), "reset_timers",
  * "search_graph" (default 1: hivf_search captures a batch shape seen twice in

@@ -414,7 +414,7 @@ def test_large_batch_multi_kernel_worklist(ctx, wide):
     try:
         _check_search(ix, csr, Q, 16, 10)
     finally:
-        ctx.set_option("tc_wide_ppl", 10)
+        ctx.set_option("tc_wide_ppl", 0)
 
 
 def test_repeated_search_graph_replay(ctx):

@@ -159,7 +159,7 @@ def test_seeded_reordered_subsearch_vs_oracle(ctx, kernel):
                 pos[b] = npos
     finally:
         ctx.set_option("scan_kernel", 0)
-        ctx.set_option("tc_wide_ppl", 10)
+        ctx.set_option("tc_wide_ppl", 0)
     for b in range(B):
         e = oheaps[b].entries()
         assert int(hn[b]) == len(e)

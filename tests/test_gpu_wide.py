@@ -21,7 +21,7 @@ def ctx():
     c.set_option("scan_kernel", 3)
     c.set_option("tc_wide_ppl", 0)
     yield c
-    c.set_option("tc_wide_ppl", 10)
+    c.set_option("tc_wide_ppl", 0)
     c.set_option("scan_kernel", 0)
 
 
