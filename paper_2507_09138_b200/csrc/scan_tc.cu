@@ -983,14 +983,16 @@ namespace {
 // of dpad*4*npad bytes laid out chunk-major [ch][npad rows][64 B] with the
 // SWIZZLE_64B XOR, so a stage's 4-chunk slice is one contiguous bulk copy
 // that lands in UMMA K-major layout.
-__global__ void __launch_bounds__(64) k_stage_wide(const float* __restrict__ qs, uint32_t dpad,
-                                                   const uint32_t* __restrict__ sorted_pairs,
-                                                   const uint32_t* __restrict__ pair_query,
-                                                   const uint32_t* __restrict__ pair_list,
-                                                   const uint32_t* __restrict__ pair_off,
-                                                   const uint32_t* __restrict__ list_cnt,
-                                                   const uint32_t* __restrict__ qshift, uint8_t* qstage) {
-  const uint32_t p = blockIdx.x;
+__global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs, uint32_t dpad,
+                                                    const uint32_t* __restrict__ sorted_pairs,
+                                                    const uint32_t* __restrict__ pair_query,
+                                                    const uint32_t* __restrict__ pair_list,
+                                                    const uint32_t* __restrict__ pair_off,
+                                                    const uint32_t* __restrict__ list_cnt,
+                                                    const uint32_t* __restrict__ qshift, uint8_t* qstage,
+                                                    uint32_t n_pairs) {
+  const uint32_t p = blockIdx.x * 8 + (threadIdx.x >> 5);  // one warp per pair
+  if (p >= n_pairs) return;
   const uint32_t pair = sorted_pairs[p];
   const uint32_t c = pair_list[pair];
   const uint32_t local = p - pair_off[c], n = list_cnt[c];
@@ -998,7 +1000,7 @@ __global__ void __launch_bounds__(64) k_stage_wide(const float* __restrict__ qs,
   const uint32_t npad = min((uint32_t)kWideQ, ((n - g * kWideQ) + 7) & ~7u);
   uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * kWideQ) * dpad * 4;
   const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)pair_query[pair] * dpad);
-  for (uint32_t g4 = threadIdx.x; g4 < dpad / 4; g4 += blockDim.x) {
+  for (uint32_t g4 = threadIdx.x & 31; g4 < dpad / 4; g4 += 32) {
     const uint32_t ch = g4 >> 2, q4 = g4 & 3;
     *reinterpret_cast<float4*>(blk + (uint64_t)ch * npad * 64 + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4)) =
         src[g4];
@@ -1014,8 +1016,8 @@ void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t*
                        const uint32_t* pair_query, const uint32_t* pair_list, const uint32_t* pair_off,
                        const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s) {
   if (n_pairs)
-    k_stage_wide<<<n_pairs, 64, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list, pair_off,
-                                        list_cnt, ws.qshift, ws.qstage);
+    k_stage_wide<<<(n_pairs + 7) / 8, 256, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list,
+                                                   pair_off, list_cnt, ws.qshift, ws.qstage, n_pairs);
 }
 
 }  // namespace hivf
