@@ -39,7 +39,8 @@ typedef enum {
   HIVF_EINTERNAL = 2,
   HIVF_ECUDA = 3,
   HIVF_ENOMEM = 4,
-  HIVF_EUNSUPPORTED = 5
+  HIVF_EUNSUPPORTED = 5,
+  HIVF_ECOMM = 6  /* multi-GPU exchange failed (NCCL error, all-gather callback error) */
 } hivf_status;
 
 /* Metric ids match hedra::Metric (proj/include/hedra/embedding.hpp:14). */
@@ -220,6 +221,77 @@ hivf_status hivf_merge_parts_device(hivf_ctx* ctx, uint32_t n_parts, uint32_t n_
                                     uint32_t k, const uint64_t* d_ids, const double* d_dists,
                                     const uint32_t* d_counts, uint64_t* d_ids_out,
                                     double* d_dists_out, uint32_t* d_counts_out);
+
+/* ---- multi-GPU list sharding -----------------
+ * The reference searches one in-memory IvfIndex (vector_index.hpp:83-113); here
+ * the lists of one logical index are split over GPUs and the per-GPU exact
+ * top-k lists are merged with merge_topk (vector_index.cpp:71-91), so results
+ * are identical to a single-GPU (or reference) search of the whole index.
+ *
+ * hivf_shard_plan: owner_out[c] = the rank holding list c, or
+ * HIVF_SHARD_STRIPED for lists whose rows are split over all ranks (rank r
+ * holds rows [n*r/N, n*(r+1)/N) of the list).  Load of a list = sizes[c] *
+ * weights[c] (weights NULL = 1: bytes; pass the list's expected scan passes per
+ * batch -- its probe frequency -- for skewed query streams).  The n_striped
+ * heaviest lists (load desc, id asc) are striped (n_striped < 0: automatic, the
+ * lists heavier than 1/16 of one rank's share), the rest go to ranks by LPT
+ * (heaviest list to the least-loaded rank, ties to the lowest rank).
+ * hivf_shard_local_lists: rank `rank`'s CSR -- local list c holds the global
+ * list-order rows [src_first_out[c], src_first_out[c] + local size), local
+ * sizes as offsets [n_clusters+1].  Every rank builds its index with ALL
+ * centroids (identical on every rank) and its local lists (others empty);
+ * hivf_index_upload_shard does that from host CSR arrays. */
+#define HIVF_SHARD_STRIPED 0xFFFFFFFFu
+hivf_status hivf_shard_plan(const uint64_t* sizes, const double* weights, uint32_t n_clusters,
+                            uint32_t nranks, int32_t n_striped, uint32_t* owner_out);
+hivf_status hivf_shard_local_lists(const uint64_t* list_offsets, const uint32_t* owner,
+                                   uint32_t n_clusters, uint32_t nranks, uint32_t rank,
+                                   uint64_t* local_offsets_out, uint64_t* src_first_out);
+hivf_status hivf_index_upload_shard(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
+                                    const float* centroids, const uint64_t* list_offsets,
+                                    const float* vectors, const uint64_t* ids,
+                                    const uint32_t* owner, uint32_t nranks, uint32_t rank,
+                                    hivf_index** out);
+
+/* A shard group searches the shards of one logical index as one: per batch,
+ * each rank assigns a slice of the batch (select_clusters), the plans are
+ * all-gathered, every rank searches its shard with the full plans, and one
+ * packed ids|dists|counts block per rank is exchanged and merged on device
+ * (merge_topk).  Three transports:
+ *   hivf_group_create        in-process: one host thread drives n shards on n
+ *                            contexts (one per GPU; several may share a
+ *                            device); exchange by a gather kernel over peer
+ *                            pointers (NVLink P2P), event-ordered.  Queries
+ *                            and results live on shards[0]'s device/stream.
+ *   hivf_group_create_nccl   one process per GPU (torchrun): ncclAllGather on
+ *                            the context stream; every rank calls every group
+ *                            function collectively with the same batch and
+ *                            gets the merged results.  unique_id: 128 bytes
+ *                            from hivf_nccl_unique_id on rank 0, broadcast by
+ *                            the caller.  NCCL is loaded at run time.
+ *   hivf_group_create_hostcb one process per rank, exchange through the
+ *                            caller's host all-gather `fn` (recv = nranks
+ *                            blocks of `bytes`, rank order; return 0 on
+ *                            success) -- e.g. torch.distributed over gloo.
+ * The shards must share dim / n_clusters / metric and the centroids, and hold
+ * disjoint row sets (hivf_shard_local_lists).  EUNSUPPORTED: nranks*k > 8192,
+ * tiered shards.  HIVF_ECOMM: NCCL / callback failure. */
+typedef struct hivf_group hivf_group;
+typedef int (*hivf_allgather_fn)(void* user, const void* send, size_t bytes, void* recv);
+hivf_status hivf_group_create(hivf_index* const* shards, uint32_t n, hivf_group** out);
+hivf_status hivf_nccl_unique_id(void* unique_id_out);
+hivf_status hivf_group_create_nccl(hivf_index* shard, uint32_t nranks, uint32_t rank,
+                                   const void* unique_id, hivf_group** out);
+hivf_status hivf_group_create_hostcb(hivf_index* shard, uint32_t nranks, uint32_t rank,
+                                     hivf_allgather_fn fn, void* user, hivf_group** out);
+hivf_status hivf_group_destroy(hivf_group* g);
+/* The sharded hivf_search_device / hivf_search (same arguments and errors). */
+hivf_status hivf_group_search_device(hivf_group* g, const float* d_queries, uint32_t n_queries,
+                                     uint32_t nprobe, uint32_t k, uint64_t* d_ids_out,
+                                     double* d_dists_out, uint32_t* d_counts_out);
+hivf_status hivf_group_search(hivf_group* g, const float* queries, uint32_t n_queries,
+                              uint32_t nprobe, uint32_t k, uint64_t* ids_out, double* dists_out,
+                              uint32_t* counts_out);
 
 /* ---- hot-cluster residency set ---------------------------------------------
  * Device side of cache::ClusterCacheState (proj/include/hedra/tiered_cache.hpp

@@ -12,7 +12,11 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libhivf.so")
 
-HIVF_OK, HIVF_EINVAL, HIVF_EINTERNAL, HIVF_ECUDA, HIVF_ENOMEM, HIVF_EUNSUPPORTED = range(6)
+HIVF_OK, HIVF_EINVAL, HIVF_EINTERNAL, HIVF_ECUDA, HIVF_ENOMEM, HIVF_EUNSUPPORTED, HIVF_ECOMM = range(7)
+SHARD_STRIPED = 0xFFFFFFFF
+
+# hivf_allgather_fn: int (*)(void* user, const void* send, size_t bytes, void* recv)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 # header-declared symbols (tests check every one is exported)
 SYMBOLS = [
@@ -26,7 +30,9 @@ SYMBOLS = [
     "hivf_train_kmeans", "hivf_compute_assignments_host", "hivf_train_kmeans_host",
     "hivf_merge_parts_device", "hivf_residency_set", "hivf_residency_get",
     "hivf_residency_sync", "hivf_last_stats",
-    "hivf_set_option",
+    "hivf_set_option", "hivf_shard_plan", "hivf_shard_local_lists", "hivf_index_upload_shard",
+    "hivf_group_create", "hivf_nccl_unique_id", "hivf_group_create_nccl", "hivf_group_create_hostcb",
+    "hivf_group_destroy", "hivf_group_search_device", "hivf_group_search",
 ]
 
 
@@ -101,6 +107,16 @@ def lib():
         "hivf_residency_sync": (i32, [vp]),
         "hivf_last_stats": (i32, [vp, P(Stats)]),
         "hivf_set_option": (i32, [vp, C.c_char_p, C.c_int64]),
+        "hivf_shard_plan": (i32, [vp, vp, u32, u32, C.c_int32, vp]),
+        "hivf_shard_local_lists": (i32, [vp, vp, u32, u32, u32, vp, vp]),
+        "hivf_index_upload_shard": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, vp, u32, u32, P(vp)]),
+        "hivf_group_create": (i32, [vp, u32, P(vp)]),
+        "hivf_nccl_unique_id": (i32, [vp]),
+        "hivf_group_create_nccl": (i32, [vp, u32, u32, vp, P(vp)]),
+        "hivf_group_create_hostcb": (i32, [vp, u32, u32, ALLGATHER_FN, vp, P(vp)]),
+        "hivf_group_destroy": (i32, [vp]),
+        "hivf_group_search_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
+        "hivf_group_search": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

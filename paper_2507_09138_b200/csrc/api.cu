@@ -16,16 +16,15 @@
 #include <string>
 #include <vector>
 
-#include "../../include/hivf.h"
-#include "common.cuh"
-#include "kernels.h"
+#include "internal.h"
 
 using namespace hivf;
 
+namespace hivf {
+std::atomic<uint64_t> g_state_gen{1};
 namespace {
-
 thread_local std::string g_err;
-
+}
 hivf_status fail(hivf_status st, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -35,264 +34,14 @@ hivf_status fail(hivf_status st, const char* fmt, ...) {
   g_err = buf;
   return st;
 }
-
-#define CK(call)                                                                         \
-  do {                                                                                   \
-    cudaError_t e_ = (call);                                                             \
-    if (e_ != cudaSuccess)                                                               \
-      return fail(e_ == cudaErrorMemoryAllocation ? HIVF_ENOMEM : HIVF_ECUDA, "%s: %s (%s:%d)", \
-                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                    \
-  } while (0)
-
-#define CKL()                                                                            \
-  do {                                                                                   \
-    cudaError_t e_ = cudaGetLastError();                                                 \
-    if (e_ != cudaSuccess)                                                               \
-      return fail(HIVF_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
-                  __LINE__);                                                             \
-  } while (0)
-
-// Bumped whenever something a captured search graph bakes in may have
-// changed: a scratch buffer reallocation, an option, an index upload/destroy
-// (see search_device_cached).
-static std::atomic<uint64_t> g_state_gen{1};
-
-// Grow-only device buffer.
-struct DBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  // grows by >= 1.5x: a stream of varying batch shapes (node-split
-  // sub-stages) settles after a few calls instead of re-allocating (cudaFree
-  // synchronises the device) whenever a batch is a little larger than before
-  cudaError_t ensure(size_t want) {
-    if (want <= bytes) return cudaSuccess;
-    want = std::max(want, bytes + bytes / 2);
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    g_state_gen.fetch_add(1);
-    want = std::max<size_t>(want, 256);
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) bytes = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  template <typename T>
-  T* as() const {
-    return reinterpret_cast<T*>(p);
-  }
-};
-
-struct HBuf {  // grow-only pinned host buffer
-  void* p = nullptr;
-  size_t bytes = 0;
-  cudaError_t ensure(size_t want) {
-    if (want <= bytes) return cudaSuccess;
-    want = std::max(want, bytes + bytes / 2);
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(want, 256));
-    if (e == cudaSuccess) bytes = std::max<size_t>(want, 256);
-    return e;
-  }
-  void release() {
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  template <typename T>
-  T* as() const {
-    return reinterpret_cast<T*>(p);
-  }
-};
-
-}  // namespace
-
-struct hivf_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  int sm_count = 148;
-  // options
-  uint32_t opt_seg_rows = 0;  // 0: chosen per index from its size (auto_seg_rows)
-  int opt_force_exact = 0;
-  // 0 auto (tensor cores when the dim fits; single-pass tf32, escalating to the
-  // split kernel when the data makes its bound too loose), 1 FFMA, 2 tcgen05
-  // split-precision, 3 tcgen05 single-pass
-  int opt_scan_kernel = 0;
-  int opt_scan_ctas = 0;
-  int opt_no_bound = 0;  // debug: disable the scan's shared per-query drop bound
-  // tiered residency: list bytes an index may keep in HBM (0 = all lists in HBM);
-  // the rest stays in a pinned host backing store read over PCIe
-  uint64_t opt_hbm_list_budget = 0;
-  // scratch
-  DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
-      list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
-      cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, qbound, rep_entries, rep_n, rep_cnt,
-      rep_d, rep_ids, qshift, qwide;
-  HBuf hstage;
-  hivf_stats stats{};
-  uint32_t last_nq = 0;
-  uint32_t last_K = 0;
-  const hivf_index* last_index = nullptr;
-  uint32_t last_kind = 0;
-  bool stats_adapted = false;
-  // phase timing (option "time_kernels"): one event set per call, resolved lazily
-  int opt_time = 0;
-  int opt_search_graph = 1;  // hivf_search replays a captured graph for a repeated batch shape
-  // the cached search graph (search_device_cached): key, exec, and the host
-  // state the captured call left behind
-  struct SearchGraph {
-    const void* ix = nullptr;
-    const float* q = nullptr;
-    const void* out = nullptr;
-    uint32_t n = 0, nprobe = 0, k = 0;
-    int kind = -1;
-    uint64_t gen = 0;
-    bool seen = false;
-    cudaGraphExec_t exec = nullptr;
-    hivf_stats stats{};
-    int last_kind = 0;
-  } sgraph;
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used = 0;
-  uint32_t timed_calls = 0;
-  double acc_assign = 0, acc_scan = 0, acc_fin = 0;
-  cudaEvent_t next_event() {
-    if (ev_used == ev_pool.size()) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      ev_pool.push_back(e);
-    }
-    return ev_pool[ev_used++];
-  }
-  void mark(int slot) {  // slot 0..3 of the current set
-    if (!opt_time) return;
-    cudaEventRecord(next_event(), stream);
-    (void)slot;
-  }
-  void resolve_timers() {
-    for (size_t i = 0; i + 4 <= ev_used; i += 4) {
-      float a = 0, b = 0, c = 0;
-      cudaEventSynchronize(ev_pool[i + 3]);
-      cudaEventElapsedTime(&a, ev_pool[i], ev_pool[i + 1]);
-      cudaEventElapsedTime(&b, ev_pool[i + 1], ev_pool[i + 2]);
-      cudaEventElapsedTime(&c, ev_pool[i + 2], ev_pool[i + 3]);
-      acc_assign += a;
-      acc_scan += b;
-      acc_fin += c;
-      ++timed_calls;
-    }
-    ev_used = 0;
-  }
-  ~hivf_ctx() {
-    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-    for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq,
-                    &pl, &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items,
-                    &n_items, &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &qin,
-                    &x_ids, &x_d, &x_cnt, &x_tot, &tau, &flags2, &qbound, &rep_entries, &rep_n, &rep_cnt,
-                    &rep_d, &rep_ids, &qshift, &qwide})
-      b->release();
-    hstage.release();
-    if (sgraph.exec) cudaGraphExecDestroy(sgraph.exec);
-    if (own_stream && stream) cudaStreamDestroy(stream);
-  }
-};
-
-struct hivf_index {
-  hivf_ctx* ctx = nullptr;
-  uint32_t dim = 0, dpad = 0, K = 0;
-  int metric = 0;
-  uint64_t N = 0;
-  std::vector<uint64_t> list_off;  // host copy
-  float* vec = nullptr;
-  uint64_t* ids = nullptr;
-  float* xnorm2 = nullptr;
-  uint64_t* d_list_off = nullptr;
-  uint32_t* maxnorm_bits = nullptr;
-  float* cent = nullptr;
-  float* cnorm2 = nullptr;
-  float* cnorm = nullptr;
-  uint32_t* list_order = nullptr;
-  int* d_err = nullptr;
-  uint64_t rows_added = 0;
-  bool finished = false;
-  double mean_assigned = -1.0;
-  uint32_t seg_rows = 4096, s_max = 1;
-  std::vector<uint8_t> resident;
-  // locator (doc id -> row), built on the first hivf_index_locate
-  uint64_t* loc_ids = nullptr;
-  uint64_t* loc_rows = nullptr;
-  // ---- tiered residency (hivf_residency_set) ----
-  bool tiered = false;           // vec is pinned host memory, hot lists copied into pool
-  float* pool = nullptr;         // HBM slots for resident lists
-  uint64_t pool_bytes = 0;
-  const float** d_list_ptr = nullptr;  // device table read by the kernels
-  std::vector<uint64_t> slot_off;      // per list: byte offset in pool, or ~0
-  std::vector<std::pair<uint64_t, uint64_t>> free_ext;  // free (offset, size) extents
-  std::vector<uint8_t> swap_in;        // per list: copy in flight
-  struct Swap {
-    cudaEvent_t done;
-    std::vector<uint32_t> lists;
-  };
-  std::vector<Swap> swaps;             // in flight, oldest first
-  cudaStream_t copy_stream = nullptr;
-  uint64_t swapped_in_bytes = 0;
-  uint64_t list_bytes(uint32_t c) const { return (list_off[c + 1] - list_off[c]) * dpad * 4; }
-  int auto_split = 0;  // auto policy: 0 single-pass tf32, 1 split-precision
-  uint32_t adapt_seen = 0, adapt_fallback = 0;
-  // scan kernel for the next call: 1 FFMA, 2 tensor-core split, 3 tensor-core single pass
-  int scan_kind() const;
-  IndexView view() const { return view_kind(scan_kind()); }
-  // view carrying the filter bound of scan kernel `kind`
-  IndexView view_kind(int kind) const {
-    IndexView v{};
-    if (kind == 2) bound_tc(dim, &v.e_a, &v.e_b, &v.e_c);
-    else if (kind == 3) bound_tc1(dim, &v.e_a, &v.e_b, &v.e_c);
-    else bound_ffma(dim, &v.e_a, &v.e_b, &v.e_c);
-    v.vec = vec;
-    v.list_ptr = tiered ? d_list_ptr : nullptr;
-    v.ids = ids;
-    v.xnorm2 = xnorm2;
-    v.list_off = d_list_off;
-    v.maxnorm = reinterpret_cast<const float*>(maxnorm_bits);
-    v.cent = cent;
-    v.cnorm2 = cnorm2;
-    v.cnorm = cnorm;
-    v.list_order = list_order;
-    v.dim = dim;
-    v.dpad = dpad;
-    v.K = K;
-    v.N = N;
-    v.seg_rows = seg_rows;
-    v.s_max = s_max;
-    v.metric = metric;
-    return v;
-  }
-  ~hivf_index() {
-    if (copy_stream) cudaStreamSynchronize(copy_stream);
-    for (auto& w : swaps) cudaEventDestroy(w.done);
-    if (copy_stream) cudaStreamDestroy(copy_stream);
-    if (tiered && vec) cudaFreeHost(vec);
-    else if (vec) cudaFree(vec);
-    for (void* p : {(void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
-                    (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err, (void*)pool,
-                    (void*)d_list_ptr, (void*)loc_ids, (void*)loc_rows})
-      if (p) cudaFree(p);
-  }
-};
+}  // namespace hivf
 
 int hivf_index::scan_kind() const {
   const int k = ctx->opt_scan_kernel;
   if (k == 1) return 1;
-  if (tc_conversion_mode() > 1) return 1;  // unknown tensor-core conversion: FFMA scan
+  if (ctx->tc_conv > 1) return 1;  // unknown tensor-core conversion: FFMA scan
   const int want = k == 2 ? 2 : k == 3 ? 3 : (auto_split ? 2 : 3);
-  if (scan_tc_qmax(dpad, want == 2) > 0) return want;
+  if (scan_tc_qmax(dpad, want == 2, 0.f, ctx->tc) > 0) return want;
   return 1;  // too wide for the tensor-core scan
 }
 
@@ -423,7 +172,7 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
     }
     c->own_stream = true;
   }
-  if (tc_conversion_mode() < 0) set_tc_conversion_mode(tc_probe_conversion(c->stream));
+  c->tc_conv = tc_conversion_mode();  // probed once per device
   *out = c;
   return HIVF_OK;
 }
@@ -431,7 +180,7 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
 hivf_status hivf_device_info(hivf_ctx* ctx, int* sm_count, int* tc_tf32_conversion) {
   if (!ctx) return fail(HIVF_EINVAL, "ctx is NULL");
   if (sm_count) *sm_count = ctx->sm_count;
-  if (tc_tf32_conversion) *tc_tf32_conversion = tc_conversion_mode();
+  if (tc_tf32_conversion) *tc_tf32_conversion = ctx->tc_conv;
   return HIVF_OK;
 }
 
@@ -486,13 +235,13 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   } else if (!strcmp(name, "tc_prof")) {  // debug: stall counters (hivf_debug_tc_prof)
     set_tc_prof((int)value);
   } else if (!strcmp(name, "tc_variant")) {  // debug only: results are inexact when != 0
-    set_tc_variant((int)value);
+    ctx->tc.variant = (int)value;
   } else if (!strcmp(name, "tc_qmax")) {  // tuning: queries per tensor-core work item
     if (value < 0 || (value > 32 && value != (int64_t)kTcWideQ) || value % 8)
       return fail(HIVF_EINVAL, "tc_qmax: 0, 8..32 step 8, or 64 (wide)");
-    set_tc_qmax((uint32_t)value);
+    ctx->tc.qmax_override = (uint32_t)value;
   } else if (!strcmp(name, "tc_wide_ppl")) {  // tuning: probes/list above which dense batches use
-    set_tc_wide_ppl((float)value);             // the wide (64-query) scan; negative = never
+    ctx->tc.wide_ppl = (float)value;           // the wide (64-query) scan; negative = never
   } else if (!strcmp(name, "time_kernels")) {
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->resolve_timers();
@@ -973,7 +722,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   const bool tc = kind != 1;
   // batch density estimate (host-side, no sync): pairs per list of the index
   float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
-  uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl) : (uint32_t)kQMax;
+  uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc) : (uint32_t)kQMax;
   WideStage ws;
   if (group == kTcWideQ) {
     // the restaged queries need (pairs + 7K) x D floats; when HBM is short
@@ -982,7 +731,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
         c->qwide.ensure((size_t)wide_stage_rows(n_pairs, ix->K) * ix->dpad * 4) != cudaSuccess) {
       (void)cudaGetLastError();
       ppl = 0.f;
-      group = scan_tc_qmax(ix->dpad, kind == 2, ppl);
+      group = scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc);
       if (group == kTcWideQ) return fail(HIVF_ENOMEM, "wide scan: query staging buffer");
     } else {
       ws.qshift = c->qshift.as<uint32_t>();
@@ -1011,7 +760,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
                    c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),
                    c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), ctas,
                    kind == 2, topk ? c->qbound.as<float>() : nullptr, topk, item_bounds ? 0 : 1, ppl,
-                   ws, c->stream);
+                   ws, c->tc, c->stream);
   else
     launch_scan(v, qv, c->items.as<ScanItem>(), c->n_items.as<uint32_t>(), c->work_ctr.as<uint32_t>(),
                 c->sorted_pairs.as<uint32_t>(), c->pq.as<uint32_t>(), c->cand_d.as<float>(),

@@ -382,13 +382,7 @@ void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t d
 }
 
 void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sm_count();
   const uint32_t qt = (qv.n + CT_Q - 1) / CT_Q;
   auto tiles = [&](uint32_t ctc) { return (uint64_t)((ix.K + ctc - 1) / ctc) * qt; };
   if (tiles(128) >= 2ull * sms)
@@ -403,13 +397,8 @@ void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float*
                           uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s) {
   const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_coarse_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_coarse_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr_set = true;
-  }
+  smem_optin((const void*)k_coarse_select, 220 * 1024);
+  smem_optin((const void*)k_coarse_fallback, 200 * 1024);
   // 512 threads: fewer (64-256, sized to the candidate count) measured slower
   // (C2 41 -> 61 us, C3 59 -> 75 us)
   k_coarse_select<<<qv.n, 512, smem, s>>>(ix, qv, dist32, nprobe, filter_eps(ix.dim),

@@ -654,18 +654,21 @@ __global__ void k_plans_to_pairs(const uint32_t* plans, uint32_t n, uint32_t npr
 }
 
 // merge_topk (vector_index.cpp:71-91) over n_parts exact per-shard lists.
+// Part p's arrays start at ids + p*s_ids, d + p*s_d, counts + p*s_cnt (an
+// all-gather of separate arrays, or of one packed ids|dists|counts block per rank).
 __global__ void k_merge_parts(uint32_t n_parts, uint32_t nq, uint32_t k, const uint64_t* ids,
                               const double* d, const uint32_t* counts, uint64_t* ids_out,
-                              double* d_out, uint32_t* counts_out, uint32_t cap) {
+                              double* d_out, uint32_t* counts_out, uint32_t cap, uint64_t s_ids,
+                              uint64_t s_d, uint64_t s_cnt) {
   extern __shared__ __align__(16) uint8_t sm[];
   double* bd = reinterpret_cast<double*>(sm);
   uint64_t* bi = reinterpret_cast<uint64_t*>(bd + cap);
   const uint32_t b = blockIdx.x;
   for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
     const uint32_t part = i / k, e = i % k;
-    bool ok = part < n_parts && e < counts[(uint64_t)part * nq + b];
-    bd[i] = ok ? d[((uint64_t)part * nq + b) * k + e] : DBL_MAX;
-    bi[i] = ok ? ids[((uint64_t)part * nq + b) * k + e] : ~0ull;
+    bool ok = part < n_parts && e < counts[(uint64_t)part * s_cnt + b];
+    bd[i] = ok ? d[(uint64_t)part * s_d + (uint64_t)b * k + e] : DBL_MAX;
+    bi[i] = ok ? ids[(uint64_t)part * s_ids + (uint64_t)b * k + e] : ~0ull;
   }
   block_sort_pairs(bd, bi, cap);
   // collapse duplicate ids to the minimum distance: after the (d, id) sort the
@@ -712,12 +715,7 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
   const RepairState R = rep ? *rep : RepairState{};
   const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 8 + (size_t)nprobe * 16 + 4 +
                       (size_t)kSlotCap * (4 + 4 + 4 + kKP * 4);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_finalize_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_exact_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_finalize_search, 200 * 1024);
   k_finalize_search<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row,
                                                     cand_thr, cand_n, filter_eps(ix.dim),
                                                     filter_abs(ix.dim), ids_out, d_out,
@@ -740,20 +738,10 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
   uint32_t cap = 512;
   while (cap < k + 256) cap <<= 1;
   const size_t smem = (size_t)cap * 16 + (size_t)ix.dpad * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_exact_search, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_exact_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_exact_search, 200 * 1024);
+  smem_optin((const void*)k_exact_merge, 200 * 1024);
   const uint32_t ns = part_ids ? exact_search_parts(nprobe, k) : 1;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sm_count();
   const uint32_t gx = std::max(1u, std::min(qv.n, (uint32_t)(4 * sms) / ns));
   if (ns <= 1) {
     k_exact_search<<<dim3(gx, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
@@ -775,13 +763,21 @@ void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const 
   uint32_t cap = 1;
   while (cap < n_parts * k) cap <<= 1;
   const size_t smem = (size_t)cap * 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_merge_parts, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_merge_parts, 200 * 1024);
   k_merge_parts<<<n_queries, 256, smem, s>>>(n_parts, n_queries, k, ids, d, counts, ids_out, d_out,
-                                             counts_out, cap);
+                                             counts_out, cap, (uint64_t)n_queries * k,
+                                             (uint64_t)n_queries * k, n_queries);
+}
+
+void launch_merge_parts_strided(uint32_t n_parts, uint32_t n_queries, uint32_t k, const uint64_t* ids,
+                                const double* d, const uint32_t* counts, uint64_t s_ids, uint64_t s_d,
+                                uint64_t s_cnt, uint64_t* ids_out, double* d_out, uint32_t* counts_out,
+                                cudaStream_t s) {
+  uint32_t cap = 1;
+  while (cap < n_parts * k) cap <<= 1;
+  smem_optin((const void*)k_merge_parts, 200 * 1024);
+  k_merge_parts<<<n_queries, 256, (size_t)cap * 16, s>>>(n_parts, n_queries, k, ids, d, counts, ids_out,
+                                                         d_out, counts_out, cap, s_ids, s_d, s_cnt);
 }
 
 // Node-split sub-search finalize lives in items.cu.
@@ -795,11 +791,7 @@ void launch_repair(const IndexView& ix, const QueryView& qv, const uint32_t* pla
   bound_ffma(ix.dim, &fa, &fb, &fc);
   k_repair_segments<<<n_ctas, 256, 0, s>>>(ix, qv, plans, nprobe, R, tau, fa, fb, fc, flags);
   const size_t smem = (size_t)2 * kCandMax * 16 + (size_t)kCandMax * 8 + (size_t)ix.dpad * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_finalize_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_finalize_repair, 200 * 1024);
   k_finalize_repair<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row, cand_thr,
                                                     cand_n, tau, R, ids_out, d_out, counts_out, flags);
 }

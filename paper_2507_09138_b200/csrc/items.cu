@@ -332,12 +332,7 @@ void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_
                            cudaStream_t s) {
   if (!n_items) return;
   const size_t smem = (size_t)kItCand * (8 + 8 + 4 + 4) + (kNprobeMax + 1) * 4 + (size_t)ix.dpad * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_finalize_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_exact_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_finalize_items, 220 * 1024);
   k_finalize_items<<<n_items, kItThreads, smem, s>>>(ix, qv, n_items, item_off, clusters, k, cand_d,
                                                      cand_row, cand_thr, cand_n, filter_eps(ix.dim),
                                                      filter_abs(ix.dim), heap_ids, heap_d, heap_n,
@@ -351,11 +346,7 @@ void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_ite
                         cudaStream_t s) {
   if (!n_items) return;
   const size_t smem = (size_t)(kExactMaxK + 1) * 16 + 256 * 16 + (size_t)ix.dpad * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_exact_items, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_exact_items, 128 * 1024);
   k_exact_items<<<n_items, 256, smem, s>>>(ix, qv, n_items, item_off, clusters, k, heap_ids, heap_d,
                                            heap_n, heap_stride, changed, flags);
 }

@@ -7,6 +7,23 @@
 
 namespace hivf {
 
+// ---- devattr.cu: per-device launch attributes (a process may drive several
+// GPUs; the opt-in and the SM count are per device, keyed by the current one)
+constexpr int kMaxDevices = 64;
+int current_device();
+int device_sm_count();
+cudaError_t smem_optin(const void* kernel, int bytes);
+
+// Tensor-core scan options of one context (hivf_set_option), passed by value
+// to the scan launcher -- never process globals, so contexts on different
+// devices (or with different tuning) do not interfere.
+struct TcOpts {
+  uint32_t qmax_override = 0;  // "tc_qmax": 0 auto
+  float wide_ppl = 0.f;        // "tc_wide_ppl": probes/list above which the wide scan runs; < 0 never
+  int variant = 0;             // "tc_variant" (debug, inexact when nonzero)
+};
+float tc_wide_ppl_default();   // env HIVF_TC_WIDE_PPL, else 0
+
 // One grouped-scan work item: rows [row0, row0+nrows) of list `list` (local
 // row numbers) against up to kQMax queries listed in item_pairs[pair0, pair0+nq).
 struct ScanItem {
@@ -122,21 +139,19 @@ uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists);
 void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,
                        const uint32_t* pair_query, const uint32_t* pair_list, const uint32_t* pair_off,
                        const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s);
-void set_tc_wide_ppl(float v);
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    int bound_update, float probes_per_list, const WideStage& ws, cudaStream_t s);
+                    int bound_update, float probes_per_list, const WideStage& ws, const TcOpts& o,
+                    cudaStream_t s);
 // queries per tensor-core work item; probes_per_list = the batch's pairs / lists
-uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list = 0.f);
-void set_tc_qmax(uint32_t q);  // tuning override (0 = auto)
-int tc_probe_conversion(cudaStream_t s);  // 0 trunc, 1 RNE, 2 unsupported
-void set_tc_conversion_mode(int m);
-void set_tc_variant(int v);  // debug knob (inexact results when nonzero)
-void set_tc_prof(int on);    // debug: per-CTA stall counters in k_scan_tc
+uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list, const TcOpts& o);
+// fp32->tf32 operand conversion of the current device's tensor cores, probed
+// once per device (0 trunc, 1 RNE, 2 unsupported -> FFMA scan)
 int tc_conversion_mode();
-int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list = 0.f);
+void set_tc_prof(int on);    // debug: per-CTA stall counters in k_scan_tc (process-wide)
+int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list, const TcOpts& o);
 void bound_ffma(uint32_t dim, double* a, double* b, double* c);
 void bound_tc(uint32_t dim, double* a, double* b, double* c);   // 3-pass split
 void bound_tc1(uint32_t dim, double* a, double* b, double* c);  // single pass
@@ -206,6 +221,17 @@ void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_ite
 void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const uint64_t* ids,
                         const double* d, const uint32_t* counts, uint64_t* ids_out,
                         double* d_out, uint32_t* counts_out, cudaStream_t s);
+
+void launch_merge_parts_strided(uint32_t n_parts, uint32_t n_queries, uint32_t k, const uint64_t* ids,
+                                const double* d, const uint32_t* counts, uint64_t s_ids, uint64_t s_d,
+                                uint64_t s_cnt, uint64_t* ids_out, double* d_out, uint32_t* counts_out,
+                                cudaStream_t s);
+// shard.cu: device-side all-gather over peer pointers (in-process shard group)
+constexpr int kMaxGroup = 16;
+struct PeerSrc {
+  const void* src[kMaxGroup];
+};
+void launch_gather_peer(const PeerSrc& src, uint32_t n_src, uint64_t bytes_each, void* dst, cudaStream_t s);
 
 constexpr uint32_t kExactMaxK = 1024;     // exact-path heap bound
 constexpr uint32_t kNprobeMax = 4096;     // exact coarse-assign bound

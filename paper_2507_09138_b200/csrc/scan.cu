@@ -491,11 +491,7 @@ void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* 
   (void)list_cursor;
   if (ix.K <= kFusedK && n_pairs <= 8192u) {  // C3 (32k pairs) is faster on the 4-kernel chain
     const size_t smem = (size_t)ix.K * 12;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_worklist_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kFusedK * 12));
-      attr = true;
-    }
+    smem_optin((const void*)k_worklist_fused, (int)(kFusedK * 12));
     k_worklist_fused<<<1, 1024, smem, s>>>(ix, group, pair_list, n_pairs, list_cnt, list_pair_off,
                                            list_item_off, sorted_pairs, items, n_items, work_ctr, qshift);
     return;
@@ -516,11 +512,7 @@ void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items
                  uint32_t* out_n, int n_ctas, cudaStream_t s) {
   ScanParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr, out_n};
   const int smem = scan_smem_bytes(ix.dpad);
-  static int attr_bytes = 0;
-  if (attr_bytes < smem) {
-    cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_bytes = smem;
-  }
+  smem_optin((const void*)k_scan, smem);
   k_scan<<<n_ctas, (kScanWarps + 1) * 32, smem, s>>>(P);
 }
 

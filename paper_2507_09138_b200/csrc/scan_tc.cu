@@ -37,6 +37,7 @@
 //   warps 6-9 epilogue: tcgen05.ld of the tile (one row per thread, one column
 //            per query), fp32 expansion distance, per-warp register top-32 per
 //            query; at item end a bitonic merge across the four warps.
+#include <mutex>
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
@@ -865,19 +866,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
 // Dynamic smem budget = the device's opt-in per-block maximum (227 KB on B200)
 // minus the kernel's static __shared__ variables, queried once.
 static int tc_budget() {
-  static int budget = -1;
-  if (budget < 0) {
-    int dev = 0, optin = 232448;
-    cudaGetDevice(&dev);
+  static int budget[kMaxDevices];
+  static bool have[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 0;
+  if (!have[dev]) {  // benign race: every thread computes the same value
+    int optin = 232448;
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
       optin = 232448;
     size_t st = 1024;
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, k_scan_tc<false>) == cudaSuccess) st = fa.sharedSizeBytes;
     if (cudaFuncGetAttributes(&fa, k_scan_tc<true>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
-    budget = optin - (int)st;
+    budget[dev] = optin - (int)st;
+    have[dev] = true;
   }
-  return budget;
+  return budget[dev];
 }
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
   const bool wide = qmax == kTcWideQ;  // no resident query group; two merge groups of 8
@@ -891,27 +895,22 @@ static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int sb = kTcStageBytes + (qmax == kTcWideQ ? kWideQBytes : 0);
   return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / sb);
 }
-static uint32_t g_tc_qmax_override = 0;
-void set_tc_qmax(uint32_t q) { g_tc_qmax_override = q; }
-
 // option "tc_wide_ppl" (env HIVF_TC_WIDE_PPL sets the process default): the
 // probes-per-list density above which single-pass batches use the wide scan
 // (< 0: never).  Default 0: alternating A/B runs on one box measured the wide
 // scan faster at every density (C1 scan 36.6 -> 33.2 us, C2 0.463 -> 0.450 ms,
 // C3 B=64 8.01 -> 7.94 ms, B=256 8.81 -> 8.72 ms, B=1024 16.3 -> 10.3 ms).
-static float env_wide_ppl() {
+float tc_wide_ppl_default() {
   const char* e = getenv("HIVF_TC_WIDE_PPL");
   return e ? (float)atof(e) : 0.f;
 }
-static float g_tc_wide_ppl = env_wide_ppl();
-void set_tc_wide_ppl(float v) { g_tc_wide_ppl = v; }
 
-uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list) {
-  const uint32_t o = g_tc_qmax_override;
+uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list, const TcOpts& opt) {
+  const uint32_t o = opt.qmax_override;
   if (o && (o != kTcWideQ || !split) && tc_ring(dpad, o, split) >= 2) return o;
   // dense batches, single pass: 64-query groups streamed with the list stages
   // (k_scan_tc<true>) -- each list tile crosses HBM->smem once per 64 probes
-  if (!split && g_tc_wide_ppl >= 0.f && probes_per_list > g_tc_wide_ppl && tc_ring(dpad, kTcWideQ, 0) >= 3)
+  if (!split && opt.wide_ppl >= 0.f && probes_per_list > opt.wide_ppl && tc_ring(dpad, kTcWideQ, 0) >= 3)
     return kTcWideQ;
   // HBM-bound batches (few probes per list): the widest group that still
   // leaves a 4-stage (128 KB) landing ring -- ring depth (bytes in flight per
@@ -926,8 +925,6 @@ uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list) {
   if (tc_ring(dpad, 8, split) >= 2) return 8;
   return 0;  // too wide for the tensor-core scan: caller uses the FFMA scan
 }
-static int g_tc_variant = 0;
-void set_tc_variant(int v) { g_tc_variant = v; }
 static unsigned long long* g_tc_prof = nullptr;  // debug stall counters (option "tc_prof")
 void set_tc_prof(int on) {
   if (on && !g_tc_prof) cudaMalloc(&g_tc_prof, 1024 * 16 * sizeof(unsigned long long));
@@ -944,12 +941,8 @@ int get_tc_prof(unsigned long long* host, int n_ctas) {
   return 1;
 }
 
-static int g_tc_conv = -1;  // set by tc_probe_conversion()
-void set_tc_conversion_mode(int m) { g_tc_conv = m; }
-int tc_conversion_mode() { return g_tc_conv; }
-
-int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list) {
-  const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list);
+int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list, const TcOpts& o) {
+  const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list, o);
   return tc_fixed_bytes(dpad, q, split) +
          (int)tc_ring(dpad, q, split) * (kTcStageBytes + (q == kTcWideQ ? kWideQBytes : 0));
 }
@@ -958,20 +951,17 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     const uint32_t* n_items, uint32_t* work_ctr, const uint32_t* sorted_pairs,
                     const uint32_t* pair_query, float* out_d, uint32_t* out_row, float* out_thr,
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
-                    int bound_update, float probes_per_list, const WideStage& ws, cudaStream_t s) {
-  const uint32_t q = scan_tc_qmax(ix.dpad, split, probes_per_list);
+                    int bound_update, float probes_per_list, const WideStage& ws, const TcOpts& o,
+                    cudaStream_t s) {
+  const uint32_t q = scan_tc_qmax(ix.dpad, split, probes_per_list, o);
+  const int conv = tc_conversion_mode();
   const bool wide = q == kTcWideQ;
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
-             out_n, q, tc_ring(ix.dpad, q, split), g_tc_conv < 0 ? 0 : g_tc_conv, g_tc_variant,
+             out_n, q, tc_ring(ix.dpad, q, split), conv > 1 ? 0 : conv, o.variant,
              wide ? 0 : split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u,
              ws.qstage, ws.qshift};
-  const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list);
-  static int attr_bytes[2] = {0, 0};
-  if (attr_bytes[wide] < smem) {
-    cudaFuncSetAttribute(wide ? k_scan_tc<true> : k_scan_tc<false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_bytes[wide] = smem;
-  }
+  const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list, o);
+  smem_optin(wide ? (const void*)k_scan_tc<true> : (const void*)k_scan_tc<false>, smem);
   if (wide) k_scan_tc<true><<<n_ctas, kTcThreads, smem, s>>>(P);
   else k_scan_tc<false><<<n_ctas, kTcThreads, smem, s>>>(P);
 }
@@ -1086,16 +1076,36 @@ __global__ void __launch_bounds__(128, 1) k_tc_probe(int* out) {
 }
 }  // namespace
 
-int tc_probe_conversion(cudaStream_t s) {
+static int tc_probe_conversion() {
   int* d = nullptr;
   int h = 2;
-  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 2;
-  k_tc_probe<<<1, 128, 0, s>>>(d);
-  if (cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    h = 2;
-  cudaFree(d);
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return 2;
+  if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+    k_tc_probe<<<1, 128, 0, s>>>(d);
+    if (cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      h = 2;
+    cudaFree(d);
+  }
+  cudaStreamDestroy(s);
+  (void)cudaGetLastError();
   return h;
+}
+
+// probed once per device, on first use (hivf_ctx_create triggers it)
+int tc_conversion_mode() {
+  static std::mutex mu;
+  static int conv[kMaxDevices];
+  static bool have[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 2;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!have[dev]) {
+    conv[dev] = tc_probe_conversion();
+    have[dev] = true;
+  }
+  return conv[dev];
 }
 }  // namespace hivf
 

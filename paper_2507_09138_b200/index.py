@@ -307,3 +307,127 @@ class IvfIndex:
         out = np.zeros(self.k_clusters, np.uint8)
         check(lib().hivf_residency_get(self.h, out.ctypes.data))
         return out.astype(bool)
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU list sharding (include/hivf.h "multi-GPU list sharding")
+# ---------------------------------------------------------------------------
+
+def shard_plan(sizes, nranks, weights=None, n_striped=-1) -> np.ndarray:
+    """owner[c] = rank holding list c, or SHARD_STRIPED (rows split over all
+    ranks); frequency-weighted LPT (hivf_shard_plan)."""
+    sz = np.ascontiguousarray(sizes, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    owner = np.zeros(len(sz), np.uint32)
+    check(lib().hivf_shard_plan(sz.ctypes.data, None if w is None else w.ctypes.data, len(sz), nranks,
+                                int(n_striped), owner.ctypes.data))
+    return owner
+
+
+def shard_local_lists(list_offsets, owner, nranks, rank):
+    """(local_offsets [K+1], src_first [K]): rank's list c holds the global
+    list-order rows [src_first[c], src_first[c] + local size)."""
+    off = np.ascontiguousarray(list_offsets, np.uint64)
+    ow = np.ascontiguousarray(owner, np.uint32)
+    K = len(ow)
+    loc = np.zeros(K + 1, np.uint64)
+    first = np.zeros(K, np.uint64)
+    check(lib().hivf_shard_local_lists(off.ctypes.data, ow.ctypes.data, K, nranks, rank, loc.ctypes.data,
+                                       first.ctypes.data))
+    return loc, first
+
+
+def upload_shard(ctx: Context, centroids, list_offsets, vectors, ids, owner, nranks, rank,
+                 metric=METRIC_L2) -> IvfIndex:
+    """Rank `rank`'s shard of a host CSR index (hivf_index_upload_shard)."""
+    cents = np.ascontiguousarray(centroids, np.float32)
+    off = np.ascontiguousarray(list_offsets, np.uint64)
+    vec = np.ascontiguousarray(vectors, np.float32)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    ow = np.ascontiguousarray(owner, np.uint32)
+    K, dim = cents.shape
+    h = C.c_void_p()
+    check(lib().hivf_index_upload_shard(ctx.h, dim, metric, K, cents.ctypes.data, off.ctypes.data,
+                                        vec.ctypes.data if vec.size else None,
+                                        ids.ctypes.data if ids.size else None, ow.ctypes.data, nranks, rank,
+                                        C.byref(h)))
+    return IvfIndex(ctx, h, dim, K, metric)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().hivf_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class ShardGroup:
+    """Shards of one logical index searched as one (hivf_group): per batch a
+    slice assign per rank, plan all-gather, local exact search, result
+    exchange and device merge_topk."""
+
+    def __init__(self, handle, shards, keep=None):
+        self.h = handle
+        self.shards = shards
+        self._keep = keep  # ctypes callback / buffers the C side refers to
+
+    @staticmethod
+    def in_process(shards):
+        """One host thread drives every shard (one context each)."""
+        arr = (C.c_void_p * len(shards))(*[s.h.value for s in shards])
+        h = C.c_void_p()
+        check(lib().hivf_group_create(arr, len(shards), C.byref(h)))
+        return ShardGroup(h, list(shards))
+
+    @staticmethod
+    def nccl(shard, nranks, rank, unique_id: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib().hivf_group_create_nccl(shard.h, nranks, rank, buf, C.byref(h)))
+        return ShardGroup(h, [shard])
+
+    @staticmethod
+    def host_allgather(shard, nranks, rank, allgather):
+        """allgather(send: bytes) -> bytes of nranks blocks in rank order."""
+        from ._lib import ALLGATHER_FN
+
+        def cb(user, send, nbytes, recv):
+            try:
+                out = allgather(C.string_at(send, nbytes))
+                assert len(out) == nbytes * nranks
+                C.memmove(recv, out, len(out))
+                return 0
+            except Exception:  # reported as HIVF_ECOMM
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        fn = ALLGATHER_FN(cb)
+        h = C.c_void_p()
+        check(lib().hivf_group_create_hostcb(shard.h, nranks, rank, fn, None, C.byref(h)))
+        return ShardGroup(h, [shard], keep=fn)
+
+    def search(self, queries, nprobe, k):
+        dim = self.shards[0].dim
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, dim)
+        B = q.shape[0]
+        ids = np.zeros((B, k), np.uint64)
+        d = np.zeros((B, k), np.float64)
+        cnt = np.zeros(B, np.uint32)
+        check(lib().hivf_group_search(self.h, q.ctypes.data, B, nprobe, k, ids.ctypes.data, d.ctypes.data,
+                                      cnt.ctypes.data))
+        return ids, d, cnt
+
+    def search_device(self, d_queries, nprobe, k, ids_out, dists_out, counts_out):
+        check(lib().hivf_group_search_device(self.h, d_queries.data_ptr(), d_queries.shape[0], nprobe, k,
+                                             ids_out.data_ptr(), dists_out.data_ptr(), counts_out.data_ptr()))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hivf_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
