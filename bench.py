@@ -13,16 +13,24 @@ of one 256-query batch.  `value` = queries/s with queries already in HBM
 queries in, results out, copies inside the timed region).  The 64 GB index is
 far larger than the 126 MB L2, so no L2 flush is needed between steps.
 
-Multi-GPU (torchrun, one process per GPU): lists are sharded across ranks by
-LPT on bytes; each rank searches its shard (exact local top-k), the per-query
-candidates are all-gathered with NCCL and merged on device
-(hivf_merge_parts_device = merge_topk).  Total index size is fixed as N grows
-("scaling": "strong").
+Multi-GPU (torchrun, one process per GPU): the library's shard group
+(hivf_group_create_nccl): lists sharded by hivf_shard_plan (LPT on bytes, or
+on probe frequency x bytes for Zipf streams, hot lists striped), per batch a
+slice assign per rank, plan all-gather, exact local search, result
+all-gather over NCCL and a device merge_topk.  Total index size and batch are
+fixed as N grows ("scaling": "strong").
+
+Parity (`parity_sample`): the GPU outputs of the TIMED steps (one output set
+per pool batch) are compared bit-for-bit with the reference on a sample -- the
+full batch of two pool batches at C1/C2, 16-query chunks of pool batches 0..3
+(64 queries) at C3/C4 -- and the same reference runs are the `cpu_baseline`
+(16 queries per chunk = every host thread of the reference's execute works).
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref: /root/reference/proj sources compiled unmodified) on the box's
-host cores: make_cursor per query + RetrievalEngine::execute(live_math=true),
-on a restricted index holding every list probed by a fixed 16-query sample.
+host cores, on the same config and the same query chunks: make_cursor per
+query + RetrievalEngine::execute(live_math=true) on a restricted index holding
+every list the chunk probes.
 """
 from __future__ import annotations
 
@@ -172,34 +180,108 @@ def all_gather_parts(out, t):
 
 
 # ---------------------------------------------------------------------------
-# index construction (GPU, chunked, exact same data on every rank)
+# shared workload description (identical in both arms -> same_config)
 # ---------------------------------------------------------------------------
 
-def build_shard(wl, ctx, rank, world):
-    """Centroids + assignments on GPU, then pack this rank's lists into HBM."""
+def config_dict(cfg, args):
+    return {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
+            "k_clusters": cfg.k_clusters, "nprobe": cfg.nprobe, "k": cfg.k, "batch": cfg.batch,
+            "zipf": cfg.zipf, "query_pool_batches": args.pool,
+            "seeds": {"corpus": 1, "queries": 2},
+            "index": "train_centroids (Lloyd on a 48K-row sample) + compute_assignments over every row",
+            "l2": "index (%.1f GB) >> 126 MB L2: no flush needed" % (cfg.n * cfg.dim * 4 / 1e9)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def sample_plan(cfg, args):
+    """The queries the reference is timed / compared on: the full batch of pool
+    batches 0..1 when the whole index is small (C1/C2); otherwise 16 queries
+    (= host threads, so every core of the reference's execute works) from each
+    of pool batches 0..3, at a different row offset in every batch (C3/C4):
+    64 queries.  Returns [(pool batch, first row, n rows)]."""
+    small = cfg.n * cfg.dim * 4 <= 8e9
+    if small:
+        return [(j, 0, cfg.batch) for j in range(min(2, args.pool))]
+    S = max(1, min(args.cpu_sample, cfg.batch))
+    out = []
+    for j in range(min(4, args.pool)):
+        first = (j * (cfg.batch // 4)) % max(1, cfg.batch - S + 1)
+        out.append((j, first, S))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# index construction (GPU, chunked; the same data on every rank)
+# ---------------------------------------------------------------------------
+
+def list_weights(ix_cents_only, wl, cfg, n_batches=8, group=64):
+    """Expected scan passes per batch of every list (its probe frequency) from
+    a warm-up sample of the query stream (batches disjoint from the timed
+    pool): mean over batches of ceil(probes / group) -- the ClusterCacheState
+    frequency counter (tiered_cache.cpp:10-14) in bytes-streamed units."""
+    K = cfg.k_clusters
+    acc = np.zeros(K)
+    for i in range(n_batches):
+        p = ix_cents_only.select_clusters(wl.queries(100_000 + i).cpu().numpy(), cfg.nprobe)
+        cnt = np.bincount(p.ravel(), minlength=K)
+        acc += np.ceil(cnt / group)
+    w = acc / n_batches
+    return np.maximum(w, 0.5 / n_batches)  # never-seen lists still balance by size
+
+
+def build_index(wl, ctx, rank, world, cents=None, assign=None):
+    """Centroids (synthetic input) + library compute_assignments, shard plan
+    (hivf_shard_plan: frequency-weighted LPT + striped hot lists), and this
+    rank's lists packed into HBM (hivf_index_begin / add_rows_at / finish)."""
     import torch
-    from bench_workload import list_layout, shard_lists
-    from paper_2507_09138_b200 import IvfIndex
+    from bench_workload import CHUNK, list_layout
+    from paper_2507_09138_b200 import IvfIndex, shard_local_lists, shard_plan
     cfg = wl.cfg
+    info = {}
     t0 = time.time()
-    cents = wl.train_centroids()
-    assign = wl.assign_all(cents)
+    if cents is None:
+        cents = wl.train_centroids()
+    torch.cuda.synchronize()
+    info["centroids_s"] = round(time.time() - t0, 2)
+    t1 = time.time()
+    if assign is None:
+        assign = wl.library_assign(ctx, cents)
+    torch.cuda.synchronize()
+    info["compute_assignments_s"] = round(time.time() - t1, 2)
+    info["compute_assignments"] = "hivf_compute_assignments (libhivf), every row"
     off, pos, order = list_layout(assign, cfg.k_clusters)
-    sizes = (off[1:] - off[:-1]).cpu().numpy()
-    owner = shard_lists(sizes, world) if world > 1 else np.zeros(cfg.k_clusters, np.int64)
-    own_t = torch.from_numpy(owner == rank).to(wl.device)
-    # shard-local CSR: lists not owned by this rank are empty
-    my_sizes = torch.where(own_t, off[1:] - off[:-1], torch.zeros_like(off[1:]))
-    my_off = torch.zeros_like(off)
-    my_off[1:] = torch.cumsum(my_sizes, 0)
-    mine_row = own_t[assign]
-    # position of each owned row inside the shard CSR
-    local_pos = my_off[assign] + (pos - off[assign])
-    log(f"rank {rank}: centroids+assign {time.time() - t0:.1f}s; lists {cfg.k_clusters}, "
-        f"sizes min {sizes.min()} mean {sizes.mean():.0f} max {sizes.max()}")
+    sizes = (off[1:] - off[:-1]).cpu().numpy().astype(np.uint64)
+    weights = None
+    if world > 1 and cfg.zipf > 0:
+        probe = IvfIndex.build_scatter(ctx, cents, np.zeros(cfg.k_clusters + 1, np.uint64), 0, 0, iter(()))
+        weights = list_weights(probe, wl, cfg)
+        probe.close()
+    owner = shard_plan(sizes, world, weights=weights) if world > 1 else np.zeros(cfg.k_clusters, np.uint32)
+    off_np = off.cpu().numpy().astype(np.uint64)
+    loc_off, src_first = shard_local_lists(off_np, owner, world, rank)
+    lo_t = torch.from_numpy((src_first - off_np[:-1]).astype(np.int64)).to(wl.device)
+    nl_t = torch.from_numpy((loc_off[1:] - loc_off[:-1]).astype(np.int64)).to(wl.device)
+    lof_t = torch.from_numpy(loc_off[:-1].astype(np.int64)).to(wl.device)
+    rank_in_list = pos - off[assign]
+    rel = rank_in_list - lo_t[assign]
+    mine_row = (rel >= 0) & (rel < nl_t[assign])
+    local_pos = lof_t[assign] + rel
+    info["shard"] = {"ranks": world, "striped_lists": int((owner == 0xFFFFFFFF).sum()),
+                     "weights": "probe frequency (warm-up batches)" if weights is not None else "bytes"}
+    log(f"rank {rank}: centroids {info['centroids_s']}s, compute_assignments {info['compute_assignments_s']}s; "
+        f"lists {cfg.k_clusters}, sizes min {sizes.min()} mean {sizes.mean():.0f} max {sizes.max()}")
 
     def chunks():
-        from bench_workload import CHUNK
         for ci in range(wl.n_chunks()):
             rows = wl.chunk(ci)
             sl = slice(ci * CHUNK, ci * CHUNK + rows.shape[0])
@@ -215,12 +297,158 @@ def build_shard(wl, ctx, rank, world):
             if rows.shape[0]:
                 yield p, rows, ids
 
-    t1 = time.time()
-    torch.cuda.empty_cache()  # k-means / assignment temporaries -> back to the driver for the lists
-    ix = IvfIndex.build_scatter(ctx, cents, my_off.cpu().numpy().astype(np.uint64), 0,
-                                int(my_off[-1].item()), chunks())
-    log(f"rank {rank}: packed {int(my_off[-1].item())} rows into HBM in {time.time() - t1:.1f}s")
-    return ix, cents, sizes, owner, assign, order, off
+    t2 = time.time()
+    torch.cuda.empty_cache()
+    n_loc = int(loc_off[-1])
+    ix = IvfIndex.build_scatter(ctx, cents, loc_off, 0, n_loc, chunks())
+    info["pack_s"] = round(time.time() - t2, 2)
+    info["local_rows"] = n_loc
+    log(f"rank {rank}: packed {n_loc} rows into HBM in {info['pack_s']}s")
+    local_sizes = (loc_off[1:] - loc_off[:-1]).astype(np.uint64)
+    return ix, cents, sizes, local_sizes, owner, assign, info
+
+
+def make_group(ix, rank, world):
+    """The library's shard group for this rank: NCCL (one process per GPU), or
+    the host all-gather transport for the HIVF_DIST_BACKEND=gloo simulation."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_09138_b200 import ShardGroup, nccl_unique_id
+    if DIST_BACKEND == "nccl":
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return ShardGroup.nccl(ix, world, rank, obj[0])
+
+    def allgather(send: bytes) -> bytes:
+        t = torch.frombuffer(bytearray(send), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return b"".join(bytes(o.numpy()) for o in out)
+    return ShardGroup.host_allgather(ix, world, rank, allgather)
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path on a sample (parity + cpu_baseline)
+# ---------------------------------------------------------------------------
+
+def restricted_ref_index(ix, cents_np, lists, local_sizes):
+    """The reference's IvfIndex holding only `lists` (their rows read back from
+    HBM in list order, i.e. index_from_assignments order); select_clusters only
+    reads centroids, so searches whose plans these lists cover equal the full
+    index's (ref_index_from_csr, oracle/ref_shim.cpp)."""
+    import oracle
+    K = cents_np.shape[0]
+    dim = cents_np.shape[1]
+    off = np.zeros(K + 1, np.uint64)
+    sz = np.zeros(K, np.uint64)
+    sz[lists] = local_sizes[lists]
+    off[1:] = np.cumsum(sz)
+    gl_off = np.zeros(K + 1, np.uint64)
+    gl_off[1:] = np.cumsum(local_sizes)
+    T = int(off[-1])
+    vec = np.empty((T, dim), np.float32)
+    ids = np.empty(T, np.uint64)
+    for c in lists:
+        n = int(sz[c])
+        if n:
+            ix.get_rows_into(int(gl_off[c]), n, vec[int(off[c]):int(off[c]) + n], ids[int(off[c]):int(off[c]) + n])
+    ri = oracle.RefIndex.from_csr(cents_np, off, vec, ids)
+    del vec, ids
+    return ri, T
+
+
+def reference_on_sample(ix, cents, cfg, args, pool_np, local_sizes, outs=None, time_it=True):
+    """For every sample chunk: restricted reference index, the reference's
+    make_cursor x S + RetrievalEngine::execute(live_math=true) (timed), and a
+    bit-exact comparison with the rows of the TIMED batch's GPU outputs."""
+    import oracle
+    cents_np = cents.cpu().numpy()
+    nproc = os.cpu_count() or 1
+    tot_ms = 0.0
+    tot_q = 0
+    exact = True
+    mism = 0
+    parts = []
+    rows_total = 0
+    results = []
+    for (j, first, S) in sample_plan(cfg, args):
+        Q = pool_np[j][first:first + S]
+        plans = ix.select_clusters(Q, cfg.nprobe)
+        lists = np.unique(plans)
+        t0 = time.time()
+        ri, T = restricted_ref_index(ix, cents_np, lists, local_sizes)
+        t_build = time.time() - t0
+        ms, oi, od, oc = ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
+        del ri
+        tot_ms += ms
+        tot_q += S
+        rows_total += T
+        results.append((j, first, S, oi, od, oc))
+        if outs is not None:
+            gi, gd, gc = (t[first:first + S] for t in outs[j])
+            ok = (np.array_equal(gc, oc) and np.array_equal(gi, oi)
+                  and np.array_equal(gd.view(np.uint64), od.view(np.uint64)))
+            exact &= ok
+            mism += int((~(gi == oi).all(1)).sum() + (gc != oc).sum())
+        parts.append({"pool_batch": j, "rows": [first, first + S], "lists": int(len(lists)),
+                      "index_rows": T, "execute_ms": round(ms, 1), "index_build_s": round(t_build, 1)})
+        log(f"reference sample: batch {j} rows {first}:{first + S}: {len(lists)} lists, {T} rows, "
+            f"execute {ms / 1e3:.2f}s (index {t_build:.1f}s)")
+    info = {"queries": tot_q, "chunks": parts, "ms": tot_ms,
+            "threads_used": min(max(S for _, _, S in sample_plan(cfg, args)), nproc), "nproc": nproc,
+            "cpu_model": cpu_model()}
+    parity = None
+    if outs is not None:
+        parity = {"queries": tot_q, "batch": cfg.batch, "from_timed_batch": True,
+                  "pool_batches": sorted({j for j, _, _ in sample_plan(cfg, args)}),
+                  "bit_exact": bool(exact), "mismatched_queries": mism,
+                  "nprobe": cfg.nprobe, "k": cfg.k,
+                  "method": "GPU outputs of the timed steps vs the reference (oracle/_ref) make_cursor + "
+                            "RetrievalEngine::execute on a restricted index of the probed lists"}
+    return info, parity, results
+
+
+def cpu_baseline_line(info, cfg):
+    return {"value": round(info["queries"] / (info["ms"] / 1e3), 3), "unit": UNIT,
+            "cores": info["threads_used"], "threads_used": info["threads_used"], "nproc": info["nproc"],
+            "cpu_model": info["cpu_model"], "kind": "reference",
+            "sample": f"{info['queries']} queries of the timed workload in {len(info['chunks'])} chunks "
+                      f"({', '.join(str(c['pool_batch']) + ':' + str(c['rows'][0]) + '-' + str(c['rows'][1]) for c in info['chunks'])}"
+                      f"; full plans, nprobe={cfg.nprobe}, k={cfg.k}); per chunk make_cursor x S + "
+                      f"RetrievalEngine::execute(live_math=true) over a restricted index of the probed lists"}
+
+
+def sharded_parity(ix, cents, cfg, args, pool_np, local_sizes, outs, rank, world):
+    """N>1: every rank runs the reference on its own shard for the sample
+    queries (exact local top-k), rank 0 folds the parts with the reference's
+    merge_topk and compares with the merged GPU outputs of the timed steps."""
+    import torch.distributed as dist
+    import oracle
+    if not oracle.ref_available():
+        return None
+    _, _, res = reference_on_sample(ix, cents, cfg, args, pool_np, local_sizes, None)
+    local = [[[(int(oi[b, e]), float(od[b, e])) for e in range(int(oc[b]))] for b in range(S)]
+             for (_, _, S, oi, od, oc) in res]
+    parts = [None] * world
+    dist.all_gather_object(parts, local)
+    if rank != 0:
+        return None
+    exact = True
+    nq = 0
+    for ci, (j, first, S, _, _, _) in enumerate(res):
+        gi, gd, gc = (t[first:first + S] for t in outs[j])
+        for b in range(S):
+            ref = []
+            for r in range(world):
+                ref = oracle.merge_topk(ref, parts[r][ci][b], cfg.k)
+            got = [(int(gi[b, e]), float(gd[b, e])) for e in range(int(gc[b]))]
+            exact &= [(i, np.float64(d).view(np.uint64)) for i, d in ref] == \
+                     [(i, np.float64(d).view(np.uint64)) for i, d in got]
+            nq += 1
+    return {"queries": nq, "batch": cfg.batch, "from_timed_batch": True, "bit_exact": bool(exact),
+            "nprobe": cfg.nprobe, "k": cfg.k,
+            "method": f"reference search per shard ({world} shards) + merge_topk vs the merged GPU "
+                      "outputs of the timed steps (hivf_group_search_device)"}
 
 
 # ---------------------------------------------------------------------------
@@ -242,119 +470,64 @@ def run_hivf(args):
     for kv in filter(None, os.environ.get("HIVF_OPTS", "").split(",")):
         name, val = kv.split("=")
         ctx.set_option(name.strip(), int(val))
-    # --shard R/N: single-GPU measurement of rank R's shard of an N-GPU job (the
-    # local search only; the all-gather + merge of the real N-GPU step is not run)
-    shard_r, shard_n = (int(x) for x in args.shard.split("/")) if args.shard else (rank, world)
+    if args.shard:
+        return run_shard_sweep(args, wl, ctx, cfg)
     if args.hbm_budget_gb > 0:  # tiered residency: lists in pinned host memory, hot set in HBM
         ctx.set_option("hbm_list_budget", int(args.hbm_budget_gb * 1e9))
-    ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, shard_r, shard_n)
+    ix, cents, sizes, local_sizes, owner, assign, build_info = build_index(wl, ctx, rank, world)
+    del assign
     B, npb, k = cfg.batch, cfg.nprobe, cfg.k
     pool = [wl.queries(i) for i in range(args.pool)]
-    residency = None
-    if args.hbm_budget_gb > 0:
-        # the ClusterCacheState target (tiered_cache.cpp:23-36): lists by access
-        # frequency over the stream (distinct lists per batch), desc, ties by id
-        t0 = time.time()
-        freq = np.zeros(cfg.k_clusters, np.int64)
-        plan_np = [ix.select_clusters(q.cpu().numpy(), npb) for q in pool]
-        for p in plan_np:
-            freq[np.unique(p)] += 1
-        hot = np.lexsort((np.arange(cfg.k_clusters), -freq)).astype(np.uint32)
-        hot = hot[freq[hot] > 0]
-        ix.set_residency(hot)
-        ix.residency_sync()
-        res = ix.residency()
-        lb = sizes.astype(np.float64) * ((cfg.dim + 15) // 16 * 16) * 4
-        scanned = np.zeros(cfg.k_clusters, bool)
-        hit = tot = 0.0
-        for p in plan_np:
-            u = np.unique(p)
-            tot += lb[u].sum()
-            hit += lb[u][res[u]].sum()
-        residency = {"hbm_list_budget_gb": args.hbm_budget_gb,
-                     "index_list_gb": round(float(lb.sum()) / 1e9, 2),
-                     "resident_lists": int(res.sum()), "resident_gb": round(float(lb[res].sum()) / 1e9, 2),
-                     "scanned_bytes_from_hbm": round(hit / max(tot, 1.0), 4),
-                     "policy": "top lists by access frequency over the query stream (freq desc, id asc)",
-                     "swap_in_s": round(time.time() - t0, 2)}
-        log(f"residency: {residency}")
-    # one packed result buffer per rank (ids | dists | counts) so the shard
-    # exchange is a single all-gather
-    Bk = B * k
-    packed = torch.empty(2 * Bk + (B + 1) // 2, dtype=torch.int64, device=wl.device)
-    ids = packed[:Bk].view(B, k)
-    dd = packed[Bk:2 * Bk].view(torch.float64).view(B, k)
-    cnt = packed[2 * Bk:].view(torch.int32)[:B]
-    split_assign = world > 1 and B % world == 0
-    if world > 1:
-        g_packed = torch.empty(world, packed.numel(), dtype=torch.int64, device=wl.device)
-        g_ids = torch.empty(world, B, k, dtype=torch.int64, device=wl.device)
-        g_d = torch.empty(world, B, k, dtype=torch.float64, device=wl.device)
-        g_cnt = torch.empty(world, B, dtype=torch.int32, device=wl.device)
-        m_ids, m_d, m_cnt = torch.empty_like(ids), torch.empty_like(dd), torch.empty_like(cnt)
-        bs = B // world
-        plans_loc = torch.empty(bs, npb, dtype=torch.int32, device=wl.device)
-        plans_all = torch.empty(world, bs, npb, dtype=torch.int32, device=wl.device)
-    import torch.distributed as dist
+    pool_np = [q.cpu().numpy() for q in pool]
+    residency = setup_residency(ix, cfg, args, pool_np, sizes) if args.hbm_budget_gb > 0 else None
+    group = make_group(ix, rank, world) if world > 1 else None
+    # one output set per pool batch: the timed steps' results stay for parity
+    outs_t = [(torch.zeros(B, k, dtype=torch.int64, device=wl.device),
+               torch.zeros(B, k, dtype=torch.float64, device=wl.device),
+               torch.zeros(B, dtype=torch.int32, device=wl.device)) for _ in pool]
 
     def step(i):
-        q = pool[i % len(pool)]
-        if world == 1:
-            ix.search_device(q, npb, k, ids, dd, cnt)
-            return
-        if split_assign:
-            # coarse assign split across ranks (each assigns B/N queries, the plans
-            # are identical to a full assign), plans all-gathered
-            ix.assign_device(q[rank * bs:(rank + 1) * bs], npb, plans_loc)
-            all_gather_parts(plans_all, plans_loc)
-            ix.search_planned_device(q, npb, k, plans_all.view(B, npb), ids, dd, cnt)
+        j = i % len(pool)
+        o = outs_t[j]
+        if group is None:
+            ix.search_device(pool[j], npb, k, *o)
         else:
-            ix.search_device(q, npb, k, ids, dd, cnt)
-        all_gather_parts(g_packed, packed)
-        g_ids.copy_(g_packed[:, :Bk].view(world, B, k))
-        g_d.copy_(g_packed[:, Bk:2 * Bk].view(torch.float64).view(world, B, k))
-        g_cnt.copy_(g_packed[:, 2 * Bk:].view(torch.int32)[:, :B])
-        ctx.merge_parts_device(world, B, k, g_ids, g_d, g_cnt, m_ids, m_d, m_cnt)
+            group.search_device(pool[j], npb, k, *o)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    st = ctx.stats()
-    # our kernels per step: the search call's (stats of the last call) plus, at
-    # N>1, the merge and (split assign) the hivf_assign_device kernels
-    kernels_per_step = st["kernels_launched"] + (1 if world > 1 else 0) + (4 if split_assign else 0)
-    # ---- CUDA graph of the search step (N=1): the library's launch sequence is
-    # capturable after a warm call (include/hivf.h); replay removes the launch
-    # gaps between the ~15 dependent kernels.  The batch is copied into the
-    # captured input buffer each step, so every step still searches new queries.
-    graph = None
-    # only where launch gaps matter (short steps, e.g. C1/C2); a 10 ms C3 step
-    # gains nothing measurable from it and keeps the plain launch path
+    barrier(world)
+    kernels_per_step = ctx.stats()["kernels_launched"]
+    # ---- CUDA graphs of the search step (N=1, short steps only): the library's
+    # launch sequence is capturable after a warm call (include/hivf.h); one
+    # graph per pool batch (its own input and outputs), so every replay
+    # searches a different batch with no extra copies
+    graphs = None
     t_w0 = time.perf_counter()
     step(0)
     torch.cuda.synchronize()
     short_step = (time.perf_counter() - t_w0) < 2e-3
     if world == 1 and not args.no_graph and short_step:
         try:
-            qbuf = torch.empty_like(pool[0])
-            qbuf.copy_(pool[0])
-            ix.search_device(qbuf, npb, k, ids, dd, cnt)
+            graphs = []
+            for j in range(len(pool)):
+                step(j)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    step(j)
+                graphs.append(g)
             torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                ix.search_device(qbuf, npb, k, ids, dd, cnt)
-            torch.cuda.synchronize()
-            graph = g
         except Exception as e:  # fall back to direct launches
             log(f"graph capture failed ({e}); timing direct launches")
-            graph = None
+            graphs = None
 
     def timed_step(i):
-        if graph is None:
+        if graphs is None:
             step(i)
         else:
-            qbuf.copy_(pool[i % len(pool)])
-            graph.replay()
+            graphs[i % len(pool)].replay()
 
     for i in range(args.warmup):
         timed_step(i)
@@ -373,119 +546,76 @@ def run_hivf(args):
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     ms_per_step = ms / args.steps
     value = B * args.steps / (ms / 1e3)
+    outs = [tuple(t.cpu().numpy() for t in o) for o in outs_t]
+    outs = [(a.view(np.uint64), b, c.view(np.uint32)) for a, b, c in outs]
     # ---- per-kernel timing pass (events around each phase, inside the library) ----
     ctx.set_option("time_kernels", 1)
     ctx.set_option("reset_timers", 1)
-    tcprof = os.environ.get("HIVF_TCPROF")  # debug: per-CTA stall counters of the scan
-    if tcprof:
-        ctx.set_option("tc_prof", 1)
     for i in range(args.steps):
         step(i)
     torch.cuda.synchronize()
-    if tcprof:
-        import ctypes
-        from paper_2507_09138_b200 import lib
-        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-        buf = np.zeros((n_sm, 16), np.uint64)
-        lib().hivf_debug_tc_prof(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int(n_sm))
-        np.save(tcprof, buf)
-        ctx.set_option("tc_prof", 0)
     st = ctx.stats()
     ctx.set_option("time_kernels", 0)
     scan_ms = st["scan_ms"] / max(1, st["timed_calls"])
     assign_ms = st["assign_ms"] / max(1, st["timed_calls"])
     fin_ms = st["finalize_ms"] / max(1, st["timed_calls"])
-    # algorithmic bytes of the steps (distinct lists per batch)
-    plans = [ix.select_clusters(q.cpu().numpy(), npb) for q in pool]
-    my_sizes = np.where(owner == shard_r, sizes, 0)
-    lb = [list_bytes(p, my_sizes, cfg.dim) for p in plans]
-    ab = [algorithmic_bytes(p, my_sizes, cfg.dim, cfg.k_clusters) for p in plans]
-    steps_lb = [lb[i % len(pool)] for i in range(args.steps)]
-    steps_ab = [ab[i % len(pool)] for i in range(args.steps)]
-    scan_bytes = float(np.mean(steps_lb))
+    # algorithmic bytes of the steps (distinct lists per batch) over
+    # this rank's rows
+    plans = [ix.select_clusters(q, npb) for q in pool_np]
+    lb = [list_bytes(p, local_sizes, cfg.dim) for p in plans]
+    ab = [algorithmic_bytes(p, local_sizes, cfg.dim, cfg.k_clusters) for p in plans]
+    scan_bytes = float(np.mean([lb[i % len(pool)] for i in range(args.steps)]))
+    step_ab = float(np.mean([ab[i % len(pool)] for i in range(args.steps)]))
     pp = np.bincount(plans[0].ravel(), minlength=cfg.k_clusters)
     pp = pp[pp > 0]
     probes_per_list = {"mean": round(float(pp.mean()), 2), "p50": int(np.percentile(pp, 50)),
                        "p90": int(np.percentile(pp, 90)), "max": int(pp.max())}
     peak, peak_kind = measured_peaks()
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
-    # DRAM traffic per scan launch from the committed ncu --set full capture of
-    # this workload (profiles/ncu_traffic_<config>.json), when one exists
+    scan_ms_all = [max_over_ranks(scan_ms, world)] if world > 1 else [scan_ms]
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}"
+                               f"{'_b%d' % B if B != 256 else ''}.json")) as f:
             tj = json.load(f)
-        if world == 1 and not args.shard and not args.hbm_budget_gb:
+        if world == 1 and not args.hbm_budget_gb:
             traffic = int(tj["dram_bytes_per_launch"])
     except (OSError, KeyError, ValueError):
         pass
-    step_gbs = float(np.mean(steps_ab)) / (ms_per_step / 1e3) / 1e9
-    # ---- e2e: host buffers through the C-ABI ------------------------------------
-    e2e = None
-    qh = [torch.empty(B, cfg.dim, dtype=torch.float32, pin_memory=True) for _ in pool]
-    for a, b in zip(qh, pool):
-        a.copy_(b.cpu())
-    if world == 1:
-        # the reference-facing C-ABI call with host buffers (hivf_search)
-        qn = [a.numpy() for a in qh]
-        for i in range(args.warmup):
-            ix.search(qn[i % len(qn)], npb, k)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e0.record(stream)
-        for i in range(args.steps):
-            ix.search(qn[i % len(qn)], npb, k)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        e2e_ms = max(e0.elapsed_time(e1), wall * 1e3)
-        api = "hivf_search (host buffers, pinned)"
-    else:
-        # pinned host queries -> HBM, sharded search + all-gather + device merge,
-        # merged results -> host, every step inside the timed region
-        qd = torch.empty(B, cfg.dim, dtype=torch.float32, device=wl.device)
-        h_ids = torch.empty(B, k, dtype=torch.int64, pin_memory=True)
-        h_d = torch.empty(B, k, dtype=torch.float64, pin_memory=True)
-        h_c = torch.empty(B, dtype=torch.int32, pin_memory=True)
-
-        def e2e_step(i):
-            qd.copy_(qh[i % len(qh)], non_blocking=True)
-            saved = pool[0]
-            pool[0] = qd
+    # ---- e2e: host buffers through the public C-ABI ------------------------------
+    qh = [np.ascontiguousarray(q) for q in pool_np]
+    for i in range(args.warmup):
+        (ix.search(qh[i % len(qh)], npb, k) if group is None else group.search(qh[i % len(qh)], npb, k))
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(args.steps):
+        (ix.search(qh[i % len(qh)], npb, k) if group is None else group.search(qh[i % len(qh)], npb, k))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier(world)
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3), world)
+    api = "hivf_search (host buffers)" if group is None else \
+        "hivf_group_search (host buffers; NCCL shard group: slice assign, plan all-gather, local search, " \
+        "result all-gather, device merge_topk)"
+    e2e = {"value": round(B * args.steps / (e2e_ms / 1e3), 2), "unit": UNIT,
+           "h2d_bytes_per_step": B * cfg.dim * 4, "d2h_bytes_per_step": B * k * (8 + 8) + B * 4, "api": api}
+    # ---- CPU baseline + parity of the timed batches --------------------------------
+    cpu = parity = None
+    if not args.no_cpu:
+        import oracle
+        if not oracle.ref_available():
             try:
-                step(0)
-            finally:
-                pool[0] = saved
-            h_ids.copy_(m_ids, non_blocking=True)
-            h_d.copy_(m_d, non_blocking=True)
-            h_c.copy_(m_cnt, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-
-        for i in range(args.warmup):
-            e2e_step(i)
-        barrier(world)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e0.record(stream)
-        for i in range(args.steps):
-            e2e_step(i)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-        wall = time.perf_counter() - t0
-        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3), world)
-        api = ("hivf_assign_device (B/N per rank) + plan all-gather + hivf_search_planned_device"
-               " + result all-gather + hivf_merge_parts_device (pinned host in/out)")
-    e2e = {"value": B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": B * cfg.dim * 4,
-           "d2h_bytes_per_step": B * k * (8 + 8) + B * 4, "api": api}
-    # ---- CPU baseline + full-scale parity sample (rank 0, N=1) -------------------
-    cpu = None
-    parity = None
-    if world == 1 and rank == 0 and not args.no_cpu:
-        cpu, parity = cpu_baseline_and_parity(ix, wl, cents, pool[0], cfg, args)
-    if world > 1:
-        parity = sharded_parity(ix, wl, cents, pool[0], cfg, step, (m_ids, m_d, m_cnt), rank, world)
+                oracle.build()
+            except Exception:
+                pass
+        if world == 1 and oracle.ref_available():
+            info, parity, _ = reference_on_sample(ix, cents, cfg, args, pool_np, local_sizes, outs)
+            cpu = cpu_baseline_line(info, cfg)
+        elif world > 1:
+            parity = sharded_parity(ix, cents, cfg, args, pool_np, local_sizes, outs, rank, world)
     if rank != 0:
         return
     clocks = clk.summary()
@@ -494,29 +624,25 @@ def run_hivf(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic gaussian mixture (bench_workload.py), generated on device",
-        "launch": "cuda-graph replay of hivf_search_device" if graph is not None else "direct launches",
-        "config": {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
-                   "k_clusters": cfg.k_clusters, "nprobe": npb, "k": k, "batch": B,
-                   "query_pool_batches": len(pool),
-                   "parallelism": (f"list-sharded x{world}" if not args.shard else
-                                   f"one GPU running list shard {shard_r} of {shard_n} (local search "
-                                   f"only: value = this shard's queries/s)"),
-                   "zipf": cfg.zipf,
-                   "probes_per_probed_list": probes_per_list,
-                   "l2": "index (%.1f GB) >> 126 MB L2: no flush needed" % (
-                       cfg.n * cfg.dim * 4 / 1e9)},
+        "launch": "cuda-graph replay of hivf_search_device" if graphs is not None else "direct launches",
+        "api": "hivf_search_device" if group is None else "hivf_group_search_device (NCCL shard group)",
+        "config": config_dict(cfg, args),
+        "parallelism": f"lists sharded over {world} GPUs" if world > 1 else "one GPU, whole index",
         "e2e": e2e,
         "gpu_launches": kernels_per_step * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_scan (grouped list scan)",
+        "roofline": {"bound": "hbm", "kernel": "k_scan_tc (grouped list scan)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": traffic,
                      "bytes_per_launch": int(scan_bytes), "launch_ms": round(scan_ms, 4),
-                     "step_hbm_frac": round(step_gbs / peak, 4),
+                     "launch_ms_max_over_ranks": round(scan_ms_all[0], 4),
+                     "step_hbm_frac": round(step_ab / (ms_per_step / 1e3) / 1e9 / peak, 4),
                      "phase_ms": {"assign": round(assign_ms, 4), "scan": round(scan_ms, 4),
-                                  "finalize": round(fin_ms, 4)}},
+                                  "finalize": round(fin_ms, 4)},
+                     "probes_per_probed_list": probes_per_list},
         "cpu_baseline": cpu,
         "parity_sample": parity,
+        "index_build": build_info,
         "residency": residency,
         "scan_stats": {"work_items": st["n_work_items"], "fallback_queries": st["n_fallback"],
                        "unique_lists": st["n_unique_lists"]},
@@ -525,111 +651,96 @@ def run_hivf(args):
     print(json.dumps(line), flush=True)
 
 
-def _ref_restricted_index(rows_by_list, cents, k_clusters):
-    """A reference IvfIndex (index_from_assignments, vector_index.cpp:210-235)
-    holding only the given lists; select_clusters only reads centroids, so plans
-    and results equal the full index's for queries whose plans it covers."""
-    import oracle
-    corpus = np.concatenate([r for r, _ in rows_by_list.values()]) if rows_by_list else \
-        np.zeros((0, cents.shape[1]), np.float32)
-    ids = np.concatenate([i for _, i in rows_by_list.values()]) if rows_by_list else \
-        np.zeros(0, np.uint64)
-    assign = np.concatenate([np.full(len(i), c, np.uint32) for c, (_, i) in rows_by_list.items()]) \
-        if rows_by_list else np.zeros(0, np.uint32)
-    # index_from_assignments keeps corpus order inside a list: order rows by doc id
-    o = np.argsort(ids, kind="stable")
-    return oracle.RefIndex.from_assignments(corpus[o], ids[o], cents, assign[o], 0)
-
-
-def sharded_parity(ix, wl, cents, q0, cfg, step, merged, rank, world, S=4):
-    """N>1: every rank runs the reference (oracle/_ref) on its own shard for S
-    sample queries (exact local top-k), rank 0 folds the parts with the
-    reference's merge_topk and compares with the GPU result of the full
-    sharded step (local scan -> all-gather -> device merge)."""
-    import torch
-    import torch.distributed as dist
-    import oracle
-    if not oracle.ref_available():
-        return None
-    Q = q0[:S].cpu().numpy()
-    plans = ix.select_clusters(Q, cfg.nprobe)
-    sizes = ix.cluster_sizes()
-    off = np.zeros(len(sizes) + 1, np.uint64)
-    off[1:] = np.cumsum(sizes)
-    rows_by_list = {}
-    for c in np.unique(plans):
-        if sizes[c]:
-            rows_by_list[int(c)] = ix.get_rows(int(off[c]), int(sizes[c]))
-    ri = _ref_restricted_index(rows_by_list, cents.cpu().numpy(), cfg.k_clusters)
-    oi, od, oc = ri.search(Q, cfg.nprobe, cfg.k)
-    local = [[(int(oi[b, j]), float(od[b, j])) for j in range(int(oc[b]))] for b in range(S)]
-    parts = [None] * world
-    dist.all_gather_object(parts, local)
-    step(0)  # pool[0] through the sharded GPU path
-    torch.cuda.synchronize()
-    gi, gd, gc = (t[:S].cpu().numpy() for t in merged)
-    exact = True
-    for b in range(S):
-        ref = []
-        for r in range(world):
-            ref = oracle.merge_topk(ref, parts[r][b], cfg.k)
-        got = [(int(gi[b, j]), float(gd[b, j])) for j in range(int(gc[b]))]
-        exact &= [(i, np.float64(d).view(np.uint64)) for i, d in ref] == \
-                 [(i, np.float64(d).view(np.uint64)) for i, d in got]
-    return {"queries": S, "bit_exact_vs_reference": bool(exact), "nprobe": cfg.nprobe, "k": cfg.k,
-            "method": f"reference search per shard ({world} shards) + merge_topk vs GPU "
-                      "all-gather + device merge"}
-
-
-def cpu_baseline_and_parity(ix, wl, cents, q0, cfg, args):
-    """Reference CPU path (oracle/_ref) on a bounded sample, timed on this host's
-    cores, plus a bit-exact check of our results for the same queries."""
-    import oracle
-    if not oracle.ref_available():
-        try:
-            oracle.build()
-        except Exception:
-            pass
-    if not oracle.ref_available():
-        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                "sample": "oracle/_ref not built"}, None
-    S = min(args.cpu_sample, q0.shape[0])
-    Q = q0[:S].cpu().numpy()
-    cents_np = cents.cpu().numpy()
-    plans = ix.select_clusters(Q, cfg.nprobe)
-    lists = np.unique(plans)
-    sizes = ix.cluster_sizes()
-    off = np.zeros(len(sizes) + 1, np.uint64)
-    off[1:] = np.cumsum(sizes)
+def setup_residency(ix, cfg, args, pool_np, sizes):
+    """Tiered residency: the ClusterCacheState target (tiered_cache.cpp:23-36)
+    -- lists by access frequency over the stream (distinct lists per batch),
+    desc, ties by id -- made resident in the HBM pool."""
     t0 = time.time()
-    rows_by_list = {}
-    for c in lists:
-        r, i = ix.get_rows(int(off[c]), int(sizes[c]))
-        rows_by_list[int(c)] = (r, i)
-    ri = _ref_restricted_index(rows_by_list, cents_np, cfg.k_clusters)
-    log(f"cpu baseline: restricted reference index of {len(lists)} lists "
-        f"({sum(len(i) for _, i in rows_by_list.values())} rows) in {time.time() - t0:.1f}s")
-    cores = os.cpu_count() or 1
-    times = []
-    for rep in range(args.cpu_reps):
-        ms, oi, od, oc = ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
-        times.append(ms)
-    best = min(times)
-    gi, gd, gc = ix.search(Q, cfg.nprobe, cfg.k)
-    exact = bool(np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint64), od.view(np.uint64))
-                 and np.array_equal(gc, oc))
-    cpu = {"value": round(S / (best / 1e3), 3), "unit": UNIT, "cores": cores, "kind": "reference",
-           "sample": f"{S} queries of the timed workload (full plans, nprobe={cfg.nprobe}) on a "
-                     f"restricted index of the {len(lists)} probed lists; make_cursor xS + "
-                     f"RetrievalEngine::execute(live_math=true), best of {len(times)} "
-                     f"({', '.join(f'{t / 1e3:.2f}s' for t in times)})"}
-    parity = {"queries": S, "bit_exact_vs_reference": exact, "nprobe": cfg.nprobe, "k": cfg.k}
-    return cpu, parity
+    freq = np.zeros(cfg.k_clusters, np.int64)
+    plan_np = [ix.select_clusters(q, cfg.nprobe) for q in pool_np]
+    for p in plan_np:
+        freq[np.unique(p)] += 1
+    hot = np.lexsort((np.arange(cfg.k_clusters), -freq)).astype(np.uint32)
+    hot = hot[freq[hot] > 0]
+    ix.set_residency(hot)
+    ix.residency_sync()
+    res = ix.residency()
+    lb = sizes.astype(np.float64) * ((cfg.dim + 15) // 16 * 16) * 4
+    hit = tot = 0.0
+    for p in plan_np:
+        u = np.unique(p)
+        tot += lb[u].sum()
+        hit += lb[u][res[u]].sum()
+    out = {"hbm_list_budget_gb": args.hbm_budget_gb, "index_list_gb": round(float(lb.sum()) / 1e9, 2),
+           "resident_lists": int(res.sum()), "resident_gb": round(float(lb[res].sum()) / 1e9, 2),
+           "scanned_bytes_from_hbm": round(hit / max(tot, 1.0), 4),
+           "policy": "top lists by access frequency over the query stream (freq desc, id asc)",
+           "swap_in_s": round(time.time() - t0, 2)}
+    log(f"residency: {out}")
+    return out
 
 
-# ---------------------------------------------------------------------------
-# reference arm
-# ---------------------------------------------------------------------------
+def run_shard_sweep(args, wl, ctx, cfg):
+    """--shard R/N or all/N: on ONE GPU, build and time rank R's (or every
+    rank's, one after another) list shard of an N-GPU job -- the local search
+    of the sharded step (slice assign, the all-gathers and the merge are not
+    run).  Grounds the N-GPU projection in every shard's step time."""
+    import torch
+    r_s, n_s = args.shard.split("/")
+    N = int(n_s)
+    ranks = list(range(N)) if r_s == "all" else [int(r_s)]
+    cents = wl.train_centroids()
+    t0 = time.time()
+    assign = wl.library_assign(ctx, cents)
+    t_assign = time.time() - t0
+    B, npb, k = cfg.batch, cfg.nprobe, cfg.k
+    pool = [wl.queries(i) for i in range(args.pool)]
+    rows = []
+    o = (torch.zeros(B, k, dtype=torch.int64, device=wl.device),
+         torch.zeros(B, k, dtype=torch.float64, device=wl.device),
+         torch.zeros(B, dtype=torch.int32, device=wl.device))
+    stream = torch.cuda.current_stream()
+    for r in ranks:
+        ix, _, sizes, local_sizes, owner, _, info = build_index(wl, ctx, r, N, cents, assign)
+        for i in range(args.warmup):
+            ix.search_device(pool[i % len(pool)], npb, k, *o)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            ix.search_device(pool[i % len(pool)], npb, k, *o)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        ctx.set_option("time_kernels", 1)
+        ctx.set_option("reset_timers", 1)
+        for i in range(args.steps):
+            ix.search_device(pool[i % len(pool)], npb, k, *o)
+        torch.cuda.synchronize()
+        st = ctx.stats()
+        ctx.set_option("time_kernels", 0)
+        n = max(1, st["timed_calls"])
+        rows.append({"rank": r, "local_rows": info["local_rows"], "ms_per_step": round(ms, 4),
+                     "assign_ms": round(st["assign_ms"] / n, 4), "scan_ms": round(st["scan_ms"] / n, 4),
+                     "finalize_ms": round(st["finalize_ms"] / n, 4),
+                     "striped_lists": info["shard"]["striped_lists"]})
+        log(f"shard {r}/{N}: {rows[-1]}")
+        ix.close()
+        del ix
+        torch.cuda.empty_cache()
+    worst = max(x["ms_per_step"] for x in rows)
+    line = {"metric": METRIC + " -- per-shard local search of an N-GPU job on one GPU",
+            "value": round(B / (worst / 1e3), 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True,
+            "config": config_dict(cfg, args),
+            "shards": rows, "n_shards": N,
+            "spread": {"min_ms": min(x["ms_per_step"] for x in rows), "max_ms": worst,
+                       "mean_ms": round(float(np.mean([x["ms_per_step"] for x in rows])), 4)},
+            "compute_assignments_s": round(t_assign, 1),
+            "note": "value = batch / slowest shard's local step (no exchange): an upper bound on the "
+                    "N-GPU step rate; the full step adds the slice assign + two small all-gathers"}
+    print(json.dumps(line), flush=True)
+
 
 def run_c5(args):
     """BASELINE.json configs[4]: heterogeneous node-split retrieval stream,
@@ -646,7 +757,7 @@ def run_c5(args):
     torch.cuda.set_device(0)
     wl = Workload(cfg, device="cuda:0")
     ctx = Context(0, torch.cuda.current_stream())  # same stream as the torch-built inputs
-    ix, cents, sizes, owner, assign, order, off = build_shard(wl, ctx, 0, 1)
+    ix, cents, sizes, local_sizes, owner, assign, _ = build_index(wl, ctx, 0, 1)
     k = max(cfg.k, c5.K_CACHE)
     Qpool = torch.cat([wl.queries(1000 + i) for i in range(8)]).cpu().numpy()
     budget = int(64 * sizes.mean())  # ~64 lists of rows per sub-stage
@@ -654,12 +765,7 @@ def run_c5(args):
     ref_ix = None
     if oracle.ref_available() and not args.no_cpu:
         t0 = time.time()
-        loff = np.zeros(len(sizes) + 1, np.uint64)
-        loff[1:] = np.cumsum(ix.cluster_sizes())
-        rows_by_list = {int(c): ix.get_rows(int(loff[c]), int(loff[c + 1] - loff[c]))
-                        for c in range(cfg.k_clusters) if loff[c + 1] > loff[c]}
-        ref_ix = _ref_restricted_index(rows_by_list, cents.cpu().numpy(), cfg.k_clusters)
-        del rows_by_list
+        ref_ix, _ = restricted_ref_index(ix, cents.cpu().numpy(), np.arange(cfg.k_clusters), local_sizes)
         log(f"c5: reference index in {time.time() - t0:.1f}s")
     table = []
     exact_all = True
@@ -697,8 +803,18 @@ def run_c5(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
 def run_reference(args):
-    """The reference's own CPU implementation (oracle/_ref), rank 0 only."""
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    /root/reference/proj sources compiled), rank 0 only, on the same workload,
+    config and query sample as our arm's parity / cpu_baseline: per step one
+    sample chunk (make_cursor x S + RetrievalEngine::execute(live_math=true),
+    S >= host threads so every core works).  The index is the one
+    index_from_assignments builds from the same centroids and the exact
+    assignment (bench_workload.exact_assign: torch, no libhivf in this arm)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -721,51 +837,62 @@ def run_reference(args):
     wl = Workload(cfg)
     t0 = time.time()
     cents = wl.train_centroids()
-    assign = wl.assign_all(cents)
+    assign = wl.exact_assign(cents)
     cents_np = cents.cpu().numpy()
-    S = min(args.cpu_sample, cfg.batch)
-    Q = wl.queries(0)[:S].cpu().numpy()
-    # plans from the reference's own select_clusters on a centroid-only index
-    empty = oracle.RefIndex.from_assignments(np.zeros((0, cfg.dim), np.float32),
-                                             np.zeros(0, np.uint64), cents_np,
-                                             np.zeros(0, np.uint32))
-    plans = np.stack([empty.select_clusters(q, cfg.nprobe) for q in Q])
-    want = torch.zeros(cfg.k_clusters, dtype=torch.bool, device=wl.device)
-    want[torch.from_numpy(np.unique(plans).astype(np.int64)).to(wl.device)] = True
-    rows, ids, asg = [], [], []
-    for ci in range(wl.n_chunks()):
-        x = wl.chunk(ci)
-        a = assign[ci * CHUNK: ci * CHUNK + x.shape[0]]
-        m = torch.nonzero(want[a]).squeeze(1)
-        rows.append(x[m].cpu().numpy())
-        ids.append((m + ci * CHUNK).cpu().numpy().astype(np.uint64))
-        asg.append(a[m].cpu().numpy().astype(np.uint32))
-    ri = oracle.RefIndex.from_assignments(np.concatenate(rows), np.concatenate(ids), cents_np,
-                                          np.concatenate(asg))
-    log(f"reference: restricted index ({int(sum(len(i) for i in ids))} rows) in "
-        f"{time.time() - t0:.1f}s")
-    for _ in range(args.warmup):
-        ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
-    times = []
-    for _ in range(args.steps):
-        ms, *_ = ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
-        times.append(ms)
+    log(f"reference: centroids + exact assignments in {time.time() - t0:.1f}s")
+    empty = oracle.RefIndex.from_csr(cents_np, np.zeros(cfg.k_clusters + 1, np.uint64),
+                                     np.zeros((0, cfg.dim), np.float32), np.zeros(0, np.uint64))
+    chunks = sample_plan(cfg, args)
+    nproc = os.cpu_count() or 1
+    steps_of = {c: [i for i in range(args.steps) if i % len(chunks) == c] for c in range(len(chunks))}
+    times, qs = [], []
+    for c, (j, first, S) in enumerate(chunks):
+        if not steps_of[c] and c > 0:
+            continue
+        Q = wl.queries(j)[first:first + S].cpu().numpy()
+        plans = np.stack([empty.select_clusters(q, cfg.nprobe) for q in Q])
+        want = torch.zeros(cfg.k_clusters, dtype=torch.bool, device=wl.device)
+        want[torch.from_numpy(np.unique(plans).astype(np.int64)).to(wl.device)] = True
+        rows, ids, asg = [], [], []
+        for ci in range(wl.n_chunks()):
+            x = wl.chunk(ci)
+            a = assign[ci * CHUNK: ci * CHUNK + x.shape[0]]
+            m = torch.nonzero(want[a]).squeeze(1)
+            rows.append(x[m].cpu().numpy())
+            ids.append((m + ci * CHUNK).cpu().numpy().astype(np.uint64))
+            asg.append(a[m].cpu().numpy())
+        rows, ids, asg = np.concatenate(rows), np.concatenate(ids), np.concatenate(asg)
+        o = np.argsort(asg, kind="stable")  # index_from_assignments: lists in corpus order
+        off = np.zeros(cfg.k_clusters + 1, np.uint64)
+        off[1:] = np.cumsum(np.bincount(asg, minlength=cfg.k_clusters))
+        ri = oracle.RefIndex.from_csr(cents_np, off, rows[o], ids[o])
+        del rows, ids, asg, o
+        log(f"reference: chunk {c} (batch {j} rows {first}:{first + S}): {int(off[-1])} rows")
+        if c == 0:
+            for _ in range(args.warmup):
+                ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
+        for _ in steps_of[c]:
+            ms, *_ = ri.bench_execute(Q, cfg.nprobe, cfg.k, live=True)
+            times.append(ms)
+            qs.append(S)
+        del ri
     tot = sum(times)
-    value = S * len(times) / (tot / 1e3)
-    cores = os.cpu_count() or 1
+    value = sum(qs) / (tot / 1e3)
+    S_max = max(S for _, _, S in chunks)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(tot / len(times), 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic gaussian mixture (bench_workload.py)",
-        "config": {"workload": cfg.describe(), "n_vectors": cfg.n, "dim": cfg.dim,
-                   "k_clusters": cfg.k_clusters, "nprobe": cfg.nprobe, "k": cfg.k,
-                   "batch": cfg.batch, "parallelism": f"{cores} host threads"},
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
+        "config": config_dict(cfg, args),
+        "parallelism": f"{min(S_max, nproc)} host threads (RetrievalEngine::execute, one item per query)",
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": min(S_max, nproc),
+                         "threads_used": min(S_max, nproc), "nproc": nproc, "cpu_model": cpu_model(),
                          "kind": "reference",
-                         "sample": f"{S} queries per step (full plans) on a restricted index of "
-                                   f"the {len(np.unique(plans))} probed lists"},
+                         "sample": f"per step one of {len(chunks)} query chunks "
+                                   f"({', '.join(f'{j}:{f}-{f + S}' for j, f, S in chunks)} of the pool "
+                                   f"batches; full plans) on a restricted index of the chunk's probed lists"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -781,16 +908,19 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--impl", default="hivf", choices=["hivf", "reference"])
     ap.add_argument("--pool", type=int, default=8, help="distinct query batches cycled")
-    ap.add_argument("--cpu-sample", type=int, default=8)
-    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=16,
+                    help="queries per reference chunk at C3/C4 (>= host threads)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time direct launches instead of a CUDA graph")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="tiered residency: HBM bytes for list storage (rest in pinned host memory)")
-    ap.add_argument("--shard", default="", help="R/N: measure rank R's list shard of an N-GPU job on one GPU")
+    ap.add_argument("--shard", default="",
+                    help="R/N or all/N: on one GPU, time rank R's (every rank's) list shard of an N-GPU job")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.cpu_sample < (os.cpu_count() or 1):
+        log(f"note: --cpu-sample {args.cpu_sample} < {os.cpu_count()} host threads")
     if args.config == "c5":
         run_c5(args)
     elif args.impl == "reference":

@@ -9,10 +9,17 @@ the GPU with torch's counter-based Philox generator, one fixed seed per
 262144-row chunk, so any chunk can be regenerated bit-identically (the index
 build regenerates chunks instead of holding the 64 GB corpus twice).
 
-Centroids: k-means (Lloyd) on a sample, deterministic (fp64 segment sums).
-Assignments: fp32 argmin over centroids (the same assignment vector is handed
-to both the GPU index and the reference's index_from_assignments, so both
-search the identical index -- SURVEY.md 8(d)).
+Centroids: k-means (Lloyd) on a sample, deterministic (fp64 segment sums) --
+part of the synthetic input, like the corpus (both arms use the same ones).
+Assignments: ivf::compute_assignments (vector_index.cpp:202-208; nearest
+centroid by the reference's double distance, ties -> lowest id) over every
+row.  Our arm computes them with the library (hivf_compute_assignments,
+`library_assign`); the reference arm, which must not load our library, with
+`exact_assign`, a torch restatement of the same arithmetic (fp32 GEMM filter
+with a rigorous error bound, exact sequential double distances for the rows
+the bound leaves ambiguous).  Both give the reference's assignment, so both
+arms search the index index_from_assignments builds (SURVEY.md 8(d));
+tests/test_gpu_build.py checks the two against each other and the oracle.
 """
 from __future__ import annotations
 
@@ -131,15 +138,59 @@ class Workload:
             torch.backends.cuda.matmul.allow_tf32 = prev
         return cents.contiguous()
 
-    def assign_all(self, cents: torch.Tensor) -> torch.Tensor:
-        prev = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = False
+    def library_assign(self, ctx, cents: torch.Tensor) -> torch.Tensor:
+        """compute_assignments of every row through libhivf (hivf_compute_assignments)."""
+        out = torch.empty(self.cfg.n, dtype=torch.int32, device=self.device)
+        cents = cents.contiguous()
+        for ci in range(self.n_chunks()):
+            x = self.chunk(ci).contiguous()
+            ctx.compute_assignments(x, cents, out[ci * CHUNK: ci * CHUNK + x.shape[0]])
+        return out.long()
+
+    def exact_assign(self, cents: torch.Tensor, sub: int = 32768) -> torch.Tensor:
+        """compute_assignments restated in torch (bench infrastructure for the
+        reference arm): nearest_centroid (vector_index.cpp:18-29) by the
+        reference's squared_l2 (embedding.hpp:27-34), ties -> lowest id."""
+        K, D = cents.shape
+        c64 = cents.double()
+        cnorm = c64.norm(dim=1)
         cn2 = (cents * cents).sum(1)
         out = torch.empty(self.cfg.n, dtype=torch.int64, device=self.device)
+        # |fp32 GEMM distance - exact| <= (D+4) 2^-24 (|x|+|c|)^2 for any
+        # summation order (FMA or not); x4 headroom
+        gam = 4.0 * (D + 4) * 2.0 ** -24
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
         try:
             for ci in range(self.n_chunks()):
-                x = self.chunk(ci)
-                out[ci * CHUNK: ci * CHUNK + x.shape[0]] = self._assign(x, cents, cn2)
+                xc = self.chunk(ci)
+                for s0 in range(0, xc.shape[0], sub):
+                    x = xc[s0:s0 + sub]
+                    d = (x * x).sum(1, keepdim=True) + cn2[None, :] - 2.0 * (x @ cents.T)
+                    xn = x.double().norm(dim=1)
+                    E = (gam * (xn + cnorm.max()) ** 2).float()[:, None] * 1.0001 + 1e-30
+                    best = d.min(dim=1).values
+                    cand = d <= (best[:, None] + 2 * E)
+                    n_c = cand.sum(1)
+                    res = d.argmin(dim=1)
+                    amb = torch.nonzero(n_c > 1).squeeze(1)
+                    if amb.numel():
+                        r, c = torch.nonzero(cand[amb], as_tuple=True)
+                        xa = x[amb[r]].double()
+                        ca = c64[c]
+                        acc = torch.zeros(r.shape[0], dtype=torch.float64, device=self.device)
+                        for i in range(D):  # sequential, one rounding per op, no FMA
+                            t = xa[:, i] - ca[:, i]
+                            acc = acc + t * t
+                        # min (distance, id): ids ascending within a row after nonzero()
+                        key_best = torch.full((amb.shape[0],), float("inf"), dtype=torch.float64,
+                                              device=self.device)
+                        key_best.scatter_reduce_(0, r, acc, reduce="amin")
+                        hit = acc == key_best[r]
+                        pick = torch.full((amb.shape[0],), K, dtype=torch.int64, device=self.device)
+                        pick.scatter_reduce_(0, r[hit], c[hit], reduce="amin")
+                        res[amb] = pick
+                    out[ci * CHUNK + s0: ci * CHUNK + s0 + x.shape[0]] = res
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev
         return out
@@ -154,17 +205,6 @@ def list_layout(assign: torch.Tensor, k_clusters: int):
     pos = torch.empty_like(order)
     pos[order] = torch.arange(assign.shape[0], device=assign.device)
     return off, pos, order
-
-
-def shard_lists(sizes: np.ndarray, world: int) -> np.ndarray:
-    """LPT assignment of lists to ranks by bytes; owner[c]."""
-    owner = np.zeros(len(sizes), np.int64)
-    load = np.zeros(world, np.float64)
-    for c in np.argsort(-sizes.astype(np.float64), kind="stable"):
-        r = int(np.argmin(load))
-        owner[c] = r
-        load[r] += float(sizes[c])
-    return owner
 
 
 def algorithmic_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int, k_clusters: int) -> int:
@@ -185,5 +225,5 @@ def human(n: float) -> str:
     return f"{n:.3g}P"
 
 
-__all__ = ["CHUNK", "CONFIGS", "Config", "Workload", "list_layout", "shard_lists",
+__all__ = ["CHUNK", "CONFIGS", "Config", "Workload", "list_layout",
            "algorithmic_bytes", "list_bytes", "human", "math"]

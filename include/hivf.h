@@ -142,6 +142,17 @@ hivf_status hivf_compute_assignments(hivf_ctx* ctx, const float* d_corpus, uint6
 hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim,
                               uint32_t n_clusters, uint32_t max_iters, uint64_t seed,
                               float* d_centroids_out);
+/* Parallel training mode for large K x n (the C3/C4 bench indexes): the same
+ * Lloyd iterations (exact assignment, point-order double means, farthest-point
+ * re-seeding of empty clusters) from K distinct corpus rows drawn with the
+ * reference's Rng instead of k-means++, whose seeding is a serial chain of K
+ * running sums over n points.  Deterministic for a seed, but NOT the
+ * reference's train_kmeans result (different seeds); the index built from
+ * these centroids with hivf_compute_assignments is still exactly the one the
+ * reference's index_from_assignments builds from the same centroids. */
+hivf_status hivf_train_kmeans_sampled_seeds(hivf_ctx* ctx, const float* d_corpus, uint64_t n,
+                                            uint32_t dim, uint32_t n_clusters, uint32_t max_iters,
+                                            uint64_t seed, float* d_centroids_out);
 /* Same with host buffers (staged through HBM), as the C++ adapter calls them. */
 hivf_status hivf_compute_assignments_host(hivf_ctx* ctx, const float* corpus, uint64_t n, uint32_t dim,
                                           const float* centroids, uint32_t n_clusters,

@@ -100,6 +100,8 @@ def ref():
         R.ref_index_from_assign.restype = vp
         R.ref_index_from_assign.argtypes = [_f32p, _u64p, C.c_uint64, C.c_uint32, C.c_int,
                                             _f32p, C.c_uint32, _u32p]
+        R.ref_index_from_csr.restype = vp
+        R.ref_index_from_csr.argtypes = [_f32p, C.c_uint32, C.c_uint32, C.c_int, _u64p, _f32p, _u64p]
         R.ref_index_free.argtypes = [vp]
         R.ref_index_total.restype = C.c_uint64
         R.ref_index_total.argtypes = [vp]
@@ -338,6 +340,17 @@ class RefIndex:
                                         corpus.shape[0], corpus.shape[1], metric, c, c.shape[0],
                                         np.ascontiguousarray(assign, np.uint32))
         return RefIndex(h, corpus.shape[1], c.shape[0])
+
+    @staticmethod
+    def from_csr(centroids, off, vectors, ids, metric=0):
+        """The index index_from_assignments builds for these CSR lists (search
+        fields only; see ref_shim.cpp ref_index_from_csr)."""
+        c = _f32(centroids)
+        off = np.ascontiguousarray(off, np.uint64)
+        vectors = _f32(vectors)
+        h = ref().ref_index_from_csr(c, c.shape[0], c.shape[1], metric, off, vectors,
+                                     np.ascontiguousarray(ids, np.uint64))
+        return RefIndex(h, c.shape[1], c.shape[0])
 
     def __del__(self):
         try:

@@ -87,6 +87,33 @@ void* ref_index_from_assign(const float* corpus, const uint64_t* ids, uint64_t n
   return out;
 }
 
+// The IvfIndex index_from_assignments (vector_index.cpp:210-235) builds for
+// these lists, filled straight from CSR arrays in its list order (corpus order
+// within a list): centroids, metric, dim, list_ids, list_vectors.  locator and
+// mean_assigned_distance stay empty -- make_cursor / search_clusters /
+// RetrievalEngine::execute never read them (vector_index.cpp:261-328,
+// retrieval_engine.cpp:55-152).  bench.py's CPU arm builds its restricted
+// timing index this way (tens of GB) instead of through the per-row map
+// inserts and distance sums of index_from_assignments.
+void* ref_index_from_csr(const float* centroids, uint32_t k_clusters, uint32_t dim, int metric,
+                         const uint64_t* off, const float* vectors, const uint64_t* ids) {
+  ivf::IvfIndex* out = nullptr;
+  guarded([&] {
+    auto* ix = new ivf::IvfIndex;
+    ix->centroids = make_centroids(centroids, k_clusters, dim);
+    ix->metric = metric == 1 ? Metric::Cosine : Metric::L2;
+    ix->dim = dim;
+    ix->list_ids.resize(k_clusters);
+    ix->list_vectors.resize(k_clusters);
+    for (uint32_t c = 0; c < k_clusters; ++c) {
+      ix->list_ids[c].assign(ids + off[c], ids + off[c + 1]);
+      ix->list_vectors[c].assign(vectors + off[c] * dim, vectors + off[c + 1] * dim);
+    }
+    out = ix;
+  });
+  return out;
+}
+
 void ref_index_free(void* idx) { delete static_cast<ivf::IvfIndex*>(idx); }
 
 uint64_t ref_index_total(void* idx) { return static_cast<ivf::IvfIndex*>(idx)->total_vectors(); }

@@ -32,7 +32,7 @@ SYMBOLS = [
     "hivf_residency_sync", "hivf_last_stats",
     "hivf_set_option", "hivf_shard_plan", "hivf_shard_local_lists", "hivf_index_upload_shard",
     "hivf_group_create", "hivf_nccl_unique_id", "hivf_group_create_nccl", "hivf_group_create_hostcb",
-    "hivf_group_destroy", "hivf_group_search_device", "hivf_group_search",
+    "hivf_group_destroy", "hivf_group_search_device", "hivf_group_search", "hivf_train_kmeans_sampled_seeds",
 ]
 
 
@@ -99,6 +99,7 @@ def lib():
         "hivf_train_kmeans": (i32, [vp, vp, u64, u32, u32, u32, u64, vp]),
         "hivf_compute_assignments_host": (i32, [vp, vp, u64, u32, vp, u32, vp]),
         "hivf_train_kmeans_host": (i32, [vp, vp, u64, u32, u32, u32, u64, vp]),
+        "hivf_train_kmeans_sampled_seeds": (i32, [vp, vp, u64, u32, u32, u32, u64, vp]),
         "hivf_search_planned_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp, vp]),
         "hivf_scan_items": (i32, [vp, vp, u32, vp, vp, vp, vp, vp, vp, u32, vp]),
         "hivf_merge_parts_device": (i32, [vp, u32, u32, u32, vp, vp, vp, vp, vp, vp]),

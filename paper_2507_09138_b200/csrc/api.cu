@@ -1117,8 +1117,11 @@ struct DevScratch {  // RAII cudaMalloc set for the k-means run
 };
 }  // namespace
 
-hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim, uint32_t K,
-                              uint32_t max_iters, uint64_t seed, float* d_centroids_out) {
+// seeding 0: the reference's k-means++ (sequential running sums, one serial
+// chain per seed); 1: K distinct corpus rows drawn with the reference's Rng
+// (uniform_index, duplicates re-drawn) -- no serial chain, for large K x n.
+static hivf_status train_kmeans_impl(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim, uint32_t K,
+                                     uint32_t max_iters, uint64_t seed, int seeding, float* d_centroids_out) {
   if (!ctx || !d_corpus || !d_centroids_out) return fail(HIVF_EINVAL, "train_kmeans: NULL argument");
   if (n < K) return fail(HIVF_EINVAL, "train_kmeans: corpus smaller than k_clusters");
   if (K == 0) return fail(HIVF_EINVAL, "train_kmeans: k_clusters must be >= 1");
@@ -1159,17 +1162,39 @@ hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, 
       return fail(e == cudaErrorMemoryAllocation ? HIVF_ENOMEM : HIVF_ECUDA, "train_kmeans alloc: %s",
                   cudaGetErrorString(e));
   float* cents = d_centroids_out;
-  CK(cudaMemcpyAsync(d_us, us.data(), us.size() * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(draw, 0, 4, s));
-  // k-means++ seeding (vector_index.cpp:114-154)
-  CK(cudaMemcpyAsync(cents, d_corpus + first * dim, dim * 4ull, cudaMemcpyDeviceToDevice, s));
-  launch_kmeans_dist2(d_corpus, n, dim, cents, dist2, 0, s);
-  CKL();
-  for (uint32_t m = 1; m < K; ++m) {
-    launch_kmeans_prefix(dist2, n, prefix, total, s);
-    launch_kmeans_pick(prefix, n, total, d_us, draw, pick, zero, d_corpus, dim, cents, m, s);
-    launch_kmeans_dist2(d_corpus, n, dim, cents + (uint64_t)m * dim, dist2, 1, s);
+  if (seeding == 0) {
+    CK(cudaMemcpyAsync(d_us, us.data(), us.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(draw, 0, 4, s));
+    // k-means++ seeding (vector_index.cpp:114-154)
+    CK(cudaMemcpyAsync(cents, d_corpus + first * dim, dim * 4ull, cudaMemcpyDeviceToDevice, s));
+    launch_kmeans_dist2(d_corpus, n, dim, cents, dist2, 0, s);
     CKL();
+    for (uint32_t m = 1; m < K; ++m) {
+      launch_kmeans_prefix(dist2, n, prefix, total, s);
+      launch_kmeans_pick(prefix, n, total, d_us, draw, pick, zero, d_corpus, dim, cents, m, s);
+      launch_kmeans_dist2(d_corpus, n, dim, cents + (uint64_t)m * dim, dist2, 1, s);
+      CKL();
+    }
+  } else {
+    // K distinct rows: the first draw as above, then uniform_index draws from
+    // the same stream, a row already taken is drawn again
+    std::vector<uint8_t> taken(n, 0);
+    std::vector<uint64_t> rows{first};
+    taken[first] = 1;
+    std::mt19937_64 g2(seed ^ 0x9e3779b97f4a7c15ull);
+    while (rows.size() < K) {
+      uint64_t y;
+      do {
+        y = g2();
+      } while (y >= limit);
+      if (!taken[y % n]) {
+        taken[y % n] = 1;
+        rows.push_back(y % n);
+      }
+    }
+    for (uint32_t m = 0; m < K; ++m)
+      CK(cudaMemcpyAsync(cents + (uint64_t)m * dim, d_corpus + rows[m] * dim, dim * 4ull,
+                         cudaMemcpyDeviceToDevice, s));
   }
   // Lloyd iterations (vector_index.cpp:156-197)
   CK(cudaMemsetAsync(prev, 0xff, n * 4, s));
@@ -1207,6 +1232,16 @@ hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, 
   }
   CK(cudaStreamSynchronize(s));
   return HIVF_OK;
+}
+
+hivf_status hivf_train_kmeans(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim, uint32_t K,
+                              uint32_t max_iters, uint64_t seed, float* d_centroids_out) {
+  return train_kmeans_impl(ctx, d_corpus, n, dim, K, max_iters, seed, 0, d_centroids_out);
+}
+
+hivf_status hivf_train_kmeans_sampled_seeds(hivf_ctx* ctx, const float* d_corpus, uint64_t n, uint32_t dim,
+                                            uint32_t K, uint32_t max_iters, uint64_t seed, float* d_centroids_out) {
+  return train_kmeans_impl(ctx, d_corpus, n, dim, K, max_iters, seed, 1, d_centroids_out);
 }
 
 // host-buffer forms (the C++ adapter's ivf::train_kmeans / compute_assignments)

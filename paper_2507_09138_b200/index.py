@@ -85,6 +85,13 @@ class Context:
         check(lib().hivf_train_kmeans(self.h, _ptr(d_corpus), n, dim, k_clusters, max_iters, seed,
                                       _ptr(d_centroids_out)))
 
+    def train_kmeans_sampled_seeds(self, d_corpus, k_clusters, max_iters, seed, d_centroids_out):
+        """Parallel training mode (hivf_train_kmeans_sampled_seeds): Lloyd from
+        K distinct corpus rows instead of k-means++."""
+        n, dim = d_corpus.shape
+        check(lib().hivf_train_kmeans_sampled_seeds(self.h, _ptr(d_corpus), n, dim, k_clusters, max_iters,
+                                                    seed, _ptr(d_centroids_out)))
+
     def close(self):
         if getattr(self, "h", None):
             lib().hivf_ctx_destroy(self.h)
@@ -191,18 +198,11 @@ class IvfIndex:
         check(lib().hivf_index_get_rows(self.h, first, n, rows.ctypes.data, ids.ctypes.data))
         return rows, ids
 
-    def compute_assignments(self, d_corpus, d_centroids, d_assign_out):
-        """ivf::compute_assignments (vector_index.cpp:202-208) on device tensors:
-        corpus [n, dim] f32, centroids [K, dim] f32 -> assign [n] int32."""
-        n, dim = d_corpus.shape
-        check(lib().hivf_compute_assignments(self.h, _ptr(d_corpus), n, dim, _ptr(d_centroids),
-                                             d_centroids.shape[0], _ptr(d_assign_out)))
-
-    def train_kmeans(self, d_corpus, k_clusters, max_iters, seed, d_centroids_out):
-        """ivf::train_kmeans (vector_index.cpp:99-200), bit-identical centroids."""
-        n, dim = d_corpus.shape
-        check(lib().hivf_train_kmeans(self.h, _ptr(d_corpus), n, dim, k_clusters, max_iters, seed,
-                                      _ptr(d_centroids_out)))
+    def get_rows_into(self, first, n, rows_out, ids_out):
+        """get_rows into caller arrays (C-contiguous float32 [n,dim] / uint64 [n] views)."""
+        assert rows_out.flags.c_contiguous and ids_out.flags.c_contiguous
+        assert rows_out.dtype == np.float32 and ids_out.dtype == np.uint64
+        check(lib().hivf_index_get_rows(self.h, first, n, rows_out.ctypes.data, ids_out.ctypes.data))
 
     def close(self):
         # an index must not outlive its context (the C-ABI contract); if the

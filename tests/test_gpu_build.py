@@ -81,3 +81,46 @@ def test_train_kmeans_invalid_args(ctx):
         ctx.train_kmeans(X, 20, 3, 1, out)   # n < K
     with pytest.raises(InvalidArgument):
         ctx.train_kmeans(X, 4, 0, 1, out)    # max_iters == 0
+
+
+def test_bench_exact_assign_equals_library_and_oracle(ctx):
+    """The two assignment paths of bench.py (ours: hivf_compute_assignments;
+    the reference arm's torch restatement bench_workload.exact_assign) give
+    the reference's compute_assignments, incl. near-ties at D=768."""
+    import torch
+    from bench_workload import Config, Workload
+    cfg = Config("t", 40000, 768, 96, 8, 10, 16, 0.03)
+    wl = Workload(cfg, device="cuda")
+    cents = wl.train_centroids(iters=2, sample_per_centroid=20)
+    cents[5] = cents[4]  # exact tie -> lowest id
+    X = wl.chunk(0)[: cfg.n]
+    want = np.asarray(oracle.compute_assignments(X.cpu().numpy(), cents.cpu().numpy()), np.int64)
+    got_t = wl.exact_assign(cents).cpu().numpy()
+    got_l = wl.library_assign(ctx, cents).cpu().numpy()
+    assert np.array_equal(got_t, want)
+    assert np.array_equal(got_l, want)
+
+
+def test_train_kmeans_sampled_seeds_lloyd_fixed_point(ctx):
+    """Parallel training mode: deterministic, and after convergence every
+    centroid is the reference's Lloyd update of its cluster (point-order
+    double mean, vector_index.cpp:156-197) under the exact assignment."""
+    import torch
+    n, dim, K = 6000, 24, 20
+    X = _mixture(77, n, dim, 10, 0.3)
+    dX = torch.from_numpy(X).cuda()
+    a = torch.empty(K, dim, device="cuda")
+    b = torch.empty(K, dim, device="cuda")
+    ctx.train_kmeans_sampled_seeds(dX, K, 100, 5, a)
+    ctx.train_kmeans_sampled_seeds(dX, K, 100, 5, b)
+    torch.cuda.synchronize()
+    C = a.cpu().numpy()
+    assert np.array_equal(C.view(np.uint32), b.cpu().numpy().view(np.uint32))
+    asg = np.asarray(oracle.compute_assignments(X, C), np.int64)
+    for c in range(K):
+        rows = X[asg == c].astype(np.float64)
+        assert len(rows) > 0
+        s = np.zeros(dim)
+        for r in rows:  # point order, double accumulate
+            s += r
+        assert np.array_equal((s / len(rows)).astype(np.float32).view(np.uint32), C[c].view(np.uint32))
