@@ -123,6 +123,11 @@ hivf_status hivf_index_info(const hivf_index* idx, uint32_t* dim, uint32_t* n_cl
                             uint64_t* n_vectors, uint64_t* hbm_bytes,
                             double* mean_assigned_distance);
 hivf_status hivf_index_cluster_sizes(const hivf_index* idx, uint64_t* sizes_out);
+/* The exact double squared_l2(row, its centroid) of every row, in list order
+ * (host buffer of n_vectors doubles).  index_from_assignments sums these in
+ * corpus order for mean_assigned_distance (vector_index.cpp:222-233); the
+ * caller owns that order, so it can reproduce the reference sum bit-exactly. */
+hivf_status hivf_index_row_distances(hivf_index* idx, double* dist_out);
 
 /* ---- index build -------------------------------------------------------------
  * Replaces ivf::compute_assignments and ivf::train_kmeans

@@ -619,6 +619,24 @@ hivf_status hivf_index_gather_rows(hivf_index* ix, const uint64_t* rows, uint32_
   return HIVF_OK;
 }
 
+hivf_status hivf_index_row_distances(hivf_index* ix, double* dist_out) {
+  if (!ix || !dist_out) return fail(HIVF_EINVAL, "hivf_index_row_distances: NULL argument");
+  if (!ix->N) return HIVF_OK;
+  if (ix->tiered) return fail(HIVF_EUNSUPPORTED, "hivf_index_row_distances: index has a host backing store");
+  CK(cudaSetDevice(ix->ctx->device));
+  cudaStream_t s = ix->ctx->stream;
+  const uint32_t np = 1024;
+  double* d = nullptr;
+  CK(cudaMalloc(&d, (size_t)(ix->N + np) * 8));
+  launch_mean_assigned(ix->view(), d + ix->N, np, s, d);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dist_out, d, (size_t)ix->N * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(HIVF_ECUDA, "hivf_index_row_distances: %s", cudaGetErrorString(e));
+  return HIVF_OK;
+}
+
 hivf_status hivf_index_info(const hivf_index* cix, uint32_t* dim, uint32_t* n_clusters,
                             uint64_t* n_vectors, uint64_t* hbm_bytes,
                             double* mean_assigned_distance) {

@@ -97,7 +97,7 @@ void launch_unpack_rows(const float* vec, const uint64_t* d_list_off, uint32_t K
 void launch_pack_centroids(const float* src, uint32_t K, uint32_t dim, uint32_t dpad, float* dst,
                            float* cnorm2, float* cnorm, int* err, cudaStream_t s);
 void launch_mean_assigned(const IndexView& ix, double* partial, uint32_t n_partial,
-                          cudaStream_t s);
+                          cudaStream_t s, double* row_dist = nullptr);
 void launch_scatter_ids(const uint64_t* ids, const uint64_t* pos, uint64_t n, uint64_t* out,
                         cudaStream_t s);
 void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cudaStream_t s);

@@ -99,7 +99,10 @@ __global__ void k_pack_centroids(const float* __restrict__ src, uint32_t K, uint
 // mean_assigned_distance (vector_index.cpp:222-233): exact per-row distance to
 // its centroid, reduced in a fixed tree (deterministic; the reference sums in
 // corpus order, so the last bits may differ -- the value is informational).
-__global__ void k_mean_assigned(IndexView ix, double* partial) {
+// With row_dist the exact per-row doubles are also written (list order), so a
+// caller can form the reference's corpus-order sum bit-exactly
+// (hivf_index_row_distances).
+__global__ void k_mean_assigned(IndexView ix, double* partial, double* row_dist) {
   __shared__ double red[256];
   double acc = 0.0;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ix.N;
@@ -115,6 +118,7 @@ __global__ void k_mean_assigned(IndexView ix, double* partial) {
     double d = 0.0;
     for (uint32_t k = 0; k < ix.dim; ++k)
       d = exact_step(d, ix.vec[swz_offset(base, n_c, lr, k, ix.dpad)], ix.cent[(uint64_t)lo * ix.dpad + k]);
+    if (row_dist) row_dist[r] = d;
     acc += d;
   }
   red[threadIdx.x] = acc;
@@ -158,8 +162,8 @@ void launch_pack_centroids(const float* src, uint32_t K, uint32_t dim, uint32_t 
 }
 
 void launch_mean_assigned(const IndexView& ix, double* partial, uint32_t n_partial,
-                          cudaStream_t s) {
-  k_mean_assigned<<<n_partial, 256, 0, s>>>(ix, partial);
+                          cudaStream_t s, double* row_dist) {
+  k_mean_assigned<<<n_partial, 256, 0, s>>>(ix, partial, row_dist);
 }
 
 void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cudaStream_t s) {

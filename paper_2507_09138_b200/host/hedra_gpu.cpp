@@ -1,6 +1,7 @@
 // hedra_gpu.cpp -- host side of the drop-in (see hedra_gpu.hpp).  Bookkeeping
 // only; every distance, scan and selection is a libhivf (sm_100a) call.
 #include "hedra_gpu.hpp"
+#include "hvec_io.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -179,100 +180,16 @@ double IvfIndex::mean_assigned_distance() const {
 }
 
 // ---- persistence (HVEC / u32, vector_index.cpp:344-473 formats) -----------------------
-namespace {
-struct File {
-  std::FILE* f = nullptr;
-  std::string path;
-  File(const std::string& p, const char* mode) : path(p) {
-    f = std::fopen(p.c_str(), mode);
-    if (!f) throw std::runtime_error(p + (mode[0] == 'w' ? ": cannot open for writing" : ": cannot open for reading"));
-  }
-  ~File() {
-    if (f) std::fclose(f);
-  }
-  void put(const void* p, std::size_t bytes) {
-    if (bytes && std::fwrite(p, 1, bytes, f) != bytes) throw std::runtime_error(path + ": write failed");
-  }
-  void get(void* p, std::size_t bytes, const char* what) {
-    if (bytes && std::fread(p, 1, bytes, f) != bytes) throw std::runtime_error(path + what);
-  }
-};
-constexpr char kHvec[4] = {'H', 'V', 'E', 'C'};
-void put_header(File& o, std::uint32_t dim, std::uint64_t count, Metric m) {
-  const std::uint32_t version = 1;
-  const std::uint8_t metric = static_cast<std::uint8_t>(m);
-  o.put(kHvec, 4);
-  o.put(&version, 4);
-  o.put(&dim, 4);
-  o.put(&count, 8);
-  o.put(&metric, 1);
-}
-void get_header(File& in, std::uint32_t* dim, std::uint64_t* count, Metric* m) {
-  char magic[4];
-  if (std::fread(magic, 1, 4, in.f) != 4 || std::memcmp(magic, kHvec, 4) != 0)
-    throw std::runtime_error(in.path + ": not a HVEC file");
-  std::uint32_t version = 0;
-  std::uint8_t metric = 0;
-  in.get(&version, 4, ": truncated read");
-  if (version != 1) throw std::runtime_error(in.path + ": unsupported HVEC version");
-  in.get(dim, 4, ": truncated read");
-  in.get(count, 8, ": truncated read");
-  in.get(&metric, 1, ": truncated read");
-  *m = static_cast<Metric>(metric);
-}
-}  // namespace
-
-void save_corpus(const std::string& path, const Corpus& corpus) {
-  File o(path, "wb");
-  put_header(o, corpus.dim, corpus.size(), corpus.metric);
-  o.put(corpus.data.data(), corpus.data.size() * sizeof(float));
-  o.put(corpus.doc_ids.data(), corpus.doc_ids.size() * sizeof(DocId));
-}
-
-Corpus load_corpus(const std::string& path) {
-  File in(path, "rb");
-  Corpus c;
-  std::uint64_t n = 0;
-  get_header(in, &c.dim, &n, &c.metric);
-  c.data.resize(n * c.dim);
-  c.doc_ids.resize(n);
-  in.get(c.data.data(), c.data.size() * sizeof(float), ": truncated corpus file");
-  in.get(c.doc_ids.data(), c.doc_ids.size() * sizeof(DocId), ": truncated corpus file");
-  return c;
-}
-
+void save_corpus(const std::string& path, const Corpus& corpus) { hvec_io::save_corpus(path, corpus); }
+Corpus load_corpus(const std::string& path) { return hvec_io::load_corpus<Corpus>(path); }
 void save_centroids(const std::string& path, const Centroids& centroids, Metric metric) {
-  File o(path, "wb");
-  put_header(o, centroids.dim, centroids.k_clusters(), metric);
-  for (const auto& r : centroids.rows) o.put(r.data(), r.size() * sizeof(float));
+  hvec_io::save_centroids(path, centroids, metric);
 }
-
-Centroids load_centroids(const std::string& path) {
-  File in(path, "rb");
-  Centroids c;
-  std::uint64_t k = 0;
-  Metric m;
-  get_header(in, &c.dim, &k, &m);
-  c.rows.assign(k, std::vector<float>(c.dim));
-  for (auto& r : c.rows) in.get(r.data(), r.size() * sizeof(float), ": truncated centroid file");
-  return c;
-}
-
+Centroids load_centroids(const std::string& path) { return hvec_io::load_centroids<Centroids>(path); }
 void save_assignments(const std::string& path, const std::vector<ClusterId>& assign) {
-  File o(path, "wb");
-  const std::uint64_t n = assign.size();
-  o.put(&n, 8);
-  o.put(assign.data(), assign.size() * sizeof(ClusterId));
+  hvec_io::save_assignments(path, assign);
 }
-
-std::vector<ClusterId> load_assignments(const std::string& path) {
-  File in(path, "rb");
-  std::uint64_t n = 0;
-  in.get(&n, 8, ": truncated read");
-  std::vector<ClusterId> a(n);
-  in.get(a.data(), a.size() * sizeof(ClusterId), ": truncated assignment file");
-  return a;
-}
+std::vector<ClusterId> load_assignments(const std::string& path) { return hvec_io::load_assignments(path); }
 
 // ---- index build ------------------------------------------------------------------
 Centroids train_kmeans(Context& ctx, const Corpus& corpus, std::size_t k_clusters, std::size_t max_iters,
