@@ -360,6 +360,19 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * bypass it). */
 hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
 
+/* ---- validation / debug (not on the search path) ---------------------------
+ * hivf_debug_tc_dot: the list scan's tensor-core dot product in isolation on
+ *   the current device (one CTA; A[128][D], B[n][D] host, n in {8, 16};
+ *   split = 1 reproduces the 3-pass split, out[128][2n] = [hi*hi + lo*hi |
+ *   hi*lo], else out[128][n]).  Used to validate the accumulation term of the
+ *   filter bound on adversarial data (tests/test_gpu_tc_bound.py).
+ * hivf_debug_bound: the filter-bound coefficients (e_a, e_b, e_c) of a scan
+ *   kind (0 FFMA, 2 split tensor-core, 3 single-pass tensor-core) at dim D.
+ * hivf_debug_tc_prof: per-CTA stall counters of the last k_scan_tc launches. */
+int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, unsigned n, int split, float* out);
+int hivf_debug_bound(int kind, unsigned D, double* e_a, double* e_b, double* e_c);
+int hivf_debug_tc_prof(unsigned long long* out, int n_ctas);
+
 #ifdef __cplusplus
 }
 #endif

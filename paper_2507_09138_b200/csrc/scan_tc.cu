@@ -1109,6 +1109,129 @@ int tc_conversion_mode() {
 }
 }  // namespace hivf
 
+// ---------------------------------------------------------------------------
+// hivf_debug_tc_dot: the scan's tensor-core dot product in isolation, to
+// validate the accumulation term of the filter bound (DESIGN.md §3,
+// bound_tc / bound_tc1) against adversarial data.  One CTA computes
+// out[r][j] = sum_d A[r][d] * B[j][d] for 128 rows and n <= 16 columns with
+// exactly the scan's MMA sequence: 64-dim stages in the SWIZZLE_64B K-major
+// layout, one tcgen05.mma M=128 x N x K=8 per 8-dim k-step, accumulating in
+// TMEM in dim order.  split = 1 reproduces the 3-pass split: the k-step
+// issues A x [q ; lo(q)] (N = 2n) and lo(A) x q onto the first n columns,
+// lo = x - conv(x) as the splitters form it; out then holds 2n columns
+// ([hi*hi + lo*hi | hi*lo]) that the epilogue adds in fp32.
+// ---------------------------------------------------------------------------
+namespace hivf {
+namespace {
+__global__ void __launch_bounds__(128, 1) k_tc_dot(const float* __restrict__ A, const float* __restrict__ B,
+                                                   uint32_t D, uint32_t n, int split, int conv,
+                                                   float* __restrict__ out) {
+  // one 16-dim chunk plane at a time (the stage's chunks are consumed in the
+  // same dim order, so the accumulation sequence is the scan's)
+  __shared__ __align__(1024) uint8_t a[kTcChunkBytes];
+  __shared__ __align__(1024) uint8_t alo[kTcChunkBytes];
+  __shared__ __align__(1024) uint8_t b[32 * 64];  // <= 32 B rows
+  __shared__ uint64_t bar;
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t nb = split ? 2 * n : n;  // B rows: [q ; lo(q)]
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t nch = (D + 15) / 16;
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    // A row `tid` (and lo(A)); B rows for tid < nb; zero past D
+    for (int g = 0; g < 4; ++g)
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t d = ch * 16 + g * 4 + e;
+        const uint32_t off = tid * 64 + ((g ^ ((tid >> 1) & 3)) << 4) + e * 4;
+        const float x = d < D ? A[(size_t)tid * D + d] : 0.f;
+        *reinterpret_cast<float*>(a + off) = x;
+        *reinterpret_cast<float*>(alo + off) = x - tf32_conv(x, conv);
+        if ((uint32_t)tid < nb) {
+          const uint32_t j = (uint32_t)tid < n ? tid : tid - n;
+          float y = d < D ? B[(size_t)j * D + d] : 0.f;
+          if ((uint32_t)tid >= n) y = y - tf32_conv(y, conv);
+          *reinterpret_cast<float*>(b + off) = y;
+        }
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const uint64_t ad = sw64_kmajor_desc(smem_u32(a)) + (uint64_t)(k2 * 2);
+        const uint64_t ld = sw64_kmajor_desc(smem_u32(alo)) + (uint64_t)(k2 * 2);
+        const uint64_t bd = sw64_kmajor_desc(smem_u32(b)) + (uint64_t)(k2 * 2);
+        mma_tf32(tmem, ad, bd, tf32_idesc(nb), (ch | k2) != 0);
+        if (split) mma_tf32(tmem, ld, bd, tf32_idesc(n), 1);
+      }
+      mma_commit(&bar);
+    }
+    mbar_wait(&bar, ch & 1);
+    tc_fence_after();
+    __syncthreads();
+  }
+  uint32_t r[32];
+  TMEM_LD32(tmem + ((warp * 32) << 16), r);
+  tmem_wait_ld();
+  for (uint32_t j = 0; j < nb; ++j) out[(size_t)tid * nb + j] = __uint_as_float(r[j]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32));
+  }
+}
+}  // namespace
+}  // namespace hivf
+
+// Debug / validation: host A[128][D], B[n][D] (n in {8, 16}), out[128][split ? 2n : n].
+extern "C" int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, unsigned n, int split,
+                                 float* out) {
+  using namespace hivf;
+  if (!A || !B || !out || D == 0 || (n != 8 && n != 16)) return 1;
+  const int conv = tc_conversion_mode();
+  if (conv > 1) return 2;
+  const size_t nb = split ? 2 * n : n;
+  float *dA = nullptr, *dB = nullptr, *dO = nullptr;
+  int rc = 0;
+  if (cudaMalloc(&dA, 128ull * D * 4) != cudaSuccess || cudaMalloc(&dB, (size_t)n * D * 4) != cudaSuccess ||
+      cudaMalloc(&dO, 128 * nb * 4) != cudaSuccess)
+    rc = 3;
+  if (!rc && (cudaMemcpy(dA, A, 128ull * D * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+              cudaMemcpy(dB, B, (size_t)n * D * 4, cudaMemcpyHostToDevice) != cudaSuccess))
+    rc = 3;
+  if (!rc) {
+    k_tc_dot<<<1, 128>>>(dA, dB, D, n, split, conv, dO);
+    if (cudaMemcpy(out, dO, 128 * nb * 4, cudaMemcpyDeviceToHost) != cudaSuccess) rc = 4;
+  }
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dO);
+  return rc;
+}
+
+// Debug: the filter-bound coefficients of a scan kind (0 FFMA, 2 split TC,
+// 3 single-pass TC) at dimension D: E = e_a |q||x| + e_b (|q|^2+|x|^2) + e_c.
+extern "C" int hivf_debug_bound(int kind, unsigned D, double* e_a, double* e_b, double* e_c) {
+  if (kind == 2) hivf::bound_tc(D, e_a, e_b, e_c);
+  else if (kind == 3) hivf::bound_tc1(D, e_a, e_b, e_c);
+  else hivf::bound_ffma(D, e_a, e_b, e_c);
+  return 0;
+}
+
 // Debug: per-CTA stall counters of the last k_scan_tc launches (accumulated
 // since option tc_prof=1): [n_ctas][16] cycles / timestamps, see TC_PROF_*.
 extern "C" int hivf_debug_tc_prof(unsigned long long* out, int n_ctas) {
