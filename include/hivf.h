@@ -22,6 +22,19 @@
  * reference computes (proj/include/hedra/embedding.hpp:27-34); ids and plan
  * orders follow the reference's (distance, id) total order
  * (proj/include/hedra/vector_index.hpp:41-44).
+ *
+ * Argument range: any nprobe in [1, K] (vector_index.cpp:264-265; plans longer
+ * than 4096 take an exact all-centroid select and the exact scan), any k in
+ * [1, 4096].  Deviations from the reference, all reported, never silent:
+ *   - k > 4096                 -> HIVF_EUNSUPPORTED (the reference has no bound)
+ *   - non-finite query / corpus / centroid values -> HIVF_EINVAL.  The
+ *     reference never checks (check_finite, embedding.hpp:45-49, is unused)
+ *     and its NaN comparisons then give an order that depends on the scan
+ *     order; the filter bounds here need finite operands, so they are rejected.
+ *   - duplicate doc ids in an uploaded index -> HIVF_EINVAL.  build_index
+ *     rejects them too (vector_index.cpp:240-244); index_from_assignments and
+ *     brute_force_search do not, the device layout's id uniqueness needs it.
+ *   - shard groups: nranks * k <= 8192 (the on-device merge buffer).
  */
 #ifndef HIVF_H_
 #define HIVF_H_

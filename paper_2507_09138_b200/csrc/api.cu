@@ -700,6 +700,18 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
   CK(c->dist32.ensure((size_t)qv.n * ix->K * 4));
   CK(c->plans.ensure((size_t)qv.n * nprobe * 4));
   CK(c->flags_c.ensure((size_t)qv.n * 4));
+  if (nprobe > kNprobeMax) {
+    // plans longer than the candidate buffers: exact distance to every
+    // centroid + a stable per-query radix sort (assign.cu, k_coarse_all)
+    size_t need = 0;
+    CK(launch_coarse_all(v, qv, nprobe, nullptr, nullptr, nullptr, &need, c->stream));
+    CK(c->coarse_all.ensure(need));
+    need = c->coarse_all.bytes;
+    CK(launch_coarse_all(v, qv, nprobe, c->plans.as<uint32_t>(), d_dists, c->coarse_all.p, &need, c->stream));
+    CK(cudaMemsetAsync(c->flags_c.p, 0, (size_t)qv.n * 4, c->stream));
+    c->stats.kernels_launched += 4;
+    return HIVF_OK;
+  }
   launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream);
   CKL();
   launch_coarse_select(v, qv, c->dist32.as<float>(), nprobe, c->plans.as<uint32_t>(), d_dists,
@@ -794,7 +806,6 @@ static hivf_status check_search_args(hivf_index* ix, uint32_t n, uint32_t nprobe
   if (!ix->finished) return fail(HIVF_EINVAL, "index not finished");
   if (k == 0) return fail(HIVF_EINVAL, "make_cursor: k must be >= 1");
   if (nprobe < 1 || nprobe > ix->K) return fail(HIVF_EINVAL, "select_clusters: nprobe out of range");
-  if (nprobe > kNprobeMax) return fail(HIVF_EUNSUPPORTED, "nprobe > %u", kNprobeMax);
   if (k > kExactMaxK) return fail(HIVF_EUNSUPPORTED, "k > %u", kExactMaxK);
   (void)n;
   return HIVF_OK;
@@ -815,7 +826,10 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
   c->last_nq = n;
   c->last_index = ix;
   c->last_K = ix->K;
-  c->last_kind = (c->opt_force_exact || k > (uint32_t)kKP) ? 0 : ix->scan_kind();
+  // plans longer than kNprobeMax (the fast path's per-query plan buffers) take
+  // the exact path, which streams any number of plan positions
+  const bool exact_only = c->opt_force_exact || k > (uint32_t)kKP || nprobe > kNprobeMax;
+  c->last_kind = exact_only ? 0 : ix->scan_kind();
   c->stats_adapted = false;
   QueryView qv;
   c->mark(0);
@@ -832,7 +846,6 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
   CK(c->pl.ensure((size_t)np * 4));
   CK(c->flags_f.ensure((size_t)n * 4));
   const IndexView v = ix->view();
-  const bool exact_only = c->opt_force_exact || k > (uint32_t)kKP;
   {
     const size_t parts = (size_t)n * exact_search_parts(nprobe, k);
     CK(c->x_ids.ensure(parts * k * 8));
@@ -941,7 +954,7 @@ static hivf_status search_device_cached(hivf_index* ix, const float* dq, uint32_
   hivf_ctx* c = ix->ctx;
   if (!c->opt_search_graph || ix->tiered || c->opt_time)
     return hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
-  const int kind = (c->opt_force_exact || k > (uint32_t)kKP) ? 0 : ix->scan_kind();
+  const int kind = (c->opt_force_exact || k > (uint32_t)kKP || nprobe > kNprobeMax) ? 0 : ix->scan_kind();
   auto& g = c->sgraph;
   const bool same = g.ix == ix && g.q == dq && g.out == ids && g.n == n && g.nprobe == nprobe && g.k == k &&
                     g.kind == kind && g.gen == g_state_gen.load();

@@ -15,6 +15,8 @@
 // kCandCap candidates) take an exact streaming path over all K.
 #include <cfloat>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -371,6 +373,41 @@ __global__ void __launch_bounds__(512) k_coarse_fallback(IndexView ix, QueryView
   }
 }
 
+// nprobe > kNprobeMax (a plan longer than the candidate buffers hold): the
+// exact fp64 distance to EVERY centroid, one thread each, written as
+// order-preserving keys (distances are >= +0, so their bit patterns order as
+// unsigned integers) with the centroid id as value; a stable radix sort per
+// query then leaves (distance, id) order because equal keys keep the
+// ascending-id input order (vector_index.cpp:272-275).
+__global__ void __launch_bounds__(256) k_coarse_all(IndexView ix, QueryView qv, unsigned long long* keys,
+                                                    uint32_t* vals) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  float* qsh = reinterpret_cast<float*>(sm);
+  const uint32_t b = blockIdx.y;
+  for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)b * ix.dpad + d];
+  __syncthreads();
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ix.K) return;
+  const float4* crow = reinterpret_cast<const float4*>(ix.cent + (uint64_t)c * ix.dpad);
+  const double d = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) { return __ldg(crow + g); });
+  keys[(uint64_t)b * ix.K + c] = (unsigned long long)__double_as_longlong(d);
+  vals[(uint64_t)b * ix.K + c] = c;
+}
+
+__global__ void k_seg_offsets(uint32_t* off, uint32_t n, uint32_t K) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n) off[i] = i * K;
+}
+
+__global__ void k_take_plans(const unsigned long long* keys, const uint32_t* vals, uint32_t K, uint32_t nprobe,
+                             uint32_t* plans, double* dists) {
+  const uint32_t b = blockIdx.y;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nprobe; i += gridDim.x * blockDim.x) {
+    plans[(uint64_t)b * nprobe + i] = vals[(uint64_t)b * K + i];
+    if (dists) dists[(uint64_t)b * nprobe + i] = __longlong_as_double((long long)keys[(uint64_t)b * K + i]);
+  }
+}
+
 }  // namespace
 
 void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t dpad, int metric,
@@ -413,4 +450,42 @@ void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t n
   k_coarse_fallback<<<qv.n, 512, smem, s>>>(ix, qv, nprobe, cap, plans, dists, flags);
 }
 
+}  // namespace hivf
+
+namespace hivf {
+// Exact select for plans longer than kNprobeMax (see k_coarse_all).  scratch
+// holds keys/values twice, the segment offsets and CUB's temporary storage;
+// *scratch_bytes returns the size needed when scratch == nullptr.
+cudaError_t launch_coarse_all(const IndexView& ix, const QueryView& qv, uint32_t nprobe, uint32_t* plans,
+                              double* dists, void* scratch, size_t* scratch_bytes, cudaStream_t s) {
+  const size_t n = (size_t)qv.n * ix.K;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t cub_bytes = 0;
+  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(
+      nullptr, cub_bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+      (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, (int)qv.n, (const uint32_t*)nullptr,
+      (const uint32_t*)nullptr, 0, 64, s);
+  if (e != cudaSuccess) return e;
+  const size_t o_k0 = 0, o_k1 = al(o_k0 + n * 8), o_v0 = al(o_k1 + n * 8), o_v1 = al(o_v0 + n * 4),
+               o_off = al(o_v1 + n * 4), o_tmp = al(o_off + (qv.n + 1) * 4ull), total = al(o_tmp + cub_bytes);
+  if (!scratch) {
+    *scratch_bytes = total;
+    return cudaSuccess;
+  }
+  if (*scratch_bytes < total) return cudaErrorInvalidValue;
+  uint8_t* base = static_cast<uint8_t*>(scratch);
+  auto* k0 = reinterpret_cast<unsigned long long*>(base + o_k0);
+  auto* k1 = reinterpret_cast<unsigned long long*>(base + o_k1);
+  auto* v0 = reinterpret_cast<uint32_t*>(base + o_v0);
+  auto* v1 = reinterpret_cast<uint32_t*>(base + o_v1);
+  auto* off = reinterpret_cast<uint32_t*>(base + o_off);
+  k_coarse_all<<<dim3((ix.K + 255) / 256, qv.n), 256, (size_t)ix.dpad * 4, s>>>(ix, qv, k0, v0);
+  k_seg_offsets<<<(qv.n + 256) / 256, 256, 0, s>>>(off, qv.n, ix.K);
+  size_t tb = cub_bytes;
+  e = cub::DeviceSegmentedRadixSort::SortPairs(base + o_tmp, tb, k0, k1, v0, v1, (int)n, (int)qv.n, off, off + 1,
+                                               0, 64, s);
+  if (e != cudaSuccess) return e;
+  k_take_plans<<<dim3((nprobe + 255) / 256, qv.n), 256, 0, s>>>(k1, v1, ix.K, nprobe, plans, dists);
+  return cudaGetLastError();
+}
 }  // namespace hivf

@@ -346,7 +346,7 @@ void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_ite
                         cudaStream_t s) {
   if (!n_items) return;
   const size_t smem = (size_t)(kExactMaxK + 1) * 16 + 256 * 16 + (size_t)ix.dpad * 4;
-  smem_optin((const void*)k_exact_items, 128 * 1024);
+  smem_optin((const void*)k_exact_items, 200 * 1024);
   k_exact_items<<<n_items, 256, smem, s>>>(ix, qv, n_items, item_off, clusters, k, heap_ids, heap_d,
                                            heap_n, heap_stride, changed, flags);
 }

@@ -110,6 +110,8 @@ void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32,
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
                           uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s);
+cudaError_t launch_coarse_all(const IndexView& ix, const QueryView& qv, uint32_t nprobe, uint32_t* plans,
+                              double* dists, void* scratch, size_t* scratch_bytes, cudaStream_t s);
 void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t nprobe,
                             uint32_t* plans, double* dists, const int* flags, cudaStream_t s);
 
@@ -233,7 +235,7 @@ struct PeerSrc {
 };
 void launch_gather_peer(const PeerSrc& src, uint32_t n_src, uint64_t bytes_each, void* dst, cudaStream_t s);
 
-constexpr uint32_t kExactMaxK = 1024;     // exact-path heap bound
+constexpr uint32_t kExactMaxK = 4096;     // exact-path heap bound
 constexpr uint32_t kNprobeMax = 4096;     // exact coarse-assign bound
 
 }  // namespace hivf
