@@ -968,6 +968,15 @@ static hivf_status search_device_cached(hivf_index* ix, const float* dq, uint32_
     CK(cudaGraphLaunch(g.exec, c->stream));
     return HIVF_OK;
   }
+  // legacy / per-thread default streams cannot be captured, and a blocking
+  // stream's capture fails while other threads use the legacy stream: replay
+  // only on non-blocking streams, and never retry a stream whose capture failed
+  unsigned int sflags = 0;
+  const bool capturable = c->stream && c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread &&
+                          cudaStreamGetFlags(c->stream, &sflags) == cudaSuccess &&
+                          (sflags & cudaStreamNonBlocking) && g.failed_stream != c->stream;
+  (void)cudaGetLastError();
+  if (!capturable) return hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
   if (same && g.seen) {  // second call with this shape: capture it
     const uint64_t gen0 = g_state_gen.load();
     cudaGraph_t graph = nullptr;
@@ -988,11 +997,14 @@ static hivf_status search_device_cached(hivf_index* ix, const float* dq, uint32_
       CK(cudaGraphLaunch(g.exec, c->stream));
       return HIVF_OK;
     }
-    g.seen = false;  // not capturable this time: plain launches
+    g.seen = false;  // not capturable: plain launches from now on for this stream
+    g.failed_stream = c->stream;
     return hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
   }
   if (g.exec) cudaGraphExecDestroy(g.exec);
+  const cudaStream_t failed = g.failed_stream;
   g = {};
+  g.failed_stream = failed;
   hivf_status st = hivf_search_device(ix, dq, n, nprobe, k, ids, dists, counts);
   if (st == HIVF_OK) {
     g.ix = ix;

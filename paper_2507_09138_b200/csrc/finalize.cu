@@ -742,7 +742,18 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
   smem_optin((const void*)k_exact_merge, 200 * 1024);
   const uint32_t ns = part_ids ? exact_search_parts(nprobe, k) : 1;
   const int sms = device_sm_count();
-  const uint32_t gx = std::max(1u, std::min(qv.n, (uint32_t)(4 * sms) / ns));
+  // grid-strided over the queries: a full wave at the kernel's occupancy (an
+  // exact-only search sends every query here; the flagged fallback few)
+  static thread_local int occ_dev = -1, occ = 0;
+  static thread_local size_t occ_smem = 0;
+  if (occ_dev != current_device() || occ_smem != smem) {
+    occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exact_search, 256, smem);
+    occ_dev = current_device();
+    occ_smem = smem;
+  }
+  const uint32_t wave = (uint32_t)std::max(1, occ) * (uint32_t)sms;
+  const uint32_t gx = std::max(1u, std::min(qv.n, wave / ns));
   if (ns <= 1) {
     k_exact_search<<<dim3(gx, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
                                                     d_out, counts_out, nullptr, tau, fa, fb, fc);

@@ -147,6 +147,7 @@ struct hivf_ctx {
     cudaGraphExec_t exec = nullptr;
     hivf_stats stats{};
     int last_kind = 0;
+    cudaStream_t failed_stream = nullptr;  // capture failed on it: plain launches there
   } sgraph;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;

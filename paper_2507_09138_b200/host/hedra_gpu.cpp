@@ -267,52 +267,79 @@ std::vector<SearchStepReport> search_clusters_batch(
   if (clusters.size() != n) throw std::invalid_argument("search_clusters_batch: size mismatch");
   std::vector<SearchStepReport> out(n);
   if (n == 0) return out;
-  // plan-order validation (vector_index.cpp:295-298) before any state changes
-  std::size_t kmax = 1;
-  for (std::size_t i = 0; i < n; ++i) {
+  // Pairs are validated in order, as the reference's sequential loop meets
+  // them (vector_index.cpp:295-298): at the first plan-order error, the earlier
+  // pairs and the failing pair's valid leading clusters are searched, later
+  // pairs are left untouched, then the error is thrown.
+  std::vector<std::size_t> take(n, 0);
+  const char* err = nullptr;
+  std::size_t n_run = n;
+  for (std::size_t i = 0; i < n && !err; ++i) {
     const SearchCursor& c = *cursors[i];
     for (std::size_t j = 0; j < clusters[i].size(); ++j) {
-      if (c.next_pos + j >= c.plan.size())
-        throw std::runtime_error("search_clusters: cursor exhausted mid-batch");
-      if (c.plan[c.next_pos + j] != clusters[i][j])
-        throw std::runtime_error("search_clusters: cluster does not match plan order");
+      if (c.next_pos + j >= c.plan.size()) {
+        err = "search_clusters: cursor exhausted mid-batch";
+        break;
+      }
+      if (c.plan[c.next_pos + j] != clusters[i][j]) {
+        err = "search_clusters: cluster does not match plan order";
+        break;
+      }
+      ++take[i];
     }
-    kmax = std::max(kmax, c.k);
+    if (err) n_run = i + 1;
   }
+  std::vector<std::size_t> item;  // pairs with clusters to scan and a heap that takes entries
+  std::size_t kmax = 1;
+  for (std::size_t i = 0; i < n_run; ++i) {
+    if (!take[i] || !cursors[i]->heap.k()) continue;
+    if (cursors[i]->query.size() != index.dim()) throw std::invalid_argument("search_clusters: dimension mismatch");
+    item.push_back(i);
+    kmax = std::max(kmax, cursors[i]->heap.k());
+  }
+  const std::size_t m = item.size();
   const std::uint32_t dim = index.dim();
-  std::vector<float> q(n * dim);
-  std::vector<std::uint32_t> off(n + 1, 0), kk(n), hn(n), cl;
-  std::vector<std::uint64_t> hid(n * kmax, 0);
-  std::vector<double> hd(n * kmax, 0.0);
-  for (std::size_t i = 0; i < n; ++i) {
-    const SearchCursor& c = *cursors[i];
-    if (c.query.size() != dim) throw std::invalid_argument("search_clusters: dimension mismatch");
-    std::copy(c.query.begin(), c.query.end(), q.begin() + i * dim);
-    cl.insert(cl.end(), clusters[i].begin(), clusters[i].end());
-    off[i + 1] = static_cast<std::uint32_t>(cl.size());
-    kk[i] = static_cast<std::uint32_t>(c.k);
-    const auto& e = c.heap.entries();
-    hn[i] = static_cast<std::uint32_t>(e.size());
-    for (std::size_t j = 0; j < e.size(); ++j) {
-      hid[i * kmax + j] = e[j].doc_id;
-      hd[i * kmax + j] = e[j].distance;
+  std::vector<std::uint32_t> off(m + 1, 0), hn(m);
+  std::vector<std::uint64_t> hid(m * kmax, 0);
+  std::vector<double> hd(m * kmax, 0.0);
+  std::vector<std::uint8_t> changed;
+  if (m) {
+    std::vector<float> q(m * dim);
+    std::vector<std::uint32_t> kk(m), cl;
+    for (std::size_t t = 0; t < m; ++t) {
+      const SearchCursor& c = *cursors[item[t]];
+      std::copy(c.query.begin(), c.query.end(), q.begin() + t * dim);
+      cl.insert(cl.end(), clusters[item[t]].begin(), clusters[item[t]].begin() + take[item[t]]);
+      off[t + 1] = static_cast<std::uint32_t>(cl.size());
+      kk[t] = static_cast<std::uint32_t>(c.heap.k());
+      const auto& e = c.heap.entries();
+      hn[t] = static_cast<std::uint32_t>(e.size());
+      for (std::size_t j = 0; j < e.size(); ++j) {
+        hid[t * kmax + j] = e[j].doc_id;
+        hd[t * kmax + j] = e[j].distance;
+      }
     }
+    changed.assign(cl.size(), 0);
+    check(hivf_scan_items(index.raw(), q.data(), static_cast<std::uint32_t>(m), off.data(), cl.data(),
+                          kk.data(), hid.data(), hd.data(), hn.data(), static_cast<std::uint32_t>(kmax),
+                          changed.data()));
   }
-  std::vector<std::uint8_t> changed(std::max<std::size_t>(1, cl.size()));
-  check(hivf_scan_items(index.raw(), q.data(), static_cast<std::uint32_t>(n), off.data(), cl.data(),
-                        kk.data(), hid.data(), hd.data(), hn.data(),
-                        static_cast<std::uint32_t>(kmax), changed.data()));
-  for (std::size_t i = 0; i < n; ++i) {
+  std::size_t t = 0;
+  for (std::size_t i = 0; i < n_run; ++i) {
     SearchCursor& c = *cursors[i];
-    c.heap.assign_sorted(hid.data() + i * kmax, hd.data() + i * kmax, hn[i]);
-    for (std::uint32_t j = off[i]; j < off[i + 1]; ++j) {
+    const bool on_device = t < m && item[t] == i;
+    if (on_device) c.heap.assign_sorted(hid.data() + t * kmax, hd.data() + t * kmax, hn[t]);
+    for (std::size_t j = 0; j < take[i]; ++j) {
+      const bool ch = on_device && changed[off[t] + j];
       ++c.next_pos;
       ++c.clusters_searched;
-      c.unchanged_streak = changed[j] ? 0 : c.unchanged_streak + 1;
-      out[i].heap_changed |= changed[j] != 0;
-      out[i].searched.push_back(cl[j]);
+      c.unchanged_streak = ch ? 0 : c.unchanged_streak + 1;
+      out[i].heap_changed |= ch;
+      out[i].searched.push_back(clusters[i][j]);
     }
+    if (on_device) ++t;
   }
+  if (err) throw std::runtime_error(err);
   return out;
 }
 
@@ -511,17 +538,24 @@ RetStepReport RetrievalEngine::execute(SubStageBatch& batch, double now_ms, bool
   rep.slow_lane_ms = slow_ns / 1e6;
   rep.fast_lane_ms = fast_ns / 1e6;
   rep.modeled_ms = std::max(rep.slow_lane_ms, rep.fast_lane_ms) + fixed_call_ms(model_);
+  // items up to the first unknown task run, then the error (the reference's
+  // sequential item order, retrieval_engine.cpp:94-100)
   std::vector<ivf::SearchCursor*> cursors;
   std::vector<std::span<const ClusterId>> spans;
+  bool unknown = false;
   for (const auto& it : batch.items) {
     auto t = tasks_.find({it.request_id, it.node_id});
-    if (t == tasks_.end()) throw std::runtime_error("execute: batch references unknown task");
+    if (t == tasks_.end()) {
+      unknown = true;
+      break;
+    }
     cursors.push_back(&t->second.cursor);
     spans.emplace_back(it.clusters.data(), it.clusters.size());
   }
   const auto t0 = std::chrono::steady_clock::now();
   const auto steps = ivf::search_clusters_batch(*index_, cursors, spans);  // one GPU sub-stage
   rep.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (unknown) throw std::runtime_error("execute: batch references unknown task");
   std::set<ClusterId> accessed;
   for (std::size_t i = 0; i < batch.items.size(); ++i) {
     const auto& it = batch.items[i];

@@ -7,10 +7,15 @@
 //                search_step)
 //   hedra::cache proj/include/hedra/tiered_cache.hpp   (ClusterCacheState)
 //   hedra::ret   proj/include/hedra/retrieval_engine.hpp (RetrievalEngine)
-// A caller switches `namespace ivf = hedra::ivf;` to `namespace ivf = hedra_gpu::ivf;`
-// (likewise ret/cache) and builds the index once with IvfIndex::from_assignments.
-// All distance / scan / selection work runs on the GPU; the host keeps the same
-// bookkeeping the reference keeps (cursors, plans, cache counters).
+// This is the self-contained form (its own namespace, an explicit Context, an
+// HBM-only IvfIndex without the reference's host members), buildable without
+// the reference tree.  The LITERAL drop-in -- the reference's own headers and
+// namespaces, IvfIndex with its data members, so the unmodified scheduler,
+// unit suites and acceptance suite compile against it -- is
+// paper_2507_09138_b200/compat/ (include/hedra/vector_index.hpp +
+// hedra_ivf_gpu.cpp).  All distance / scan / selection work runs on the GPU in
+// both; the host keeps the reference's bookkeeping (cursors, plans, cache
+// counters).
 #pragma once
 
 #include <cstdint>
