@@ -237,11 +237,13 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   } else if (!strcmp(name, "tc_variant")) {  // debug only: results are inexact when != 0
     ctx->tc.variant = (int)value;
   } else if (!strcmp(name, "tc_qmax")) {  // tuning: queries per tensor-core work item
-    if (value < 0 || (value > 32 && value != (int64_t)kTcWideQ) || value % 8)
-      return fail(HIVF_EINVAL, "tc_qmax: 0, 8..32 step 8, or 64 (wide)");
+    if (value < 0 || (value > 32 && !tc_is_wide((uint32_t)value)) || value % 8)
+      return fail(HIVF_EINVAL, "tc_qmax: 0, 8..32 step 8, 64 or 128 (wide)");
     ctx->tc.qmax_override = (uint32_t)value;
   } else if (!strcmp(name, "tc_wide_ppl")) {  // tuning: probes/list above which dense batches use
     ctx->tc.wide_ppl = (float)value;           // the wide (64-query) scan; negative = never
+  } else if (!strcmp(name, "tc_wide2_ppl")) {  // tuning: probes/list above which the 128-query
+    ctx->tc.wide2_ppl = (float)value;          // groups are used; negative = never
   } else if (!strcmp(name, "time_kernels")) {
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->resolve_timers();
@@ -754,7 +756,8 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
   uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc) : (uint32_t)kQMax;
   WideStage ws;
-  if (group == kTcWideQ) {
+  ws.group = group;
+  if (tc_is_wide(group)) {
     // the restaged queries need (pairs + 7K) x D floats; when HBM is short
     // (index near the budget) the batch takes the narrow kernel instead
     if (c->qshift.ensure(ix->K * 4ull) != cudaSuccess ||
@@ -762,7 +765,8 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
       (void)cudaGetLastError();
       ppl = 0.f;
       group = scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc);
-      if (group == kTcWideQ) return fail(HIVF_ENOMEM, "wide scan: query staging buffer");
+      if (tc_is_wide(group)) return fail(HIVF_ENOMEM, "wide scan: query staging buffer");
+      ws.group = group;
     } else {
       ws.qshift = c->qshift.as<uint32_t>();
       ws.qstage = c->qwide.as<uint8_t>();

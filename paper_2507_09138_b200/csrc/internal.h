@@ -118,7 +118,7 @@ struct hivf_ctx {
   // the rest stays in a pinned host backing store read over PCIe
   uint64_t opt_hbm_list_budget = 0;
   int tc_conv = 2;  // this device's fp32->tf32 operand conversion (tc_conversion_mode)
-  TcOpts tc{0, tc_wide_ppl_default(), 0};  // tensor-core scan tuning (tc_qmax, tc_wide_ppl, tc_variant)
+  TcOpts tc{0, tc_wide_ppl_default(), 0, tc_wide2_ppl_default()};  // tensor-core scan tuning (tc_qmax, tc_wide_ppl, tc_variant)
   // scratch
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,

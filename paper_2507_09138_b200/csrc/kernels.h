@@ -21,8 +21,10 @@ struct TcOpts {
   uint32_t qmax_override = 0;  // "tc_qmax": 0 auto
   float wide_ppl = 0.f;        // "tc_wide_ppl": probes/list above which the wide scan runs; < 0 never
   int variant = 0;             // "tc_variant" (debug, inexact when nonzero)
+  float wide2_ppl = 40.f;      // "tc_wide2_ppl": above it, 128-query groups; < 0 never
 };
 float tc_wide_ppl_default();   // env HIVF_TC_WIDE_PPL, else 0
+float tc_wide2_ppl_default();  // env HIVF_TC_WIDE2_PPL, else 40
 
 // One grouped-scan work item: rows [row0, row0+nrows) of list `list` (local
 // row numbers) against up to kQMax queries listed in item_pairs[pair0, pair0+nq).
@@ -133,9 +135,14 @@ int scan_smem_bytes(uint32_t dpad);
 // restaged query rows (launch_stage_wide) and per-list staging shifts
 // (launch_build_worklist's qshift).  Unused (zeros) for the narrow scan.
 constexpr uint32_t kTcWideQ = 64;
+// 128-query groups (k_scan_tc<128>, dense batches): half as many list passes
+// as 64-query groups, 16-deep per-warp candidate lists
+constexpr uint32_t kTcWide2Q = 128;
+inline bool tc_is_wide(uint32_t q) { return q == kTcWideQ || q == kTcWide2Q; }
 struct WideStage {
   uint8_t* qstage = nullptr;  // wide_stage_rows() x dpad floats
   uint32_t* qshift = nullptr;
+  uint32_t group = kTcWideQ;  // staged query-group size (the scan's qmax)
 };
 uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists);
 void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,

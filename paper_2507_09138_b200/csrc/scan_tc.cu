@@ -55,8 +55,6 @@ constexpr int kTcCps = 4;          // 16-dim chunks per pipeline stage (64 dims)
 constexpr int kTcMaxA = 8;         // max depth of the A landing ring
 constexpr int kTcLo = 4;           // depth of the A_lo ring (in TMEM, 64 columns per slot)
 constexpr int kMergeQ = 16;        // queries per round of the item-end cross-warp merge (wide: 8)
-constexpr int kWideQ = (int)kTcWideQ;  // wide mode: queries per group (two epilogue groups of 32)
-constexpr int kWideQBytes = kTcCps * kWideQ * 64;  // wide mode: query slice per stage (16 KB)
 constexpr int kItemQ = 4;          // published work items in flight (producer runs ahead)
 constexpr int kTcChunkBytes = kTcTile * kChunk * 4;       // 8 KB
 constexpr int kTcStageBytes = kTcCps * kTcChunkBytes;     // 32 KB
@@ -95,8 +93,8 @@ struct TcParams {
   // the sub-stage -- updating them from later clusters would change the
   // reference's per-cluster `changed` flags), 1: items publish their k-th
   uint32_t bound_update;
-  // wide mode (k_scan_tc<true>): query groups of up
-  // to 64 streamed with the list stages from a restaged copy (launch_stage_wide):
+  // wide mode (k_scan_tc<64|128>): query groups of up
+  // to 64 / 128 streamed with the list stages from a restaged copy (launch_stage_wide):
   // group block at staged row (pair0 + qshift[list]), chunk-major [ch][npad
   // rows][64 B] in the SWIZZLE_64B pattern, so a stage's query slice is one copy
   const uint8_t* qstage;
@@ -236,12 +234,285 @@ __device__ __forceinline__ float tf32_conv(float x, int mode) {
 #define TC_PROF_ADD(slot) \
   if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - _t0))
 
-template <bool kWide>
+// (d^, row) order of the candidate lists
+__device__ __forceinline__ bool cand_less(float a, uint32_t ar, float b, uint32_t br) {
+  return a < b || (a == b && ar < br);
+}
+// Ascending bitonic sort of one (d^, row) pair per lane across the warp.
+__device__ __forceinline__ void warp_sort32(float& v, uint32_t& r, int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      const float pv = __shfl_xor_sync(FULL, v, jj);
+      const uint32_t pr = __shfl_xor_sync(FULL, r, jj);
+      const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
+      if (keep_min == cand_less(pv, pr, v, r)) {
+        v = pv;
+        r = pr;
+      }
+    }
+  }
+}
+// Bitonic clean over lanes (xor steps from `top` down to 1): a bitonic
+// sequence per (2*top)-lane block becomes ascending.
+__device__ __forceinline__ void warp_clean(float& v, uint32_t& r, int lane, int top) {
+#pragma unroll
+  for (int jj = 16; jj > 0; jj >>= 1) {
+    if (jj > top) continue;
+    const float pv = __shfl_xor_sync(FULL, v, jj);
+    const uint32_t pr = __shfl_xor_sync(FULL, r, jj);
+    const bool keep_min = (lane & jj) == 0;
+    if (keep_min == cand_less(pv, pr, v, r)) {
+      v = pv;
+      r = pr;
+    }
+  }
+}
+
+// One tile's candidates of a query pair (a: lanes' va, b: vb; inf = none)
+// merged into the pair's 16-deep lists (lanes 0-15: a, 16-31: b).  Out of
+// line: the per-pair loop around it stays small enough to unroll, so the
+// lists stay in registers.
+struct Cand {
+  float v;
+  uint32_t r;
+};
+__device__ __noinline__ Cand merge_pair16(float sa, float sb, uint32_t grow, float yv, uint32_t yr, int lane) {
+  uint32_t ra = sa < kInfF ? grow : kNoRow, rb = sb < kInfF ? grow : kNoRow;
+  if (__any_sync(FULL, ra != kNoRow)) warp_sort32(sa, ra, lane);
+  if (__any_sync(FULL, rb != kNoRow)) warp_sort32(sb, rb, lane);
+  // best 16 of query a in lanes 0-15, of query b in lanes 16-31
+  const float sb16 = __shfl_sync(FULL, sb, lane & 15);
+  const uint32_t rb16 = __shfl_sync(FULL, rb, lane & 15);
+  const bool upper = lane >= 16;
+  const float xv = upper ? sb16 : sa;
+  const uint32_t xr = upper ? rb16 : ra;
+  // per half: min(list, reversed candidates) is bitonic -> clean 8..1
+  const float rv = __shfl_xor_sync(FULL, xv, 15);
+  const uint32_t rr = __shfl_xor_sync(FULL, xr, 15);
+  if (cand_less(rv, rr, yv, yr)) {
+    yv = rv;
+    yr = rr;
+  }
+  warp_clean(yv, yr, lane, 8);
+  return Cand{yv, yr};
+}
+
+// Epilogue of k_scan_tc<128>: group h = 0 (warps 6-9) takes the item's
+// queries 0..63, h = 1 (warps 2-5) queries 64..127 (TMEM columns
+// 128*buffer + 64h + [0, 64)), each warp its lane quadrant of the tile.  Per
+// warp and query the best 16 rows are kept: register slot s holds local
+// queries 2s (lanes 0-15) and 2s+1 (lanes 16-31), ascending (d^, row); a tile's
+// candidates of a query pair are bitonic-sorted across the warp and the best
+// 16 merged into each half.  Item end: the four warps' 16-lists of a query
+// merge into the (query, segment) output of 32 with the drop threshold
+//   T = min(32nd kept when 32 are kept, each full warp list's 16th, the
+//       smallest drop bound used)
+// -- every row not reported has d^ >= T (rows a full 16-list dropped are >=
+// its 16th; rows the bound dropped are >= that bound).
+__device__ __forceinline__ void epilogue128(const TcParams& P, uint32_t tmem_base, uint32_t nacc, uint32_t& tb,
+                                         uint32_t& tph, uint64_t* ifull, uint64_t* iempty, uint64_t* tfull,
+                                         uint64_t* tempty, const ScanItem* s_item, const int* s_valid,
+                                         float* md, uint32_t* mr, int warp, int lane) {
+  __shared__ float s_gm[2][kTcEpiWarps][64];   // smallest drop bound used, per warp and query
+  __shared__ float s_w16[2][kTcEpiWarps][64];  // 16th of a full warp list (else inf)
+  const uint32_t quad = warp & 3;
+  const uint32_t ew = (warp - 2) & 3;
+  const uint32_t h = warp < 2 + kTcSplitWarps ? 1u : 0u;
+  const bool upper = lane >= 16;
+  float* gmd = md + h * (kTcEpiWarps * 8 * 16);
+  uint32_t* gmr = mr + h * (kTcEpiWarps * 8 * 16);
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+    mbar_wait_parked(&ifull[slot], iph);
+    if (!s_valid[slot]) break;
+    const ScanItem item = s_item[slot];
+    const uint32_t nq = item.nq > 64 * h ? min(64u, item.nq - 64 * h) : 0u;
+    // lane j: metadata of local queries j (m = 0) and 32 + j (m = 1)
+    float w_qn2[2] = {0.f, 0.f}, w_E[2] = {0.f, 0.f};
+    uint32_t w_qi[2] = {0, 0}, w_slot[2] = {0, 0};
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const uint32_t q = 32 * m + lane;
+      if (q < nq) {
+        const uint32_t pair = P.sorted_pairs[item.pair0 + 64 * h + q];
+        w_qi[m] = P.pair_query[pair];
+        w_qn2[m] = P.qv.qn2[w_qi[m]];
+        w_slot[m] = pair * P.ix.s_max + item.seg;
+        w_E[m] = seg_bound(P.ix, P.qv.qnorm[w_qi[m]], P.ix.maxnorm[item.list]);
+      }
+    }
+    const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
+    const uint64_t lbeg = P.ix.list_off[item.list];
+    float ld[32];
+    uint32_t lr[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      ld[j] = kInfF;
+      lr[j] = kNoRow;
+    }
+    float xn_next = 0.f;
+    {
+      const uint32_t srow0 = quad * 32 + lane;
+      if (srow0 < item.nrows) xn_next = __ldg(P.ix.xnorm2 + lbeg + item.row0 + srow0);
+    }
+    float gmin[2] = {kInfF, kInfF};
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t srow = t * kTcTile + quad * 32 + lane;
+      const bool valid = srow < item.nrows;
+      const float xn = xn_next;
+      {
+        const uint32_t nrow = srow + kTcTile;
+        xn_next = (nrow < item.nrows) ? __ldg(P.ix.xnorm2 + lbeg + item.row0 + nrow) : 0.f;
+      }
+      {
+        TC_PROF_T0();
+        mbar_wait_parked(&tfull[tb], tph);
+        if (lane == 0) TC_PROF_ADD(8);
+      }
+      tc_fence_after();
+      const uint32_t ta = tmem_base + ((quad * 32) << 16) + tb * 128 + 64 * h;
+      float gl[2] = {kInfF, kInfF};
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        if (P.topk && 32 * m + lane < nq) {
+          const float u = __ldcg(P.qbound + w_qi[m]);
+          if (u < 3.0e38f) gl[m] = drop_bound(u, w_E[m]);
+        }
+        gmin[m] = fminf(gmin[m], gl[m]);
+      }
+      const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
+      // two halves of 32 query columns (32 accumulator registers live at a time);
+      // the buffer is released after the second load
+      if (nq == 0) {  // nothing of this item in the group's columns: free the buffer
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[tb]);
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        if (32 * hh >= (int)nq) break;
+        uint32_t acc[32];
+        TMEM_LD32(ta + 32 * hh, acc);
+        tmem_wait_ld();
+        if (hh == 1 || nq <= 32) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[tb]);
+        }
+#pragma unroll
+        for (int sl = 0; sl < 16; ++sl) {  // query pair (2sp, 2sp+1), sp = 16hh + sl
+          const int sp = 16 * hh + sl;
+          const int qa = 2 * sp, qb = 2 * sp + 1;
+          if (qa >= (int)nq) break;
+          const float qa2 = __shfl_sync(FULL, w_qn2[hh], qa & 31);
+          const float qb2 = __shfl_sync(FULL, w_qn2[hh], qb & 31);
+          const float va = valid ? __fmaf_rn(-2.f, __uint_as_float(acc[qa & 31]), __fadd_rn(xn, qa2)) : kInfF;
+          const float vb = (valid && qb < (int)nq)
+                               ? __fmaf_rn(-2.f, __uint_as_float(acc[qb & 31]), __fadd_rn(xn, qb2))
+                               : kInfF;
+          const float ga = __shfl_sync(FULL, gl[hh], qa & 31);
+          const float gb = __shfl_sync(FULL, gl[hh], qb & 31);
+          const float tha = fminf(__shfl_sync(FULL, ld[sp], 15), ga);
+          const float thb = fminf(__shfl_sync(FULL, ld[sp], 31), gb);
+          const bool ca = va < tha, cb = vb < thb;
+          if (!__any_sync(FULL, ca || cb)) continue;
+          const Cand m = merge_pair16(ca ? va : kInfF, cb ? vb : kInfF, grow, ld[sp], lr[sp], lane);
+          ld[sp] = m.v;
+          lr[sp] = m.r;
+        }
+      }
+      if (++tb == nacc) {
+        tb = 0;
+        tph ^= 1;
+      }
+    }
+    // ---- item end: merge the four warps' 16-lists of each query, 8 queries per round ----
+    const long long _tm = P.prof ? clock64() : 0;
+#pragma unroll
+    for (int h0 = 0; h0 < 64; h0 += 8) {
+      if (h0 >= (int)nq) break;
+      named_bar_sync(2 + h, kTcEpiWarps * 32);  // the previous round's reads are done
+      if (h0 == 0) {
+        s_gm[h][ew][lane] = gmin[0];
+        s_gm[h][ew][32 + lane] = gmin[1];
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int q = h0 + jj;
+        const int sp = q >> 1;
+        if ((q & 1) == (int)upper) {
+          gmd[(ew * 8 + jj) * 16 + (lane & 15)] = ld[sp];
+          gmr[(ew * 8 + jj) * 16 + (lane & 15)] = lr[sp];
+          if ((lane & 15) == 15) s_w16[h][ew][q] = lr[sp] != kNoRow ? ld[sp] : kInfF;
+        }
+      }
+      named_bar_sync(2 + h, kTcEpiWarps * 32);
+      for (uint32_t jj = ew; jj < 8 && h0 + jj < nq; jj += kTcEpiWarps) {
+        const uint32_t q = h0 + jj;
+        // warps 0|1 and 2|3: ascending 16 + reversed 16 = bitonic 32 -> clean
+        float x, y;
+        uint32_t xr, yr;
+        {
+          const int w0 = 0, w1 = 1;
+          const int src = upper ? 31 - lane : lane;
+          x = gmd[((upper ? w1 : w0) * 8 + jj) * 16 + (src & 15)];
+          xr = gmr[((upper ? w1 : w0) * 8 + jj) * 16 + (src & 15)];
+          y = gmd[((upper ? 3 : 2) * 8 + jj) * 16 + (src & 15)];
+          yr = gmr[((upper ? 3 : 2) * 8 + jj) * 16 + (src & 15)];
+        }
+        warp_clean(x, xr, lane, 16);
+        warp_clean(y, yr, lane, 16);
+        // best 32 of both: min(x, reversed y) is bitonic -> clean
+        const float ry = __shfl_sync(FULL, y, 31 - lane);
+        const uint32_t ryr = __shfl_sync(FULL, yr, 31 - lane);
+        if (cand_less(ry, ryr, x, xr)) {
+          x = ry;
+          xr = ryr;
+        }
+        warp_clean(x, xr, lane, 16);
+        const uint32_t m = q >> 5;
+        const uint32_t oslot = __shfl_sync(FULL, m ? w_slot[1] : w_slot[0], q & 31);
+        const float Ej = __shfl_sync(FULL, m ? w_E[1] : w_E[0], q & 31);
+        const uint32_t qij = __shfl_sync(FULL, m ? w_qi[1] : w_qi[0], q & 31);
+        P.out_d[(uint64_t)oslot * kKP + lane] = x;
+        P.out_row[(uint64_t)oslot * kKP + lane] = xr;
+        const uint32_t n_valid = __popc(__ballot_sync(FULL, xr != kNoRow));
+        const float last = __shfl_sync(FULL, x, 31);
+        const float gm = fminf(fminf(s_gm[h][0][q], s_gm[h][1][q]), fminf(s_gm[h][2][q], s_gm[h][3][q]));
+        const float w16 = fminf(fminf(s_w16[h][0][q], s_w16[h][1][q]), fminf(s_w16[h][2][q], s_w16[h][3][q]));
+        const float vk = __shfl_sync(FULL, x, (int)(P.topk ? P.topk - 1 : 0));
+        if (lane == 0) {
+          P.out_thr[oslot] = fminf(fminf(n_valid == kKP ? last : kInfF, gm), w16);
+          P.out_n[oslot] = n_valid;
+          if (P.bound_update && n_valid >= P.topk) {  // this item's k-th upper bound
+            float u = __fadd_ru(vk, Ej);
+            if (!(u > 0.f)) u = 0.f;
+            atomicMin(reinterpret_cast<int*>(P.qbound + qij), __float_as_int(u));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&iempty[slot]);
+      if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 9], (unsigned long long)(clock64() - _tm));
+    }
+  }
+}
+
+// kQ = 0: narrow (resident query group of <= 32, split precision possible);
+// kQ = 64 / 128: wide (query groups streamed with the list stages, single-pass
+// tf32; 128: 16-deep per-warp lists, two epilogue groups of 64 queries)
+template <int kQ>
 __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
-  // wide: warps 2-5 are a second epilogue group (queries 32..63 of the item)
+  // wide: warps 2-5 are a second epilogue group (queries kQ/2.. of the item)
   // instead of stagers/splitters; single-pass tf32 only
+  constexpr bool kWide = kQ != 0;
   constexpr int kMQ = kWide ? 8 : kMergeQ;
-  constexpr uint32_t kSB = kTcStageBytes + (kWide ? kWideQBytes : 0);  // ring stage bytes
+  constexpr uint32_t kSB = kTcStageBytes + kTcCps * kQ * 64;  // ring stage bytes (A tile [+ query slice])
+  constexpr uint32_t kAccW = kQ == 128 ? 128u : 64u;          // TMEM columns per accumulator buffer
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t dpad = P.ix.dpad;
@@ -251,7 +522,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   const bool split = !kWide && P.split != 0;
   // TMEM accumulator ring: split mode shares TMEM with the A_lo ring; single
   // mode spreads over the whole 512 columns to absorb epilogue jitter
-  const uint32_t nacc = split ? 2u : (uint32_t)kAccMax;
+  const uint32_t nacc = split ? 2u : (kQ == 128 ? 4u : (uint32_t)kAccMax);
   const uint32_t qblk = (split ? 2 : 1) * qmax * 64;                // per chunk: [raw rows | lo rows]
   uint8_t* aring = smem;                                            // SA x kSB (raw A [| query slice])
   uint8_t* qsm = smem + SA * kSB;                                   // nch x qblk (narrow only)
@@ -449,7 +720,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           if (lane == 0) TC_PROF_ADD(2);
         }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + tb * 64;  // accumulator columns [0, 128)
+        const uint32_t d_tmem = tmem_base + tb * kAccW;  // this tile's accumulator columns
         for (uint32_t sg = 0; sg < nstg; ++sg) {
           const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
           const uint32_t a = ra, pa = rpa, l = rl, pl = rpl;
@@ -621,6 +892,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         }
       }
     }
+  } else if constexpr (kQ == 128) {
+    epilogue128(P, tmem_base, nacc, tb, tph, ifull, iempty, tfull, tempty, s_item, s_valid,
+                reinterpret_cast<float*>(md), reinterpret_cast<uint32_t*>(mr), warp, lane);
   } else {
     // ---------------- epilogue warps ----------------
     // narrow: warps 6-9, queries 0..31.  wide: group h = 0 (warps 6-9) takes
@@ -876,15 +1150,16 @@ static int tc_budget() {
       optin = 232448;
     size_t st = 1024;
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_scan_tc<false>) == cudaSuccess) st = fa.sharedSizeBytes;
-    if (cudaFuncGetAttributes(&fa, k_scan_tc<true>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_scan_tc<0>) == cudaSuccess) st = fa.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa, k_scan_tc<64>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_scan_tc<128>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
     budget[dev] = optin - (int)st;
     have[dev] = true;
   }
   return budget[dev];
 }
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
-  const bool wide = qmax == kTcWideQ;  // no resident query group; two merge groups of 8
+  const bool wide = tc_is_wide(qmax);  // no resident query group; two merge groups of 8
   return 1024 + (wide ? 0 : (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64) +
          (wide ? 2 * 8 : kMergeQ) * kTcEpiWarps * 32 * 8 +       // merge scratch
          8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 16 +
@@ -892,7 +1167,7 @@ static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int left = tc_budget() - tc_fixed_bytes(dpad, qmax, split);
-  const int sb = kTcStageBytes + (qmax == kTcWideQ ? kWideQBytes : 0);
+  const int sb = kTcStageBytes + (tc_is_wide(qmax) ? kTcCps * (int)qmax * 64 : 0);
   return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / sb);
 }
 // option "tc_wide_ppl" (env HIVF_TC_WIDE_PPL sets the process default): the
@@ -904,12 +1179,22 @@ float tc_wide_ppl_default() {
   const char* e = getenv("HIVF_TC_WIDE_PPL");
   return e ? (float)atof(e) : 0.f;
 }
+// option "tc_wide2_ppl" (env HIVF_TC_WIDE2_PPL): the density above which the
+// wide scan takes 128-query groups (k_scan_tc<128>: a list probed by 65-128
+// queries is streamed once instead of twice; 3 ring stages of 64 KB)
+float tc_wide2_ppl_default() {
+  const char* e = getenv("HIVF_TC_WIDE2_PPL");
+  return e ? (float)atof(e) : 40.f;
+}
 
 uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list, const TcOpts& opt) {
   const uint32_t o = opt.qmax_override;
-  if (o && (o != kTcWideQ || !split) && tc_ring(dpad, o, split) >= 2) return o;
+  if (o && (!tc_is_wide(o) || !split) && tc_ring(dpad, o, split) >= 2) return o;
+  if (!split && opt.wide2_ppl >= 0.f && opt.wide_ppl >= 0.f && probes_per_list > opt.wide2_ppl &&
+      tc_ring(dpad, kTcWide2Q, 0) >= 3)
+    return kTcWide2Q;
   // dense batches, single pass: 64-query groups streamed with the list stages
-  // (k_scan_tc<true>) -- each list tile crosses HBM->smem once per 64 probes
+  // (k_scan_tc<64>) -- each list tile crosses HBM->smem once per 64 probes
   if (!split && opt.wide_ppl >= 0.f && probes_per_list > opt.wide_ppl && tc_ring(dpad, kTcWideQ, 0) >= 3)
     return kTcWideQ;
   // HBM-bound batches (few probes per list): the widest group that still
@@ -944,7 +1229,7 @@ int get_tc_prof(unsigned long long* host, int n_ctas) {
 int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list, const TcOpts& o) {
   const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list, o);
   return tc_fixed_bytes(dpad, q, split) +
-         (int)tc_ring(dpad, q, split) * (kTcStageBytes + (q == kTcWideQ ? kWideQBytes : 0));
+         (int)tc_ring(dpad, q, split) * (kTcStageBytes + (tc_is_wide(q) ? kTcCps * (int)q * 64 : 0));
 }
 
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
@@ -955,15 +1240,22 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     cudaStream_t s) {
   const uint32_t q = scan_tc_qmax(ix.dpad, split, probes_per_list, o);
   const int conv = tc_conversion_mode();
-  const bool wide = q == kTcWideQ;
+  const bool wide = tc_is_wide(q);
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
              out_n, q, tc_ring(ix.dpad, q, split), conv > 1 ? 0 : conv, o.variant,
              wide ? 0 : split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u,
              ws.qstage, ws.qshift};
   const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list, o);
-  smem_optin(wide ? (const void*)k_scan_tc<true> : (const void*)k_scan_tc<false>, smem);
-  if (wide) k_scan_tc<true><<<n_ctas, kTcThreads, smem, s>>>(P);
-  else k_scan_tc<false><<<n_ctas, kTcThreads, smem, s>>>(P);
+  if (q == kTcWide2Q) {
+    smem_optin((const void*)k_scan_tc<128>, smem);
+    k_scan_tc<128><<<n_ctas, kTcThreads, smem, s>>>(P);
+  } else if (wide) {
+    smem_optin((const void*)k_scan_tc<64>, smem);
+    k_scan_tc<64><<<n_ctas, kTcThreads, smem, s>>>(P);
+  } else {
+    smem_optin((const void*)k_scan_tc<0>, smem);
+    k_scan_tc<0><<<n_ctas, kTcThreads, smem, s>>>(P);
+  }
 }
 
 namespace {
@@ -980,15 +1272,15 @@ __global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs
                                                     const uint32_t* __restrict__ pair_off,
                                                     const uint32_t* __restrict__ list_cnt,
                                                     const uint32_t* __restrict__ qshift, uint8_t* qstage,
-                                                    uint32_t n_pairs) {
+                                                    uint32_t n_pairs, uint32_t G) {
   const uint32_t p = blockIdx.x * 8 + (threadIdx.x >> 5);  // one warp per pair
   if (p >= n_pairs) return;
   const uint32_t pair = sorted_pairs[p];
   const uint32_t c = pair_list[pair];
   const uint32_t local = p - pair_off[c], n = list_cnt[c];
-  const uint32_t g = local / kWideQ, row = local % kWideQ;
-  const uint32_t npad = min((uint32_t)kWideQ, ((n - g * kWideQ) + 7) & ~7u);
-  uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * kWideQ) * dpad * 4;
+  const uint32_t g = local / G, row = local % G;
+  const uint32_t npad = min(G, ((n - g * G) + 7) & ~7u);
+  uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * G) * dpad * 4;
   const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)pair_query[pair] * dpad);
   for (uint32_t g4 = threadIdx.x & 31; g4 < dpad / 4; g4 += 32) {
     const uint32_t ch = g4 >> 2, q4 = g4 & 3;
@@ -1007,7 +1299,7 @@ void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t*
                        const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s) {
   if (n_pairs)
     k_stage_wide<<<(n_pairs + 7) / 8, 256, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list,
-                                                   pair_off, list_cnt, ws.qshift, ws.qstage, n_pairs);
+                                                   pair_off, list_cnt, ws.qshift, ws.qstage, n_pairs, ws.group);
 }
 
 }  // namespace hivf

@@ -1,8 +1,11 @@
-"""GPU parity of the wide tensor-core scan (k_scan_tc<true>: 64-query groups
-streamed with the list stages, two epilogue groups) -- the dense-batch path
-(DESIGN.md "Dense batches").  Forced on with option tc_wide_ppl = 0 on the
-single-pass tf32 kernel; same bar as test_gpu_parity: ids bit-exact, distances
-bit-equal doubles against the C restatement of the reference."""
+"""GPU parity of the wide tensor-core scans -- the dense-batch path (DESIGN.md
+"Dense batches"): k_scan_tc<64> (64-query groups streamed with the list
+stages, two epilogue groups of 32 with 32-deep per-warp lists) and
+k_scan_tc<128> (128-query groups, two epilogue groups of 64 with 16-deep
+per-warp lists).  Forced on with options tc_wide_ppl = 0 and tc_wide2_ppl
+(-1: 64-query groups only, 0: 128-query groups always) on the single-pass
+tf32 kernel; same bar as test_gpu_parity: ids bit-exact, distances bit-equal
+doubles against the C restatement of the reference."""
 import numpy as np
 import pytest
 
@@ -11,8 +14,8 @@ from test_gpu_parity import _check_search, _random_index
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def ctx():
+@pytest.fixture(scope="module", params=[-1, 0], ids=["groups64", "groups128"])
+def ctx(request):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -20,13 +23,15 @@ def ctx():
     c = Context(0)
     c.set_option("scan_kernel", 3)
     c.set_option("tc_wide_ppl", 0)
+    c.set_option("tc_wide2_ppl", request.param)
     yield c
     c.set_option("tc_wide_ppl", 0)
+    c.set_option("tc_wide2_ppl", 40)
     c.set_option("scan_kernel", 0)
 
 
 # B x nprobe / K spans groups with < 8, 8..32 (second epilogue group idle),
-# 33..64 and > 64 (several groups) queries per list
+# 33..64, 65..128 and > 128 (several groups) queries per list
 @pytest.mark.parametrize("dim,n,K,nprobe,k,B", [
     (16, 3000, 32, 8, 10, 40),
     (48, 8000, 16, 16, 20, 90),
@@ -34,6 +39,8 @@ def ctx():
     (768, 30000, 64, 16, 10, 250),
     (100, 6000, 20, 20, 1, 70),
     (64, 9000, 24, 24, 32, 200),
+    (768, 40000, 32, 12, 10, 700),
+    (32, 20000, 8, 8, 16, 1000),
 ])
 def test_wide_scan_vs_oracle(ctx, dim, n, K, nprobe, k, B):
     rng = np.random.default_rng(dim * 13 + K + B)
