@@ -548,6 +548,18 @@ def run_hivf(args):
     value = B * args.steps / (ms / 1e3)
     outs = [tuple(t.cpu().numpy() for t in o) for o in outs_t]
     outs = [(a.view(np.uint64), b, c.view(np.uint32)) for a, b, c in outs]
+    # ---- optional scan stall counters (HIVF_TCPROF=<out.npy>; profiles/tcprof.py) ----
+    if os.environ.get("HIVF_TCPROF"):
+        from paper_2507_09138_b200 import lib
+        ctx.set_option("tc_prof", 1)
+        for i in range(args.steps):
+            step(i)
+        torch.cuda.synchronize()
+        prof = np.zeros((ctx.device_info()["sm_count"], 16), np.uint64)
+        lib().hivf_debug_tc_prof(prof.ctypes.data, prof.shape[0])
+        ctx.set_option("tc_prof", 0)
+        np.save(os.environ["HIVF_TCPROF"], prof)
+        log(f"scan stall counters over {args.steps} steps -> {os.environ['HIVF_TCPROF']}")
     # ---- per-kernel timing pass (events around each phase, inside the library) ----
     ctx.set_option("time_kernels", 1)
     ctx.set_option("reset_timers", 1)

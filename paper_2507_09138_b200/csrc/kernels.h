@@ -21,10 +21,10 @@ struct TcOpts {
   uint32_t qmax_override = 0;  // "tc_qmax": 0 auto
   float wide_ppl = 0.f;        // "tc_wide_ppl": probes/list above which the wide scan runs; < 0 never
   int variant = 0;             // "tc_variant" (debug, inexact when nonzero)
-  float wide2_ppl = 40.f;      // "tc_wide2_ppl": above it, 128-query groups; < 0 never
+  float wide2_ppl = 24.f;      // "tc_wide2_ppl": above it, 128-query groups; < 0 never
 };
 float tc_wide_ppl_default();   // env HIVF_TC_WIDE_PPL, else 0
-float tc_wide2_ppl_default();  // env HIVF_TC_WIDE2_PPL, else 40
+float tc_wide2_ppl_default();  // env HIVF_TC_WIDE2_PPL, else 24
 
 // One grouped-scan work item: rows [row0, row0+nrows) of list `list` (local
 // row numbers) against up to kQMax queries listed in item_pairs[pair0, pair0+nq).

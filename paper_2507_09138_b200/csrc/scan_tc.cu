@@ -1181,10 +1181,12 @@ float tc_wide_ppl_default() {
 }
 // option "tc_wide2_ppl" (env HIVF_TC_WIDE2_PPL): the density above which the
 // wide scan takes 128-query groups (k_scan_tc<128>: a list probed by 65-128
-// queries is streamed once instead of twice; 3 ring stages of 64 KB)
+// queries is streamed once instead of twice; 3 ring stages of 64 KB).  C3
+// measured (profiles/r2_c3_batch_sweep.txt): B=512 (16/list) equal, B=1024
+// (32/list) 91.2k -> 93.4k q/s, B=2048 110k -> 151k.
 float tc_wide2_ppl_default() {
   const char* e = getenv("HIVF_TC_WIDE2_PPL");
-  return e ? (float)atof(e) : 40.f;
+  return e ? (float)atof(e) : 24.f;
 }
 
 uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list, const TcOpts& opt) {

@@ -26,7 +26,7 @@ def ctx(request):
     c.set_option("tc_wide2_ppl", request.param)
     yield c
     c.set_option("tc_wide_ppl", 0)
-    c.set_option("tc_wide2_ppl", 40)
+    c.set_option("tc_wide2_ppl", 24)
     c.set_option("scan_kernel", 0)
 
 
