@@ -355,6 +355,8 @@ typedef struct {
   double scan_ms;              /* accumulated CUDA-event time: grouped list scan kernel */
   double finalize_ms;          /* accumulated CUDA-event time: re-rank + fallback kernels */
   uint32_t scan_kernel;        /* last call: 0 exact only, 1 FFMA, 2 tcgen05 split, 3 tcgen05 single */
+  uint32_t scan_group;         /* last call: queries per scan work item (8..32 narrow, 64 / 128 wide,
+                                  256 = the CTA-pair scan) */
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
@@ -362,10 +364,12 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * rest stays in pinned host memory, see residency),
  * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
  * 3 tcgen05 single-pass), "tc_qmax" (queries per scan work item: 8..32 step 8,
- * or 64 = the wide scan), "tc_wide_ppl" (probes per list above which a
+ * or 64 / 128 / 256 = the wide scans), "tc_wide_ppl" (probes per list above which a
  * single-pass batch uses the wide 64-query scan; default 0 = every single-pass
  * batch (measured faster at all densities), negative = never;
- * process default from env HIVF_TC_WIDE_PPL), "time_kernels" (record events
+ * process default from env HIVF_TC_WIDE_PPL), "tc_wide2_ppl" (above it 128-query
+ * groups, default 24, env HIVF_TC_WIDE2_PPL), "tc_pair_ppl" (above it 256-query
+ * groups on CTA pairs, default 96, env HIVF_TC_PAIR_PPL), "time_kernels" (record events
  * around each phase and accumulate into hivf_stats), "reset_timers",
  * "search_graph" (default 1: hivf_search captures a batch shape seen twice in
  * a row into a CUDA graph and replays it; any option write, buffer growth or
@@ -383,6 +387,10 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
  *   kind (0 FFMA, 2 split tensor-core, 3 single-pass tensor-core) at dim D.
  * hivf_debug_tc_prof: per-CTA stall counters of the last k_scan_tc launches. */
 int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, unsigned n, int split, float* out);
+/* hivf_debug_tc2_dot: the same for a CTA pair (cta_group::2, M = 256): A[256][D],
+ *   B[n][D] (n in {16, 32}); bsplit = 1 puts B rows [c*n/2, (c+1)*n/2) in CTA c,
+ *   0 puts all of B in both; out[256][n] (row r from CTA r / 128). */
+int hivf_debug_tc2_dot(const float* A, const float* B, unsigned D, unsigned n, int bsplit, float* out);
 int hivf_debug_bound(int kind, unsigned D, double* e_a, double* e_b, double* e_c);
 int hivf_debug_tc_prof(unsigned long long* out, int n_ctas);
 

@@ -33,7 +33,7 @@ SYMBOLS = [
     "hivf_set_option", "hivf_shard_plan", "hivf_shard_local_lists", "hivf_index_upload_shard",
     "hivf_group_create", "hivf_nccl_unique_id", "hivf_group_create_nccl", "hivf_group_create_hostcb",
     "hivf_group_destroy", "hivf_group_search_device", "hivf_group_search", "hivf_train_kmeans_sampled_seeds",
-    "hivf_index_row_distances", "hivf_debug_tc_dot", "hivf_debug_bound", "hivf_debug_tc_prof",
+    "hivf_index_row_distances", "hivf_debug_tc_dot", "hivf_debug_bound", "hivf_debug_tc_prof", "hivf_debug_tc2_dot",
 ]
 
 
@@ -56,7 +56,7 @@ class Stats(C.Structure):
                 ("n_fallback", C.c_uint32), ("n_unique_lists", C.c_uint32),
                 ("scan_bytes", C.c_uint64), ("timed_calls", C.c_uint32),
                 ("assign_ms", C.c_double), ("scan_ms", C.c_double), ("finalize_ms", C.c_double),
-                ("scan_kernel", C.c_uint32)]
+                ("scan_kernel", C.c_uint32), ("scan_group", C.c_uint32)]
 
 
 _lib = None
@@ -94,6 +94,7 @@ def lib():
         "hivf_index_cluster_sizes": (i32, [vp, vp]),
         "hivf_index_row_distances": (i32, [vp, vp]),
         "hivf_debug_tc_dot": (i32, [vp, vp, u32, u32, i32, vp]),
+        "hivf_debug_tc2_dot": (i32, [vp, vp, u32, u32, i32, vp]),
         "hivf_debug_bound": (i32, [i32, u32, P(f64), P(f64), P(f64)]),
         "hivf_debug_tc_prof": (i32, [vp, i32]),
         "hivf_assign": (i32, [vp, vp, u32, u32, vp, vp]),

@@ -238,12 +238,14 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->tc.variant = (int)value;
   } else if (!strcmp(name, "tc_qmax")) {  // tuning: queries per tensor-core work item
     if (value < 0 || (value > 32 && !tc_is_wide((uint32_t)value)) || value % 8)
-      return fail(HIVF_EINVAL, "tc_qmax: 0, 8..32 step 8, 64 or 128 (wide)");
+      return fail(HIVF_EINVAL, "tc_qmax: 0, 8..32 step 8, 64, 128 or 256 (wide)");
     ctx->tc.qmax_override = (uint32_t)value;
   } else if (!strcmp(name, "tc_wide_ppl")) {  // tuning: probes/list above which dense batches use
     ctx->tc.wide_ppl = (float)value;           // the wide (64-query) scan; negative = never
   } else if (!strcmp(name, "tc_wide2_ppl")) {  // tuning: probes/list above which the 128-query
     ctx->tc.wide2_ppl = (float)value;          // groups are used; negative = never
+  } else if (!strcmp(name, "tc_pair_ppl")) {   // tuning: probes/list above which 256-query groups
+    ctx->tc.pair_ppl = (float)value;           // run on CTA pairs (k_scan_pair); negative = never
   } else if (!strcmp(name, "time_kernels")) {
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->resolve_timers();
@@ -299,6 +301,7 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
     }
   }
   s.scan_kernel = ctx->last_kind;
+  s.scan_group = ctx->last_group;
   *out = s;
   return HIVF_OK;
 }
@@ -730,12 +733,24 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
 // topk > 0 (a search for the k nearest): the tensor-core scan shares a per-query
 // drop bound across items (scan_tc.cu); 0 (node-split items, seeded heaps) off.
 // item_bounds: node-split path -- fixed per-item bounds already in c->qbound
+// *slots_view: the view finalize / repair must read the candidate slots with
+// (the CTA-pair scan reports two slots per segment, IndexView::seg_split).
 static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pairs, bool timed,
-                            int kind_override = 0, uint32_t topk = 0, bool item_bounds = false) {
+                            int kind_override = 0, uint32_t topk = 0, bool item_bounds = false,
+                            IndexView* slots_view = nullptr) {
   hivf_ctx* c = ix->ctx;
   const int kind = kind_override ? kind_override : ix->scan_kind();
-  const IndexView v = ix->view_kind(kind);
-  const size_t nslots = (size_t)std::max<uint32_t>(n_pairs, 1) * ix->s_max;
+  IndexView v = ix->view_kind(kind);
+  // batch density estimate (host-side, no sync): pairs per list of the index
+  float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
+  const bool tc = kind != 1;
+  uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc) : (uint32_t)kQMax;
+  if (group == kTcPairQ) {
+    v.seg_split = 2;
+    v.s_max = 2 * ix->s_max;
+  }
+  if (slots_view) *slots_view = v;
+  const size_t nslots = (size_t)std::max<uint32_t>(n_pairs, 1) * v.s_max;
   CK(c->list_cnt.ensure(ix->K * 4ull));
   CK(c->list_poff.ensure(ix->K * 4ull));
   CK(c->list_cur.ensure(ix->K * 4ull));
@@ -751,12 +766,9 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   // slots of empty lists are never written by the scan; zero counts so the
   // finalize pass reads "no candidates" there
   CK(cudaMemsetAsync(c->cand_n.p, 0, nslots * 4, c->stream));
-  const bool tc = kind != 1;
-  // batch density estimate (host-side, no sync): pairs per list of the index
-  float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
-  uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc) : (uint32_t)kQMax;
   WideStage ws;
   ws.group = group;
+  c->last_group = group;
   if (tc_is_wide(group)) {
     // the restaged queries need (pairs + 7K) x D floats; when HBM is short
     // (index near the budget) the batch takes the narrow kernel instead
@@ -767,6 +779,10 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
       group = scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc);
       if (tc_is_wide(group)) return fail(HIVF_ENOMEM, "wide scan: query staging buffer");
       ws.group = group;
+      c->last_group = group;
+      v.seg_split = 1;  // narrow kernel: one slot per segment
+      v.s_max = ix->s_max;
+      if (slots_view) *slots_view = v;
     } else {
       ws.qshift = c->qshift.as<uint32_t>();
       ws.qstage = c->qwide.as<uint8_t>();
@@ -864,7 +880,8 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
     CKL();
   }
   if (!exact_only) {
-    if ((st = run_scan(ix, qv, np, true, 0, c->opt_no_bound ? 0 : k)) != HIVF_OK) return st;
+    IndexView vs = v;  // the candidate slots' view (two per segment after the CTA-pair scan)
+    if ((st = run_scan(ix, qv, np, true, 0, c->opt_no_bound ? 0 : k, false, &vs)) != HIVF_OK) return st;
     c->mark(2);
     CK(c->tau.ensure((size_t)n * 4));
     // in-place repair of segments whose completeness proof failed
@@ -880,7 +897,7 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
     CK(cudaMemsetAsync(c->rep_n.p, 0, 4, c->stream));
     RepairState R{c->rep_entries.as<uint64_t>(), c->rep_n.as<uint32_t>(), rep_cap, c->rep_cnt.as<uint32_t>(),
                   c->rep_d.as<double>(), c->rep_ids.as<uint64_t>(), per_q};
-    launch_finalize_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(),
+    launch_finalize_search(vs, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(),
                            c->cand_row.as<uint32_t>(), c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(),
                            d_ids_out, d_dists_out, d_counts_out, c->flags_f.as<int>(), c->tau.as<float>(),
                            &R, c->stream);
@@ -888,11 +905,11 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
     // pass-1 flags survive for the auto policy (flags2 carries the repair outcome)
     CK(c->flags2.ensure((size_t)n * 4));
     CK(cudaMemcpyAsync(c->flags2.p, c->flags_f.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream));
-    launch_repair(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
+    launch_repair(vs, qv, c->plans.as<uint32_t>(), nprobe, k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
                   c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), c->tau.as<float>(), R, c->sm_count * 4,
                   d_ids_out, d_dists_out, d_counts_out, c->flags2.as<int>(), c->stream);
     CKL();
-    launch_exact_search(v, qv, c->plans.as<uint32_t>(), nprobe, k, c->flags2.as<int>(), d_ids_out,
+    launch_exact_search(vs, qv, c->plans.as<uint32_t>(), nprobe, k, c->flags2.as<int>(), d_ids_out,
                         d_dists_out, d_counts_out, c->x_ids.as<uint64_t>(), c->x_d.as<double>(),
                         c->x_cnt.as<uint32_t>(), c->x_tot.as<uint64_t>(), c->tau.as<float>(), c->stream);
     CKL();
@@ -1430,8 +1447,9 @@ hivf_status hivf_scan_items(hivf_index* ix, const float* queries, uint32_t n_ite
       launch_item_bounds(d_hd, d_hn, d_k, heap_stride, n_items, c->qbound.as<float>(), s);
       CKL();
     }
-    if ((st = run_scan(ix, qv, n_pairs, false, 0, use_bounds ? 1u : 0u, use_bounds)) != HIVF_OK) return st;
-    launch_finalize_items(v, qv, n_items, d_off, d_cl, d_k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
+    IndexView vs = v;  // the candidate slots' view
+    if ((st = run_scan(ix, qv, n_pairs, false, 0, use_bounds ? 1u : 0u, use_bounds, &vs)) != HIVF_OK) return st;
+    launch_finalize_items(vs, qv, n_items, d_off, d_cl, d_k, c->cand_d.as<float>(), c->cand_row.as<uint32_t>(),
                           c->cand_thr.as<float>(), c->cand_n.as<uint32_t>(), d_hi, d_hd, d_hn, heap_stride, d_ch,
                           d_fb, s);
     CKL();

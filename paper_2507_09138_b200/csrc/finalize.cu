@@ -69,8 +69,7 @@ __device__ void block_sort_pairs(double* d, IdT* id, uint32_t n) {
 }
 
 __device__ __forceinline__ uint32_t nseg_of(const IndexView& ix, uint32_t c) {
-  const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
-  return (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+  return slots_of(ix, ix.list_off[c + 1] - ix.list_off[c]);
 }
 
 // One CTA per query.
@@ -116,7 +115,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
       const uint32_t c = plans[(uint64_t)b * nprobe + p];
       const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
       pc[p] = c;
-      pns[p] = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+      pns[p] = slots_of(ix, rows);
       pE[p] = seg_bound(ix, qn, ix.maxnorm[c]);
       tot += rows;
     }
@@ -328,9 +327,9 @@ __global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView
     const uint32_t p = t / ix.s_max, sg = t % ix.s_max;
     const uint32_t c = plans[(uint64_t)b * nprobe + p];
     const uint64_t beg = ix.list_off[c], n_c = ix.list_off[c + 1] - beg;
-    const uint64_t s0 = (uint64_t)sg * ix.seg_rows, s1 = min(n_c, s0 + ix.seg_rows);
-    const uint64_t lr = s0 + (uint64_t)ch * kRepChunk + threadIdx.x;
-    if (s0 + (uint64_t)ch * kRepChunk >= s1) continue;
+    const uint64_t s0 = (uint64_t)(sg / ix.seg_split) * ix.seg_rows;
+    if (s0 + (uint64_t)ch * kRepChunk * ix.seg_split >= n_c) continue;  // chunk past the list
+    const uint64_t lr = slot_row(ix, sg, n_c, (uint64_t)ch * kRepChunk + threadIdx.x);
     const float tq = tau[b];
     const float* qs = qv.qs + (uint64_t)b * ix.dpad;
     double E;
@@ -338,7 +337,7 @@ __global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView
       const double q = qv.qnorm[b], x = ix.maxnorm[c];
       E = fa * q * x + fb * (q * q + x * x) + fc;
     }
-    if (lr >= s1) continue;
+    if (lr == ~0ull) continue;
     const float* lb = list_base(ix, c, beg);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll 16
@@ -402,7 +401,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_repair(
     const uint32_t c = plans[(uint64_t)b * nprobe + p];
     const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
     if (lane == 0) atomicAdd(&s_total, (unsigned long long)rows);
-    const uint32_t ns = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+    const uint32_t ns = slots_of(ix, rows);
     const float E = seg_bound(ix, qn, ix.maxnorm[c]);
     for (uint32_t sg = 0; sg < ns; ++sg) {
       const uint64_t slot = slot0 + (uint64_t)p * ix.s_max + sg;

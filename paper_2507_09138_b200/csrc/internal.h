@@ -118,7 +118,7 @@ struct hivf_ctx {
   // the rest stays in a pinned host backing store read over PCIe
   uint64_t opt_hbm_list_budget = 0;
   int tc_conv = 2;  // this device's fp32->tf32 operand conversion (tc_conversion_mode)
-  TcOpts tc{0, tc_wide_ppl_default(), 0, tc_wide2_ppl_default()};  // tensor-core scan tuning (tc_qmax, tc_wide_ppl, tc_variant)
+  TcOpts tc{0, tc_wide_ppl_default(), 0, tc_wide2_ppl_default(), tc_pair_ppl_default()};  // tensor-core scan tuning (tc_qmax, tc_wide_ppl, tc_variant)
   // scratch
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
@@ -130,6 +130,7 @@ struct hivf_ctx {
   uint32_t last_K = 0;
   const hivf_index* last_index = nullptr;
   uint32_t last_kind = 0;
+  uint32_t last_group = 0;  // queries per scan work item of the last scan
   bool stats_adapted = false;
   // phase timing (option "time_kernels"): one event set per call, resolved lazily
   int opt_time = 0;
@@ -261,6 +262,7 @@ struct hivf_index {
     v.N = N;
     v.seg_rows = seg_rows;
     v.s_max = s_max;
+    v.seg_split = 1;
     v.metric = metric;
     return v;
   }

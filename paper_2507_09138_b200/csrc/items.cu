@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
       const uint32_t c = clusters[j0 + j];
       const float E = seg_bound(ix, qn, ix.maxnorm[c]);
       const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
-      const uint32_t ns = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
+      const uint32_t ns = slots_of(ix, rows);
       float lj = kInf;
       for (uint32_t s = 0; s < ns; ++s) {
         const uint64_t slot = (uint64_t)(j0 + j) * ix.s_max + s;

@@ -22,9 +22,11 @@ struct TcOpts {
   float wide_ppl = 0.f;        // "tc_wide_ppl": probes/list above which the wide scan runs; < 0 never
   int variant = 0;             // "tc_variant" (debug, inexact when nonzero)
   float wide2_ppl = 24.f;      // "tc_wide2_ppl": above it, 128-query groups; < 0 never
+  float pair_ppl = 96.f;       // "tc_pair_ppl": above it, 256-query groups on CTA pairs; < 0 never
 };
 float tc_wide_ppl_default();   // env HIVF_TC_WIDE_PPL, else 0
 float tc_wide2_ppl_default();  // env HIVF_TC_WIDE2_PPL, else 24
+float tc_pair_ppl_default();   // env HIVF_TC_PAIR_PPL, else 96
 
 // One grouped-scan work item: rows [row0, row0+nrows) of list `list` (local
 // row numbers) against up to kQMax queries listed in item_pairs[pair0, pair0+nq).
@@ -55,7 +57,11 @@ struct IndexView {
   uint32_t dim, dpad, K;
   uint64_t N;
   uint32_t seg_rows;        // rows per scan segment (multiple of kRowBlock)
-  uint32_t s_max;           // max segments per list
+  uint32_t s_max;           // max candidate slots per list (segments x seg_split)
+  // candidate slots per segment: 1, or 2 for the CTA-pair scan (k_scan_pair),
+  // whose CTA c reports the segment's 128-row tiles of parity c as slot
+  // 2*segment + c (slot_rows below)
+  uint32_t seg_split;
   int metric;
   // filter bound of the scan kernel that produced the candidates:
   // |d32 - delta| <= e_a*|q|*|x| + e_b*(|q|^2 + |x|^2) + e_c
@@ -63,6 +69,22 @@ struct IndexView {
 };
 
 #ifdef __CUDACC__
+// candidate slots of a list of `rows` rows
+__device__ __forceinline__ uint32_t slots_of(const IndexView& ix, uint64_t rows) {
+  return (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows) * ix.seg_split;
+}
+// i-th row (list-local) of slot `slot` of a list with n_c rows, or ~0 past its end
+__device__ __forceinline__ uint64_t slot_row(const IndexView& ix, uint32_t slot, uint64_t n_c, uint64_t i) {
+  const uint64_t s0 = (uint64_t)(slot / ix.seg_split) * ix.seg_rows;
+  const uint64_t s1 = n_c < s0 + ix.seg_rows ? n_c : s0 + ix.seg_rows;
+  uint64_t r;
+  if (ix.seg_split == 1) {
+    r = s0 + i;
+  } else {  // tiles of parity slot % 2
+    r = s0 + ((i >> 7) * 2 + (slot & 1)) * 128 + (i & 127);
+  }
+  return r < s1 ? r : ~0ull;
+}
 // base of list c's chunk-major block (swz_offset(0, n_c, row, d) indexes into it)
 __device__ __forceinline__ const float* list_base(const IndexView& ix, uint32_t c, uint64_t lbeg) {
   return ix.list_ptr ? ix.list_ptr[c] : ix.vec + lbeg * ix.dpad;
@@ -138,7 +160,10 @@ constexpr uint32_t kTcWideQ = 64;
 // 128-query groups (k_scan_tc<128>, dense batches): half as many list passes
 // as 64-query groups, 16-deep per-warp candidate lists
 constexpr uint32_t kTcWide2Q = 128;
-inline bool tc_is_wide(uint32_t q) { return q == kTcWideQ || q == kTcWide2Q; }
+// 256-query groups on a CTA pair (k_scan_pair, cta_group::2), densest batches;
+// candidate slots per segment x2 (IndexView::seg_split)
+constexpr uint32_t kTcPairQ = 256;
+inline bool tc_is_wide(uint32_t q) { return q == kTcWideQ || q == kTcWide2Q || q == kTcPairQ; }
 struct WideStage {
   uint8_t* qstage = nullptr;  // wide_stage_rows() x dpad floats
   uint32_t* qshift = nullptr;

@@ -286,6 +286,13 @@ __global__ void k_count_pairs(const uint32_t* pair_list, uint32_t n_pairs, uint3
   if (p < n_pairs) atomicAdd(&cnt[pair_list[p]], 1u);
 }
 
+// Staged query rows a list reserves for the wide scans: 8-row aligned blocks,
+// 16-row aligned for the CTA-pair scan's 256-query groups (each CTA of the
+// pair takes half of a group's padded rows).
+__device__ __forceinline__ uint32_t qpad(uint32_t n, uint32_t group) {
+  return group >= 256 ? (n + 15) & ~15u : (n + 7) & ~7u;
+}
+
 // Single CTA: exclusive scans (in list_order, largest lists first) of the pair
 // counts and of the work items each list generates.
 __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t group,
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
     const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
     tp += n;
     ti += n ? nseg * ((n + group - 1) / group) : 0;
-    tq += (n + 7) & ~7u;
+    tq += qpad(n, group);
   }
   sp[threadIdx.x] = tp;
   si[threadIdx.x] = ti;
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
     if (qshift) qshift[c] = oq - op;
     op += n;
     oi += n ? nseg * ((n + group - 1) / group) : 0;
-    oq += (n + 7) & ~7u;
+    oq += qpad(n, group);
   }
   if (threadIdx.x == 1023) {
     *n_items = si[1023];
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(1024) k_worklist_fused(IndexView ix, uint32_t 
     const uint32_t nseg = (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows);
     tp += n;
     ti += n ? nseg * ((n + group - 1) / group) : 0;
-    tq += (n + 7) & ~7u;
+    tq += qpad(n, group);
   }
   sp[threadIdx.x] = tp;
   si[threadIdx.x] = ti;
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(1024) k_worklist_fused(IndexView ix, uint32_t 
     }
     op += n;
     oi += n ? nseg * ((n + group - 1) / group) : 0;
-    oq += (n + 7) & ~7u;
+    oq += qpad(n, group);
   }
   if (threadIdx.x == 1023) {
     *n_items = si[1023];

@@ -1135,12 +1135,475 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
 
 }  // namespace
 
+// ===========================================================================
+// k_scan_pair: the wide scan on a CTA PAIR (cluster of 2, tcgen05 cta_group::2)
+// for the densest batches -- query groups of up to 256 per list tile.
+//
+// One tcgen05.mma.cta_group::2 (issued by the leader CTA) multiplies M = 256
+// rows x N = 256 queries x K = 8: CTA c supplies its own 128 rows (A) and
+// queries [c*N/2, (c+1)*N/2) of the group (its half of B), and receives its
+// 128 rows x all N columns in its own TMEM (layout measured by
+// hivf_debug_tc2_dot).  So each SM streams 32 KB of list + 32 KB of query
+// slice per 64-dim stage for 128 x 256 dot products -- half the SM ingress per
+// dot product of the single-CTA 128-query scan, and one list pass for up to
+// 256 probing queries.
+//
+// Rows: CTA c takes the 128-row tiles of parity c of each segment and reports
+// them as candidate slot 2*segment + c (IndexView::seg_split = 2: finalize and
+// repair address the same rows through slots_of / slot_row), so the two CTAs
+// never merge candidates.  Work: pair p walks items p, p + P, ... (P pairs;
+// both CTAs compute the same sequence, the work list is LPT-ordered).
+//
+// Per CTA, 10 warps: warp 0 producer (own A tile + own half of the query
+// slice per stage into a 3-deep 64 KB ring); warp 1 = MMA issuer in the
+// leader, relay in the peer (forwards "my stage landed" to the leader's pfull
+// barrier); warps 2-9 = two epilogue groups of 128 queries with 8-deep
+// per-warp lists (register slot s: queries 4s..4s+3, 8 lanes each).
+// Cross-CTA barriers: the leader's tcgen05.commit multicasts `empty` and
+// `tfull` to both CTAs; the peer's relay and epilogue arrive remotely on the
+// leader's `pfull` / `tempty`.
+// ===========================================================================
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t tf32_idesc_m(uint32_t m, uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+constexpr uint32_t kPairQ = 256;
+constexpr int kPG = 4;                        // epilogue groups (4 warps each, one per TMEM lane quadrant)
+constexpr int kPQ = (int)kPairQ / kPG;        // query columns per group
+constexpr int kPairThreads = (2 + kPG * kTcEpiWarps) * 32;
+constexpr int kPairQB = kTcCps * 128 * 64;  // one CTA's half of a 256-query slice (32 KB)
+
+__device__ __forceinline__ uint32_t mapa_peer(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// One tile's candidates of a query quad (4 queries, inf = not a candidate)
+// merged into the quad's 8-deep lists (lanes 8j..8j+7: query j).
+__device__ __noinline__ Cand merge_quad8(float s0, float s1, float s2, float s3, uint32_t grow, float yv,
+                                         uint32_t yr, int lane) {
+  float xv = kInfF;
+  uint32_t xr = kNoRow;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float sv = j == 0 ? s0 : j == 1 ? s1 : j == 2 ? s2 : s3;
+    uint32_t sr = sv < kInfF ? grow : kNoRow;
+    if (__any_sync(FULL, sr != kNoRow)) warp_sort32(sv, sr, lane);
+    const float bv = __shfl_sync(FULL, sv, lane & 7);  // best 8 of query j
+    const uint32_t br = __shfl_sync(FULL, sr, lane & 7);
+    if ((lane >> 3) == j) {
+      xv = bv;
+      xr = br;
+    }
+  }
+  // per 8-lane group: min(list, reversed candidates) is bitonic -> clean 4..1
+  const float rv = __shfl_xor_sync(FULL, xv, 7);
+  const uint32_t rr = __shfl_xor_sync(FULL, xr, 7);
+  if (cand_less(rv, rr, yv, yr)) {
+    yv = rv;
+    yr = rr;
+  }
+  warp_clean(yv, yr, lane, 4);
+  return Cand{yv, yr};
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_scan_pair(TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kSB = kTcStageBytes + kPairQB;  // A tile + this CTA's half query slice
+  const uint32_t dpad = P.ix.dpad;
+  const uint32_t nch = dpad / kChunk;
+  const uint32_t nstg = (nch + kTcCps - 1) / kTcCps;
+  const uint32_t SA = P.sa;
+  uint8_t* aring = smem;
+  float* md = reinterpret_cast<float*>(smem + SA * kSB);  // merge scratch [kPG groups][4 warps][8 q][8]
+  uint32_t* mr = reinterpret_cast<uint32_t*>(md + kPG * kTcEpiWarps * 8 * 8);
+  __shared__ uint64_t full[kTcMaxA], empty[kTcMaxA], pfull[kTcMaxA], tfull[2], tempty[2];
+  __shared__ uint64_t ifull[kItemQ], iempty[kItemQ];
+  __shared__ ScanItem s_item[kItemQ];
+  __shared__ int s_valid[kItemQ];
+  __shared__ uint32_t s_tmem;
+  __shared__ float s_gm[kPG][kTcEpiWarps][kPQ];
+  __shared__ float s_w8[kPG][kTcEpiWarps][kPQ];
+  // per-query metadata of the current item, [item parity][group][query]
+  __shared__ float s_qn2[2][kPG][kPQ], s_E[2][kPG][kPQ];
+  __shared__ uint32_t s_qi[2][kPG][kPQ], s_oslot[2][kPG][kPQ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const uint32_t pair_id = blockIdx.x >> 1, n_pairs_grid = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < SA; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&pfull[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kPG * kTcEpiWarps);  // both CTAs' epilogue warps
+    }
+    for (int i = 0; i < kItemQ; ++i) {
+      mbar_init(&ifull[i], 1);
+      mbar_init(&iempty[i], 1 + kPG * kTcEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = s_tmem;
+  if (P.prof && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.prof[blockIdx.x * 16 + 5] = g;
+  }
+
+  uint32_t ra = 0, rpa = 0;
+  uint32_t tb = 0, tph = 0;
+  if (warp == 0) {
+    // ---------------- producer: static item sequence, own A tiles + own query half ----------------
+    if (lane == 0) {
+      const uint32_t n_items = *P.n_items;
+      for (uint32_t i = 0;; ++i) {
+        const uint32_t it = pair_id + i * n_pairs_grid;
+        const bool valid = it < n_items;
+        const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+        mbar_wait(&iempty[slot], iph ^ 1);
+        ScanItem item{};
+        if (valid) item = P.items[it];
+        s_item[slot] = item;
+        s_valid[slot] = valid;
+        mbar_arrive(&ifull[slot]);
+        if (!valid) break;
+        if (P.prof) P.prof[blockIdx.x * 16 + 7] += 1;
+        const uint64_t lbeg = P.ix.list_off[item.list];
+        const uint64_t n_c = P.ix.list_off[item.list + 1] - lbeg;
+        const float* lbase = list_base(P.ix, item.list, lbeg);
+        const uint32_t npad = (item.nq + 15) & ~15u, hrows = npad / 2;
+        const uint32_t qbytes = hrows * 64;  // per chunk, this CTA's half
+        // the group's staged block: [half][ch][hrows][64 B]
+        const uint8_t* qsrc = P.qstage + (uint64_t)(item.pair0 + P.qshift[item.list]) * dpad * 4 +
+                              (uint64_t)crank * nch * qbytes;
+        const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
+        const uint32_t npt = (ntiles + 1) / 2;
+        for (uint32_t pt = 0; pt < npt; ++pt) {
+          const uint32_t t = 2 * pt + crank;  // this CTA's tile of the pair-tile
+          const uint32_t r0 = item.row0 + t * kTcTile;
+          const uint32_t nr = t < ntiles ? min((uint32_t)kTcTile, item.nrows - t * kTcTile) : 0u;
+          for (uint32_t sg = 0; sg < nstg; ++sg) {
+            const uint32_t c0 = sg * kTcCps, cn = min((uint32_t)kTcCps, nch - c0);
+            const uint32_t a = ra, pa = rpa;
+            {
+              TC_PROF_T0();
+              mbar_wait(&empty[a], pa ^ 1);
+              TC_PROF_ADD(3);
+            }
+            mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4 + cn * qbytes);
+            if (nr == kTcTile) {
+              bulk_g2s(aring + a * kSB, lbase + tile_chunk_offset(n_c, dpad, r0, c0), cn * kTcChunkBytes,
+                       &full[a]);
+            } else if (nr) {
+              for (uint32_t c = 0; c < cn; ++c)
+                bulk_g2s(aring + a * kSB + c * kTcChunkBytes, lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c),
+                         nr * kChunk * 4, &full[a]);
+            }
+            bulk_g2s(aring + a * kSB + kTcStageBytes, qsrc + (uint64_t)c0 * qbytes, cn * qbytes, &full[a]);
+            if (++ra == SA) { ra = 0; rpa ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- leader: MMA issuer; peer: relay of landed stages ----------------
+    const uint32_t pfull_peer0 = leader ? 0u : mapa_peer(&pfull[0], 0);
+    const uint32_t tmask_idesc = 0;  // (unused)
+    (void)tmask_idesc;
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+      mbar_wait(&ifull[slot], iph);
+      if (!__shfl_sync(FULL, s_valid[slot], 0)) break;
+      const uint32_t nq_i = __shfl_sync(FULL, s_item[slot].nq, 0);
+      const uint32_t nrows_i = __shfl_sync(FULL, s_item[slot].nrows, 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&iempty[slot]);
+      const uint32_t npad = (nq_i + 15) & ~15u;
+      const uint32_t ntiles = (nrows_i + kTcTile - 1) / kTcTile;
+      const uint32_t npt = (ntiles + 1) / 2;
+      const uint32_t idesc = tf32_idesc_m(256, npad);
+      const uint64_t adesc0 = sw64_kmajor_desc(smem_u32(aring));
+      for (uint32_t pt = 0; pt < npt; ++pt) {
+        if (leader) {
+          TC_PROF_T0();
+          mbar_wait_cl(&tempty[tb], tph ^ 1);
+          if (lane == 0) TC_PROF_ADD(2);
+          tc_fence_after();
+        }
+        const uint32_t d_tmem = tmem_base + tb * 256;
+        for (uint32_t sg = 0; sg < nstg; ++sg) {
+          const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
+          const uint32_t a = ra, pa = rpa;
+          if (leader) {
+            {
+              TC_PROF_T0();
+              mbar_wait(&full[a], pa);        // own stage landed
+              if (lane == 0) TC_PROF_ADD(1);
+            }
+            {
+              TC_PROF_T0();
+              mbar_wait_cl(&pfull[a], pa);    // the peer's stage landed
+              if (lane == 0) TC_PROF_ADD(0);
+            }
+            tc_fence_after();
+            const long long _ti = P.prof ? clock64() : 0;
+            const uint64_t adesc = adesc0 + (uint64_t)(a * (kSB >> 4));
+            const uint64_t qd0 = adesc + (uint64_t)(kTcStageBytes >> 4);
+#pragma unroll
+            for (uint32_t c = 0; c < (uint32_t)kTcCps; ++c) {
+              if (c >= cn) break;
+              const uint64_t qd = qd0 + (uint64_t)(c * (npad / 2 * 4));  // (npad/2)*64 B per chunk
+#pragma unroll
+              for (uint32_t k2 = 0; k2 < 2; ++k2) {
+                const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
+                if (lane == 0) mma2_tf32(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
+              }
+            }
+            if (lane == 0) mma2_commit_both(&empty[a]);  // the slot is free in both CTAs
+            __syncwarp();
+            if (P.prof && lane == 0) {
+              atomicAdd(&P.prof[blockIdx.x * 16 + 12], (unsigned long long)(clock64() - _ti));
+              atomicAdd(&P.prof[blockIdx.x * 16 + 13], 1ull);
+            }
+          } else {
+            mbar_wait(&full[a], pa);
+            if (lane == 0) mbar_arrive_remote(pfull_peer0 + a * 8);
+            __syncwarp();
+          }
+          if (++ra == SA) { ra = 0; rpa ^= 1; }
+        }
+        if (leader) {
+          if (lane == 0) mma2_commit_both(&tfull[tb]);
+          __syncwarp();
+        }
+        if (++tb == 2) { tb = 0; tph ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue: two groups of 128 queries, 8-deep per-warp lists ----------------
+    const uint32_t quad = warp & 3;                 // TMEM lane quadrant of this warp
+    const uint32_t ew = (warp - 2) & 3;             // warp within its group
+    const uint32_t h = (uint32_t)(warp - 2) >> 2;   // group: query columns [kPQ h, kPQ (h+1))
+    const uint32_t tempty_leader = mapa_peer(&tempty[0], 0);
+    float* gmd = md + h * (kTcEpiWarps * 8 * 8);
+    uint32_t* gmr = mr + h * (kTcEpiWarps * 8 * 8);
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t slot = i % kItemQ, iph = (i / kItemQ) & 1;
+      mbar_wait_parked(&ifull[slot], iph);
+      if (!s_valid[slot]) break;
+      const ScanItem item = s_item[slot];
+      const uint32_t nq = item.nq > kPQ * h ? min((uint32_t)kPQ, item.nq - kPQ * h) : 0u;
+      const uint32_t ip = i & 1;
+      float* m_qn2 = s_qn2[ip][h];
+      float* m_E = s_E[ip][h];
+      uint32_t* m_qi = s_qi[ip][h];
+      uint32_t* m_oslot = s_oslot[ip][h];
+      {  // the group's per-query metadata (warp ew owns queries 16 ew .. 16 ew + 15)
+        const uint32_t q = 16 * ew + lane;
+        if (lane < 16 && q < nq) {
+          const uint32_t pair = P.sorted_pairs[item.pair0 + kPQ * h + q];
+          const uint32_t qi = P.pair_query[pair];
+          m_qi[q] = qi;
+          m_qn2[q] = P.qv.qn2[qi];
+          m_oslot[q] = pair * P.ix.s_max + 2 * item.seg + crank;
+          m_E[q] = seg_bound(P.ix, P.qv.qnorm[qi], P.ix.maxnorm[item.list]);
+        }
+        named_bar_sync(2 + h, kTcEpiWarps * 32);
+      }
+      const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
+      const uint32_t npt = (ntiles + 1) / 2;
+      const uint64_t lbeg = P.ix.list_off[item.list];
+      float ld[kPQ / 4];  // slot s: queries 4s..4s+3, 8 lanes each
+      uint32_t lr[kPQ / 4];
+#pragma unroll
+      for (int j = 0; j < kPQ / 4; ++j) {
+        ld[j] = kInfF;
+        lr[j] = kNoRow;
+      }
+      float gmin[2] = {kInfF, kInfF};
+      for (uint32_t pt = 0; pt < npt; ++pt) {
+        const uint32_t t = 2 * pt + crank;
+        const uint32_t srow = t * kTcTile + quad * 32 + lane;  // segment-local row
+        const bool valid = srow < item.nrows;
+        const float xn = valid ? __ldg(P.ix.xnorm2 + lbeg + item.row0 + srow) : 0.f;
+        {
+          TC_PROF_T0();
+          mbar_wait_parked(&tfull[tb], tph);
+          if (lane == 0) TC_PROF_ADD(8);
+        }
+        tc_fence_after();
+        const long long _te = P.prof ? clock64() : 0;
+        float gl[2] = {kInfF, kInfF};
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          if (P.topk && 32 * m + lane < nq) {
+            const float u = __ldcg(P.qbound + m_qi[32 * m + lane]);
+            if (u < 3.0e38f) gl[m] = drop_bound(u, m_E[32 * m + lane]);
+          }
+          gmin[m] = fminf(gmin[m], gl[m]);
+        }
+        const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
+        const uint32_t ta = tmem_base + ((quad * 32) << 16) + tb * 256 + kPQ * h;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {  // 32 query columns at a time
+          if (32 * m >= (int)nq) break;
+          uint32_t acc[32];
+          TMEM_LD32(ta + 32 * m, acc);
+          tmem_wait_ld();
+#pragma unroll
+          for (int sl = 0; sl < 8; ++sl) {  // query quad (4sp .. 4sp+3), sp = 8m + sl
+            const int sp = 8 * m + sl;
+            if (4 * sp >= (int)nq) break;
+            float v[4];
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int q = 4 * sp + j;  // group-local query; acc column q & 31
+              const float q2 = q < (int)nq ? m_qn2[q] : 0.f;
+              const float g = __shfl_sync(FULL, gl[m], q & 31);
+              const float th = fminf(__shfl_sync(FULL, ld[sp], 8 * j + 7), g);
+              const float x = (valid && q < (int)nq)
+                                  ? __fmaf_rn(-2.f, __uint_as_float(acc[q & 31]), __fadd_rn(xn, q2))
+                                  : kInfF;
+              v[j] = x < th ? x : kInfF;
+              any |= x < th;
+            }
+            if (!__any_sync(FULL, any)) continue;
+            const Cand r = merge_quad8(v[0], v[1], v[2], v[3], grow, ld[sp], lr[sp], lane);
+            ld[sp] = r.v;
+            lr[sp] = r.r;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[tb]);
+          else mbar_arrive_remote(tempty_leader + tb * 8);
+          if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 11], (unsigned long long)(clock64() - _te));
+        }
+        if (++tb == 2) { tb = 0; tph ^= 1; }
+      }
+      // ---- item end: the four warps' 8-lists of each query -> its 32 candidates ----
+      const long long _tm = P.prof ? clock64() : 0;
+#pragma unroll
+      for (int h0 = 0; h0 < kPQ; h0 += 8) {
+        if (h0 >= (int)nq) break;
+        named_bar_sync(2 + h, kTcEpiWarps * 32);
+        if (h0 == 0) {
+#pragma unroll
+          for (int m = 0; m < 2; ++m) s_gm[h][ew][32 * m + lane] = gmin[m];
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int q = h0 + jj;
+          const int sp = q >> 2;
+          if ((lane >> 3) == (q & 3)) {
+            gmd[(ew * 8 + jj) * 8 + (lane & 7)] = ld[sp];
+            gmr[(ew * 8 + jj) * 8 + (lane & 7)] = lr[sp];
+            if ((lane & 7) == 7) s_w8[h][ew][q] = lr[sp] != kNoRow ? ld[sp] : kInfF;
+          }
+        }
+        named_bar_sync(2 + h, kTcEpiWarps * 32);
+        for (uint32_t jj = ew; jj < 8 && h0 + jj < nq; jj += kTcEpiWarps) {
+          const uint32_t q = h0 + jj;
+          float x = gmd[((lane >> 3) * 8 + jj) * 8 + (lane & 7)];
+          uint32_t xr = gmr[((lane >> 3) * 8 + jj) * 8 + (lane & 7)];
+          warp_sort32(x, xr, lane);
+          const uint32_t oslot = m_oslot[q];
+          const float Ej = m_E[q];
+          const uint32_t qij = m_qi[q];
+          P.out_d[(uint64_t)oslot * kKP + lane] = x;
+          P.out_row[(uint64_t)oslot * kKP + lane] = xr;
+          const uint32_t n_valid = __popc(__ballot_sync(FULL, xr != kNoRow));
+          const float gm = fminf(fminf(s_gm[h][0][q], s_gm[h][1][q]), fminf(s_gm[h][2][q], s_gm[h][3][q]));
+          const float w8 = fminf(fminf(s_w8[h][0][q], s_w8[h][1][q]), fminf(s_w8[h][2][q], s_w8[h][3][q]));
+          const float vk = __shfl_sync(FULL, x, (int)(P.topk ? P.topk - 1 : 0));
+          if (lane == 0) {
+            P.out_thr[oslot] = fminf(gm, w8);
+            P.out_n[oslot] = n_valid;
+            if (P.bound_update && n_valid >= P.topk) {
+              float u = __fadd_ru(vk, Ej);
+              if (!(u > 0.f)) u = 0.f;
+              atomicMin(reinterpret_cast<int*>(P.qbound + qij), __float_as_int(u));
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&iempty[slot]);
+        if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 9], (unsigned long long)(clock64() - _tm));
+      }
+    }
+  }
+  if (P.prof && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.prof[blockIdx.x * 16 + 6] = g;
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with TMEM and the cross-CTA barriers
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
 // Shared-memory plan: the unsplit query group stays resident for the whole
 // item; what is left feeds the A landing ring (bytes in flight per SM).
 // Dynamic smem budget = the device's opt-in per-block maximum (227 KB on B200)
 // minus the kernel's static __shared__ variables, queried once.
-static int tc_budget() {
-  static int budget[kMaxDevices];
+// Per kernel (by its query-group size q): narrow 8..32, wide 64 / 128, pair 256.
+static int tc_budget(uint32_t q) {
+  static int budget[kMaxDevices][4];
   static bool have[kMaxDevices] = {};
   const int dev = current_device();
   if (dev < 0 || dev >= kMaxDevices) return 0;
@@ -1148,26 +1611,31 @@ static int tc_budget() {
     int optin = 232448;
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
       optin = 232448;
-    size_t st = 1024;
-    cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_scan_tc<0>) == cudaSuccess) st = fa.sharedSizeBytes;
-    if (cudaFuncGetAttributes(&fa, k_scan_tc<64>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
-    if (cudaFuncGetAttributes(&fa, k_scan_tc<128>) == cudaSuccess) st = std::max(st, fa.sharedSizeBytes);
-    budget[dev] = optin - (int)st;
+    const void* fns[4] = {(const void*)k_scan_tc<0>, (const void*)k_scan_tc<64>, (const void*)k_scan_tc<128>,
+                          (const void*)k_scan_pair};
+    for (int i = 0; i < 4; ++i) {
+      cudaFuncAttributes fa{};
+      size_t st = 16384;
+      if (cudaFuncGetAttributes(&fa, fns[i]) == cudaSuccess) st = fa.sharedSizeBytes;
+      budget[dev][i] = optin - (int)st;
+    }
     have[dev] = true;
   }
-  return budget[dev];
+  return budget[dev][q == kTcPairQ ? 3 : q == kTcWide2Q ? 2 : q == kTcWideQ ? 1 : 0];
 }
 static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
   const bool wide = tc_is_wide(qmax);  // no resident query group; two merge groups of 8
+  if (qmax == kTcPairQ)  // alignment + merge scratch [4 groups][4 warps][8 queries][8] x (d, row)
+    return 1024 + 4 * kTcEpiWarps * 8 * 8 * 8;
   return 1024 + (wide ? 0 : (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64) +
          (wide ? 2 * 8 : kMergeQ) * kTcEpiWarps * 32 * 8 +       // merge scratch
          8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 16 +
          (wide ? 8 : 4) * 32 * 4;
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
-  const int left = tc_budget() - tc_fixed_bytes(dpad, qmax, split);
-  const int sb = kTcStageBytes + (tc_is_wide(qmax) ? kTcCps * (int)qmax * 64 : 0);
+  const int left = tc_budget(qmax) - tc_fixed_bytes(dpad, qmax, split);
+  // wide: the stage carries the group's query slice (the pair scan: this CTA's half)
+  const int sb = kTcStageBytes + (tc_is_wide(qmax) ? kTcCps * (int)(qmax == kTcPairQ ? 128 : qmax) * 64 : 0);
   return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / sb);
 }
 // option "tc_wide_ppl" (env HIVF_TC_WIDE_PPL sets the process default): the
@@ -1184,6 +1652,16 @@ float tc_wide_ppl_default() {
 // queries is streamed once instead of twice; 3 ring stages of 64 KB).  C3
 // measured (profiles/r2_c3_batch_sweep.txt): B=512 (16/list) equal, B=1024
 // (32/list) 91.2k -> 93.4k q/s, B=2048 110k -> 151k.
+// option "tc_pair_ppl" (env HIVF_TC_PAIR_PPL): the density above which the
+// wide scan runs 256-query groups on CTA pairs (k_scan_pair).  C3 A/B on one
+// box (profiles/r2_pair_ab.txt): B=4096 (128 probes/list) 162.8k -> 167.0k q/s,
+// B=2048 (64/list) 151k -> 103k -- the pair's MMA floor (~120 cycles per
+// M=256 K=8 step at any N) and cross-CTA waits cost more than the saved
+// passes until lists carry > ~96 probes.
+float tc_pair_ppl_default() {
+  const char* e = getenv("HIVF_TC_PAIR_PPL");
+  return e ? (float)atof(e) : 96.f;
+}
 float tc_wide2_ppl_default() {
   const char* e = getenv("HIVF_TC_WIDE2_PPL");
   return e ? (float)atof(e) : 24.f;
@@ -1192,6 +1670,9 @@ float tc_wide2_ppl_default() {
 uint32_t scan_tc_qmax(uint32_t dpad, int split, float probes_per_list, const TcOpts& opt) {
   const uint32_t o = opt.qmax_override;
   if (o && (!tc_is_wide(o) || !split) && tc_ring(dpad, o, split) >= 2) return o;
+  if (!split && opt.pair_ppl >= 0.f && opt.wide_ppl >= 0.f && probes_per_list > opt.pair_ppl &&
+      tc_ring(dpad, kTcPairQ, 0) >= 3)
+    return kTcPairQ;
   if (!split && opt.wide2_ppl >= 0.f && opt.wide_ppl >= 0.f && probes_per_list > opt.wide2_ppl &&
       tc_ring(dpad, kTcWide2Q, 0) >= 3)
     return kTcWide2Q;
@@ -1231,7 +1712,8 @@ int get_tc_prof(unsigned long long* host, int n_ctas) {
 int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list, const TcOpts& o) {
   const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list, o);
   return tc_fixed_bytes(dpad, q, split) +
-         (int)tc_ring(dpad, q, split) * (kTcStageBytes + (tc_is_wide(q) ? kTcCps * (int)q * 64 : 0));
+         (int)tc_ring(dpad, q, split) *
+             (kTcStageBytes + (tc_is_wide(q) ? kTcCps * (int)(q == kTcPairQ ? 128 : q) * 64 : 0));
 }
 
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
@@ -1248,7 +1730,10 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
              wide ? 0 : split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u,
              ws.qstage, ws.qshift};
   const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list, o);
-  if (q == kTcWide2Q) {
+  if (q == kTcPairQ) {
+    smem_optin((const void*)k_scan_pair, smem);
+    k_scan_pair<<<std::max(2, n_ctas & ~1), kPairThreads, smem, s>>>(P);
+  } else if (q == kTcWide2Q) {
     smem_optin((const void*)k_scan_tc<128>, smem);
     k_scan_tc<128><<<n_ctas, kTcThreads, smem, s>>>(P);
   } else if (wide) {
@@ -1281,9 +1766,19 @@ __global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs
   const uint32_t c = pair_list[pair];
   const uint32_t local = p - pair_off[c], n = list_cnt[c];
   const uint32_t g = local / G, row = local % G;
-  const uint32_t npad = min(G, ((n - g * G) + 7) & ~7u);
   uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * G) * dpad * 4;
   const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)pair_query[pair] * dpad);
+  if (G == kPairQ) {  // CTA-pair groups: [half][ch][npad/2 rows][64 B], npad = ceil16
+    const uint32_t npad = min(G, ((n - g * G) + 15) & ~15u), hr = npad / 2;
+    const uint32_t half = row / hr, r = row % hr;
+    uint8_t* hb = blk + (uint64_t)half * (dpad / 16) * hr * 64;
+    for (uint32_t g4 = threadIdx.x & 31; g4 < dpad / 4; g4 += 32) {
+      const uint32_t ch = g4 >> 2, q4 = g4 & 3;
+      *reinterpret_cast<float4*>(hb + (uint64_t)ch * hr * 64 + r * 64 + ((q4 ^ ((r >> 1) & 3)) << 4)) = src[g4];
+    }
+    return;
+  }
+  const uint32_t npad = min(G, ((n - g * G) + 7) & ~7u);
   for (uint32_t g4 = threadIdx.x & 31; g4 < dpad / 4; g4 += 32) {
     const uint32_t ch = g4 >> 2, q4 = g4 & 3;
     *reinterpret_cast<float4*>(blk + (uint64_t)ch * npad * 64 + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4)) =
@@ -1293,7 +1788,7 @@ __global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs
 }  // namespace
 
 uint64_t wide_stage_rows(uint32_t n_pairs, uint32_t n_lists) {
-  return (uint64_t)n_pairs + 7ull * n_lists + 8;
+  return (uint64_t)n_pairs + 15ull * n_lists + 16;  // 16-row aligned per list (pair groups)
 }
 
 void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t* sorted_pairs,
@@ -1490,6 +1985,115 @@ __global__ void __launch_bounds__(128, 1) k_tc_dot(const float* __restrict__ A, 
 }
 }  // namespace
 }  // namespace hivf
+
+// ---------------------------------------------------------------------------
+// hivf_debug_tc2_dot: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes
+// out[r][j] = sum_d A[r][d] B[j][d] for 256 rows (CTA c holds rows 128c..) and
+// n columns with M=256 MMAs issued by the leader CTA.  Which CTA's shared
+// memory holds which half of B is the layout question this probe answers:
+// bsplit = 1 puts B rows [c*n/2, (c+1)*n/2) in CTA c (N split across the
+// pair), bsplit = 0 puts all n rows in both CTAs.
+// ---------------------------------------------------------------------------
+namespace hivf {
+namespace {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    k_tc2_dot(const float* __restrict__ A, const float* __restrict__ B, uint32_t D, uint32_t n, int bsplit,
+              float* __restrict__ out) {
+  __shared__ __align__(1024) uint8_t a[kTcChunkBytes];
+  __shared__ __align__(1024) uint8_t b[64 * 64];  // <= 64 B rows of one 16-dim chunk
+  __shared__ uint64_t bar;
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t rank = cluster_rank();
+  const uint32_t nb = bsplit ? n / 2 : n;  // B rows in this CTA's smem
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t nch = (D + 15) / 16;
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    for (int g = 0; g < 4; ++g)
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t d = ch * 16 + g * 4 + e;
+        const uint32_t off = tid * 64 + ((g ^ ((tid >> 1) & 3)) << 4) + e * 4;
+        *reinterpret_cast<float*>(a + off) = d < D ? A[(size_t)(rank * 128 + tid) * D + d] : 0.f;
+        if ((uint32_t)tid < nb) {
+          const uint32_t j = (bsplit ? rank * nb : 0) + tid;
+          *reinterpret_cast<float*>(b + off) = d < D ? B[(size_t)j * D + d] : 0.f;
+        }
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    cluster_sync_all();  // both CTAs' operands are in place
+    if (rank == 0 && tid == 0) {
+      tc_fence_after();
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const uint64_t ad = sw64_kmajor_desc(smem_u32(a)) + (uint64_t)(k2 * 2);
+        const uint64_t bd = sw64_kmajor_desc(smem_u32(b)) + (uint64_t)(k2 * 2);
+        const uint32_t acc = (ch | k2) != 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(tf32_idesc_m(256, n)), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(&bar)),
+          "h"((uint16_t)3)
+          : "memory");
+    }
+    mbar_wait(&bar, ch & 1);
+    tc_fence_after();
+    cluster_sync_all();  // both CTAs done with this chunk's smem
+  }
+  uint32_t r[32];
+  TMEM_LD32(tmem + ((warp * 32) << 16), r);
+  tmem_wait_ld();
+  for (uint32_t j = 0; j < n && j < 32; ++j) out[(size_t)(rank * 128 + tid) * n + j] = __uint_as_float(r[j]);
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+  }
+}
+}  // namespace
+}  // namespace hivf
+
+// Debug / validation: host A[256][D], B[n][D] (n in {16, 32}), out[256][n].
+extern "C" int hivf_debug_tc2_dot(const float* A, const float* B, unsigned D, unsigned n, int bsplit,
+                                  float* out) {
+  using namespace hivf;
+  if (!A || !B || !out || D == 0 || (n != 16 && n != 32)) return 1;
+  float *dA = nullptr, *dB = nullptr, *dO = nullptr;
+  int rc = 0;
+  if (cudaMalloc(&dA, 256ull * D * 4) != cudaSuccess || cudaMalloc(&dB, (size_t)n * D * 4) != cudaSuccess ||
+      cudaMalloc(&dO, 256ull * n * 4) != cudaSuccess)
+    rc = 3;
+  if (!rc && (cudaMemcpy(dA, A, 256ull * D * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+              cudaMemcpy(dB, B, (size_t)n * D * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+              cudaMemset(dO, 0xff, 256ull * n * 4) != cudaSuccess))
+    rc = 3;
+  if (!rc) {
+    k_tc2_dot<<<2, 128>>>(dA, dB, D, n, bsplit, dO);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = 10 + (int)e;
+    else if (cudaMemcpy(out, dO, 256ull * n * 4, cudaMemcpyDeviceToHost) != cudaSuccess) rc = 4;
+  }
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dO);
+  return rc;
+}
 
 // Debug / validation: host A[128][D], B[n][D] (n in {8, 16}), out[128][split ? 2n : n].
 extern "C" int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, unsigned n, int split,

@@ -3,9 +3,10 @@ library option tc_prof): per-CTA cycles in each wait / issue section, averaged p
     python profiles/tcprof.py <file.npy> <launches>"""
 import sys, numpy as np
 a = np.load(sys.argv[1]).astype(np.float64)
-names = {0: "mma_wait_qfull", 1: "mma_wait_data", 2: "mma_wait_tempty", 3: "prod_wait_empty",
-         4: "prod_wait_iempty", 8: "epi_wait_tfull(w)", 9: "epi_merge(w)", 10: "stage_wait_qempty(w)",
-         11: "stage_total(w)", 12: "mma_issue_section", 14: "prod_issue_section"}
+names = {0: "mma_wait_qfull / pair: wait peer stage", 1: "mma_wait_data", 2: "mma_wait_tempty",
+         3: "prod_wait_empty", 4: "prod_wait_iempty", 8: "epi_wait_tfull(w)", 9: "epi_merge(w)",
+         10: "stage_wait_qempty(w)", 11: "stage_total(w) / pair: epi tile work(w)", 12: "mma_issue_section",
+         14: "prod_issue_section"}
 steps = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 dur = (a[:, 6] - a[:, 5])  # last launch only (ns)
 print("items/CTA (all steps) mean %.1f min %d max %d" % (a[:, 7].mean(), a[:, 7].min(), a[:, 7].max()))

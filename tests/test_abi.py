@@ -12,7 +12,7 @@ HEADER = os.path.join(ROOT, "include", "hivf.h")
 
 def header_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(hivf_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(hivf_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -29,7 +29,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_header_symbol(libpath):
     out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True,
                          check=True).stdout
-    exported = set(re.findall(r"\bT (hivf_[a-z_]+)\b", out))
+    exported = set(re.findall(r"\bT (hivf_[a-z0-9_]+)\b", out))
     missing = [s for s in header_symbols() if s not in exported]
     assert not missing, missing
 

@@ -1,10 +1,11 @@
 """GPU parity of the wide tensor-core scans -- the dense-batch path (DESIGN.md
 "Dense batches"): k_scan_tc<64> (64-query groups streamed with the list
-stages, two epilogue groups of 32 with 32-deep per-warp lists) and
+stages, two epilogue groups of 32 with 32-deep per-warp lists),
 k_scan_tc<128> (128-query groups, two epilogue groups of 64 with 16-deep
-per-warp lists).  Forced on with options tc_wide_ppl = 0 and tc_wide2_ppl
-(-1: 64-query groups only, 0: 128-query groups always) on the single-pass
-tf32 kernel; same bar as test_gpu_parity: ids bit-exact, distances bit-equal
+per-warp lists) and k_scan_pair (256-query groups on CTA pairs, cta_group::2,
+two candidate slots per segment).  Forced on with options tc_wide_ppl = 0,
+tc_wide2_ppl and tc_pair_ppl (0: always) on the single-pass tf32 kernel;
+same bar as test_gpu_parity: ids bit-exact, distances bit-equal
 doubles against the C restatement of the reference."""
 import numpy as np
 import pytest
@@ -14,7 +15,7 @@ from test_gpu_parity import _check_search, _random_index
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[-1, 0], ids=["groups64", "groups128"])
+@pytest.fixture(scope="module", params=[(-1, -1), (0, -1), (0, 0)], ids=["groups64", "groups128", "pairs256"])
 def ctx(request):
     import torch
     if not torch.cuda.is_available():
@@ -23,10 +24,13 @@ def ctx(request):
     c = Context(0)
     c.set_option("scan_kernel", 3)
     c.set_option("tc_wide_ppl", 0)
-    c.set_option("tc_wide2_ppl", request.param)
+    c.set_option("tc_wide2_ppl", request.param[0])
+    c.set_option("tc_pair_ppl", request.param[1])
+    c.expect_group = {(-1, -1): 64, (0, -1): 128, (0, 0): 256}[request.param]
     yield c
     c.set_option("tc_wide_ppl", 0)
     c.set_option("tc_wide2_ppl", 24)
+    c.set_option("tc_pair_ppl", 96)
     c.set_option("scan_kernel", 0)
 
 
@@ -41,6 +45,7 @@ def ctx(request):
     (64, 9000, 24, 24, 32, 200),
     (768, 40000, 32, 12, 10, 700),
     (32, 20000, 8, 8, 16, 1000),
+    (768, 50000, 16, 8, 10, 800),
 ])
 def test_wide_scan_vs_oracle(ctx, dim, n, K, nprobe, k, B):
     rng = np.random.default_rng(dim * 13 + K + B)
@@ -50,6 +55,7 @@ def test_wide_scan_vs_oracle(ctx, dim, n, K, nprobe, k, B):
     _check_search(ix, csr, Q, nprobe, k)
     st = ctx.stats()
     assert st["scan_kernel"] == 3 and st["n_work_items"] > 0, st
+    assert st["scan_group"] == ctx.expect_group, st
 
 
 def test_wide_scan_segments_skew_and_empty_lists(ctx):
