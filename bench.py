@@ -819,6 +819,47 @@ def run_c5(args):
 # reference arm
 # ---------------------------------------------------------------------------
 
+def run_c5_sched(args):
+    """BASELINE.json configs[4] through the reference's UNMODIFIED scheduler:
+    compat/_build/{gpu,cpu}/hedra_c5 (sched::run, LiveTransport) on a C2-shaped
+    index (1M x 768, IVF-1024, nprobe 32), a 400-request HyDE / multistep /
+    IRG mix.  --impl hivf runs the GPU engine (libhivf behind the reference
+    API), --impl reference the reference's own retrieval engine (16 host
+    threads) under the same scheduler and workload.  The line reports the
+    retrieval sub-stage latency p50/p99 (the "substage" trace events) and the
+    request latency p50/p99 of the ExperimentReport."""
+    import subprocess
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    flavour = "cpu" if args.impl == "reference" else "gpu"
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "paper_2507_09138_b200", "compat", "_build",
+                       flavour, "hedra_c5")
+    if not os.path.exists(exe):
+        print(json.dumps({"impl": args.impl, "unavailable": f"{exe} not built (compat/build.py)"}))
+        return
+    n_req = 400 if flavour == "gpu" else 100
+    cmd = [exe, "--n", "1000000", "--dim", "768", "--topics", "256", "--clusters", "1024", "--spread", "0.03",
+           "--requests", str(n_req), "--rate", "40", "--nprobe", "32", "--kmeans-sample", "48000",
+           "--clock", "live", "--mix", "hyde=0.3,multistep=0.4,irg=0.3"]
+    if flavour == "cpu":
+        cmd += ["--kmeans-iters", "4"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        print(json.dumps({"impl": args.impl, "unavailable": r.stderr[-300:]}))
+        return
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    line = {"metric": "C5 retrieval sub-stage latency under sched::run (live clock), p50", "value":
+            d["substage_ms"]["p50"], "unit": "ms", "higher_is_better": False, "n_gpus": 1,
+            "config": {"workload": "heterogeneous RAG stream (HyDE / multistep / IRG) through the reference scheduler",
+                       "index": d["corpus"] + f" IVF-{d['clusters']}", "nprobe": d["nprobe"], "requests": d["requests"]},
+            "substage_ms": d["substage_ms"], "items_per_substage": d["items_per_substage"],
+            "request_latency_ms": {"p50": d["latency_p50_ms"], "p99": d["latency_p99_ms"]},
+            "per_vector_ns": d["per_vector_ns"], "engine": d["engine"], "completed": d["completed"]}
+    if args.impl == "reference":
+        line["impl"] = "reference"
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """The reference's own CPU implementation (oracle/_ref: the unmodified
     /root/reference/proj sources compiled), rank 0 only, on the same workload,
@@ -935,6 +976,8 @@ def main():
         log(f"note: --cpu-sample {args.cpu_sample} < {os.cpu_count()} host threads")
     if args.config == "c5":
         run_c5(args)
+    elif args.config == "c5sched":
+        run_c5_sched(args)
     elif args.impl == "reference":
         run_reference(args)
     else:

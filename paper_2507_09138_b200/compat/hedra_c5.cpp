@@ -22,6 +22,7 @@
 #include <map>
 #include <sstream>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "hedra/bench.hpp"
@@ -167,6 +168,10 @@ int main(int argc, char** argv) {
 #endif
   }
   const double t_calib = secs(t0);
+#ifdef HEDRA_GPU_COMPAT
+  // serving warm-up: device scratch for sub-stages up to 64 items x nprobe
+  gpu::reserve_substage(index, 64, a.nprobe, 32);
+#endif
 
   harness::TraceSink sink;
   t0 = std::chrono::steady_clock::now();
@@ -183,6 +188,18 @@ int main(int argc, char** argv) {
     }
   std::vector<double> lat, items;
   for (const auto& [t, ms] : substage_ms) lat.push_back(ms);
+  // the slowest sub-stages (start time, duration, items): where the tail comes from
+  std::vector<std::tuple<double, double, std::size_t>> slow;
+  for (const auto& [t, ms] : substage_ms) slow.emplace_back(ms, t, substages[t]);
+  std::sort(slow.rbegin(), slow.rend());
+  std::string slowest = "[";
+  for (std::size_t i = 0; i < slow.size() && i < 12; ++i) {
+    char b[96];
+    std::snprintf(b, sizeof(b), "%s[%.1f, %.3f, %zu]", i ? ", " : "", std::get<1>(slow[i]), std::get<0>(slow[i]),
+                  std::get<2>(slow[i]));
+    slowest += b;
+  }
+  slowest += "]";
   for (const auto& [t, n] : substages) items.push_back(static_cast<double>(n));
   double item_sum = 0.0;
   for (double v : items) item_sum += v;
@@ -195,7 +212,8 @@ int main(int argc, char** argv) {
       "\"items_per_substage\": {\"mean\": %.2f, \"p50\": %.0f, \"max\": %.0f}, "
       "\"retrieval_stages\": %llu, \"mean_clusters_searched\": %.3f, \"cache_hit_rate\": %.4f, "
       "\"speculation_accuracy\": %.4f, \"setup_s\": {\"corpus\": %.2f, \"kmeans\": %.2f, \"index\": %.2f, "
-      "\"calibrate\": %.2f}, \"run_s\": %.3f, \"report_json_bytes\": %zu}\n",
+      "\"calibrate\": %.2f}, \"run_s\": %.3f, \"report_json_bytes\": %zu, "
+      "\"slowest_substages_t_ms_items\": %s}\n",
 #ifdef HEDRA_GPU_COMPAT
       "gpu",
 #else
@@ -209,6 +227,6 @@ int main(int argc, char** argv) {
       items.empty() ? 0.0 : *std::max_element(items.begin(), items.end()),
       static_cast<unsigned long long>(report.retrieval_stages), report.mean_clusters_searched,
       report.cache_hit_rate.value_or(-1.0), report.speculation_accuracy.value_or(-1.0), t_corpus, t_kmeans, t_index,
-      t_calib, t_run, report.to_json().size());
+      t_calib, t_run, report.to_json().size(), slowest.c_str());
   return 0;
 }

@@ -613,6 +613,33 @@ double measure_per_vector_ns_impl(const IvfIndex& index, std::size_t repeats) {
 }  // namespace hedra::ivf::gpu
 
 namespace hedra::gpu {
+void reserve_substage(const ivf::IvfIndex& index, std::size_t n_items, std::size_t clusters_per_item,
+                      std::size_t k) {
+  const std::size_t K = index.k_clusters();
+  if (!K || !n_items || !clusters_per_item || !k) return;
+  const std::size_t per = std::min(clusters_per_item, K);
+  // realistic sub-stages (a query at its first cluster's centroid): a
+  // degenerate query would fail the scan's filter proofs and tip the index's
+  // automatic scan-precision policy
+  std::vector<float> q(n_items * index.dim, 0.f);
+  for (std::size_t i = 0; i < n_items; ++i) {
+    const auto& c = index.centroids.rows[i % K];
+    std::copy(c.begin(), c.end(), q.begin() + i * index.dim);
+  }
+  std::vector<std::uint32_t> off(n_items + 1), cl(n_items * per), kk(n_items, static_cast<std::uint32_t>(k)),
+      hn(n_items, 0);
+  for (std::size_t i = 0; i <= n_items; ++i) off[i] = static_cast<std::uint32_t>(i * per);
+  for (std::size_t i = 0; i < n_items; ++i)
+    for (std::size_t j = 0; j < per; ++j) cl[i * per + j] = static_cast<std::uint32_t>((i + j) % K);
+  std::vector<std::uint64_t> hid(n_items * k);
+  std::vector<double> hd(n_items * k);
+  std::vector<std::uint8_t> changed(cl.size());
+  auto& dev = ivf::gpu::device_of(index);
+  std::lock_guard<std::mutex> g(dev.ctx->mu);
+  ivf::gpu::check(hivf_scan_items(dev.ix, q.data(), static_cast<std::uint32_t>(n_items), off.data(), cl.data(),
+                                  kk.data(), hid.data(), hd.data(), hn.data(), static_cast<std::uint32_t>(k),
+                                  changed.data()));
+}
 std::vector<ivf::SearchStepReport> search_clusters_batch(const ivf::IvfIndex& index,
                                                          std::span<ivf::SearchCursor* const> cursors,
                                                          std::span<const std::span<const ClusterId>> clusters) {

@@ -44,6 +44,13 @@ std::vector<ivf::TopKResult> brute_force_search_batch(const ivf::Corpus& corpus,
 // with the CPU scan, proj/src/bench.cpp:139-163).
 double measure_per_vector_ns(const ivf::IvfIndex& index, std::size_t repeats = 3);
 
+// Serving warm-up: one sub-stage of n_items items x clusters_per_item clusters
+// with k-heaps, so the device scratch of later sub-stages up to that size is
+// already allocated (allocation synchronises the device; a live scheduler
+// would otherwise pay it inside its first sub-stages).
+void reserve_substage(const ivf::IvfIndex& index, std::size_t n_items, std::size_t clusters_per_item,
+                      std::size_t k);
+
 // Device calls issued through this layer since start (kernel-path evidence).
 std::size_t device_calls();
 

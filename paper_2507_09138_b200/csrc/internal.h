@@ -48,17 +48,17 @@ extern std::atomic<uint64_t> g_state_gen;
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  // grows by >= 1.5x: a stream of varying batch shapes (node-split
+  // grows by >= 2x from 64 KB: a stream of varying batch shapes (node-split
   // sub-stages) settles after a few calls instead of re-allocating (cudaFree
   // synchronises the device) whenever a batch is a little larger than before
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
-    want = std::max(want, bytes + bytes / 2);
+    want = std::max(want, 2 * bytes);
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
     g_state_gen.fetch_add(1);
-    want = std::max<size_t>(want, 256);
+    want = std::max<size_t>(want, 64 << 10);  // 64 KB floor: small sub-stages never regrow
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) bytes = want;
     return e;
@@ -79,12 +79,13 @@ struct HBuf {  // grow-only pinned host buffer
   size_t bytes = 0;
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
-    want = std::max(want, bytes + bytes / 2);
+    // pinned allocations cost milliseconds and synchronise: start at 1 MB, double
+    want = std::max(std::max(want, 2 * bytes), (size_t)1 << 20);
     if (p) cudaFreeHost(p);
     p = nullptr;
     bytes = 0;
-    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(want, 256));
-    if (e == cudaSuccess) bytes = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) bytes = want;
     return e;
   }
   void release() {
