@@ -533,6 +533,11 @@ def run_hivf(args):
         timed_step(i)
     torch.cuda.synchronize()
     # ---- timed region (value) ----------------------------------------------------
+    # HIVF_NCU_RANGE=1: the profiler range is the timed region only (ncu
+    # --profile-from-start off), so launch lists skip the index build
+    ncu_range = bool(os.environ.get("HIVF_NCU_RANGE"))
+    if ncu_range:
+        torch.cuda.cudart().cudaProfilerStart()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier(world)
@@ -543,6 +548,8 @@ def run_hivf(args):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
+    if ncu_range:
+        torch.cuda.cudart().cudaProfilerStop()
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     ms_per_step = ms / args.steps
     value = B * args.steps / (ms / 1e3)
