@@ -717,7 +717,13 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
     c->stats.kernels_launched += 4;
     return HIVF_OK;
   }
-  launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream);
+  const uint32_t splits = coarse_dist_splits(v, qv.n);
+  float* part = nullptr;
+  if (splits > 1) {
+    CK(c->coarse_part.ensure((size_t)splits * qv.n * ix->K * 4));
+    part = c->coarse_part.as<float>();
+  }
+  launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream, part);
   CKL();
   launch_coarse_select(v, qv, c->dist32.as<float>(), nprobe, c->plans.as<uint32_t>(), d_dists,
                        c->flags_c.as<int>(), c->stream);

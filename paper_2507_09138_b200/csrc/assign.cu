@@ -76,9 +76,14 @@ __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32
 // small-K / small-B batches (C1, C2) are not run on a fraction of the GPU.
 constexpr int CT_Q = 32, CT_K = 16;
 
-template <int CTC>
+// kSplit: blockIdx.z takes dims [z * kspan, (z + 1) * kspan) and writes its
+// partial dot product to out[z][q][c] (combined by k_coarse_combine): small
+// batches on small codebooks (C2: 256 x 1024 centroids) fill the GPU through
+// the reduction dimension.  The dot product is then a different summation
+// tree of the same D terms, which filter_eps (gamma_D, any order) covers.
+template <int CTC, bool kSplit = false>
 __global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView qv,
-                                                         float* __restrict__ out) {
+                                                         float* __restrict__ out, uint32_t kspan = 0) {
   constexpr int NT = CTC * 2;  // threads
   constexpr int NA = CTC * CT_K / 4;  // float4 loads per A k-tile
   constexpr int NB = CT_Q * CT_K / 4;  // float4 loads per B k-tile
@@ -115,8 +120,10 @@ __global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView
                   : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  fetch(0);
-  for (uint32_t k0 = 0; k0 < ix.dpad; k0 += CT_K) {
+  const uint32_t kb = kSplit ? blockIdx.z * kspan : 0u;
+  const uint32_t ke = kSplit ? min(ix.dpad, kb + kspan) : ix.dpad;
+  fetch(kb);
+  for (uint32_t k0 = kb; k0 < ke; k0 += CT_K) {
 #pragma unroll
     for (int t = 0; t < PA; ++t) {
       const int f = tid + t * NT;
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView
       }
     }
     __syncthreads();
-    fetch(k0 + CT_K);
+    if (k0 + CT_K < ke) fetch(k0 + CT_K);
 #pragma unroll
     for (int kk = 0; kk < CT_K; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&As[kk][tc * 4]);
@@ -160,9 +167,26 @@ __global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView
     for (int i = 0; i < 4; ++i) {
       const uint32_t c = c0 + tc * 4 + i;
       if (c >= ix.K) continue;
-      const float s = __fadd_rn(ix.cnorm2[c], qv.qn2[q]);
-      out[(uint64_t)q * ix.K + c] = __fmaf_rn(-2.f, acc[i][j], s);
+      if (kSplit) {
+        out[((uint64_t)blockIdx.z * qv.n + q) * ix.K + c] = acc[i][j];
+      } else {
+        const float s = __fadd_rn(ix.cnorm2[c], qv.qn2[q]);
+        out[(uint64_t)q * ix.K + c] = __fmaf_rn(-2.f, acc[i][j], s);
+      }
     }
+  }
+}
+
+// Partial dot products (z = 0..S-1, summed in z order: deterministic) ->
+// fp32 expansion distance, as the unsplit kernel forms it.
+__global__ void k_coarse_combine(IndexView ix, QueryView qv, const float* __restrict__ part, uint32_t S,
+                                 float* __restrict__ out) {
+  const uint64_t n = (uint64_t)qv.n * ix.K;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    float dot = part[i];
+    for (uint32_t z = 1; z < S; ++z) dot = __fadd_rn(dot, part[(uint64_t)z * n + i]);
+    const uint32_t q = (uint32_t)(i / ix.K), c = (uint32_t)(i % ix.K);
+    out[i] = __fmaf_rn(-2.f, dot, __fadd_rn(ix.cnorm2[c], qv.qn2[q]));
   }
 }
 
@@ -418,10 +442,28 @@ void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t d
                                    err);
 }
 
-void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s) {
+uint32_t coarse_dist_splits(const IndexView& ix, uint32_t n_queries) {
+  const int sms = device_sm_count();
+  const uint64_t t32 = (uint64_t)((ix.K + 31) / 32) * ((n_queries + CT_Q - 1) / CT_Q);
+  if (t32 >= 2ull * sms || ix.dpad < 256) return 1;
+  uint32_t S = 1;
+  while (S * 2 <= ix.dpad / 64 && t32 * S < 4ull * sms) S *= 2;  // >= 64 dims per split
+  return S;
+}
+
+void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s,
+                        float* part) {
   const int sms = device_sm_count();
   const uint32_t qt = (qv.n + CT_Q - 1) / CT_Q;
   auto tiles = [&](uint32_t ctc) { return (uint64_t)((ix.K + ctc - 1) / ctc) * qt; };
+  const uint32_t S = part ? coarse_dist_splits(ix, qv.n) : 1u;
+  if (S > 1) {
+    const uint32_t span = (ix.dpad / S + CT_K - 1) / CT_K * CT_K;
+    k_coarse_dist<32, true><<<dim3((ix.K + 31) / 32, qt, S), 64, 0, s>>>(ix, qv, part, span);
+    const uint64_t n = (uint64_t)qv.n * ix.K;
+    k_coarse_combine<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4ull * sms), 256, 0, s>>>(ix, qv, part, S, dist32);
+    return;
+  }
   if (tiles(128) >= 2ull * sms)
     k_coarse_dist<128><<<dim3((ix.K + 127) / 128, qt), 256, 0, s>>>(ix, qv, dist32);
   else if (tiles(64) >= 2ull * sms)

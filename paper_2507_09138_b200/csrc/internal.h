@@ -124,7 +124,7 @@ struct hivf_ctx {
   DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
       cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, qbound, rep_entries, rep_n, rep_cnt,
-      rep_d, rep_ids, qshift, qwide, coarse_all;
+      rep_d, rep_ids, qshift, qwide, coarse_all, coarse_part;
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;

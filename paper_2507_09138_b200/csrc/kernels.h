@@ -130,7 +130,11 @@ void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cuda
 void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t dpad, int metric,
                          bool normalize, float* qs, float* qn2, float* qnorm, int* err,
                          cudaStream_t s);
-void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s);
+// part (optional, coarse_dist_splits() x n_queries x K floats): scratch for the
+// split-K form on small batches / codebooks
+uint32_t coarse_dist_splits(const IndexView& ix, uint32_t n_queries);
+void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s,
+                        float* part = nullptr);
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
                           uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s);
