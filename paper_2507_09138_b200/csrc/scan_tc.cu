@@ -1178,7 +1178,13 @@ constexpr uint32_t kPairQ = 256;
 constexpr int kPG = 4;                        // epilogue groups (4 warps each, one per TMEM lane quadrant)
 constexpr int kPQ = (int)kPairQ / kPG;        // query columns per group
 constexpr int kPairThreads = (2 + kPG * kTcEpiWarps) * 32;
-constexpr int kPairQB = kTcCps * 128 * 64;  // one CTA's half of a 256-query slice (32 KB)
+// 64-dim pipeline stages (4 chunks), as the single-CTA scans.  32-dim stages
+// (6 slots instead of 3, same bytes in flight) measured 1.5x slower at C3
+// B=4096 (31.9 vs 20.8 ms): the pair's per-stage handshakes (relay,
+// multicast commit) cost more than the finer slots win.
+constexpr int kPCps = 4;
+constexpr int kPairStageA = kPCps * kTcChunkBytes;  // 16 KB of list rows
+constexpr int kPairQB = kPCps * 128 * 64;           // one CTA's half of a 256-query slice (16 KB)
 
 __device__ __forceinline__ uint32_t mapa_peer(const void* p, uint32_t cta) {
   uint32_t r;
@@ -1245,10 +1251,10 @@ __device__ __noinline__ Cand merge_quad8(float s0, float s1, float s2, float s3,
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_scan_pair(TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t kSB = kTcStageBytes + kPairQB;  // A tile + this CTA's half query slice
+  constexpr uint32_t kSB = kPairStageA + kPairQB;  // A tile stage + this CTA's half query slice
   const uint32_t dpad = P.ix.dpad;
   const uint32_t nch = dpad / kChunk;
-  const uint32_t nstg = (nch + kTcCps - 1) / kTcCps;
+  const uint32_t nstg = (nch + kPCps - 1) / kPCps;
   const uint32_t SA = P.sa;
   uint8_t* aring = smem;
   float* md = reinterpret_cast<float*>(smem + SA * kSB);  // merge scratch [kPG groups][4 warps][8 q][8]
@@ -1331,7 +1337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
           const uint32_t r0 = item.row0 + t * kTcTile;
           const uint32_t nr = t < ntiles ? min((uint32_t)kTcTile, item.nrows - t * kTcTile) : 0u;
           for (uint32_t sg = 0; sg < nstg; ++sg) {
-            const uint32_t c0 = sg * kTcCps, cn = min((uint32_t)kTcCps, nch - c0);
+            const uint32_t c0 = sg * kPCps, cn = min((uint32_t)kPCps, nch - c0);
             const uint32_t a = ra, pa = rpa;
             {
               TC_PROF_T0();
@@ -1347,7 +1353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
                 bulk_g2s(aring + a * kSB + c * kTcChunkBytes, lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c),
                          nr * kChunk * 4, &full[a]);
             }
-            bulk_g2s(aring + a * kSB + kTcStageBytes, qsrc + (uint64_t)c0 * qbytes, cn * qbytes, &full[a]);
+            bulk_g2s(aring + a * kSB + kPairStageA, qsrc + (uint64_t)c0 * qbytes, cn * qbytes, &full[a]);
             if (++ra == SA) { ra = 0; rpa ^= 1; }
           }
         }
@@ -1380,7 +1386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
         }
         const uint32_t d_tmem = tmem_base + tb * 256;
         for (uint32_t sg = 0; sg < nstg; ++sg) {
-          const uint32_t cn = min((uint32_t)kTcCps, nch - sg * kTcCps);
+          const uint32_t cn = min((uint32_t)kPCps, nch - sg * kPCps);
           const uint32_t a = ra, pa = rpa;
           if (leader) {
             {
@@ -1396,9 +1402,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
             tc_fence_after();
             const long long _ti = P.prof ? clock64() : 0;
             const uint64_t adesc = adesc0 + (uint64_t)(a * (kSB >> 4));
-            const uint64_t qd0 = adesc + (uint64_t)(kTcStageBytes >> 4);
+            const uint64_t qd0 = adesc + (uint64_t)(kPairStageA >> 4);
 #pragma unroll
-            for (uint32_t c = 0; c < (uint32_t)kTcCps; ++c) {
+            for (uint32_t c = 0; c < (uint32_t)kPCps; ++c) {
               if (c >= cn) break;
               const uint64_t qd = qd0 + (uint64_t)(c * (npad / 2 * 4));  // (npad/2)*64 B per chunk
 #pragma unroll
@@ -1635,7 +1641,8 @@ static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int left = tc_budget(qmax) - tc_fixed_bytes(dpad, qmax, split);
   // wide: the stage carries the group's query slice (the pair scan: this CTA's half)
-  const int sb = kTcStageBytes + (tc_is_wide(qmax) ? kTcCps * (int)(qmax == kTcPairQ ? 128 : qmax) * 64 : 0);
+  const int sb = qmax == kTcPairQ ? kPairStageA + kPairQB
+                                  : kTcStageBytes + (tc_is_wide(qmax) ? kTcCps * (int)qmax * 64 : 0);
   return left <= 0 ? 0 : (uint32_t)min(kTcMaxA, left / sb);
 }
 // option "tc_wide_ppl" (env HIVF_TC_WIDE_PPL sets the process default): the
@@ -1713,7 +1720,8 @@ int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list, const Tc
   const uint32_t q = scan_tc_qmax(dpad, split, probes_per_list, o);
   return tc_fixed_bytes(dpad, q, split) +
          (int)tc_ring(dpad, q, split) *
-             (kTcStageBytes + (tc_is_wide(q) ? kTcCps * (int)(q == kTcPairQ ? 128 : q) * 64 : 0));
+             (q == kTcPairQ ? kPairStageA + kPairQB
+                            : kTcStageBytes + (tc_is_wide(q) ? kTcCps * (int)q * 64 : 0));
 }
 
 void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* items,
