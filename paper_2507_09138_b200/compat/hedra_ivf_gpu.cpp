@@ -194,6 +194,14 @@ TopKResult TopKResult::truncated(std::size_t k) const {
   return out;
 }
 
+bool TopKResult::operator==(const TopKResult& rhs) const {
+  if (entries_.size() != rhs.entries_.size()) return false;
+  for (std::size_t i = 0; i < entries_.size(); ++i)
+    if (entries_[i].doc_id != rhs.entries_[i].doc_id || entries_[i].distance != rhs.entries_[i].distance)
+      return false;
+  return true;
+}
+
 std::vector<DocId> TopKResult::doc_ids() const {
   std::vector<DocId> out;
   out.reserve(entries_.size());
