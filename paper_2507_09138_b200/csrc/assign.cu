@@ -32,6 +32,7 @@ constexpr int kCandCap = 4096;
 __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32_t dim,
                                uint32_t dpad, int metric, int normalize, float* __restrict__ qs,
                                float* __restrict__ qn2, float* __restrict__ qnorm, int* err) {
+  pdl_wait();
   const uint32_t b = blockIdx.x;
   if (b >= n) return;
   __shared__ double s_norm;
@@ -84,6 +85,7 @@ constexpr int CT_Q = 32, CT_K = 16;
 template <int CTC, bool kSplit = false>
 __global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView qv,
                                                          float* __restrict__ out, uint32_t kspan = 0) {
+  pdl_wait();
   constexpr int NT = CTC * 2;  // threads
   constexpr int NA = CTC * CT_K / 4;  // float4 loads per A k-tile
   constexpr int NB = CT_Q * CT_K / 4;  // float4 loads per B k-tile
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(CTC * 2) k_coarse_dist(IndexView ix, QueryView
 // fp32 expansion distance, as the unsplit kernel forms it.
 __global__ void k_coarse_combine(IndexView ix, QueryView qv, const float* __restrict__ part, uint32_t S,
                                  float* __restrict__ out) {
+  pdl_wait();
   const uint64_t n = (uint64_t)qv.n * ix.K;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     float dot = part[i];
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
                                                        uint32_t nprobe, double eps, double ab,
                                                        uint32_t* __restrict__ plans,
                                                        double* __restrict__ dists, int* flags) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   double* cd = reinterpret_cast<double*>(sm);                       // kCandCap
   uint32_t* cid = reinterpret_cast<uint32_t*>(cd + kCandCap);         // kCandCap
@@ -340,6 +344,7 @@ __global__ void __launch_bounds__(512) k_coarse_fallback(IndexView ix, QueryView
                                                          uint32_t* __restrict__ plans,
                                                          double* __restrict__ dists,
                                                          const int* flags) {
+  pdl_wait();
   const uint32_t b = blockIdx.x;
   if (!flags[b]) return;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -438,7 +443,7 @@ void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t d
                          bool normalize, float* qs, float* qn2, float* qnorm, int* err,
                          cudaStream_t s) {
   if (n == 0) return;
-  k_prep_queries<<<n, 128, 0, s>>>(q_in, n, dim, dpad, metric, normalize ? 1 : 0, qs, qn2, qnorm,
+  launch_pdl(k_prep_queries, dim3(n), dim3(128), 0, s, q_in, n, dim, dpad, metric, normalize ? 1 : 0, qs, qn2, qnorm,
                                    err);
 }
 
@@ -459,17 +464,17 @@ void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32,
   const uint32_t S = part ? coarse_dist_splits(ix, qv.n) : 1u;
   if (S > 1) {
     const uint32_t span = (ix.dpad / S + CT_K - 1) / CT_K * CT_K;
-    k_coarse_dist<32, true><<<dim3((ix.K + 31) / 32, qt, S), 64, 0, s>>>(ix, qv, part, span);
+    launch_pdl(k_coarse_dist<32, true>, dim3(dim3((ix.K + 31) / 32, qt, S)), dim3(64), 0, s, ix, qv, part, span);
     const uint64_t n = (uint64_t)qv.n * ix.K;
-    k_coarse_combine<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4ull * sms), 256, 0, s>>>(ix, qv, part, S, dist32);
+    launch_pdl(k_coarse_combine, dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 4ull * sms)), dim3(256), 0, s, ix, qv, part, S, dist32);
     return;
   }
   if (tiles(128) >= 2ull * sms)
-    k_coarse_dist<128><<<dim3((ix.K + 127) / 128, qt), 256, 0, s>>>(ix, qv, dist32);
+    launch_pdl(k_coarse_dist<128>, dim3(dim3((ix.K + 127) / 128, qt)), dim3(256), 0, s, ix, qv, dist32, 0u);
   else if (tiles(64) >= 2ull * sms)
-    k_coarse_dist<64><<<dim3((ix.K + 63) / 64, qt), 128, 0, s>>>(ix, qv, dist32);
+    launch_pdl(k_coarse_dist<64>, dim3(dim3((ix.K + 63) / 64, qt)), dim3(128), 0, s, ix, qv, dist32, 0u);
   else
-    k_coarse_dist<32><<<dim3((ix.K + 31) / 32, qt), 64, 0, s>>>(ix, qv, dist32);
+    launch_pdl(k_coarse_dist<32>, dim3(dim3((ix.K + 31) / 32, qt)), dim3(64), 0, s, ix, qv, dist32, 0u);
 }
 
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
@@ -480,7 +485,7 @@ void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float*
   smem_optin((const void*)k_coarse_fallback, 200 * 1024);
   // 512 threads: fewer (64-256, sized to the candidate count) measured slower
   // (C2 41 -> 61 us, C3 59 -> 75 us)
-  k_coarse_select<<<qv.n, 512, smem, s>>>(ix, qv, dist32, nprobe, filter_eps(ix.dim),
+  launch_pdl(k_coarse_select, dim3(qv.n), dim3(512), smem, s, ix, qv, dist32, nprobe, filter_eps(ix.dim),
                                           filter_abs(ix.dim), plans, dists, flags);
 }
 
@@ -489,7 +494,7 @@ void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t n
   uint32_t cap = 1024;
   while (cap < nprobe + 512) cap <<= 1;
   const size_t smem = (size_t)cap * 12 + (size_t)ix.dpad * 4;
-  k_coarse_fallback<<<qv.n, 512, smem, s>>>(ix, qv, nprobe, cap, plans, dists, flags);
+  launch_pdl(k_coarse_fallback, dim3(qv.n), dim3(512), smem, s, ix, qv, nprobe, cap, plans, dists, flags);
 }
 
 }  // namespace hivf

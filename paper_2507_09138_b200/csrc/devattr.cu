@@ -6,6 +6,7 @@
 // hivf_group_create).  Every launcher therefore goes through these helpers,
 // keyed by the calling thread's current device (the C-ABI entry points set it
 // to the context's device before launching).
+#include <cstdlib>
 #include <mutex>
 #include <map>
 #include <utility>
@@ -19,6 +20,14 @@ std::mutex g_mu;
 std::map<std::pair<int, const void*>, int> g_optin;  // bytes opted in per (device, kernel)
 int g_sms[kMaxDevices] = {};
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HIVF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int current_device() {
   int d = 0;

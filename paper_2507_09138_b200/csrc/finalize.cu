@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     double ab, uint64_t* __restrict__ ids_out, double* __restrict__ d_out,
     uint32_t* __restrict__ counts_out, int* flags, float* __restrict__ tau_out,
     RepairState rep) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   double* cdist = reinterpret_cast<double*>(sm);                 // kCandMax
   uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kCandMax);  // kCandMax
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(256) k_repair_segments(IndexView ix, QueryView
                                                          uint32_t nprobe, RepairState R,
                                                          const float* __restrict__ tau, double fa,
                                                          double fb, double fc, int* flags) {
+  pdl_wait();
   const uint32_t chunks = (ix.seg_rows + kRepChunk - 1) / kRepChunk;
   const uint32_t n_units = min(*R.n, R.cap) * chunks;
   for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_repair(
     const float* __restrict__ cand_thr, const uint32_t* __restrict__ cand_n,
     const float* __restrict__ tau, RepairState R, uint64_t* __restrict__ ids_out,
     double* __restrict__ d_out, uint32_t* __restrict__ counts_out, int* flags) {
+  pdl_wait();
   const uint32_t b = blockIdx.x;
   if (flags[b] != 2) return;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -479,6 +482,7 @@ __global__ void __launch_bounds__(256) k_exact_search(IndexView ix, QueryView qv
                                                       double* d_out, uint32_t* counts_out,
                                                       uint64_t* part_total, const float* tau,
                                                       double fa, double fb, double fc) {
+  pdl_wait();
   // grid-stride over queries: the grid is sized for ~one wave, so a batch
   // with no flagged query costs a few hundred idle CTAs, not B x nsplit; each
   // CTA checks the flags of its next blockDim.x queries at once and works
@@ -609,6 +613,7 @@ __global__ void __launch_bounds__(256) k_exact_merge(uint32_t nsplit, uint32_t k
                                                      const uint64_t* part_total,
                                                      uint64_t* ids_out, double* d_out,
                                                      uint32_t* counts_out) {
+  pdl_wait();
   const uint32_t b = blockIdx.x;
   if (flags && !flags[b]) return;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -640,6 +645,7 @@ __global__ void __launch_bounds__(256) k_exact_merge(uint32_t nsplit, uint32_t k
 // are validated: an id >= K is replaced by 0 in the working copy and flags err.
 __global__ void k_plans_to_pairs(const uint32_t* plans, uint32_t n, uint32_t nprobe, uint32_t K,
                                  uint32_t* pq, uint32_t* pl, uint32_t* plans_out, int* err) {
+  pdl_wait();
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n * nprobe) return;
   uint32_t c = plans[p];
@@ -659,6 +665,7 @@ __global__ void k_merge_parts(uint32_t n_parts, uint32_t nq, uint32_t k, const u
                               const double* d, const uint32_t* counts, uint64_t* ids_out,
                               double* d_out, uint32_t* counts_out, uint32_t cap, uint64_t s_ids,
                               uint64_t s_d, uint64_t s_cnt) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   double* bd = reinterpret_cast<double*>(sm);
   uint64_t* bi = reinterpret_cast<uint64_t*>(bd + cap);
@@ -701,7 +708,7 @@ void launch_plans_to_pairs(const uint32_t* plans, uint32_t n_queries, uint32_t n
                            cudaStream_t s) {
   const uint32_t n = n_queries * nprobe;
   if (!n) return;
-  k_plans_to_pairs<<<(n + 255) / 256, 256, 0, s>>>(plans, n_queries, nprobe, K, pair_query, pair_list,
+  launch_pdl(k_plans_to_pairs, dim3((n + 255) / 256), dim3(256), 0, s, plans, n_queries, nprobe, K, pair_query, pair_list,
                                                     plans_out, err);
 }
 
@@ -715,7 +722,7 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
   const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 8 + (size_t)nprobe * 16 + 4 +
                       (size_t)kSlotCap * (4 + 4 + 4 + kKP * 4);
   smem_optin((const void*)k_finalize_search, 200 * 1024);
-  k_finalize_search<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row,
+  launch_pdl(k_finalize_search, dim3(qv.n), dim3(kFinThreads), smem, s, ix, qv, plans, nprobe, k, cand_d, cand_row,
                                                     cand_thr, cand_n, filter_eps(ix.dim),
                                                     filter_abs(ix.dim), ids_out, d_out,
                                                     counts_out, flags, tau_out, R);
@@ -754,15 +761,15 @@ void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_
   const uint32_t wave = (uint32_t)std::max(1, occ) * (uint32_t)sms;
   const uint32_t gx = std::max(1u, std::min(qv.n, wave / ns));
   if (ns <= 1) {
-    k_exact_search<<<dim3(gx, 1), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, ids_out,
+    launch_pdl(k_exact_search, dim3(dim3(gx, 1)), dim3(256), smem, s, ix, qv, plans, nprobe, k, cap, flags, ids_out,
                                                     d_out, counts_out, nullptr, tau, fa, fb, fc);
     return;
   }
-  k_exact_search<<<dim3(gx, ns), 256, smem, s>>>(ix, qv, plans, nprobe, k, cap, flags, part_ids,
+  launch_pdl(k_exact_search, dim3(dim3(gx, ns)), dim3(256), smem, s, ix, qv, plans, nprobe, k, cap, flags, part_ids,
                                                    part_d, part_cnt, part_total, tau, fa, fb, fc);
   uint32_t mcap = 1;
   while (mcap < ns * k) mcap <<= 1;
-  k_exact_merge<<<qv.n, 256, (size_t)mcap * 16, s>>>(ns, k, mcap, flags, part_ids, part_d,
+  launch_pdl(k_exact_merge, dim3(qv.n), dim3(256), (size_t)mcap * 16, s, ns, k, mcap, flags, part_ids, part_d,
                                                      part_cnt, part_total, ids_out, d_out,
                                                      counts_out);
 }
@@ -774,7 +781,7 @@ void launch_merge_parts(uint32_t n_parts, uint32_t n_queries, uint32_t k, const 
   while (cap < n_parts * k) cap <<= 1;
   const size_t smem = (size_t)cap * 16;
   smem_optin((const void*)k_merge_parts, 200 * 1024);
-  k_merge_parts<<<n_queries, 256, smem, s>>>(n_parts, n_queries, k, ids, d, counts, ids_out, d_out,
+  launch_pdl(k_merge_parts, dim3(n_queries), dim3(256), smem, s, n_parts, n_queries, k, ids, d, counts, ids_out, d_out,
                                              counts_out, cap, (uint64_t)n_queries * k,
                                              (uint64_t)n_queries * k, n_queries);
 }
@@ -786,7 +793,7 @@ void launch_merge_parts_strided(uint32_t n_parts, uint32_t n_queries, uint32_t k
   uint32_t cap = 1;
   while (cap < n_parts * k) cap <<= 1;
   smem_optin((const void*)k_merge_parts, 200 * 1024);
-  k_merge_parts<<<n_queries, 256, (size_t)cap * 16, s>>>(n_parts, n_queries, k, ids, d, counts, ids_out,
+  launch_pdl(k_merge_parts, dim3(n_queries), dim3(256), (size_t)cap * 16, s, n_parts, n_queries, k, ids, d, counts, ids_out,
                                                          d_out, counts_out, cap, s_ids, s_d, s_cnt);
 }
 
@@ -799,10 +806,10 @@ void launch_repair(const IndexView& ix, const QueryView& qv, const uint32_t* pla
                    uint64_t* ids_out, double* d_out, uint32_t* counts_out, int* flags, cudaStream_t s) {
   double fa = 0, fb = 0, fc = 0;
   bound_ffma(ix.dim, &fa, &fb, &fc);
-  k_repair_segments<<<n_ctas, 256, 0, s>>>(ix, qv, plans, nprobe, R, tau, fa, fb, fc, flags);
+  launch_pdl(k_repair_segments, dim3(n_ctas), dim3(256), 0, s, ix, qv, plans, nprobe, R, tau, fa, fb, fc, flags);
   const size_t smem = (size_t)2 * kCandMax * 16 + (size_t)kCandMax * 8 + (size_t)ix.dpad * 4;
   smem_optin((const void*)k_finalize_repair, 200 * 1024);
-  k_finalize_repair<<<qv.n, kFinThreads, smem, s>>>(ix, qv, plans, nprobe, k, cand_d, cand_row, cand_thr,
+  launch_pdl(k_finalize_repair, dim3(qv.n), dim3(kFinThreads), smem, s, ix, qv, plans, nprobe, k, cand_d, cand_row, cand_thr,
                                                     cand_n, tau, R, ids_out, d_out, counts_out, flags);
 }
 

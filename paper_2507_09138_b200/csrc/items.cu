@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     const float* __restrict__ cand_thr, const uint32_t* __restrict__ cand_n, double eps,
     double ab, uint64_t* heap_ids, double* heap_d, uint32_t* heap_n, uint32_t stride,
     uint8_t* changed, int* flags) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   double* cdist = reinterpret_cast<double*>(sm);                // kItCand
   uint64_t* cid = reinterpret_cast<uint64_t*>(cdist + kItCand);  // kItCand
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(256) k_exact_items(IndexView ix, QueryView qv,
                                                      uint64_t* heap_ids, double* heap_d,
                                                      uint32_t* heap_n, uint32_t stride,
                                                      uint8_t* changed, const int* flags) {
+  pdl_wait();
   const uint32_t it = blockIdx.x;
   if (flags && !flags[it]) return;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -333,7 +335,7 @@ void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_
   if (!n_items) return;
   const size_t smem = (size_t)kItCand * (8 + 8 + 4 + 4) + (kNprobeMax + 1) * 4 + (size_t)ix.dpad * 4;
   smem_optin((const void*)k_finalize_items, 220 * 1024);
-  k_finalize_items<<<n_items, kItThreads, smem, s>>>(ix, qv, n_items, item_off, clusters, k, cand_d,
+  launch_pdl(k_finalize_items, dim3(n_items), dim3(kItThreads), smem, s, ix, qv, n_items, item_off, clusters, k, cand_d,
                                                      cand_row, cand_thr, cand_n, filter_eps(ix.dim),
                                                      filter_abs(ix.dim), heap_ids, heap_d, heap_n,
                                                      heap_stride, changed, flags);
@@ -347,7 +349,7 @@ void launch_exact_items(const IndexView& ix, const QueryView& qv, uint32_t n_ite
   if (!n_items) return;
   const size_t smem = (size_t)(kExactMaxK + 1) * 16 + 256 * 16 + (size_t)ix.dpad * 4;
   smem_optin((const void*)k_exact_items, 200 * 1024);
-  k_exact_items<<<n_items, 256, smem, s>>>(ix, qv, n_items, item_off, clusters, k, heap_ids, heap_d,
+  launch_pdl(k_exact_items, dim3(n_items), dim3(256), smem, s, ix, qv, n_items, item_off, clusters, k, heap_ids, heap_d,
                                            heap_n, heap_stride, changed, flags);
 }
 
@@ -357,6 +359,7 @@ namespace {
 // without touching the per-cluster `changed` semantics.
 __global__ void k_item_bounds(const double* heap_d, const uint32_t* heap_n, const uint32_t* k, uint32_t stride,
                               uint32_t n_items, float* out) {
+  pdl_wait();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
   const uint32_t n = heap_n[i];
@@ -372,7 +375,7 @@ __global__ void k_item_bounds(const double* heap_d, const uint32_t* heap_n, cons
 
 void launch_item_bounds(const double* heap_d, const uint32_t* heap_n, const uint32_t* k, uint32_t stride,
                         uint32_t n_items, float* out, cudaStream_t s) {
-  if (n_items) k_item_bounds<<<(n_items + 255) / 256, 256, 0, s>>>(heap_d, heap_n, k, stride, n_items, out);
+  if (n_items) launch_pdl(k_item_bounds, dim3((n_items + 255) / 256), dim3(256), 0, s, heap_d, heap_n, k, stride, n_items, out);
 }
 
 }  // namespace hivf

@@ -68,7 +68,31 @@ struct IndexView {
   double e_a, e_b, e_c;
 };
 
+// Programmatic dependent launch on the search path: each kernel is launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization and waits for its
+// predecessor's completion (griddepcontrol.wait) as its first instruction, so
+// the launch of kernel i+1 overlaps the tail of kernel i instead of following
+// it.  No early trigger: dependents never occupy SM slots while they wait.
+// Env HIVF_PDL=0 turns it off (plain stream order).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 #ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // candidate slots of a list of `rows` rows
 __device__ __forceinline__ uint32_t slots_of(const IndexView& ix, uint64_t rows) {
   return (uint32_t)((rows + ix.seg_rows - 1) / ix.seg_rows) * ix.seg_split;

@@ -195,6 +195,7 @@ __device__ __forceinline__ void consume_item(const ScanParams& P, const ScanItem
 }
 
 __global__ void __launch_bounds__((kScanWarps + 1) * 32, 1) k_scan(ScanParams P) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   float* stage = reinterpret_cast<float*>(smem);
   float* qsm = reinterpret_cast<float*>(smem + kStages * kStageBytes);
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__((kScanWarps + 1) * 32, 1) k_scan(ScanParams P)
 // ---- work-list construction (all on device: no host round trip) -------------
 
 __global__ void k_count_pairs(const uint32_t* pair_list, uint32_t n_pairs, uint32_t* cnt) {
+  pdl_wait();
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n_pairs) atomicAdd(&cnt[pair_list[p]], 1u);
 }
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
                                                        uint32_t* pair_off, uint32_t* cursor,
                                                        uint32_t* item_off, uint32_t* n_items,
                                                        uint32_t* work_ctr, uint32_t* qshift) {
+  pdl_wait();
   // qshift (wide tensor-core scan, optional): each list's pair range restaged
   // at an 8-row aligned offset, staged row = pair position + qshift[c]
   __shared__ uint32_t sp[1024], si[1024], sq[1024];
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(1024) k_list_offsets(IndexView ix, uint32_t gr
 
 __global__ void k_scatter_pairs(const uint32_t* pair_list, uint32_t n_pairs, const uint32_t* pair_off,
                                 uint32_t* cursor, uint32_t* sorted_pairs) {
+  pdl_wait();
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const uint32_t c = pair_list[p];
@@ -361,6 +365,7 @@ __global__ void k_scatter_pairs(const uint32_t* pair_list, uint32_t n_pairs, con
 __global__ void k_make_items(IndexView ix, uint32_t group, const uint32_t* cnt,
                              const uint32_t* pair_off,
                              const uint32_t* item_off, ScanItem* items) {
+  pdl_wait();
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ix.K) return;
   const uint32_t n = cnt[c];
@@ -399,6 +404,7 @@ __global__ void __launch_bounds__(1024) k_worklist_fused(IndexView ix, uint32_t 
                                                          uint32_t* sorted_pairs, ScanItem* items,
                                                          uint32_t* n_items, uint32_t* work_ctr,
                                                          uint32_t* qshift) {
+  pdl_wait();
   extern __shared__ uint32_t wsm[];
   uint32_t* cnt = wsm;            // [K]
   uint32_t* poff = cnt + ix.K;    // [K]
@@ -499,18 +505,18 @@ void launch_build_worklist(const IndexView& ix, uint32_t group, const uint32_t* 
   if (ix.K <= kFusedK && n_pairs <= 8192u) {  // C3 (32k pairs) is faster on the 4-kernel chain
     const size_t smem = (size_t)ix.K * 12;
     smem_optin((const void*)k_worklist_fused, (int)(kFusedK * 12));
-    k_worklist_fused<<<1, 1024, smem, s>>>(ix, group, pair_list, n_pairs, list_cnt, list_pair_off,
+    launch_pdl(k_worklist_fused, dim3(1), dim3(1024), smem, s, ix, group, pair_list, n_pairs, list_cnt, list_pair_off,
                                            list_item_off, sorted_pairs, items, n_items, work_ctr, qshift);
     return;
   }
   cudaMemsetAsync(list_cnt, 0, sizeof(uint32_t) * ix.K, s);
-  if (n_pairs) k_count_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_cnt);
-  k_list_offsets<<<1, 1024, 0, s>>>(ix, group, list_cnt, list_pair_off, list_cursor, list_item_off,
+  if (n_pairs) launch_pdl(k_count_pairs, dim3((n_pairs + 255) / 256), dim3(256), 0, s, pair_list, n_pairs, list_cnt);
+  launch_pdl(k_list_offsets, dim3(1), dim3(1024), 0, s, ix, group, list_cnt, list_pair_off, list_cursor, list_item_off,
                                     n_items, work_ctr, qshift);
   if (n_pairs)
-    k_scatter_pairs<<<(n_pairs + 255) / 256, 256, 0, s>>>(pair_list, n_pairs, list_pair_off,
+    launch_pdl(k_scatter_pairs, dim3((n_pairs + 255) / 256), dim3(256), 0, s, pair_list, n_pairs, list_pair_off,
                                                           list_cursor, sorted_pairs);
-  k_make_items<<<(ix.K + 255) / 256, 256, 0, s>>>(ix, group, list_cnt, list_pair_off, list_item_off, items);
+  launch_pdl(k_make_items, dim3((ix.K + 255) / 256), dim3(256), 0, s, ix, group, list_cnt, list_pair_off, list_item_off, items);
 }
 
 void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items,
@@ -520,7 +526,7 @@ void launch_scan(const IndexView& ix, const QueryView& qv, const ScanItem* items
   ScanParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr, out_n};
   const int smem = scan_smem_bytes(ix.dpad);
   smem_optin((const void*)k_scan, smem);
-  k_scan<<<n_ctas, (kScanWarps + 1) * 32, smem, s>>>(P);
+  launch_pdl(k_scan, dim3(n_ctas), dim3((kScanWarps + 1) * 32), smem, s, P);
 }
 
 }  // namespace hivf

@@ -507,6 +507,7 @@ __device__ __forceinline__ void epilogue128(const TcParams& P, uint32_t tmem_bas
 // tf32; 128: 16-deep per-warp lists, two epilogue groups of 64 queries)
 template <int kQ>
 __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
+  pdl_wait();
   // wide: warps 2-5 are a second epilogue group (queries kQ/2.. of the item)
   // instead of stagers/splitters; single-pass tf32 only
   constexpr bool kWide = kQ != 0;
@@ -1249,6 +1250,7 @@ __device__ __noinline__ Cand merge_quad8(float s0, float s1, float s2, float s3,
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_scan_pair(TcParams P) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kSB = kPairStageA + kPairQB;  // A tile stage + this CTA's half query slice
@@ -1740,16 +1742,16 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
   const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list, o);
   if (q == kTcPairQ) {
     smem_optin((const void*)k_scan_pair, smem);
-    k_scan_pair<<<std::max(2, n_ctas & ~1), kPairThreads, smem, s>>>(P);
+    launch_pdl(k_scan_pair, dim3(std::max(2, n_ctas & ~1)), dim3(kPairThreads), smem, s, P);
   } else if (q == kTcWide2Q) {
     smem_optin((const void*)k_scan_tc<128>, smem);
-    k_scan_tc<128><<<n_ctas, kTcThreads, smem, s>>>(P);
+    launch_pdl(k_scan_tc<128>, dim3(n_ctas), dim3(kTcThreads), smem, s, P);
   } else if (wide) {
     smem_optin((const void*)k_scan_tc<64>, smem);
-    k_scan_tc<64><<<n_ctas, kTcThreads, smem, s>>>(P);
+    launch_pdl(k_scan_tc<64>, dim3(n_ctas), dim3(kTcThreads), smem, s, P);
   } else {
     smem_optin((const void*)k_scan_tc<0>, smem);
-    k_scan_tc<0><<<n_ctas, kTcThreads, smem, s>>>(P);
+    launch_pdl(k_scan_tc<0>, dim3(n_ctas), dim3(kTcThreads), smem, s, P);
   }
 }
 
@@ -1768,6 +1770,7 @@ __global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs
                                                     const uint32_t* __restrict__ list_cnt,
                                                     const uint32_t* __restrict__ qshift, uint8_t* qstage,
                                                     uint32_t n_pairs, uint32_t G) {
+  pdl_wait();
   const uint32_t p = blockIdx.x * 8 + (threadIdx.x >> 5);  // one warp per pair
   if (p >= n_pairs) return;
   const uint32_t pair = sorted_pairs[p];
@@ -1803,7 +1806,7 @@ void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t*
                        const uint32_t* pair_query, const uint32_t* pair_list, const uint32_t* pair_off,
                        const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s) {
   if (n_pairs)
-    k_stage_wide<<<(n_pairs + 7) / 8, 256, 0, s>>>(qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list,
+    launch_pdl(k_stage_wide, dim3((n_pairs + 7) / 8), dim3(256), 0, s, qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list,
                                                    pair_off, list_cnt, ws.qshift, ws.qstage, n_pairs, ws.group);
 }
 
