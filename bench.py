@@ -714,23 +714,31 @@ def run_shard_sweep(args, wl, ctx, cfg):
     t_assign = time.time() - t0
     B, npb, k = cfg.batch, cfg.nprobe, cfg.k
     pool = [wl.queries(i) for i in range(args.pool)]
+    pool_np = [q.cpu().numpy() for q in pool]
     rows = []
-    o = (torch.zeros(B, k, dtype=torch.int64, device=wl.device),
-         torch.zeros(B, k, dtype=torch.float64, device=wl.device),
-         torch.zeros(B, dtype=torch.int32, device=wl.device))
+    # one output set per pool batch: the timed steps' results stay for parity
+    outs_t = [(torch.zeros(B, k, dtype=torch.int64, device=wl.device),
+               torch.zeros(B, k, dtype=torch.float64, device=wl.device),
+               torch.zeros(B, dtype=torch.int32, device=wl.device)) for _ in pool]
+    o = outs_t[0]
     stream = torch.cuda.current_stream()
     for r in ranks:
         ix, _, sizes, local_sizes, owner, _, info = build_index(wl, ctx, r, N, cents, assign)
         for i in range(args.warmup):
-            ix.search_device(pool[i % len(pool)], npb, k, *o)
+            ix.search_device(pool[i % len(pool)], npb, k, *outs_t[i % len(pool)])
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
-            ix.search_device(pool[i % len(pool)], npb, k, *o)
+            ix.search_device(pool[i % len(pool)], npb, k, *outs_t[i % len(pool)])
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
+        parity = None
+        if not args.no_cpu:  # this shard's exact local top-k vs the reference on the shard's lists
+            outs = [tuple(t.cpu().numpy() for t in ot) for ot in outs_t]
+            outs = [(a.view(np.uint64), b, c.view(np.uint32)) for a, b, c in outs]
+            _, parity, _ = reference_on_sample(ix, cents, cfg, args, pool_np, local_sizes, outs, time_it=False)
         ctx.set_option("time_kernels", 1)
         ctx.set_option("reset_timers", 1)
         for i in range(args.steps):
@@ -742,7 +750,9 @@ def run_shard_sweep(args, wl, ctx, cfg):
         rows.append({"rank": r, "local_rows": info["local_rows"], "ms_per_step": round(ms, 4),
                      "assign_ms": round(st["assign_ms"] / n, 4), "scan_ms": round(st["scan_ms"] / n, 4),
                      "finalize_ms": round(st["finalize_ms"] / n, 4),
-                     "striped_lists": info["shard"]["striped_lists"]})
+                     "striped_lists": info["shard"]["striped_lists"],
+                     "parity_sample": parity and {kk: parity[kk] for kk in ("queries", "from_timed_batch",
+                                                                          "bit_exact", "mismatched_queries")}})
         log(f"shard {r}/{N}: {rows[-1]}")
         ix.close()
         del ix
