@@ -380,6 +380,53 @@ std::vector<TopKResult> search(const IvfIndex& index, const std::vector<Embeddin
   return out;
 }
 
+std::vector<TopKResult> brute_force_search(Context& ctx, const Corpus& corpus,
+                                           const std::vector<Embedding>& queries, std::size_t k) {
+  if (k == 0) throw std::invalid_argument("brute_force_search: k must be >= 1");
+  std::vector<TopKResult> out(queries.size(), TopKResult(k));
+  if (corpus.size() == 0 || queries.empty()) return out;
+  if (corpus.data.size() != corpus.size() * corpus.dim)
+    throw std::invalid_argument("brute_force_search: corpus data / doc_ids size mismatch");
+  const std::uint32_t dim = corpus.dim;
+  std::vector<float> rows;
+  const float* v = corpus.data.data();
+  if (corpus.metric == Metric::Cosine) {  // the reference normalizes every row it scores
+    rows.resize(corpus.data.size());
+    for (std::size_t i = 0; i < corpus.size(); ++i) {
+      const Embedding e = normalized(corpus.embedding(i));
+      std::copy(e.begin(), e.end(), rows.begin() + i * dim);
+    }
+    v = rows.data();
+  }
+  const std::vector<float> cent(dim, 0.0f);
+  const std::uint64_t off[2] = {0, corpus.size()};
+  hivf_index* ix = nullptr;
+  check(hivf_index_upload(ctx.raw(), dim, static_cast<int>(corpus.metric), 1, cent.data(), off, v,
+                          corpus.doc_ids.data(), &ix));
+  std::vector<float> q(queries.size() * dim);
+  for (std::size_t i = 0; i < queries.size(); ++i) {
+    if (queries[i].size() != dim) {
+      hivf_index_destroy(ix);
+      throw std::invalid_argument("squared_l2: dimension mismatch");
+    }
+    std::copy(queries[i].begin(), queries[i].end(), q.begin() + i * dim);
+  }
+  const std::size_t kk = std::min<std::size_t>(k, corpus.size());
+  std::vector<std::uint64_t> ids(queries.size() * kk);
+  std::vector<double> d(queries.size() * kk);
+  std::vector<std::uint32_t> cnt(queries.size());
+  const hivf_status st = hivf_search(ix, q.data(), static_cast<std::uint32_t>(queries.size()), 1,
+                                     static_cast<std::uint32_t>(kk), ids.data(), d.data(), cnt.data());
+  hivf_index_destroy(ix);
+  check(st);
+  for (std::size_t i = 0; i < queries.size(); ++i) out[i].assign_sorted(ids.data() + i * kk, d.data() + i * kk, cnt[i]);
+  return out;
+}
+
+TopKResult brute_force_search(Context& ctx, const Corpus& corpus, const Embedding& query, std::size_t k) {
+  return brute_force_search(ctx, corpus, std::vector<Embedding>{query}, k)[0];
+}
+
 }  // namespace ivf
 
 // ---- cache::ClusterCacheState ------------------------------------------------------

@@ -215,6 +215,15 @@ std::vector<SearchStepReport> search_clusters_batch(
 std::vector<TopKResult> search(const IvfIndex& index, const std::vector<Embedding>& queries,
                                std::size_t nprobe, std::size_t k);
 
+// brute_force_search (vector_index.cpp:330-342): every corpus row, exact
+// distances, (distance, id) order -- on the device through a one-list index
+// of the corpus (cosine: rows and queries normalized as the reference does).
+// Batched form uploads the corpus once.  Duplicate doc ids -> invalid_argument
+// (the device index needs unique ids; the reference would keep the minimum).
+std::vector<TopKResult> brute_force_search(Context& ctx, const Corpus& corpus,
+                                           const std::vector<Embedding>& queries, std::size_t k);
+TopKResult brute_force_search(Context& ctx, const Corpus& corpus, const Embedding& query, std::size_t k);
+
 }  // namespace ivf
 
 namespace cache {

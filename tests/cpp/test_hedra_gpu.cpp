@@ -483,6 +483,36 @@ TEST_GPU(build_index_equals_from_assignments_and_brute_force) {
   }
 }
 
+TEST_GPU(brute_force_search_matches_reference) {  // vector_index.cpp:330-342
+  ivf::Context ctx(0);
+  for (int metric = 0; metric < 2; ++metric) {
+    const Data d = random_data(400 + metric, 2500, 20, 4);
+    ivf::Corpus corpus;
+    corpus.dim = d.dim;
+    corpus.metric = metric ? Metric::Cosine : Metric::L2;
+    corpus.data = d.x;
+    corpus.doc_ids = d.ids;
+    std::mt19937_64 g(11 + metric);
+    std::vector<Embedding> qs;
+    for (int t = 0; t < 24; ++t) qs.push_back(rand_query(g, d.dim, metric ? 2.0 : 1.0));
+    const auto got = ivf::brute_force_search(ctx, corpus, qs, 10);
+    CHECK(got.size() == qs.size());
+    for (std::size_t t = 0; t < qs.size(); ++t) CHECK(got[t] == brute(d, qs[t], 10, metric));
+    CHECK(ivf::brute_force_search(ctx, corpus, qs[3], 10) == got[3]);
+    // k above the corpus size: every row, in order
+    ivf::Corpus small = corpus;
+    small.data.resize(7 * d.dim);
+    small.doc_ids.resize(7);
+    Data ds = d;
+    ds.x.resize(7 * d.dim);
+    ds.ids.resize(7);
+    CHECK(ivf::brute_force_search(ctx, small, qs[0], 50) == brute(ds, qs[0], 50, metric));
+  }
+  ivf::Corpus empty;
+  empty.dim = 4;
+  CHECK(ivf::brute_force_search(ctx, empty, Embedding(4, 1.0f), 5).empty());
+}
+
 TEST_GPU(train_kmeans_contract) {
   ivf::Context ctx(0);
   const Data d = random_data(17, 2000, 8, 4);
