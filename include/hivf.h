@@ -381,7 +381,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value);
  * hivf_debug_tc_dot: the list scan's tensor-core dot product in isolation on
  *   the current device (one CTA; A[128][D], B[n][D] host, n in {8, 16};
  *   split = 1 reproduces the 3-pass split, out[128][2n] = [hi*hi + lo*hi |
- *   hi*lo], else out[128][n]).  Used to validate the accumulation term of the
+ *   hi*lo], split = 2 the fp16 filter's kind::f16 MMA on RN-converted fp16
+ *   operands (K = 16 per step), else out[128][n]).  Used to validate the accumulation term of the
  *   filter bound on adversarial data (tests/test_gpu_tc_bound.py).
  * hivf_debug_bound: the filter-bound coefficients (e_a, e_b, e_c) of a scan
  *   kind (0 FFMA, 2 split tensor-core, 3 single-pass tensor-core) at dim D.

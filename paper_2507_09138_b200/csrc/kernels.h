@@ -217,6 +217,7 @@ int scan_tc_smem_bytes(uint32_t dpad, int split, float probes_per_list, const Tc
 void bound_ffma(uint32_t dim, double* a, double* b, double* c);
 void bound_tc(uint32_t dim, double* a, double* b, double* c);   // 3-pass split
 void bound_tc1(uint32_t dim, double* a, double* b, double* c);  // single pass
+void bound_h16(uint32_t dim, double* a, double* b, double* c);  // single pass over the fp16 filter copy
 
 // ---- kmeans.cu (index build: train_kmeans / Lloyd, vector_index.cpp:99-200)
 void launch_kmeans_dist2(const float* X, uint64_t n, uint32_t dim, const float* c, double* dist2, int mode,

@@ -23,6 +23,7 @@
 //   item end         cross-warp bitonic merge -> 32 (dist32, row) per
 //                    (query, segment) + drop threshold, for the exact re-rank
 //                    in finalize.cu.
+#include <cmath>
 #include <cfloat>
 
 #include "common.cuh"
@@ -562,6 +563,22 @@ namespace hivf {
 void bound_tc1(uint32_t dim, double* a, double* b, double* c) {
   const double u = 5.9604644775390625e-08, u53 = 1.1102230246251565e-16;
   const double alpha = (0x1p-9 + 0x1p-20 + 0.5 * (double)dim * 0x1p-22) * 1.01;
+  *a = 1.5 * (2.0 * alpha + 4.0 * u + 2.0 * (3.0 * dim + 6.0) * u53);
+  *b = 1.5 * (4.0 * u + (3.0 * dim + 6.0) * u53);
+  *c = filter_abs(dim);
+}
+// Tensor-core scan over the fp16 filter copy (kind::f16): every row and query
+// is scaled by a power of two (exact) so |element| < 2^15, then rounded to
+// fp16 (RN: <= 2^-11 relative per element, both operands -> (2^-10 + 2^-22)
+// |x||q| by Cauchy-Schwarz); elements below the fp16 normal range carry at
+// most 2^-25 absolute in scaled units, <= 2^-39 |v| after unscaling, summing
+// to <= 2 sqrt(D) 2^-38 |x||q|; the fp32 accumulation keeps the single-pass
+// tf32 allowance (D/16 k-steps here, D/8 there).  Unscaling is a power-of-2
+// multiply folded into the distance's fma (exact).  x1.5 headroom.
+void bound_h16(uint32_t dim, double* a, double* b, double* c) {
+  const double u = 5.9604644775390625e-08, u53 = 1.1102230246251565e-16;
+  const double alpha =
+      (0x1p-10 + 0x1p-22 + 2.0 * std::sqrt((double)dim) * 0x1p-38 + 0.5 * (double)dim * 0x1p-22) * 1.01;
   *a = 1.5 * (2.0 * alpha + 4.0 * u + 2.0 * (3.0 * dim + 6.0) * u53);
   *b = 1.5 * (4.0 * u + (3.0 * dim + 6.0) * u53);
   *c = filter_abs(dim);

@@ -42,6 +42,8 @@
 #include <cstdlib>
 #include <cfloat>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -81,7 +83,7 @@ struct TcParams {
   uint32_t qmax;  // queries per item (8..32)
   uint32_t sa;    // A landing-ring depth (16 KB stages)
   int conv;       // tensor-core tf32 conversion (0 trunc, 1 RNE)
-  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA, bit2 skip all MMAs, bit3 skip odd k-steps (results then inexact), bit4 spin-wait epilogue
+  int variant;    // debug: bit0 skip split math, bit1 skip lo(A) MMA, bit2 skip all MMAs, bit3 skip odd k-steps (results then inexact), bit4 spin-wait epilogue, bit5 skip the pair scan's tile epilogue
   int split;      // 1: 3-pass split precision, 0: single-pass tf32 (looser bound)
   unsigned long long* prof;  // debug: per-CTA stall counters [gridDim.x][16] (nullptr = off)
   // shared per-query drop bound: U_q = min over
@@ -124,6 +126,19 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// kind::f16 with fp16 operands (A, B type 0) and an f32 accumulator: K = 16 per
+// instruction, i.e. the same 32 B of each operand row per k-step as tf32's K = 8
+__device__ __forceinline__ uint32_t f16_idesc_m(uint32_t m, uint32_t n) {
+  return (1u << 4) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
@@ -1412,7 +1427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
 #pragma unroll
               for (uint32_t k2 = 0; k2 < 2; ++k2) {
                 const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
-                if (lane == 0) mma2_tf32(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
+                if (lane == 0 && !(P.variant & 4)) mma2_tf32(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
               }
             }
             if (lane == 0) mma2_commit_both(&empty[a]);  // the slot is free in both CTAs
@@ -1490,6 +1505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
         tc_fence_after();
         const long long _te = P.prof ? clock64() : 0;
         float gl[2] = {kInfF, kInfF};
+        if (!(P.variant & 32)) {  // debug bit5: skip the tile's epilogue math
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           if (P.topk && 32 * m + lane < nq) {
@@ -1529,6 +1545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
             ld[sp] = r.v;
             lr[sp] = r.r;
           }
+        }
         }
         tc_fence_before();
         __syncwarp();
@@ -1934,7 +1951,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_dot(const float* __restrict__ A, 
   __shared__ uint64_t bar;
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t nb = split ? 2 * n : n;  // B rows: [q ; lo(q)]
+  const uint32_t nb = split == 1 ? 2 * n : n;  // B rows: [q ; lo(q)]
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
@@ -1949,7 +1966,33 @@ __global__ void __launch_bounds__(128, 1) k_tc_dot(const float* __restrict__ A, 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t nch = (D + 15) / 16;
+  if (split == 2) {  // kind::f16: fp16 operands (RN conversion here), 32-dim chunks, K = 16 per MMA
+    const uint32_t nch16 = (D + 31) / 32;
+    for (uint32_t ch = 0; ch < nch16; ++ch) {
+      for (int g = 0; g < 4; ++g)
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t d = ch * 32 + g * 8 + e;
+          const uint32_t off = tid * 64 + ((g ^ ((tid >> 1) & 3)) << 4) + e * 2;
+          *reinterpret_cast<__half*>(a + off) = __float2half_rn(d < D ? A[(size_t)tid * D + d] : 0.f);
+          if ((uint32_t)tid < n) *reinterpret_cast<__half*>(b + off) = __float2half_rn(d < D ? B[(size_t)tid * D + d] : 0.f);
+        }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        for (int k2 = 0; k2 < 2; ++k2) {
+          const uint64_t ad = sw64_kmajor_desc(smem_u32(a)) + (uint64_t)(k2 * 2);
+          const uint64_t bd = sw64_kmajor_desc(smem_u32(b)) + (uint64_t)(k2 * 2);
+          mma_f16(tmem, ad, bd, f16_idesc_m(128, n), (ch | k2) != 0);
+        }
+        mma_commit(&bar);
+      }
+      mbar_wait(&bar, ch & 1);
+      tc_fence_after();
+      __syncthreads();
+    }
+  }
+  const uint32_t nch = split == 2 ? 0u : (D + 15) / 16;
   for (uint32_t ch = 0; ch < nch; ++ch) {
     // A row `tid` (and lo(A)); B rows for tid < nb; zero past D
     for (int g = 0; g < 4; ++g)
@@ -2113,7 +2156,7 @@ extern "C" int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, uns
   if (!A || !B || !out || D == 0 || (n != 8 && n != 16)) return 1;
   const int conv = tc_conversion_mode();
   if (conv > 1) return 2;
-  const size_t nb = split ? 2 * n : n;
+  const size_t nb = split == 1 ? 2 * n : n;
   float *dA = nullptr, *dB = nullptr, *dO = nullptr;
   int rc = 0;
   if (cudaMalloc(&dA, 128ull * D * 4) != cudaSuccess || cudaMalloc(&dB, (size_t)n * D * 4) != cudaSuccess ||
@@ -2137,6 +2180,7 @@ extern "C" int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, uns
 extern "C" int hivf_debug_bound(int kind, unsigned D, double* e_a, double* e_b, double* e_c) {
   if (kind == 2) hivf::bound_tc(D, e_a, e_b, e_c);
   else if (kind == 3) hivf::bound_tc1(D, e_a, e_b, e_c);
+  else if (kind == 4) hivf::bound_h16(D, e_a, e_b, e_c);
   else hivf::bound_ffma(D, e_a, e_b, e_c);
   return 0;
 }

@@ -52,10 +52,10 @@ def tc_dot(L, A, B, split):
     A = np.ascontiguousarray(A, np.float32)
     B = np.ascontiguousarray(B, np.float32)
     n = B.shape[0]
-    out = np.zeros((128, 2 * n if split else n), np.float32)
+    out = np.zeros((128, 2 * n if split == 1 else n), np.float32)
     rc = L.hivf_debug_tc_dot(A.ctypes.data, B.ctypes.data, A.shape[1], n, int(split), out.ctypes.data)
     assert rc == 0, rc
-    if split:  # the epilogue's combine: fp32 add of [hi*hi + lo*hi] and [hi*lo]
+    if split == 1:  # the epilogue's combine: fp32 add of [hi*hi + lo*hi] and [hi*lo]
         return (out[:, :n] + out[:, n:]).astype(np.float32)
     return out
 
@@ -188,6 +188,63 @@ def test_accumulation_error_inside_model(L):
         report[f"e_a_kind{kind}"] = ea.value
     os.makedirs("gpurun_out", exist_ok=True)
     with open(os.path.join("gpurun_out", "tc_bound.json"), "w") as f:
+        json.dump(report, f, indent=1)
+
+
+def f16(x):
+    """Round-to-nearest to fp16 (values in the fp16 normal range stay exact afterwards)."""
+    return np.asarray(x, np.float32).astype(np.float16).astype(np.float32)
+
+
+def alpha_h16(dim):
+    # bound_h16 (scan.cu): RN fp16 operands (2^-11 each, Cauchy-Schwarz), the
+    # subnormal floor after the per-vector power-of-2 scaling, and the same
+    # accumulation allowance as the single-pass tf32 scan (twice the k-steps)
+    return 2 ** -10 + 2 ** -22 + 2 * np.sqrt(dim) * 2 ** -38 + 0.5 * dim * 2 ** -22, 0.5 * dim * 2 ** -22
+
+
+def test_f16_accumulation_error_inside_model(L):
+    """The fp16 filter copy's MMA (kind::f16, K = 16 per step, f32 accumulate):
+    the same adversarial accumulation cases on fp16-exact operands, then raw
+    fp32 operands through the RN conversion, against bound_h16."""
+    import ctypes as C
+    rng = np.random.default_rng(8)
+    report = {"D": D, "accumulation_only": {}, "full_dot": {}}
+    ea, eb, ec = C.c_double(), C.c_double(), C.c_double()
+    assert L.hivf_debug_bound(4, D, C.byref(ea), C.byref(eb), C.byref(ec)) == 0
+    a_full, a_acc = alpha_h16(D)
+    assert ea.value >= 2 * a_full * 1.4
+    worst = 0.0
+    for name, A, B in adversarial_cases(rng):
+        if name == "exponent_spread":  # keep inside the fp16 normal range
+            A = np.sign(A) * 2.0 ** rng.uniform(-14, 0, A.shape)
+            B = np.sign(B) * 2.0 ** rng.uniform(-14, 0, B.shape)
+        A, B = f16(A), f16(B)
+        r = ratios(L, A, B, 2).max()
+        report["accumulation_only"][name] = {"max_err_over_xq": float(r), "frac_of_accumulation_model": float(r / a_acc),
+                                             "frac_of_e_a": float(2 * r / ea.value)}
+        worst = max(worst, r / a_acc)
+        assert r <= a_acc, (name, r, a_acc)
+        assert 2 * r / ea.value <= 0.25, name
+    assert worst <= 0.5, worst
+    report["worst_frac_of_accumulation_model"] = float(worst)
+    full = {
+        "gaussian": (rng.standard_normal((128, D)) * 900.0, rng.standard_normal((16, D)) * 700.0),
+        "max_rounding": (np.full((128, D), 1.0 + 1023.5 / 1024, np.float32) *
+                         rng.choice([1, 2, 4], (128, D)).astype(np.float32),
+                         np.full((16, D), 1.0 + 1023.5 / 1024, np.float32)),
+        "spread_raw": (2.0 ** rng.uniform(-10, 14, (128, D)) * rng.choice([-1, 1], (128, D)),
+                       2.0 ** rng.uniform(-10, 14, (16, D)) * rng.choice([-1, 1], (16, D))),
+    }
+    for name, (A, B) in full.items():
+        A = np.asarray(A, np.float32)
+        B = np.asarray(B, np.float32)
+        r = ratios(L, A, B, 2).max()
+        report["full_dot"][name] = {"max_err_over_xq": float(r), "frac_of_alpha": float(r / a_full)}
+        assert r <= a_full, (name, r, a_full)
+    report["e_a_kind4"] = ea.value
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(os.path.join("gpurun_out", "tc_bound_f16.json"), "w") as f:
         json.dump(report, f, indent=1)
 
 
