@@ -581,8 +581,9 @@ def run_hivf(args):
     # algorithmic bytes of the steps (distinct lists per batch) over
     # this rank's rows
     plans = [ix.select_clusters(q, npb) for q in pool_np]
-    lb = [list_bytes(p, local_sizes, cfg.dim) for p in plans]
-    ab = [algorithmic_bytes(p, local_sizes, cfg.dim, cfg.k_clusters) for p in plans]
+    elem = st["scan_filter_bits"] // 8  # 2: the scan streamed the fp16 filter copy
+    lb = [list_bytes(p, local_sizes, cfg.dim, elem) for p in plans]
+    ab = [algorithmic_bytes(p, local_sizes, cfg.dim, cfg.k_clusters, elem) for p in plans]
     scan_bytes = float(np.mean([lb[i % len(pool)] for i in range(args.steps)]))
     step_ab = float(np.mean([ab[i % len(pool)] for i in range(args.steps)]))
     pp = np.bincount(plans[0].ravel(), minlength=cfg.k_clusters)
@@ -595,7 +596,7 @@ def run_hivf(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}"
-                               f"{'_b%d' % B if B != 256 else ''}.json")) as f:
+                               f"{'_b%d' % B if B != 256 else ''}{'_h16' if elem == 2 else ''}.json")) as f:
             tj = json.load(f)
         if world == 1 and not args.hbm_budget_gb:
             traffic = int(tj["dram_bytes_per_launch"])
@@ -641,7 +642,11 @@ def run_hivf(args):
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        # filter: fp16 filter copy x fp16 queries, fp32 accumulate (or tf32 over the
+        # fp32 lists); results: the reference's exact fp64 distances
+        "dtype": "f16+f32+f64" if elem == 2 else "f32+f64",
+        "filter": "fp16 filter copy (DESIGN.md 3a), exact fp64 re-rank" if elem == 2 else "fp32 lists (tf32), exact fp64 re-rank",
         "data": "synthetic gaussian mixture (bench_workload.py), generated on device",
         "launch": "cuda-graph replay of hivf_search_device" if graphs is not None else "direct launches",
         "api": "hivf_search_device" if group is None else "hivf_group_search_device (NCCL shard group)",

@@ -207,14 +207,16 @@ def list_layout(assign: torch.Tensor, k_clusters: int):
     return off, pos, order
 
 
-def algorithmic_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int, k_clusters: int) -> int:
-    """distinct probed lists streamed once + centroids + queries."""
+def algorithmic_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int, k_clusters: int, elem: int = 4) -> int:
+    """distinct probed lists streamed once (elem bytes per
+    element: 4 for the fp32 lists, 2 when the scan reads the fp16 filter copy)
+    + centroids + queries."""
     uniq = np.unique(plans)
-    return int(sizes[uniq].sum()) * 4 * dim + k_clusters * 4 * dim + plans.shape[0] * 4 * dim
+    return int(sizes[uniq].sum()) * elem * dim + k_clusters * 4 * dim + plans.shape[0] * 4 * dim
 
 
-def list_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int) -> int:
-    return int(sizes[np.unique(plans)].sum()) * 4 * dim
+def list_bytes(plans: np.ndarray, sizes: np.ndarray, dim: int, elem: int = 4) -> int:
+    return int(sizes[np.unique(plans)].sum()) * elem * dim
 
 
 def human(n: float) -> str:

@@ -349,7 +349,8 @@ typedef struct {
   uint32_t n_work_items;       /* grouped-scan work items of the last call */
   uint32_t n_fallback;         /* queries that took an exact fallback path (last call) */
   uint32_t n_unique_lists;     /* distinct lists probed by the last batch */
-  uint64_t scan_bytes;         /* algorithmic list bytes of the last batch (sum n_c*dim*4) */
+  uint64_t scan_bytes;         /* algorithmic list bytes of the last batch (sum n_c*dim*4, or
+                                  n_c*dim*2 when the scan read the fp16 filter copy) */
   uint32_t timed_calls;        /* calls accumulated below (option "time_kernels") */
   double assign_ms;            /* accumulated CUDA-event time: coarse assign kernels */
   double scan_ms;              /* accumulated CUDA-event time: grouped list scan kernel */
@@ -357,6 +358,7 @@ typedef struct {
   uint32_t scan_kernel;        /* last call: 0 exact only, 1 FFMA, 2 tcgen05 split, 3 tcgen05 single */
   uint32_t scan_group;         /* last call: queries per scan work item (8..32 narrow, 64 / 128 wide,
                                   256 = the CTA-pair scan) */
+  uint32_t scan_filter_bits;   /* last call: 16 = the scan read the fp16 filter copy, 32 = the fp32 lists */
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",

@@ -56,7 +56,8 @@ class Stats(C.Structure):
                 ("n_fallback", C.c_uint32), ("n_unique_lists", C.c_uint32),
                 ("scan_bytes", C.c_uint64), ("timed_calls", C.c_uint32),
                 ("assign_ms", C.c_double), ("scan_ms", C.c_double), ("finalize_ms", C.c_double),
-                ("scan_kernel", C.c_uint32), ("scan_group", C.c_uint32)]
+                ("scan_kernel", C.c_uint32), ("scan_group", C.c_uint32),
+                ("scan_filter_bits", C.c_uint32)]
 
 
 _lib = None

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -215,6 +216,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   g_state_gen.fetch_add(1);  // any option may change what a captured search graph launches
   if (!strcmp(name, "search_graph")) {
     ctx->opt_search_graph = value != 0;
+  } else if (!strcmp(name, "filter_h16")) {  // 1: fp16 filter copy built at index finish and used
+    ctx->opt_h16 = value != 0;
   } else if (!strcmp(name, "seg_rows")) {  // 0: automatic (auto_seg_rows)
     if (value != 0 && (value < kRowBlock || value % kRowBlock))
       return fail(HIVF_EINVAL, "seg_rows must be a multiple of %d", kRowBlock);
@@ -282,7 +285,7 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
     for (uint32_t c = 0; c < ctx->last_K; ++c)
       if (cnt[c]) {
         ++s.n_unique_lists;
-        s.scan_bytes += (off[c + 1] - off[c]) * (uint64_t)ctx->last_index->dim * 4;
+        s.scan_bytes += (off[c + 1] - off[c]) * (uint64_t)ctx->last_index->dim * (ctx->last_filter_bits / 8);
       }
   }
   if (ctx->last_nq && ctx->flags_f.p && ctx->flags_c.p) {
@@ -302,6 +305,7 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
   }
   s.scan_kernel = ctx->last_kind;
   s.scan_group = ctx->last_group;
+  s.scan_filter_bits = ctx->last_filter_bits;
   *out = s;
   return HIVF_OK;
 }
@@ -463,6 +467,40 @@ hivf_status hivf_index_get_rows(hivf_index* ix, uint64_t first_row, uint64_t n_r
   return HIVF_OK;
 }
 
+// fp16 filter copy: per-list power-of-2 scale
+// from the list's norm bound, then the rows rounded to fp16 in the scan layout.
+// Optional: not for tiered (host-backed) indexes, and skipped -- the scan then
+// reads the fp32 lists -- when a list's scale is out of range or HBM is short.
+static void build_h16(hivf_index* ix) {
+  if (ix->tiered || ix->N == 0) return;
+  cudaStream_t s = ix->ctx->stream;
+  std::vector<float> mx(ix->K);
+  if (cudaMemcpy(mx.data(), ix->maxnorm_bits, ix->K * 4ull, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  std::vector<float> sc(ix->K);
+  for (uint32_t c = 0; c < ix->K; ++c) {
+    const int e = h16_exp(mx[c]);
+    if (e < -kH16ExpMax || e > kH16ExpMax) return;
+    sc[c] = std::ldexp(1.f, -e);
+  }
+  const uint32_t dph = (ix->dim + 31) / 32 * 32;
+  ix->dpf = dph / 2;
+  if (cudaMalloc(&ix->vech, ix->N * ix->dpf * 4ull) != cudaSuccess ||
+      cudaMalloc(&ix->lsc, ix->K * 4ull) != cudaSuccess) {
+    (void)cudaGetLastError();
+    cudaFree(ix->vech);
+    cudaFree(ix->lsc);
+    ix->vech = ix->lsc = nullptr;
+    return;
+  }
+  cudaMemcpyAsync(ix->lsc, sc.data(), ix->K * 4ull, cudaMemcpyHostToDevice, s);
+  launch_pack_h16(ix->vec, ix->d_list_off, ix->K, ix->dpad, ix->dpf, ix->N, ix->lsc, ix->vech, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    cudaFree(ix->vech);
+    cudaFree(ix->lsc);
+    ix->vech = ix->lsc = nullptr;
+  }
+}
+
 hivf_status hivf_index_finish(hivf_index* ix) {
   if (!ix) return fail(HIVF_EINVAL, "index is NULL");
   cudaStream_t s = ix->ctx->stream;
@@ -488,6 +526,7 @@ hivf_status hivf_index_finish(hivf_index* ix) {
   CK(cudaStreamSynchronize(s));
   if (err == 1) return fail(HIVF_EINVAL, "index: non-finite value in vectors or centroids");
   if (err == 2) return fail(HIVF_EINVAL, "build_index: duplicate doc_id");
+  if (ix->ctx->opt_h16) build_h16(ix);
   ix->finished = true;
   return HIVF_OK;
 }
@@ -687,14 +726,17 @@ static hivf_status prep_queries(hivf_index* ix, const float* d_q, uint32_t n, bo
   CK(c->qs.ensure((size_t)n * ix->dpad * 4));
   CK(c->qn2.ensure((size_t)n * 4));
   CK(c->qnorm.ensure((size_t)n * 4));
+  CK(c->qsc.ensure((size_t)n * 4));
   CK(c->err.ensure(4));
   launch_prep_queries(d_q, n, ix->dim, ix->dpad, ix->metric, normalize, c->qs.as<float>(),
-                      c->qn2.as<float>(), c->qnorm.as<float>(), c->err.as<int>(), c->stream);
+                      c->qn2.as<float>(), c->qnorm.as<float>(), c->qsc.as<float>(), c->err.as<int>(),
+                      c->stream);
   CKL();
   c->stats.kernels_launched += 1;
   qv->qs = c->qs.as<float>();
   qv->qn2 = c->qn2.as<float>();
   qv->qnorm = c->qnorm.as<float>();
+  qv->qsc = c->qsc.as<float>();
   qv->n = n;
   return HIVF_OK;
 }
@@ -750,7 +792,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   // batch density estimate (host-side, no sync): pairs per list of the index
   float ppl = (float)n_pairs / (float)std::max<uint32_t>(1, ix->K);
   const bool tc = kind != 1;
-  uint32_t group = tc ? scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc) : (uint32_t)kQMax;
+  uint32_t group = tc ? scan_tc_qmax(v.dpf, kind == 2, ppl, c->tc) : (uint32_t)kQMax;
   if (group == kTcPairQ) {
     v.seg_split = 2;
     v.s_max = 2 * ix->s_max;
@@ -775,6 +817,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   WideStage ws;
   ws.group = group;
   c->last_group = group;
+  c->last_filter_bits = (tc && v.vech) ? 16 : 32;
   if (tc_is_wide(group)) {
     // the restaged queries need (pairs + 7K) x D floats; when HBM is short
     // (index near the budget) the batch takes the narrow kernel instead
@@ -782,7 +825,7 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
         c->qwide.ensure((size_t)wide_stage_rows(n_pairs, ix->K) * ix->dpad * 4) != cudaSuccess) {
       (void)cudaGetLastError();
       ppl = 0.f;
-      group = scan_tc_qmax(ix->dpad, kind == 2, ppl, c->tc);
+      group = scan_tc_qmax(v.dpf, kind == 2, ppl, c->tc);
       if (tc_is_wide(group)) return fail(HIVF_ENOMEM, "wide scan: query staging buffer");
       ws.group = group;
       c->last_group = group;

@@ -31,7 +31,8 @@ constexpr int kCandCap = 4096;
 // an upper bound of |q| for the filter bound.
 __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32_t dim,
                                uint32_t dpad, int metric, int normalize, float* __restrict__ qs,
-                               float* __restrict__ qn2, float* __restrict__ qnorm, int* err) {
+                               float* __restrict__ qn2, float* __restrict__ qnorm, float* __restrict__ qsc,
+                               int* err) {
   pdl_wait();
   const uint32_t b = blockIdx.x;
   if (b >= n) return;
@@ -66,7 +67,10 @@ __global__ void k_prep_queries(const float* __restrict__ qin, uint32_t n, uint32
     double acc = 0.0;
     for (uint32_t w = 0; w < (blockDim.x + 31) / 32; ++w) acc += s_part[w];
     qn2[b] = __double2float_rn(acc);
-    qnorm[b] = __double2float_ru(sqrt(acc) * (1.0 + 1e-6));
+    const float qb = __double2float_ru(sqrt(acc) * (1.0 + 1e-6));
+    qnorm[b] = qb;
+    const int e = h16_exp(qb);  // fp16 filter: q 2^e has every |element| < 2^15
+    qsc[b] = (e < -kH16ExpMax || e > kH16ExpMax) ? 0.f : ldexpf(1.f, -e);
   }
 }
 
@@ -440,10 +444,10 @@ __global__ void k_take_plans(const unsigned long long* keys, const uint32_t* val
 }  // namespace
 
 void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t dpad, int metric,
-                         bool normalize, float* qs, float* qn2, float* qnorm, int* err,
+                         bool normalize, float* qs, float* qn2, float* qnorm, float* qsc, int* err,
                          cudaStream_t s) {
   if (n == 0) return;
-  launch_pdl(k_prep_queries, dim3(n), dim3(128), 0, s, q_in, n, dim, dpad, metric, normalize ? 1 : 0, qs, qn2, qnorm,
+  launch_pdl(k_prep_queries, dim3(n), dim3(128), 0, s, q_in, n, dim, dpad, metric, normalize ? 1 : 0, qs, qn2, qnorm, qsc,
                                    err);
 }
 

@@ -109,6 +109,9 @@ struct hivf_ctx {
   // options
   uint32_t opt_seg_rows = 0;  // 0: chosen per index from its size (auto_seg_rows)
   int opt_force_exact = 0;
+  // fp16 filter copy (option "filter_h16"): built at index finish when 1 and
+  // used by the single-pass tensor-core scan while 1
+  int opt_h16 = 1;
   // 0 auto (tensor cores when the dim fits; single-pass tf32, escalating to the
   // split kernel when the data makes its bound too loose), 1 FFMA, 2 tcgen05
   // split-precision, 3 tcgen05 single-pass
@@ -121,7 +124,7 @@ struct hivf_ctx {
   int tc_conv = 2;  // this device's fp32->tf32 operand conversion (tc_conversion_mode)
   TcOpts tc{0, tc_wide_ppl_default(), 0, tc_wide2_ppl_default(), tc_pair_ppl_default()};  // tensor-core scan tuning (tc_qmax, tc_wide_ppl, tc_variant)
   // scratch
-  DBuf qs, qn2, qnorm, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
+  DBuf qs, qn2, qnorm, qsc, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
       cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, qbound, rep_entries, rep_n, rep_cnt,
       rep_d, rep_ids, qshift, qwide, coarse_all, coarse_part;
@@ -132,6 +135,7 @@ struct hivf_ctx {
   const hivf_index* last_index = nullptr;
   uint32_t last_kind = 0;
   uint32_t last_group = 0;  // queries per scan work item of the last scan
+  uint32_t last_filter_bits = 32;  // 16: the last scan read the fp16 filter copy
   bool stats_adapted = false;
   // phase timing (option "time_kernels"): one event set per call, resolved lazily
   int opt_time = 0;
@@ -184,7 +188,7 @@ struct hivf_ctx {
   }
   ~hivf_ctx() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-    for (DBuf* b : {&qs, &qn2, &qnorm, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq,
+    for (DBuf* b : {&qs, &qn2, &qnorm, &qsc, &err, &dist32, &plans, &pdists, &flags_c, &flags_f, &pq,
                     &pl, &list_cnt, &list_poff, &list_cur, &list_ioff, &sorted_pairs, &items,
                     &n_items, &work_ctr, &cand_d, &cand_row, &cand_thr, &cand_n, &out_ids, &qin,
                     &x_ids, &x_d, &x_cnt, &x_tot, &tau, &flags2, &qbound, &rep_entries, &rep_n, &rep_cnt,
@@ -203,6 +207,10 @@ struct hivf_index {
   uint64_t N = 0;
   std::vector<uint64_t> list_off;  // host copy
   float* vec = nullptr;
+  // fp16 filter copy (nullptr: none): N rows x dpf floats, per-list unscale lsc
+  float* vech = nullptr;
+  float* lsc = nullptr;
+  uint32_t dpf = 0;
   uint64_t* ids = nullptr;
   float* xnorm2 = nullptr;
   uint64_t* d_list_off = nullptr;
@@ -244,9 +252,14 @@ struct hivf_index {
   // view carrying the filter bound of scan kernel `kind`
   IndexView view_kind(int kind) const {
     IndexView v{};
+    const bool h16 = kind == 3 && vech && ctx->opt_h16;
     if (kind == 2) bound_tc(dim, &v.e_a, &v.e_b, &v.e_c);
+    else if (h16) bound_h16(dim, &v.e_a, &v.e_b, &v.e_c);
     else if (kind == 3) bound_tc1(dim, &v.e_a, &v.e_b, &v.e_c);
     else bound_ffma(dim, &v.e_a, &v.e_b, &v.e_c);
+    v.vech = h16 ? vech : nullptr;
+    v.lsc = h16 ? lsc : nullptr;
+    v.dpf = h16 ? dpf : dpad;
     v.vec = vec;
     v.list_ptr = tiered ? d_list_ptr : nullptr;
     v.ids = ids;
@@ -273,7 +286,7 @@ struct hivf_index {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (tiered && vec) cudaFreeHost(vec);
     else if (vec) cudaFree(vec);
-    for (void* p : {(void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
+    for (void* p : {(void*)vech, (void*)lsc, (void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
                     (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err, (void*)pool,
                     (void*)d_list_ptr, (void*)loc_ids, (void*)loc_rows})
       if (p) cudaFree(p);

@@ -2,6 +2,7 @@
 // kernel translation units.  Host-only C++; not part of the public ABI.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -66,6 +67,14 @@ struct IndexView {
   // filter bound of the scan kernel that produced the candidates:
   // |d32 - delta| <= e_a*|q|*|x| + e_b*(|q|^2 + |x|^2) + e_c
   double e_a, e_b, e_c;
+  // fp16 filter copy: the lists again, each row
+  // scaled by its list's power of two 2^e_l and rounded to fp16, in the same
+  // tile-major SWIZZLE_64B layout (64 B = 32 dims per chunk row).  Set only in
+  // views of the single-pass tensor-core scan over an index that has it (the
+  // bound above is then bound_h16); nullptr otherwise.
+  const float* vech;        // addressed in float units: dpf floats per row
+  const float* lsc;         // [K] 2^-e_l (unscale of the list's rows)
+  uint32_t dpf;             // floats per filter row: dpad, or ceil32(dim) / 2 with vech
 };
 
 // Programmatic dependent launch on the search path: each kernel is launched
@@ -120,6 +129,7 @@ struct QueryView {
   const float* qs;      // [nq][dpad] search-space queries, zero padded
   const float* qn2;     // [nq] fp32(|q|^2)
   const float* qnorm;   // [nq] upper bound of |q|
+  const float* qsc;     // [nq] 2^-e_q, the fp16 filter's unscale of the query (0: out of range)
   uint32_t n;
 };
 
@@ -152,8 +162,23 @@ void launch_check_dup_ids(const uint64_t* sorted_ids, uint64_t n, int* err, cuda
 
 // ---- assign.cu
 void launch_prep_queries(const float* q_in, uint32_t n, uint32_t dim, uint32_t dpad, int metric,
-                         bool normalize, float* qs, float* qn2, float* qnorm, int* err,
+                         bool normalize, float* qs, float* qn2, float* qnorm, float* qsc, int* err,
                          cudaStream_t s);
+// fp16 filter copy: per-list scale exponent from the list's norm bound
+// (|x_i| 2^e < 2^15), 0 for empty lists; the same rule per query (h16_exp)
+__host__ __device__ inline int h16_exp(float norm_bound) {
+  if (!(norm_bound > 0.f)) return 0;
+  int e2 = 0;
+#ifdef __CUDA_ARCH__
+  e2 = ilogbf(norm_bound);
+#else
+  e2 = std::ilogb(norm_bound);
+#endif
+  return 14 - e2;
+}
+constexpr int kH16ExpMax = 60;  // |e| beyond this: the scale products could leave the fp32 normal range
+void launch_pack_h16(const float* vec, const uint64_t* d_list_off, uint32_t K, uint32_t dpad, uint32_t dpf,
+                     uint64_t N, const float* lsc, float* vech, cudaStream_t s);
 // part (optional, coarse_dist_splits() x n_queries x K floats): scratch for the
 // split-K form on small batches / codebooks
 uint32_t coarse_dist_splits(const IndexView& ix, uint32_t n_queries);

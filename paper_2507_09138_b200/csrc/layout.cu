@@ -5,6 +5,7 @@
 // row-major in list order (exactly the order index_from_assignments appends
 // them); output is the chunk-major, 16B-group-swizzled layout the scan kernel
 // streams with 1-D bulk copies (common.cuh).
+#include <cuda_fp16.h>
 #include <cfloat>
 
 #include "common.cuh"
@@ -57,6 +58,45 @@ __global__ void k_pack_lists(const float* __restrict__ src, uint64_t r_first,
     atomicMax(maxnorm_bits + c, __float_as_uint(nrm));  // non-negative floats order as uints
   }
 }
+
+// fp16 filter copy: one thread per 16-B
+// granule (8 dims) of a row, read from the fp32 tile-major copy, scaled by the
+// list's 2^e_l (exact) and rounded to fp16 (RN) into the same tile-major
+// SWIZZLE_64B pattern with 32-dim chunks (dpf floats = 2 dpf halfs per row).
+__global__ void k_pack_h16(const float* __restrict__ vec, const uint64_t* __restrict__ list_off, uint32_t K,
+                           uint32_t dpad, uint32_t dpf, uint64_t N, const float* __restrict__ lsc,
+                           float* __restrict__ vech) {
+  const uint32_t gpr = dpf / 4;  // granules per row
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= N * gpr) return;
+  const uint64_t r = gid / gpr;
+  const uint32_t G = (uint32_t)(gid % gpr), ch = G >> 2, gi = G & 3;
+  uint32_t lo = 0, hi = K;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (list_off[mid + 1] <= r) lo = mid + 1; else hi = mid;
+  }
+  const uint32_t c = lo;
+  const uint64_t n_c = list_off[c + 1] - list_off[c];
+  const uint64_t lr = r - list_off[c];
+  const float up = 1.f / lsc[c];  // 2^e_l
+  __align__(16) __half h[8];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const uint32_t d = ch * 32 + gi * 8 + p * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (d < dpad) v = *reinterpret_cast<const float4*>(vec + swz_offset(list_off[c] * (uint64_t)dpad, n_c, lr, d, dpad));
+    h[p * 4 + 0] = __float2half_rn(v.x * up);
+    h[p * 4 + 1] = __float2half_rn(v.y * up);
+    h[p * 4 + 2] = __float2half_rn(v.z * up);
+    h[p * 4 + 3] = __float2half_rn(v.w * up);
+  }
+  const uint64_t r0 = lr - lr % kTileRows;
+  const uint64_t o = list_off[c] * (uint64_t)dpf + tile_chunk_offset(n_c, dpf, r0, ch) + (lr - r0) * kChunk +
+                     (uint64_t)((gi ^ ((uint32_t)(lr >> 1) & 3u)) * 4);
+  *reinterpret_cast<uint4*>(vech + o) = *reinterpret_cast<const uint4*>(h);
+}
+
 
 // Inverse of the packing: rows [first, first+n) back to row-major.
 __global__ void k_unpack_rows(const float* __restrict__ vec, const uint64_t* __restrict__ list_off,
@@ -136,6 +176,13 @@ __global__ void k_check_dup(const uint64_t* sorted, uint64_t n, int* err) {
 }
 
 }  // namespace
+
+void launch_pack_h16(const float* vec, const uint64_t* d_list_off, uint32_t K, uint32_t dpad, uint32_t dpf,
+                     uint64_t N, const float* lsc, float* vech, cudaStream_t s) {
+  const uint64_t total = N * (dpf / 4);
+  if (!total) return;
+  k_pack_h16<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(vec, d_list_off, K, dpad, dpf, N, lsc, vech);
+}
 
 void launch_pack_lists(const float* src_rows, uint64_t r_first, const uint64_t* pos,
                        uint64_t n_rows, uint32_t dim, uint32_t dpad, const uint64_t* d_list_off,

@@ -141,6 +141,15 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b,
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -244,6 +253,39 @@ __device__ __forceinline__ float tf32_conv(float x, int mode) {
   return __uint_as_float(r);
 }
 
+// fp16 filter copy (IndexView::vech): list
+// c's filter rows (dpf floats each), and the distance's dot coefficient
+// -2 2^-(e_q + e_l) (exact power of 2; -2 on the fp32 copy).  0 marks a query
+// whose scale is out of range: its segments report no candidates and a -inf
+// threshold, so finalize re-scans them exactly.
+__device__ __forceinline__ const float* filter_base(const IndexView& ix, uint32_t c, uint64_t lbeg) {
+  return ix.vech ? ix.vech + lbeg * ix.dpf : list_base(ix, c, lbeg);
+}
+__device__ __forceinline__ float dot_coef(const IndexView& ix, const QueryView& qv, uint32_t qi, uint32_t c) {
+  return ix.vech ? -2.f * qv.qsc[qi] * ix.lsc[c] : -2.f;
+}
+// a query is out of the fp16 filter's range (its coefficient is 0)
+__device__ __forceinline__ bool coef_bad(float m2) { return m2 == 0.f; }
+// fp16 query row: the 8 dims [8 gh, 8 gh + 8) of q 2^e_q (zero past dpad) as one 16-B granule
+__device__ __forceinline__ uint4 h16_granule(const float* qrow, uint32_t dpad, uint32_t gh, float up) {
+  __align__(16) __half h[8];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const uint32_t d = gh * 8 + p * 4;
+    const float4 v = d < dpad ? *reinterpret_cast<const float4*>(qrow + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+    h[p * 4 + 0] = __float2half_rn(v.x * up);
+    h[p * 4 + 1] = __float2half_rn(v.y * up);
+    h[p * 4 + 2] = __float2half_rn(v.z * up);
+    h[p * 4 + 3] = __float2half_rn(v.w * up);
+  }
+  return *reinterpret_cast<const uint4*>(h);
+}
+// the query's up-scale 2^e_q (1 when out of range: its results are discarded)
+__device__ __forceinline__ float h16_up(const QueryView& qv, uint32_t qi) {
+  const float sc = qv.qsc[qi];
+  return sc > 0.f ? 1.f / sc : 1.f;
+}
+
 // debug profiling (P.prof != nullptr): cycles spent in selected waits, per CTA
 #define TC_PROF_T0() const long long _t0 = P.prof ? clock64() : 0
 #define TC_PROF_ADD(slot) \
@@ -345,7 +387,7 @@ __device__ __forceinline__ void epilogue128(const TcParams& P, uint32_t tmem_bas
     const ScanItem item = s_item[slot];
     const uint32_t nq = item.nq > 64 * h ? min(64u, item.nq - 64 * h) : 0u;
     // lane j: metadata of local queries j (m = 0) and 32 + j (m = 1)
-    float w_qn2[2] = {0.f, 0.f}, w_E[2] = {0.f, 0.f};
+    float w_qn2[2] = {0.f, 0.f}, w_E[2] = {0.f, 0.f}, w_m2[2] = {-2.f, -2.f};
     uint32_t w_qi[2] = {0, 0}, w_slot[2] = {0, 0};
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
@@ -356,6 +398,7 @@ __device__ __forceinline__ void epilogue128(const TcParams& P, uint32_t tmem_bas
         w_qn2[m] = P.qv.qn2[w_qi[m]];
         w_slot[m] = pair * P.ix.s_max + item.seg;
         w_E[m] = seg_bound(P.ix, P.qv.qnorm[w_qi[m]], P.ix.maxnorm[item.list]);
+        w_m2[m] = dot_coef(P.ix, P.qv, w_qi[m], item.list);
       }
     }
     const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
@@ -423,9 +466,11 @@ __device__ __forceinline__ void epilogue128(const TcParams& P, uint32_t tmem_bas
           if (qa >= (int)nq) break;
           const float qa2 = __shfl_sync(FULL, w_qn2[hh], qa & 31);
           const float qb2 = __shfl_sync(FULL, w_qn2[hh], qb & 31);
-          const float va = valid ? __fmaf_rn(-2.f, __uint_as_float(acc[qa & 31]), __fadd_rn(xn, qa2)) : kInfF;
+          const float ma = __shfl_sync(FULL, w_m2[hh], qa & 31);
+          const float mb = __shfl_sync(FULL, w_m2[hh], qb & 31);
+          const float va = valid ? __fmaf_rn(ma, __uint_as_float(acc[qa & 31]), __fadd_rn(xn, qa2)) : kInfF;
           const float vb = (valid && qb < (int)nq)
-                               ? __fmaf_rn(-2.f, __uint_as_float(acc[qb & 31]), __fadd_rn(xn, qb2))
+                               ? __fmaf_rn(mb, __uint_as_float(acc[qb & 31]), __fadd_rn(xn, qb2))
                                : kInfF;
           const float ga = __shfl_sync(FULL, gl[hh], qa & 31);
           const float gb = __shfl_sync(FULL, gl[hh], qb & 31);
@@ -491,17 +536,19 @@ __device__ __forceinline__ void epilogue128(const TcParams& P, uint32_t tmem_bas
         const uint32_t oslot = __shfl_sync(FULL, m ? w_slot[1] : w_slot[0], q & 31);
         const float Ej = __shfl_sync(FULL, m ? w_E[1] : w_E[0], q & 31);
         const uint32_t qij = __shfl_sync(FULL, m ? w_qi[1] : w_qi[0], q & 31);
+        const bool bad = coef_bad(__shfl_sync(FULL, m ? w_m2[1] : w_m2[0], q & 31));
         P.out_d[(uint64_t)oslot * kKP + lane] = x;
         P.out_row[(uint64_t)oslot * kKP + lane] = xr;
-        const uint32_t n_valid = __popc(__ballot_sync(FULL, xr != kNoRow));
+        const uint32_t n_kept = __popc(__ballot_sync(FULL, xr != kNoRow));
+        const uint32_t n_valid = bad ? 0u : n_kept;
         const float last = __shfl_sync(FULL, x, 31);
         const float gm = fminf(fminf(s_gm[h][0][q], s_gm[h][1][q]), fminf(s_gm[h][2][q], s_gm[h][3][q]));
         const float w16 = fminf(fminf(s_w16[h][0][q], s_w16[h][1][q]), fminf(s_w16[h][2][q], s_w16[h][3][q]));
         const float vk = __shfl_sync(FULL, x, (int)(P.topk ? P.topk - 1 : 0));
         if (lane == 0) {
-          P.out_thr[oslot] = fminf(fminf(n_valid == kKP ? last : kInfF, gm), w16);
+          P.out_thr[oslot] = bad ? -kInfF : fminf(fminf(n_valid == kKP ? last : kInfF, gm), w16);
           P.out_n[oslot] = n_valid;
-          if (P.bound_update && n_valid >= P.topk) {  // this item's k-th upper bound
+          if (P.bound_update && !bad && n_valid >= P.topk) {  // this item's k-th upper bound
             float u = __fadd_ru(vk, Ej);
             if (!(u > 0.f)) u = 0.f;
             atomicMin(reinterpret_cast<int*>(P.qbound + qij), __float_as_int(u));
@@ -532,7 +579,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t dpad = P.ix.dpad;
-  const uint32_t nch = dpad / kChunk;
+  // list / query rows as the MMA reads them: fp32 (tf32) or the fp16 filter copy
+  const bool h16 = P.ix.vech != nullptr;
+  const uint32_t dpf = P.ix.dpf;
+  const uint32_t nch = dpf / kChunk;
   const uint32_t qmax = P.qmax;
   const uint32_t SA = P.sa;
   const bool split = !kWide && P.split != 0;
@@ -564,6 +614,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
   float (*s_E)[32] = reinterpret_cast<float (*)[32]>(s_slot + kItemQ);            // [kItemQ][32]
   uint32_t (*s_qi)[32] = reinterpret_cast<uint32_t (*)[32]>(s_E + kItemQ);        // [kItemQ][32]
   float (*s_g)[32] = reinterpret_cast<float (*)[32]>(s_qi + kItemQ);              // [groups*4][32]
+  float (*s_m2)[32] = reinterpret_cast<float (*)[32]>(s_g + kGroups * 4);         // [kItemQ][32] dot coefficients
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -649,9 +700,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         uint32_t pf = valid_n ? 0 : 2;  // prefetch progress of the next item
         const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
         const uint64_t n_c = lend - lbeg;
-        const float* lbase = list_base(P.ix, item.list, lbeg);
+        const float* lbase = filter_base(P.ix, item.list, lbeg);
         const uint32_t qbytes = kWide ? ((item.nq + 7) & ~7u) * 64 : 0;  // per chunk
-        const uint8_t* qsrc = kWide ? P.qstage + (uint64_t)(item.pair0 + qsh) * dpad * 4 : nullptr;
+        const uint8_t* qsrc = kWide ? P.qstage + (uint64_t)(item.pair0 + qsh) * dpf * 4 : nullptr;
         for (uint32_t t = 0; t < ntiles; ++t) {
           const uint32_t r0 = item.row0 + t * kTcTile;
           const uint32_t nr = min((uint32_t)kTcTile, item.nrows - t * kTcTile);
@@ -666,12 +717,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
             const long long _tp = P.prof ? clock64() : 0;
             mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4 + cn * qbytes);
             if (nr == kTcTile) {  // full tile: the stage is one contiguous span
-              bulk_g2s(aring + a * kSB, lbase + tile_chunk_offset(n_c, dpad, r0, c0),
+              bulk_g2s(aring + a * kSB, lbase + tile_chunk_offset(n_c, dpf, r0, c0),
                        cn * kTcChunkBytes, &full[a]);
             } else {  // short last tile: its chunk planes are nr rows apart
               for (uint32_t c = 0; c < cn; ++c)
                 bulk_g2s(aring + a * kSB + c * kTcChunkBytes,
-                         lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c), nr * kChunk * 4, &full[a]);
+                         lbase + tile_chunk_offset(n_c, dpf, r0, c0 + c), nr * kChunk * 4, &full[a]);
             }
             if (kWide)  // the group's query rows of these chunks (L2-resident restaged copy)
               bulk_g2s(aring + a * kSB + kTcStageBytes, qsrc + (uint64_t)c0 * qbytes, cn * qbytes, &full[a]);
@@ -719,7 +770,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       if (lane == 0) mbar_arrive(&iempty[slot]);
       const uint32_t npad = (nq_i + 7) & ~7u;
       const uint32_t ntiles = (nrows_i + kTcTile - 1) / kTcTile;
-      const uint32_t idesc2 = tf32_idesc(split ? 2 * npad : npad);
+      const uint32_t idesc2 = h16 ? f16_idesc_m(kTcTile, npad) : tf32_idesc(split ? 2 * npad : npad);
       const uint32_t idesc1 = tf32_idesc(npad);
       const uint64_t qdesc0 = sw64_kmajor_desc(smem_u32(qsm));
       const uint64_t adesc0 = sw64_kmajor_desc(smem_u32(aring));
@@ -765,7 +816,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
                 const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
                 const uint32_t accum = (sg | c | k2) != 0;
                 // cols [0,npad): hi(A) hi(q);  cols [npad,2npad): hi(A) lo(q)
-                if (!(P.variant & 8) || k2 == 0) mma_tf32_elect(d_tmem, ad, qd + 2 * k2, idesc2, accum);
+                if (!(P.variant & 8) || k2 == 0) {
+                  if (h16) mma_f16_elect(d_tmem, ad, qd + 2 * k2, idesc2, accum);
+                  else mma_tf32_elect(d_tmem, ad, qd + 2 * k2, idesc2, accum);
+                }
                 // cols [0,npad) += lo(A) hi(q), A from TMEM (8 columns per k-step)
                 if (split && !(P.variant & 2))
                   mma_tf32_ta_elect(d_tmem, alo + c * 16 + k2 * 8, qd + 2 * k2, idesc1);
@@ -818,6 +872,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           s_slot[slot][n] = pair * P.ix.s_max + item.seg;
           s_E[slot][n] = seg_bound(P.ix, P.qv.qnorm[my_qi], P.ix.maxnorm[item.list]);
           s_qi[slot][n] = my_qi;
+          s_m2[slot][n] = dot_coef(P.ix, P.qv, my_qi, item.list);
         }
       }
       const long long _ts = P.prof ? clock64() : 0;
@@ -827,7 +882,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         if (lane == 0) TC_PROF_ADD(10);
       }
       const uint32_t nmine = npad > sw ? (npad - sw + 3) / 4 : 0;
-      for (uint32_t m0 = 0; m0 < nmine; m0 += 2) {
+      if (h16) {  // fp16 filter: the query rows scaled by 2^e_q, 8 dims per 16-B granule
+        for (uint32_t m = 0; m < nmine; ++m) {
+          const uint32_t n = sw + 4 * m;
+          const uint32_t qi = __shfl_sync(FULL, my_qi, m & 7);
+          const float up = n < nq ? h16_up(P.qv, qi) : 1.f;
+          const float* qrow = P.qv.qs + (uint64_t)qi * dpad;
+          for (uint32_t gh = lane; gh < dpf / 4; gh += 32) {
+            const uint32_t ch = gh >> 2, g = gh & 3;
+            const uint4 x = n < nq ? h16_granule(qrow, dpad, gh, up) : make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(qsm + ch * qblk + n * 64 + ((g ^ ((n >> 1) & 3)) << 4)) = x;
+          }
+        }
+      }
+      for (uint32_t m0 = 0; !h16 && m0 < nmine; m0 += 2) {
         for (uint32_t e0 = 0; e0 * 32 < ng; e0 += 8) {
           float4 v[2][8];
 #pragma unroll
@@ -928,7 +996,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
       const uint32_t npad = (nq + 7) & ~7u;
       // wide: per-query metadata in registers (lane j = query 32h + j), loaded
       // here instead of by stager warps
-      float w_qn2 = 0.f, w_E = 0.f;
+      float w_qn2 = 0.f, w_E = 0.f, w_m2 = -2.f;
       uint32_t w_qi = 0, w_slot = 0;
       if (kWide && lane < nq) {
         const uint32_t pair = P.sorted_pairs[item.pair0 + 32 * h + lane];
@@ -936,6 +1004,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
         w_qn2 = P.qv.qn2[w_qi];
         w_slot = pair * P.ix.s_max + item.seg;
         w_E = seg_bound(P.ix, P.qv.qnorm[w_qi], P.ix.maxnorm[item.list]);
+        w_m2 = dot_coef(P.ix, P.qv, w_qi, item.list);
       }
       const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
       const uint64_t lbeg = P.ix.list_off[item.list];
@@ -996,7 +1065,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           const float dot = split ? __fadd_rn(__uint_as_float(acc[j]), __uint_as_float(acc2[j]))
                                   : __uint_as_float(acc[j]);
           const float qn2j = kWide ? __shfl_sync(FULL, w_qn2, j) : s_qn2[slot][j];
-          const float v = valid ? __fmaf_rn(-2.f, dot, __fadd_rn(xn, qn2j))
+          const float m2j = kWide ? __shfl_sync(FULL, w_m2, j) : (h16 ? s_m2[slot][j] : -2.f);
+          const float v = valid ? __fmaf_rn(m2j, dot, __fadd_rn(xn, qn2j))
                                 : __int_as_float(0x7f800000);
           const float gj = __shfl_sync(FULL, gl, j);
           float th = fminf(__shfl_sync(FULL, ld[j], 31), gj);
@@ -1109,18 +1179,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           const uint32_t oslot = kWide ? __shfl_sync(FULL, w_slot, j) : s_slot[slot][j];
           const float Ej = kWide ? __shfl_sync(FULL, w_E, j) : s_E[slot][j];
           const uint32_t qij = kWide ? __shfl_sync(FULL, w_qi, j) : s_qi[slot][j];
+          const float m2o = kWide ? __shfl_sync(FULL, w_m2, j) : s_m2[slot][j];
+          const bool bad = h16 && coef_bad(m2o);
           P.out_d[(uint64_t)oslot * kKP + lane] = v;
           P.out_row[(uint64_t)oslot * kKP + lane] = r;
-          const uint32_t n_valid = __popc(__ballot_sync(FULL, r != kNoRow));
+          const uint32_t n_kept = __popc(__ballot_sync(FULL, r != kNoRow));
+          const uint32_t n_valid = bad ? 0u : n_kept;
           const float last = __shfl_sync(FULL, v, 31);
           // every row not kept has d^ >= the 32nd kept value (when 32 are kept)
           // or >= a drop bound this item used (bounds only decrease)
           const float gm = fminf(fminf(gs_g[0][j], gs_g[1][j]), fminf(gs_g[2][j], gs_g[3][j]));
           const float vk = __shfl_sync(FULL, v, (int)(P.topk ? P.topk - 1 : 0));
           if (lane == 0) {
-            P.out_thr[oslot] = fminf(n_valid == kKP ? last : kInfF, gm);
+            P.out_thr[oslot] = bad ? -kInfF : fminf(n_valid == kKP ? last : kInfF, gm);
             P.out_n[oslot] = n_valid;
-            if (P.bound_update && n_valid >= P.topk) {  // this item's k-th upper bound
+            if (P.bound_update && !bad && n_valid >= P.topk) {  // this item's k-th upper bound
               float u = __fadd_ru(vk, Ej);
               if (!(u > 0.f)) u = 0.f;
               atomicMin(reinterpret_cast<int*>(P.qbound + qij), __float_as_int(u));
@@ -1227,6 +1300,14 @@ __device__ __forceinline__ void mma2_tf32(uint32_t d_tmem, uint64_t a, uint64_t 
       "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void mma2_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -1269,8 +1350,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kSB = kPairStageA + kPairQB;  // A tile stage + this CTA's half query slice
-  const uint32_t dpad = P.ix.dpad;
-  const uint32_t nch = dpad / kChunk;
+  const bool h16 = P.ix.vech != nullptr;        // fp16 filter copy (dpf floats per row) or fp32
+  const uint32_t dpf = P.ix.dpf;
+  const uint32_t nch = dpf / kChunk;
   const uint32_t nstg = (nch + kPCps - 1) / kPCps;
   const uint32_t SA = P.sa;
   uint8_t* aring = smem;
@@ -1286,6 +1368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
   // per-query metadata of the current item, [item parity][group][query]
   __shared__ float s_qn2[2][kPG][kPQ], s_E[2][kPG][kPQ];
   __shared__ uint32_t s_qi[2][kPG][kPQ], s_oslot[2][kPG][kPQ];
+  __shared__ float s_m2[2][kPG][kPQ];  // dot coefficient (dot_coef)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
@@ -1341,11 +1424,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
         if (P.prof) P.prof[blockIdx.x * 16 + 7] += 1;
         const uint64_t lbeg = P.ix.list_off[item.list];
         const uint64_t n_c = P.ix.list_off[item.list + 1] - lbeg;
-        const float* lbase = list_base(P.ix, item.list, lbeg);
+        const float* lbase = filter_base(P.ix, item.list, lbeg);
         const uint32_t npad = (item.nq + 15) & ~15u, hrows = npad / 2;
         const uint32_t qbytes = hrows * 64;  // per chunk, this CTA's half
         // the group's staged block: [half][ch][hrows][64 B]
-        const uint8_t* qsrc = P.qstage + (uint64_t)(item.pair0 + P.qshift[item.list]) * dpad * 4 +
+        const uint8_t* qsrc = P.qstage + (uint64_t)(item.pair0 + P.qshift[item.list]) * dpf * 4 +
                               (uint64_t)crank * nch * qbytes;
         const uint32_t ntiles = (item.nrows + kTcTile - 1) / kTcTile;
         const uint32_t npt = (ntiles + 1) / 2;
@@ -1363,11 +1446,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
             }
             mbar_arrive_expect_tx(&full[a], cn * nr * kChunk * 4 + cn * qbytes);
             if (nr == kTcTile) {
-              bulk_g2s(aring + a * kSB, lbase + tile_chunk_offset(n_c, dpad, r0, c0), cn * kTcChunkBytes,
+              bulk_g2s(aring + a * kSB, lbase + tile_chunk_offset(n_c, dpf, r0, c0), cn * kTcChunkBytes,
                        &full[a]);
             } else if (nr) {
               for (uint32_t c = 0; c < cn; ++c)
-                bulk_g2s(aring + a * kSB + c * kTcChunkBytes, lbase + tile_chunk_offset(n_c, dpad, r0, c0 + c),
+                bulk_g2s(aring + a * kSB + c * kTcChunkBytes, lbase + tile_chunk_offset(n_c, dpf, r0, c0 + c),
                          nr * kChunk * 4, &full[a]);
             }
             bulk_g2s(aring + a * kSB + kPairStageA, qsrc + (uint64_t)c0 * qbytes, cn * qbytes, &full[a]);
@@ -1392,7 +1475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
       const uint32_t npad = (nq_i + 15) & ~15u;
       const uint32_t ntiles = (nrows_i + kTcTile - 1) / kTcTile;
       const uint32_t npt = (ntiles + 1) / 2;
-      const uint32_t idesc = tf32_idesc_m(256, npad);
+      const uint32_t idesc = h16 ? f16_idesc_m(256, npad) : tf32_idesc_m(256, npad);
       const uint64_t adesc0 = sw64_kmajor_desc(smem_u32(aring));
       for (uint32_t pt = 0; pt < npt; ++pt) {
         if (leader) {
@@ -1427,7 +1510,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
 #pragma unroll
               for (uint32_t k2 = 0; k2 < 2; ++k2) {
                 const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
-                if (lane == 0 && !(P.variant & 4)) mma2_tf32(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
+                if (lane == 0 && !(P.variant & 4)) {
+                  if (h16) mma2_f16(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
+                  else mma2_tf32(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
+                }
               }
             }
             if (lane == 0) mma2_commit_both(&empty[a]);  // the slot is free in both CTAs
@@ -1467,6 +1553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
       const uint32_t ip = i & 1;
       float* m_qn2 = s_qn2[ip][h];
       float* m_E = s_E[ip][h];
+      float* m_m2 = s_m2[ip][h];
       uint32_t* m_qi = s_qi[ip][h];
       uint32_t* m_oslot = s_oslot[ip][h];
       {  // the group's per-query metadata (warp ew owns queries 16 ew .. 16 ew + 15)
@@ -1478,6 +1565,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
           m_qn2[q] = P.qv.qn2[qi];
           m_oslot[q] = pair * P.ix.s_max + 2 * item.seg + crank;
           m_E[q] = seg_bound(P.ix, P.qv.qnorm[qi], P.ix.maxnorm[item.list]);
+          m_m2[q] = dot_coef(P.ix, P.qv, qi, item.list);
         }
         named_bar_sync(2 + h, kTcEpiWarps * 32);
       }
@@ -1532,10 +1620,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
             for (int j = 0; j < 4; ++j) {
               const int q = 4 * sp + j;  // group-local query; acc column q & 31
               const float q2 = q < (int)nq ? m_qn2[q] : 0.f;
+              const float m2 = q < (int)nq ? m_m2[q] : -2.f;
               const float g = __shfl_sync(FULL, gl[m], q & 31);
               const float th = fminf(__shfl_sync(FULL, ld[sp], 8 * j + 7), g);
               const float x = (valid && q < (int)nq)
-                                  ? __fmaf_rn(-2.f, __uint_as_float(acc[q & 31]), __fadd_rn(xn, q2))
+                                  ? __fmaf_rn(m2, __uint_as_float(acc[q & 31]), __fadd_rn(xn, q2))
                                   : kInfF;
               v[j] = x < th ? x : kInfF;
               any |= x < th;
@@ -1585,16 +1674,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
           const uint32_t oslot = m_oslot[q];
           const float Ej = m_E[q];
           const uint32_t qij = m_qi[q];
+          const bool bad = coef_bad(m_m2[q]);
           P.out_d[(uint64_t)oslot * kKP + lane] = x;
           P.out_row[(uint64_t)oslot * kKP + lane] = xr;
-          const uint32_t n_valid = __popc(__ballot_sync(FULL, xr != kNoRow));
+          const uint32_t n_kept = __popc(__ballot_sync(FULL, xr != kNoRow));
+          const uint32_t n_valid = bad ? 0u : n_kept;
           const float gm = fminf(fminf(s_gm[h][0][q], s_gm[h][1][q]), fminf(s_gm[h][2][q], s_gm[h][3][q]));
           const float w8 = fminf(fminf(s_w8[h][0][q], s_w8[h][1][q]), fminf(s_w8[h][2][q], s_w8[h][3][q]));
           const float vk = __shfl_sync(FULL, x, (int)(P.topk ? P.topk - 1 : 0));
           if (lane == 0) {
-            P.out_thr[oslot] = fminf(gm, w8);
+            P.out_thr[oslot] = bad ? -kInfF : fminf(gm, w8);
             P.out_n[oslot] = n_valid;
-            if (P.bound_update && n_valid >= P.topk) {
+            if (P.bound_update && !bad && n_valid >= P.topk) {
               float u = __fadd_ru(vk, Ej);
               if (!(u > 0.f)) u = 0.f;
               atomicMin(reinterpret_cast<int*>(P.qbound + qij), __float_as_int(u));
@@ -1655,7 +1746,7 @@ static int tc_fixed_bytes(uint32_t dpad, uint32_t qmax, int split) {
   return 1024 + (wide ? 0 : (int)(dpad / kChunk) * (split ? 2 : 1) * (int)qmax * 64) +
          (wide ? 2 * 8 : kMergeQ) * kTcEpiWarps * 32 * 8 +       // merge scratch
          8 * (2 * kTcMaxA + 2 * kTcLo + 2 * kAccMax + 2 * kItemQ + 2) + kItemQ * 32 * 16 +
-         (wide ? 8 : 4) * 32 * 4;
+         (wide ? 8 : 4) * 32 * 4 + kItemQ * 32 * 4;
 }
 static uint32_t tc_ring(uint32_t dpad, uint32_t qmax, int split) {
   const int left = tc_budget(qmax) - tc_fixed_bytes(dpad, qmax, split);
@@ -1749,14 +1840,14 @@ void launch_scan_tc(const IndexView& ix, const QueryView& qv, const ScanItem* it
                     uint32_t* out_n, int n_ctas, int split, float* qbound, uint32_t topk,
                     int bound_update, float probes_per_list, const WideStage& ws, const TcOpts& o,
                     cudaStream_t s) {
-  const uint32_t q = scan_tc_qmax(ix.dpad, split, probes_per_list, o);
+  const uint32_t q = scan_tc_qmax(ix.dpf, split, probes_per_list, o);
   const int conv = tc_conversion_mode();
   const bool wide = tc_is_wide(q);
   TcParams P{ix, qv, items, n_items, work_ctr, sorted_pairs, pair_query, out_d, out_row, out_thr,
-             out_n, q, tc_ring(ix.dpad, q, split), conv > 1 ? 0 : conv, o.variant,
+             out_n, q, tc_ring(ix.dpf, q, split), conv > 1 ? 0 : conv, o.variant,
              wide ? 0 : split, g_tc_prof, qbound, qbound ? topk : 0u, (qbound && bound_update) ? 1u : 0u,
              ws.qstage, ws.qshift};
-  const int smem = scan_tc_smem_bytes(ix.dpad, split, probes_per_list, o);
+  const int smem = scan_tc_smem_bytes(ix.dpf, split, probes_per_list, o);
   if (q == kTcPairQ) {
     smem_optin((const void*)k_scan_pair, smem);
     launch_pdl(k_scan_pair, dim3(std::max(2, n_ctas & ~1)), dim3(kPairThreads), smem, s, P);
@@ -1779,7 +1870,8 @@ namespace {
 // of dpad*4*npad bytes laid out chunk-major [ch][npad rows][64 B] with the
 // SWIZZLE_64B XOR, so a stage's 4-chunk slice is one contiguous bulk copy
 // that lands in UMMA K-major layout.
-__global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs, uint32_t dpad,
+__global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs, uint32_t dpad, uint32_t dpf,
+                                                    const float* __restrict__ qsc,
                                                     const uint32_t* __restrict__ sorted_pairs,
                                                     const uint32_t* __restrict__ pair_query,
                                                     const uint32_t* __restrict__ pair_list,
@@ -1794,8 +1886,30 @@ __global__ void __launch_bounds__(256) k_stage_wide(const float* __restrict__ qs
   const uint32_t c = pair_list[pair];
   const uint32_t local = p - pair_off[c], n = list_cnt[c];
   const uint32_t g = local / G, row = local % G;
-  uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * G) * dpad * 4;
-  const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)pair_query[pair] * dpad);
+  uint8_t* blk = qstage + (uint64_t)(pair_off[c] + qshift[c] + g * G) * dpf * 4;
+  const uint32_t qi = pair_query[pair];
+  const float4* src = reinterpret_cast<const float4*>(qs + (uint64_t)qi * dpad);
+  if (qsc) {  // fp16 filter copy: q 2^e_q in fp16, 32-dim chunks (16-B granules of 8 dims)
+    const float up = qsc[qi] > 0.f ? 1.f / qsc[qi] : 1.f;
+    const float* qrow = qs + (uint64_t)qi * dpad;
+    uint32_t nrow = 0, r = row;
+    uint8_t* base = blk;
+    if (G == kPairQ) {
+      const uint32_t npad = min(G, ((n - g * G) + 15) & ~15u), hr = npad / 2;
+      const uint32_t half = row / hr;
+      r = row % hr;
+      nrow = hr;
+      base = blk + (uint64_t)half * (dpf / 16) * hr * 64;
+    } else {
+      nrow = min(G, ((n - g * G) + 7) & ~7u);
+    }
+    for (uint32_t gh = threadIdx.x & 31; gh < dpf / 4; gh += 32) {
+      const uint32_t ch = gh >> 2, q4 = gh & 3;
+      *reinterpret_cast<uint4*>(base + (uint64_t)ch * nrow * 64 + r * 64 + ((q4 ^ ((r >> 1) & 3)) << 4)) =
+          h16_granule(qrow, dpad, gh, up);
+    }
+    return;
+  }
   if (G == kPairQ) {  // CTA-pair groups: [half][ch][npad/2 rows][64 B], npad = ceil16
     const uint32_t npad = min(G, ((n - g * G) + 15) & ~15u), hr = npad / 2;
     const uint32_t half = row / hr, r = row % hr;
@@ -1823,7 +1937,8 @@ void launch_stage_wide(const IndexView& ix, const QueryView& qv, const uint32_t*
                        const uint32_t* pair_query, const uint32_t* pair_list, const uint32_t* pair_off,
                        const uint32_t* list_cnt, uint32_t n_pairs, const WideStage& ws, cudaStream_t s) {
   if (n_pairs)
-    launch_pdl(k_stage_wide, dim3((n_pairs + 7) / 8), dim3(256), 0, s, qv.qs, ix.dpad, sorted_pairs, pair_query, pair_list,
+    launch_pdl(k_stage_wide, dim3((n_pairs + 7) / 8), dim3(256), 0, s, qv.qs, ix.dpad, ix.vech ? ix.dpf : ix.dpad,
+               ix.vech ? qv.qsc : nullptr, sorted_pairs, pair_query, pair_list,
                                                    pair_off, list_cnt, ws.qshift, ws.qstage, n_pairs, ws.group);
 }
 

@@ -265,20 +265,31 @@ def test_tensor_core_conversion_probe(ctx):
 
 
 def test_auto_escalates_to_split_on_large_norms(ctx):
-    """Auto mode starts with the single-pass tf32 scan and, when the data makes
-    its bound too loose (norms >> neighbor gaps), switches the index to the
-    split-precision kernel; results are exact throughout."""
+    """Auto mode starts with the single-pass tf32 scan (fp32 lists: the fp16
+    filter copy off) and, when the data makes its bound too loose (norms >>
+    neighbor gaps), switches the index to the split-precision kernel; results
+    are exact throughout.  The fp16 filter copy's bound is half as wide: the
+    same data stays on the single pass with fewer fallbacks."""
     rng = np.random.default_rng(21)
     ix, csr, X, centers = _random_index(ctx, rng, 20000, 256, 32)
     Q = (centers[rng.integers(0, len(centers), 64)] +
          rng.standard_normal((64, 256)).astype(np.float32) * 0.3).astype(np.float32)
     ctx.set_option("scan_kernel", 0)
-    _check_search(ix, csr, Q, 8, 10)
-    first = ctx.stats()["scan_kernel"]
-    _check_search(ix, csr, Q, 8, 10)
-    second = ctx.stats()
-    assert first == 3
+    ctx.set_option("filter_h16", 0)
+    try:
+        _check_search(ix, csr, Q, 8, 10)
+        first = ctx.stats()
+        _check_search(ix, csr, Q, 8, 10)
+        second = ctx.stats()
+    finally:
+        ctx.set_option("filter_h16", 1)
+    assert first["scan_kernel"] == 3 and first["scan_filter_bits"] == 32
     assert second["scan_kernel"] == 2 and second["n_fallback"] <= 3, second
+    ix2, csr2, X2, centers2 = _random_index(ctx, np.random.default_rng(21), 20000, 256, 32)
+    _check_search(ix2, csr2, Q, 8, 10)
+    h = ctx.stats()
+    assert h["scan_kernel"] == 3 and h["scan_filter_bits"] == 16, h
+    assert h["n_fallback"] < first["n_fallback"], (h, first)
 
 
 def test_unit_norm_data_split_no_fallback(ctx):
@@ -441,3 +452,30 @@ def test_repeated_search_graph_replay(ctx):
         _check_search(ix, csr, batch(40), 8, 10)
     finally:
         ctx.set_option("search_graph", 1)
+
+
+def test_fp16_filter_copy_parity_and_out_of_range_queries(ctx):
+    """The fp16 filter copy on its own: single-pass scans with
+    and without it give the reference's bits; queries whose power-of-2 scale is
+    out of range (|q| < 2^-46) report no candidates and a -inf threshold, so
+    their segments are re-scanned exactly."""
+    rng = np.random.default_rng(31)
+    ix, csr, X, centers = _random_index(ctx, rng, 12000, 100, 24)
+    Q = (centers[rng.integers(0, len(centers), 48)] +
+         rng.standard_normal((48, 100)).astype(np.float32) * 0.3).astype(np.float32)
+    ctx.set_option("scan_kernel", 3)
+    try:
+        for h in (1, 0):
+            ctx.set_option("filter_h16", h)
+            _check_search(ix, csr, Q, 6, 10)
+            assert ctx.stats()["scan_filter_bits"] == (16 if h else 32)
+        ctx.set_option("filter_h16", 1)
+        tiny = Q.copy()
+        tiny[::3] *= np.float32(1e-16)  # |q| ~ 1e-15 ~ 2^-50: scale out of range
+        _check_search(ix, csr, tiny, 6, 10)
+        st = ctx.stats()
+        assert st["scan_filter_bits"] == 16
+        assert st["n_fallback"] >= 16, st
+    finally:
+        ctx.set_option("filter_h16", 1)
+        ctx.set_option("scan_kernel", 0)
