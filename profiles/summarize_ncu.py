@@ -1,7 +1,7 @@
 """Summaries committed under profiles/ from gpurun_out/ ncu outputs.
 
     python profiles/summarize_ncu.py launches <launches.csv> <out.txt> <title>
-    python profiles/summarize_ncu.py full <report.ncu-rep> <out.json> <config> <algorithmic_bytes>
+    python profiles/summarize_ncu.py full <report.ncu-rep> <out.json> <config> <algorithmic_bytes> [<traffic.json>]
 """
 import collections
 import csv
@@ -34,7 +34,7 @@ def launches(path, out, title):
     print("\n".join(lines))
 
 
-def full(rep, out, config, alg_bytes):
+def full(rep, out, config, alg_bytes, traffic_out=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -66,7 +66,7 @@ def full(rep, out, config, alg_bytes):
     json.dump(o, open(out, "w"), indent=1)
     json.dump({"config": config, "kernel": "k_scan_tc", "dram_bytes_per_launch": int(traffic),
                "source": out + " (ncu --set full, one launch)"},
-              open(out.replace("r1_ncu_k_scan_tc_", "ncu_traffic_"), "w"), indent=1)
+              open(traffic_out or out.replace("r1_ncu_k_scan_tc_", "ncu_traffic_"), "w"), indent=1)
     print(json.dumps(o, indent=1)[:900])
 
 
@@ -74,4 +74,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(*sys.argv[2:5])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5])
+        full(*sys.argv[2:7])
