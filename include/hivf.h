@@ -396,6 +396,13 @@ int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, unsigned n, in
 int hivf_debug_tc2_dot(const float* A, const float* B, unsigned D, unsigned n, int bsplit, float* out);
 int hivf_debug_bound(int kind, unsigned D, double* e_a, double* e_b, double* e_c);
 int hivf_debug_tc_prof(unsigned long long* out, int n_ctas);
+/* hivf_debug_mma_rate: cycles per MMA of the scan's step shapes in isolation
+ *   (mode 0 f16 SS, 1 tf32 SS, 2 f16 with A in TMEM, 3 tcgen05.cp of the A
+ *   k-step + f16 TS MMA, 4 + j f16 SS round robin over 1 + j accumulators;
+ *   M = 128, N = n), A[128][32], B[256][32] host;
+ *   d_out[128][32] = the accumulator (first 32 columns). */
+int hivf_debug_mma_rate(int mode, unsigned n, unsigned reps, const float* A, const float* B, double* cycles_out,
+                        float* d_out);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,7 @@ SYMBOLS = [
     "hivf_set_option", "hivf_shard_plan", "hivf_shard_local_lists", "hivf_index_upload_shard",
     "hivf_group_create", "hivf_nccl_unique_id", "hivf_group_create_nccl", "hivf_group_create_hostcb",
     "hivf_group_destroy", "hivf_group_search_device", "hivf_group_search", "hivf_train_kmeans_sampled_seeds",
-    "hivf_index_row_distances", "hivf_debug_tc_dot", "hivf_debug_bound", "hivf_debug_tc_prof", "hivf_debug_tc2_dot",
+    "hivf_index_row_distances", "hivf_debug_tc_dot", "hivf_debug_bound", "hivf_debug_tc_prof", "hivf_debug_tc2_dot", "hivf_debug_mma_rate",
 ]
 
 
@@ -98,6 +98,7 @@ def lib():
         "hivf_debug_tc2_dot": (i32, [vp, vp, u32, u32, i32, vp]),
         "hivf_debug_bound": (i32, [i32, u32, P(f64), P(f64), P(f64)]),
         "hivf_debug_tc_prof": (i32, [vp, i32]),
+        "hivf_debug_mma_rate": (i32, [i32, u32, u32, vp, vp, vp, vp]),
         "hivf_assign": (i32, [vp, vp, u32, u32, vp, vp]),
         "hivf_search": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),
         "hivf_search_device": (i32, [vp, vp, u32, u32, u32, vp, vp, vp]),

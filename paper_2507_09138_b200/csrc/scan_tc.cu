@@ -150,6 +150,57 @@ __device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a, uint6
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+
+// One pipeline stage's MMAs (cn <= 4 chunks x 2 k-steps) in ONE warp-collective
+// asm block: elect.sync once, descriptors advanced with 64-bit adds inside the
+// block (A: +512 per 8 KB chunk, +2 per 32-B k-step; B: +qs per chunk), so the
+// issuing warp moves its operands to uniform registers once per stage instead
+// of once per instruction (the per-instruction R2UR / elect sequence cost
+// ~130 cycles per MMA, profiles/r2_mma_rate.txt).  acc0: accumulate into D on
+// the stage's first k-step.
+#define HIVF_MMA_STAGE8(CG, KIND)                                                            \
+  asm volatile(                                                                            \
+      "{\n\t.reg .pred p, t, e, c1, c2, c3;\n\t.reg .b64 a, b, bq, q;\n\t"                 \
+      "setp.ne.b32 p, %4, 0;\n\t"                                                          \
+      "setp.eq.u32 t, 0, 0;\n\t"                                                           \
+      "cvt.u64.u32 q, %6;\n\t"                                                             \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                    \
+      "setp.gt.and.u32 c1, %5, 1, e;\n\t"                                                  \
+      "setp.gt.and.u32 c2, %5, 2, e;\n\t"                                                  \
+      "setp.gt.and.u32 c3, %5, 3, e;\n\t"                                                  \
+      "@e tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], %1, %2, %3, p;\n\t"                \
+      "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"                                         \
+      "@e tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, b, %3, t;\n\t"                  \
+      "add.s64 a, %1, 512;\n\tadd.s64 bq, %2, q;\n\t"                                      \
+      "@c1 tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, bq, %3, t;\n\t"                \
+      "add.s64 a, a, 2;\n\tadd.s64 b, bq, 2;\n\t"                                          \
+      "@c1 tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, b, %3, t;\n\t"                 \
+      "add.s64 a, %1, 1024;\n\tadd.s64 bq, bq, q;\n\t"                                     \
+      "@c2 tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, bq, %3, t;\n\t"                \
+      "add.s64 a, a, 2;\n\tadd.s64 b, bq, 2;\n\t"                                          \
+      "@c2 tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, b, %3, t;\n\t"                 \
+      "add.s64 a, %1, 1536;\n\tadd.s64 bq, bq, q;\n\t"                                     \
+      "@c3 tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, bq, %3, t;\n\t"                \
+      "add.s64 a, a, 2;\n\tadd.s64 b, bq, 2;\n\t"                                          \
+      "@c3 tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem), \
+      "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(cn), "r"(qs))
+__device__ __forceinline__ void mma_stage8_tf32(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                                uint32_t acc0, uint32_t cn, uint32_t qs) {
+  HIVF_MMA_STAGE8("1", "tf32");
+}
+__device__ __forceinline__ void mma_stage8_f16(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                               uint32_t acc0, uint32_t cn, uint32_t qs) {
+  HIVF_MMA_STAGE8("1", "f16");
+}
+// the same for a CTA pair (cta_group::2, issued by the leader CTA's MMA warp)
+__device__ __forceinline__ void mma2_stage8_tf32(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                                 uint32_t acc0, uint32_t cn, uint32_t qs) {
+  HIVF_MMA_STAGE8("2", "tf32");
+}
+__device__ __forceinline__ void mma2_stage8_f16(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                                uint32_t acc0, uint32_t cn, uint32_t qs) {
+  HIVF_MMA_STAGE8("2", "f16");
+}
 __device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -805,7 +856,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_scan_tc(TcParams P) {
           const uint64_t qdw = adesc + (uint64_t)(kTcStageBytes >> 4);
           const uint32_t alo = tmem_base + kTmemAcc + l * kTmemLoCols;  // A_lo in TMEM, lane = row
           const uint32_t c0 = sg * kTcCps;
-          if (!(P.variant & 4)) {
+          if (!(P.variant & 4) && !split && !(P.variant & 8)) {
+            // single pass: the stage's MMAs in one asm block (operands to uniform registers once)
+            const uint64_t qd0 = kWide ? qdw : qdesc0 + (uint64_t)(c0 * (qblk >> 4));
+            const uint32_t qs = kWide ? npad * 4 : (qblk >> 4);
+            if (h16) mma_stage8_f16(d_tmem, adesc, qd0, idesc2, sg != 0, cn, qs);
+            else mma_stage8_tf32(d_tmem, adesc, qd0, idesc2, sg != 0, cn, qs);
+          } else if (!(P.variant & 4)) {
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kTcCps; ++c) {
               if (c >= cn) break;
@@ -1503,18 +1560,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
             const long long _ti = P.prof ? clock64() : 0;
             const uint64_t adesc = adesc0 + (uint64_t)(a * (kSB >> 4));
             const uint64_t qd0 = adesc + (uint64_t)(kPairStageA >> 4);
-#pragma unroll
-            for (uint32_t c = 0; c < (uint32_t)kPCps; ++c) {
-              if (c >= cn) break;
-              const uint64_t qd = qd0 + (uint64_t)(c * (npad / 2 * 4));  // (npad/2)*64 B per chunk
-#pragma unroll
-              for (uint32_t k2 = 0; k2 < 2; ++k2) {
-                const uint64_t ad = adesc + (uint64_t)((c * kTcChunkBytes + k2 * 32) >> 4);
-                if (lane == 0 && !(P.variant & 4)) {
-                  if (h16) mma2_f16(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
-                  else mma2_tf32(d_tmem, ad, qd + 2 * k2, idesc, (sg | c | k2) != 0);
-                }
-              }
+            // the stage's MMAs in one warp-collective asm block; (npad/2)*64 B of queries per chunk
+            if (!(P.variant & 4)) {
+              if (h16) mma2_stage8_f16(d_tmem, adesc, qd0, idesc, sg != 0, cn, npad * 2);
+              else mma2_stage8_tf32(d_tmem, adesc, qd0, idesc, sg != 0, cn, npad * 2);
             }
             if (lane == 0) mma2_commit_both(&empty[a]);  // the slot is free in both CTAs
             __syncwarp();
@@ -2287,6 +2336,158 @@ extern "C" int hivf_debug_tc_dot(const float* A, const float* B, unsigned D, uns
   cudaFree(dA);
   cudaFree(dB);
   cudaFree(dO);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// hivf_debug_mma_rate: issue rate of the scan's MMA step shapes in isolation
+// (one CTA, operands resident, `reps` back-to-back MMAs into one accumulator):
+//   mode 0  kind::f16  M=128 x N x K=16, A and B from shared memory (SS)
+//   mode 1  kind::tf32 M=128 x N x K=8,  SS
+//   mode 2  kind::f16, A from TMEM (TS), A written once
+//   mode 3  tcgen05.cp 128x256b (A k-step smem -> TMEM) + TS MMA per k-step
+//   mode 4+j  f16 SS round robin over 1+j independent accumulators (n <= 32)
+//   mode 12 f16 SS, whole stages of 8 MMAs per asm block (mma_stage8_f16)
+// cycles_out[0] = cycles per MMA; d_out[128][min(n,32)] = the accumulator
+// (A rows = a[r][0..31], B rows = b[j][0..31] fp16 / tf32 values cycled
+// over the reps), so modes 0, 2 and 3 can be compared bit for bit.
+// ---------------------------------------------------------------------------
+namespace hivf {
+namespace {
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_cp_128x256(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+__global__ void __launch_bounds__(128, 1) k_mma_rate(int mode, uint32_t n, uint32_t reps, const float* A,
+                                                     const float* B, double* cyc, float* dout) {
+  extern __shared__ __align__(1024) uint8_t mr_smem[];
+  uint8_t* a = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mr_smem) + 1023) & ~uintptr_t(1023));
+  uint8_t* b = a + 4 * 128 * 64;  // a: 4 chunk planes (mode 12 walks them), b: 256 rows
+  __shared__ uint64_t bar;
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 4 * 128 * 64 / 4; i += 128) reinterpret_cast<uint32_t*>(a)[i] = 0u;
+  __syncthreads();
+  // one 64-B row slice per operand row: f16 -> 32 dims, tf32 -> 16 dims
+  for (int g = 0; g < 4; ++g) {
+    const uint32_t off = tid * 64 + ((g ^ ((tid >> 1) & 3)) << 4);
+    for (int e = 0; e < (mode == 1 ? 4 : 8); ++e) {
+      if (mode == 1) {
+        reinterpret_cast<float*>(a + off)[e] = A[tid * 32 + g * 4 + e];
+      } else {
+        reinterpret_cast<__half*>(a + off)[e] = __float2half_rn(A[tid * 32 + g * 8 + e]);
+      }
+    }
+  }
+  for (uint32_t j = tid; j < 256; j += 128)
+    for (int g = 0; g < 4; ++g) {
+      const uint32_t off = j * 64 + ((g ^ ((j >> 1) & 3)) << 4);
+      for (int e = 0; e < (mode == 1 ? 4 : 8); ++e) {
+        const float v = j < n ? B[j * 32 + (mode == 1 ? g * 4 : g * 8) + e] : 0.f;
+        if (mode == 1) reinterpret_cast<float*>(b + off)[e] = v;
+        else reinterpret_cast<__half*>(b + off)[e] = __float2half_rn(v);
+      }
+    }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem, atm = tmem + 256;  // D: columns [0, n); A in TMEM: columns 256.. (8 per k-step)
+  const uint64_t ad0 = sw64_kmajor_desc(smem_u32(a)), bd0 = sw64_kmajor_desc(smem_u32(b));
+  const uint32_t idesc = mode == 1 ? tf32_idesc(n) : f16_idesc_m(128, n);
+  if (mode == 12 && warp == 0) {  // whole stages (4 chunks x 2 k-steps) per asm block, warp-collective
+    const long long t0 = clock64();
+    for (uint32_t r = 0; r < reps; r += 8) mma_stage8_f16(tmem, ad0, bd0, idesc, r != 0, 4, 0);
+    if (lane == 0) {
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+      cyc[0] = (double)(clock64() - t0) / reps;
+    }
+    __syncwarp();
+  }
+  if (tid == 0 && mode != 12) {
+    if (mode == 2) {  // A once into TMEM (both k-steps of the slice)
+      tc_cp_128x256(atm, ad0);
+      tc_cp_128x256(atm + 8, ad0 + 2);
+    }
+    tc_fence_after();
+    const long long t0 = clock64();
+    for (uint32_t r = 0; r < reps; ++r) {
+      const uint32_t k2 = r & 1;
+      if (mode >= 4) {  // f16 SS into (mode - 3) independent accumulators, round robin (32 columns apart)
+        const uint32_t nd = (uint32_t)mode - 3, di = r % nd;
+        mma_f16(tmem + 32 * di, ad0 + 2 * k2, bd0 + 2 * k2, idesc, r >= nd);
+      } else if (mode == 0) mma_f16(tmem, ad0 + 2 * k2, bd0 + 2 * k2, idesc, r != 0);
+      else if (mode == 1) mma_tf32(tmem, ad0 + 2 * k2, bd0 + 2 * k2, idesc, r != 0);
+      else if (mode == 2) mma_f16_ts(tmem, atm + 8 * k2, bd0 + 2 * k2, idesc, r != 0);
+      else {
+        const uint32_t slot = atm + 8 * (r & 7);
+        tc_cp_128x256(slot, ad0 + 2 * k2);
+        mma_f16_ts(tmem, slot, bd0 + 2 * k2, idesc, r != 0);
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    cyc[0] = (double)(t1 - t0) / reps;
+  }
+  __syncthreads();
+  tc_fence_after();
+  uint32_t r32[32];
+  TMEM_LD32(tmem + ((warp * 32) << 16), r32);
+  tmem_wait_ld();
+  for (uint32_t j = 0; j < 32 && j < n; ++j) dout[tid * 32 + j] = __uint_as_float(r32[j]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+}  // namespace
+}  // namespace hivf
+
+extern "C" int hivf_debug_mma_rate(int mode, unsigned n, unsigned reps, const float* A, const float* B,
+                                   double* cycles_out, float* d_out) {
+  using namespace hivf;
+  if (mode < 0 || mode > 12 || n < 8 || n > 256 || n % 8 || !A || !B || !cycles_out || !d_out) return 1;
+  if (mode >= 4 && mode < 12 && n > 32) return 1;
+  float *dA = nullptr, *dB = nullptr, *dO = nullptr;
+  double* dC = nullptr;
+  int rc = 0;
+  if (cudaMalloc(&dA, 128 * 32 * 4) != cudaSuccess || cudaMalloc(&dB, 256 * 32 * 4) != cudaSuccess ||
+      cudaMalloc(&dO, 128 * 32 * 4) != cudaSuccess || cudaMalloc(&dC, 8) != cudaSuccess)
+    rc = 3;
+  if (!rc) {
+    cudaMemcpy(dA, A, 128 * 32 * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, B, 256 * 32 * 4, cudaMemcpyHostToDevice);
+    cudaMemset(dO, 0, 128 * 32 * 4);
+    const int smem = 1024 + 4 * 128 * 64 + 256 * 64;
+    cudaFuncSetAttribute(k_mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mma_rate<<<1, 128, smem>>>(mode, n, reps, dA, dB, dC, dO);
+    if (cudaMemcpy(cycles_out, dC, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(d_out, dO, 128 * 32 * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = 4;
+  }
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dO);
+  cudaFree(dC);
   return rc;
 }
 
