@@ -364,6 +364,9 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
  * "hbm_list_budget" (bytes of list storage an index may keep in HBM; the
  * rest stays in pinned host memory, see residency),
+ * "filter_h16" (default 1: hivf_index_finish builds the fp16 filter copy of the
+ * lists -- 0.5x the fp32 list bytes more HBM -- and single-pass scans stream it;
+ * 0: no copy / the scans read the fp32 lists; results identical),
  * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
  * 3 tcgen05 single-pass), "tc_qmax" (queries per scan work item: 8..32 step 8,
  * or 64 / 128 / 256 = the wide scans), "tc_wide_ppl" (probes per list above which a
