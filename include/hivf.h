@@ -364,6 +364,9 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
  * "hbm_list_budget" (bytes of list storage an index may keep in HBM; the
  * rest stays in pinned host memory, see residency),
+ * "seed_rows" (default 32, 0 = off, <= 64) / "seed_ppl" (default 16): batches
+ * with at least seed_ppl probes per list seed each query's shared drop bound
+ * with the exact distances of seed_rows rows of its nearest probed list,
  * "filter_h16" (default 1: hivf_index_finish builds the fp16 filter copy of the
  * lists -- 0.5x the fp32 list bytes more HBM -- and single-pass scans stream it;
  * 0: no copy / the scans read the fp32 lists; results identical),

@@ -216,6 +216,11 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   g_state_gen.fetch_add(1);  // any option may change what a captured search graph launches
   if (!strcmp(name, "search_graph")) {
     ctx->opt_search_graph = value != 0;
+  } else if (!strcmp(name, "seed_rows")) {  // rows per query seeding the drop bound (0 off, <= 64)
+    if (value < 0 || value > 64) return fail(HIVF_EINVAL, "seed_rows must be in [0, 64]");
+    ctx->opt_seed_rows = (uint32_t)value;
+  } else if (!strcmp(name, "seed_ppl")) {  // probes per list from which the seed runs
+    ctx->opt_seed_ppl = (float)value;
   } else if (!strcmp(name, "filter_h16")) {  // 1: fp16 filter copy built at index finish and used
     ctx->opt_h16 = value != 0;
   } else if (!strcmp(name, "seg_rows")) {  // 0: automatic (auto_seg_rows)
@@ -852,6 +857,13 @@ static hivf_status run_scan(hivf_index* ix, const QueryView& qv, uint32_t n_pair
   if (tc && topk && !item_bounds) {  // shared drop bounds start at "none" (0x7f7f7f7f ~ 3.4e38)
     CK(c->qbound.ensure((size_t)qv.n * 4));
     CK(cudaMemsetAsync(c->qbound.p, 0x7f, (size_t)qv.n * 4, c->stream));
+    // dense batches: seed them from exact distances of a few rows of each
+    // query's nearest list (options "seed_rows", "seed_ppl")
+    if (c->opt_seed_rows >= topk && ppl >= c->opt_seed_ppl && qv.n && n_pairs % qv.n == 0) {
+      launch_seed_bounds(v, qv, c->plans.as<uint32_t>(), n_pairs / qv.n, topk, c->opt_seed_rows,
+                         c->qbound.as<float>(), c->stream);
+      CKL();
+    }
   }
   if (timed) c->mark(1);
   if (tc)

@@ -734,6 +734,62 @@ uint32_t exact_search_parts(uint32_t nprobe, uint32_t k) {
   return ns ? ns : 1;
 }
 
+namespace {
+// Seed of the shared drop bound: per query, the
+// exact double distance (the reference's sequential arithmetic, exact_step) of
+// the first `rows` rows of its nearest probed list with at least that many
+// rows (first 4 plan positions); the k-th smallest, rounded up, is an upper
+// bound on the query's true k-th distance over its probes (k distinct probed
+// rows), so the scan can drop rows from its first tile on instead of after the
+// query's first finished item.  One CTA (64 threads, one row each) per query.
+__global__ void __launch_bounds__(64) k_seed_bounds(IndexView ix, QueryView qv, const uint32_t* __restrict__ plans,
+                                                    uint32_t nprobe, uint32_t k, uint32_t rows,
+                                                    float* __restrict__ qbound) {
+  pdl_wait();
+  const uint32_t b = blockIdx.x, t = threadIdx.x;
+  __shared__ double sd[64];
+  uint32_t c = ~0u;
+  uint64_t lbeg = 0, n_c = 0;
+  for (uint32_t p = 0; p < nprobe && p < 4; ++p) {
+    const uint32_t cc = plans[(uint64_t)b * nprobe + p];
+    if (cc >= ix.K) continue;
+    const uint64_t lb = ix.list_off[cc], n = ix.list_off[cc + 1] - lb;
+    if (n >= rows) {
+      c = cc;
+      lbeg = lb;
+      n_c = n;
+      break;
+    }
+  }
+  if (c == ~0u) return;  // uniform: no list with enough rows, no seed
+  const float* q = qv.qs + (uint64_t)b * ix.dpad;
+  const float* base = list_base(ix, c, lbeg);
+  double acc = __longlong_as_double(0x7ff0000000000000ll);
+  if (t < rows) {
+    acc = 0.0;
+    for (uint32_t d = 0; d < ix.dim; ++d) acc = exact_step(acc, base[swz_offset(0, n_c, t, d, ix.dpad)], q[d]);
+  }
+  sd[t] = acc;
+  __syncthreads();
+  if (t == 0) {  // k-th smallest of <= 64 values
+    double kth = 0.0;
+    for (uint32_t j = 0; j < rows; ++j) {
+      uint32_t below = 0;
+      for (uint32_t i = 0; i < rows; ++i) below += sd[i] < sd[j] || (sd[i] == sd[j] && i < j);
+      if (below == k - 1) kth = sd[j];
+    }
+    const float u = __double2float_ru(kth);
+    if (u < 3.0e38f) atomicMin(reinterpret_cast<int*>(qbound + b), __float_as_int(u));
+  }
+}
+}  // namespace
+
+void launch_seed_bounds(const IndexView& ix, const QueryView& qv, const uint32_t* plans, uint32_t nprobe,
+                        uint32_t k, uint32_t rows, float* qbound, cudaStream_t s) {
+  if (!qv.n || rows < k || rows > 64) return;
+  launch_pdl(k_seed_bounds, dim3(qv.n), dim3(64), 0, s, ix, qv, plans, nprobe, k, rows, qbound);
+}
+
 void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
                          uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
                          double* d_out, uint32_t* counts_out, uint64_t* part_ids,

@@ -112,6 +112,10 @@ struct hivf_ctx {
   // fp16 filter copy (option "filter_h16"): built at index finish when 1 and
   // used by the single-pass tensor-core scan while 1
   int opt_h16 = 1;
+  // drop-bound seed (launch_seed_bounds): rows per query, and the batch density
+  // (pairs per list) from which it runs
+  uint32_t opt_seed_rows = 32;
+  float opt_seed_ppl = 16.f;
   // 0 auto (tensor cores when the dim fits; single-pass tf32, escalating to the
   // split kernel when the data makes its bound too loose), 1 FFMA, 2 tcgen05
   // split-precision, 3 tcgen05 single-pass

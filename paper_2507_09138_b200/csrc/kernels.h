@@ -287,6 +287,10 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
 // part_* scratch (n_queries x exact_search_parts() x k) enables the multi-CTA
 // path; pass nullptr for one CTA per query.
 uint32_t exact_search_parts(uint32_t nprobe, uint32_t k);
+// seed of the shared drop bound: exact distances of `rows` (<= 64) rows of each
+// query's nearest probed list (finalize.cu)
+void launch_seed_bounds(const IndexView& ix, const QueryView& qv, const uint32_t* plans, uint32_t nprobe,
+                        uint32_t k, uint32_t rows, float* qbound, cudaStream_t s);
 void launch_exact_search(const IndexView& ix, const QueryView& qv, const uint32_t* plans,
                          uint32_t nprobe, uint32_t k, const int* flags, uint64_t* ids_out,
                          double* d_out, uint32_t* counts_out, uint64_t* part_ids,

@@ -86,3 +86,22 @@ def test_wide_and_narrow_agree_on_dense_batch(ctx):
     for x, y in zip(a, b):
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
     _check_search(ix, csr, Q, 16, 10)
+
+
+def test_drop_bound_seed_same_results(ctx):
+    """The drop-bound seed (exact distances of a few rows of each query's
+    nearest list) only removes work: seeded and unseeded scans give the
+    reference's bits."""
+    rng = np.random.default_rng(44)
+    ix, csr, X, centers = _random_index(ctx, rng, 30000, 96, 24)
+    Q = (centers[rng.integers(0, len(centers), 600)] +
+         rng.standard_normal((600, 96)).astype(np.float32) * 0.3).astype(np.float32)
+    try:
+        for rows, ppl in ((32, 0), (64, 0), (10, 0), (0, 0)):
+            ctx.set_option("seed_rows", rows)
+            ctx.set_option("seed_ppl", ppl)
+            _check_search(ix, csr, Q, 8, 10)
+            _check_search(ix, csr, Q, 3, 1)
+    finally:
+        ctx.set_option("seed_rows", 32)
+        ctx.set_option("seed_ppl", 16)
