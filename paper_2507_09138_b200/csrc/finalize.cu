@@ -25,7 +25,8 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kFinThreads = 256;
 constexpr int kCandMax = 512;
-constexpr uint32_t kSlotCap = 320;  // staged (plan position, segment) slots per query
+constexpr uint32_t kSlotCap = 320;  // staged (plan position, segment) slots per query and chunk
+constexpr uint32_t kSpCap = 2048;   // (plan position, segment) slot ids per query held in smem
 constexpr uint32_t kRepMax = 64;    // failing segments per query repaired in place
 constexpr int kRepChunk = 256;      // rows per repair work unit
 constexpr float kInf = __builtin_inff();
@@ -129,8 +130,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   // their candidate lists staged into smem with all threads' loads in flight
   // (the scan's outputs are read once, latency paid once).
   uint32_t* soff = pns + nprobe;                              // nprobe + 1
-  uint32_t* sp = soff + nprobe + 1;                           // kSlotCap
-  uint32_t* sn = sp + kSlotCap;                               // kSlotCap
+  uint32_t* sp = soff + nprobe + 1;                           // kSpCap
+  uint32_t* sn = sp + kSpCap;                                 // kSlotCap
   float* sthr = reinterpret_cast<float*>(sn + kSlotCap);      // kSlotCap
   float* sdv = sthr + kSlotCap;                               // kSlotCap x 32
   __shared__ uint32_t s_nslots;
@@ -157,22 +158,32 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
   __syncthreads();
   const uint32_t V = s_nslots;
   const uint64_t slot0 = (uint64_t)b * nprobe * ix.s_max;
-  if (V <= kSlotCap) {
+  if (V <= kSpCap) {
+    // staged in chunks of kSlotCap slots: every thread's loads of a chunk in
+    // flight at once (the CTA-pair scan's two slots per segment take V past
+    // one chunk at C3: 128 probes x ~4 slots)
     for (uint32_t p = threadIdx.x; p < nprobe; p += blockDim.x)
       for (uint32_t t = 0; t < pns[p]; ++t) sp[soff[p] + t] = p * ix.s_max + t;  // p*s_max+s
     __syncthreads();
-    for (uint32_t v = threadIdx.x; v < V; v += blockDim.x) {
-      sn[v] = cand_n[slot0 + sp[v]];
-      sthr[v] = cand_thr[slot0 + sp[v]];
-    }
-    for (uint32_t idx = threadIdx.x; idx < V * kKP; idx += blockDim.x)
-      sdv[idx] = cand_d[(slot0 + sp[idx / kKP]) * kKP + (idx % kKP)];
-    __syncthreads();
+    auto stage = [&](uint32_t v0, uint32_t nv) {
+      for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
+        sn[v] = cand_n[slot0 + sp[v0 + v]];
+        sthr[v] = cand_thr[slot0 + sp[v0 + v]];
+      }
+      for (uint32_t idx = threadIdx.x; idx < nv * kKP; idx += blockDim.x)
+        sdv[idx] = cand_d[(slot0 + sp[v0 + idx / kKP]) * kKP + (idx % kKP)];
+      __syncthreads();
+    };
     // 1. tau = k-th smallest upper bound
     float cur = kInf;
-    for (uint32_t v = warp; v < V; v += NW) {
-      const float E = pE[sp[v] / ix.s_max];
-      cur = warp_merge32(cur, lane < (int)sn[v] ? __fadd_ru(sdv[v * kKP + lane], E) : kInf);
+    for (uint32_t v0 = 0; v0 < V; v0 += kSlotCap) {
+      const uint32_t nv = min(kSlotCap, V - v0);
+      stage(v0, nv);
+      for (uint32_t v = warp; v < nv; v += NW) {
+        const float E = pE[sp[v0 + v] / ix.s_max];
+        cur = warp_merge32(cur, lane < (int)sn[v] ? __fadd_ru(sdv[v * kKP + lane], E) : kInf);
+      }
+      __syncthreads();
     }
     wl[warp][lane] = cur;
     __syncthreads();
@@ -184,27 +195,33 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     }
     __syncthreads();
     const float tau = s_tau;
-    // 2. candidates + completeness
-    for (uint32_t v = warp; v < V; v += NW) {
-      const uint32_t p = sp[v] / ix.s_max;
-      const float E = pE[p];
-      const bool take = lane < (int)sn[v] && __fsub_rd(sdv[v * kKP + lane], E) <= tau;
-      const unsigned msk = __ballot_sync(FULL, take);
-      uint32_t base = 0;
-      if (lane == 0 && msk) base = atomicAdd(&s_cnt, (uint32_t)__popc(msk));
-      base = __shfl_sync(FULL, base, 0);
-      if (take) {
-        const uint32_t pos = base + __popc(msk & ((1u << lane) - 1));
-        if (pos < kCandMax) {
-          crow[pos] = cand_row[(slot0 + sp[v]) * kKP + lane];
-          clist[pos] = pc[p];
+    // 2. candidates + completeness (one chunk: still staged from pass 1)
+    for (uint32_t v0 = 0; v0 < V; v0 += kSlotCap) {
+      const uint32_t nv = min(kSlotCap, V - v0);
+      if (V > kSlotCap) stage(v0, nv);
+      for (uint32_t v = warp; v < nv; v += NW) {
+        const uint32_t sv = sp[v0 + v];
+        const uint32_t p = sv / ix.s_max;
+        const float E = pE[p];
+        const bool take = lane < (int)sn[v] && __fsub_rd(sdv[v * kKP + lane], E) <= tau;
+        const unsigned msk = __ballot_sync(FULL, take);
+        uint32_t base = 0;
+        if (lane == 0 && msk) base = atomicAdd(&s_cnt, (uint32_t)__popc(msk));
+        base = __shfl_sync(FULL, base, 0);
+        if (take) {
+          const uint32_t pos = base + __popc(msk & ((1u << lane) - 1));
+          if (pos < kCandMax) {
+            crow[pos] = cand_row[(slot0 + sv) * kKP + lane];
+            clist[pos] = pc[p];
+          }
+        }
+        if (lane == 0 && __fsub_rd(sthr[v], E) <= tau) {
+          s_bad = 1;
+          const uint32_t f = atomicAdd(&s_nfail, 1u);
+          if (f < kRepMax) s_fail[f] = sv;
         }
       }
-      if (lane == 0 && __fsub_rd(sthr[v], E) <= tau) {
-        s_bad = 1;
-        const uint32_t f = atomicAdd(&s_nfail, 1u);
-        if (f < kRepMax) s_fail[f] = sp[v];
-      }
+      __syncthreads();
     }
   } else {
     // more segments than fit in smem: read the scan's outputs from global
@@ -720,7 +737,7 @@ void launch_finalize_search(const IndexView& ix, const QueryView& qv, const uint
                             const RepairState* rep, cudaStream_t s) {
   const RepairState R = rep ? *rep : RepairState{};
   const size_t smem = (size_t)kCandMax * (8 + 8 + 4 + 4) + (size_t)ix.dpad * 8 + (size_t)nprobe * 16 + 4 +
-                      (size_t)kSlotCap * (4 + 4 + 4 + kKP * 4);
+                      (size_t)kSpCap * 4 + (size_t)kSlotCap * (4 + 4 + kKP * 4);
   smem_optin((const void*)k_finalize_search, 200 * 1024);
   launch_pdl(k_finalize_search, dim3(qv.n), dim3(kFinThreads), smem, s, ix, qv, plans, nprobe, k, cand_d, cand_row,
                                                     cand_thr, cand_n, filter_eps(ix.dim),
