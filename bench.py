@@ -661,6 +661,8 @@ def run_hivf(args):
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": traffic,
                      "bytes_per_launch": int(scan_bytes), "launch_ms": round(scan_ms, 4),
+                     "bytes_basis": ("distinct probed rows x dim x 2 B (the fp16 filter copy the scan streams)"
+                                     if elem == 2 else "distinct probed rows x dim x 4 B (fp32 lists)"),
                      "launch_ms_max_over_ranks": round(scan_ms_all[0], 4),
                      "step_hbm_frac": round(step_ab / (ms_per_step / 1e3) / 1e9 / peak, 4),
                      "phase_ms": {"assign": round(assign_ms, 4), "scan": round(scan_ms, 4),
