@@ -33,6 +33,11 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kItThreads = 128;
 constexpr int kItCand = 2048;
+// an item's candidate slots (clusters x s_max) and per-cluster metadata staged
+// into smem by all threads before the sequential per-cluster pass (the pass
+// then runs on smem instead of a chain of dependent global loads per cluster)
+constexpr uint32_t kItStage = 256;
+constexpr uint32_t kItStageCl = 128;
 constexpr float kInf = __builtin_inff();
 
 __device__ __forceinline__ float it_merge32(float cur, float v) {
@@ -45,6 +50,35 @@ __device__ __forceinline__ float it_merge32(float cur, float v) {
     x = ((lane & s) == 0) ? fminf(x, p) : fmaxf(x, p);
   }
   return x;
+}
+
+// Ascending bitonic sort / clean of one (distance, id) pair per lane (pair_less order).
+__device__ __forceinline__ void warp_sort_pairs(double& d, uint64_t& id, int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      const double pd = __shfl_xor_sync(FULL, d, jj);
+      const uint64_t pi = __shfl_xor_sync(FULL, id, jj);
+      const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
+      if (keep_min == pair_less(pd, pi, d, id)) {
+        d = pd;
+        id = pi;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void warp_clean_pairs(double& d, uint64_t& id, int lane) {
+#pragma unroll
+  for (int jj = 16; jj > 0; jj >>= 1) {
+    const double pd = __shfl_xor_sync(FULL, d, jj);
+    const uint64_t pi = __shfl_xor_sync(FULL, id, jj);
+    const bool keep_min = (lane & jj) == 0;
+    if (keep_min == pair_less(pd, pi, d, id)) {
+      d = pd;
+      id = pi;
+    }
+  }
 }
 
 // TopKResult::insert (vector_index.cpp:38-53) on a warp-register heap:
@@ -97,6 +131,12 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
   uint32_t* clist = crow + kItCand;                              // kItCand
   uint32_t* cj_off = clist + kItCand;                            // (m_items+1) candidate offsets per cluster
   float* qsh = reinterpret_cast<float*>(cj_off + kNprobeMax + 1);  // dpad
+  float* st_d = qsh + ix.dpad;                                   // kItStage x 32
+  float* st_thr = st_d + kItStage * kKP;                         // kItStage
+  uint32_t* st_n = reinterpret_cast<uint32_t*>(st_thr + kItStage);  // kItStage
+  uint32_t* st_c = st_n + kItStage;                              // kItStageCl: cluster id
+  uint32_t* st_ns = st_c + kItStageCl;                           // kItStageCl: slots
+  float* st_E = reinterpret_cast<float*>(st_ns + kItStageCl);    // kItStageCl: filter bound
   __shared__ int s_bad;
   const uint32_t it = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,6 +151,23 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     if (threadIdx.x == 0) flags[it] = 1;
     return;
   }
+  const bool staged = mcl <= kItStageCl && mcl * ix.s_max <= kItStage;
+  if (staged) {
+    const uint64_t sbase = (uint64_t)j0 * ix.s_max;
+    const uint32_t S = mcl * ix.s_max;
+    for (uint32_t j = threadIdx.x; j < mcl; j += blockDim.x) {
+      const uint32_t c = clusters[j0 + j];
+      st_c[j] = c;
+      st_ns[j] = slots_of(ix, ix.list_off[c + 1] - ix.list_off[c]);
+      st_E[j] = seg_bound(ix, qn, ix.maxnorm[c]);
+    }
+    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+      st_n[i] = cand_n[sbase + i];
+      st_thr[i] = cand_thr[sbase + i];
+    }
+    for (uint32_t i = threadIdx.x; i < S * kKP; i += blockDim.x) st_d[i] = cand_d[sbase * kKP + i];
+    __syncthreads();
+  }
   // A + candidate collection (warp 0, in plan order -> candidates grouped by cluster)
   if (warp == 0) {
     const uint32_t n0 = heap_n[it];
@@ -120,15 +177,16 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     uint32_t cnt = 0;
     bool bad = false;
     for (uint32_t j = 0; j < mcl; ++j) {
-      const uint32_t c = clusters[j0 + j];
-      const float E = seg_bound(ix, qn, ix.maxnorm[c]);
-      const uint64_t rows = ix.list_off[c + 1] - ix.list_off[c];
-      const uint32_t ns = slots_of(ix, rows);
+      const uint32_t c = staged ? st_c[j] : clusters[j0 + j];
+      const float E = staged ? st_E[j] : seg_bound(ix, qn, ix.maxnorm[c]);
+      const uint32_t ns = staged ? st_ns[j] : slots_of(ix, ix.list_off[c + 1] - ix.list_off[c]);
       float lj = kInf;
       for (uint32_t s = 0; s < ns; ++s) {
         const uint64_t slot = (uint64_t)(j0 + j) * ix.s_max + s;
-        const uint32_t n = cand_n[slot];
-        const float v = lane < (int)n ? __fadd_ru(cand_d[slot * kKP + lane], E) : kInf;
+        const uint32_t si = j * ix.s_max + s;
+        const uint32_t n = staged ? st_n[si] : cand_n[slot];
+        const float v =
+            lane < (int)n ? __fadd_ru(staged ? st_d[si * kKP + lane] : cand_d[slot * kKP + lane], E) : kInf;
         lj = it_merge32(lj, v);
       }
       const float tau_j = __shfl_sync(FULL, lj, (int)k - 1);
@@ -137,8 +195,10 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
       if (lane == 0) cj_off[j] = cnt;
       for (uint32_t s = 0; s < ns; ++s) {
         const uint64_t slot = (uint64_t)(j0 + j) * ix.s_max + s;
-        const uint32_t n = cand_n[slot];
-        const bool take = lane < (int)n && __fsub_rd(cand_d[slot * kKP + lane], E) <= lim;
+        const uint32_t si = j * ix.s_max + s;
+        const uint32_t n = staged ? st_n[si] : cand_n[slot];
+        const bool take =
+            lane < (int)n && __fsub_rd(staged ? st_d[si * kKP + lane] : cand_d[slot * kKP + lane], E) <= lim;
         const unsigned m = __ballot_sync(FULL, take);
         if (take) {
           const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1));
@@ -148,7 +208,7 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
           }
         }
         cnt += __popc(m);
-        if (__fsub_rd(cand_thr[slot], E) <= lim) bad = true;
+        if (__fsub_rd(staged ? st_thr[si] : cand_thr[slot], E) <= lim) bad = true;
       }
       cur = it_merge32(cur, lj);
     }
@@ -176,28 +236,68 @@ __global__ void __launch_bounds__(kItThreads) k_finalize_items(
     cid[i] = ix.ids[crow[i]];
   }
   __syncthreads();
-  // C. sequential replay of TopKResult::insert, cluster by cluster
+  // C. replay, cluster by cluster (vector_index.cpp:296-317 inserting the
+  // cluster's rows into TopKResult, :38-53).  The heap after cluster j is the
+  // top-k of the heap before it and the cluster's rows (a set in the
+  // (distance, id) order, whatever the insertion order), and the cluster
+  // changed the heap iff one of its rows entered -- its last accepted row is
+  // never evicted within the cluster, so that is: a row beats the worst of a
+  // full heap (or the heap is not full) -- or it lowered a duplicate id's
+  // distance.  So each round of <= 32 candidates is one warp-wide merge:
+  // bitonic sort, reversed min against the heap, bitonic clean.
   if (warp == 0) {
     uint32_t n = heap_n[it];
     double hd = lane < (int)n ? heap_d[(uint64_t)it * stride + lane] : DBL_MAX;
     uint64_t hid = lane < (int)n ? heap_ids[(uint64_t)it * stride + lane] : ~0ull;
     for (uint32_t j = 0; j < mcl; ++j) {
       bool ch = false;
-      // rows of one list in ascending row order, like the reference loop
       const uint32_t b0 = cj_off[j], b1 = cj_off[j + 1];
-      for (uint32_t a = b0; a < b1; ++a) {
-        // pick the a-th smallest row among [b0, b1) (tiny sets: selection)
-        uint32_t best = a;
-        for (uint32_t t = a + 1; t < b1; ++t)
-          if (crow[t] < crow[best]) best = t;
-        __syncwarp();
-        if (lane == 0 && best != a) {
-          const double td = cdist[a]; cdist[a] = cdist[best]; cdist[best] = td;
-          const uint64_t ti = cid[a]; cid[a] = cid[best]; cid[best] = ti;
-          const uint32_t tr = crow[a]; crow[a] = crow[best]; crow[best] = tr;
+      for (uint32_t a0 = b0; k && a0 < b1; a0 += 32) {  // k = 0: nothing can enter
+        bool valid = a0 + lane < b1;
+        double cd = valid ? cdist[a0 + lane] : DBL_MAX;
+        uint64_t ci = valid ? cid[a0 + lane] : ~0ull;
+        // ids already in the heap: a smaller distance replaces the entry, else the row is a no-op
+        bool removed = false;
+        for (uint32_t t = 0; t < n; ++t) {
+          const uint64_t ht = __shfl_sync(FULL, hid, t);
+          const double hdt = __shfl_sync(FULL, hd, t);
+          const unsigned dm = __ballot_sync(FULL, valid && ci == ht);
+          if (!dm) continue;
+          const int src = __ffs(dm) - 1;
+          if (__shfl_sync(FULL, cd, src) < hdt) {
+            if (lane == (int)t) {
+              hd = DBL_MAX;
+              hid = ~0ull;
+            }
+            removed = true;
+            ch = true;
+          } else if (lane == src) {
+            valid = false;
+            cd = DBL_MAX;
+            ci = ~0ull;
+          }
         }
-        __syncwarp();
-        ch |= warp_heap_insert(hd, hid, n, k, cid[a], cdist[a]);
+        if (removed) {
+          warp_sort_pairs(hd, hid, lane);
+          n = __popc(__ballot_sync(FULL, lane < (int)n && !(hd == DBL_MAX && hid == ~0ull)));
+        }
+        const double wd = __shfl_sync(FULL, hd, (int)k - 1);
+        const uint64_t wi = __shfl_sync(FULL, hid, (int)k - 1);
+        const uint32_t nv = __popc(__ballot_sync(FULL, valid));
+        ch |= __any_sync(FULL, valid && (n < k || pair_less(cd, ci, wd, wi)));
+        warp_sort_pairs(cd, ci, lane);
+        const double rd = __shfl_sync(FULL, cd, 31 - lane);
+        const uint64_t ri = __shfl_sync(FULL, ci, 31 - lane);
+        if (pair_less(rd, ri, hd, hid)) {
+          hd = rd;
+          hid = ri;
+        }
+        warp_clean_pairs(hd, hid, lane);
+        if (lane >= (int)k) {
+          hd = DBL_MAX;
+          hid = ~0ull;
+        }
+        n = min(k, n + nv);
       }
       if (lane == 0) changed[j0 + j] = ch ? 1 : 0;
     }
@@ -333,7 +433,8 @@ void launch_finalize_items(const IndexView& ix, const QueryView& qv, uint32_t n_
                            uint32_t* heap_n, uint32_t heap_stride, uint8_t* changed, int* flags,
                            cudaStream_t s) {
   if (!n_items) return;
-  const size_t smem = (size_t)kItCand * (8 + 8 + 4 + 4) + (kNprobeMax + 1) * 4 + (size_t)ix.dpad * 4;
+  const size_t smem = (size_t)kItCand * (8 + 8 + 4 + 4) + (kNprobeMax + 1) * 4 + (size_t)ix.dpad * 4 +
+                      (size_t)kItStage * (kKP + 2) * 4 + (size_t)kItStageCl * 12;
   smem_optin((const void*)k_finalize_items, 220 * 1024);
   launch_pdl(k_finalize_items, dim3(n_items), dim3(kItThreads), smem, s, ix, qv, n_items, item_off, clusters, k, cand_d,
                                                      cand_row, cand_thr, cand_n, filter_eps(ix.dim),
