@@ -369,7 +369,8 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * with the exact distances of seed_rows rows of its nearest probed list,
  * "filter_h16" (default 1: hivf_index_finish builds the fp16 filter copy of the
  * lists -- 0.5x the fp32 list bytes more HBM -- and single-pass scans stream it;
- * 0: no copy / the scans read the fp32 lists; results identical),
+ * 0: no copy / the scans read the fp32 lists; results identical; process
+ * default from env HIVF_FILTER_H16),
  * "scan_ctas", "scan_kernel" (0 auto, 1 FFMA, 2 tcgen05 split-precision,
  * 3 tcgen05 single-pass), "tc_qmax" (queries per scan work item: 8..32 step 8,
  * or 64 / 128 / 256 = the wide scans), "tc_wide_ppl" (probes per list above which a

@@ -174,6 +174,9 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
     c->own_stream = true;
   }
   c->tc_conv = tc_conversion_mode();  // probed once per device
+  // process default of option "filter_h16" (env HIVF_FILTER_H16=0 runs every
+  // scan on the fp32 lists, e.g. the whole GPU suite on that path)
+  if (const char* e = getenv("HIVF_FILTER_H16")) c->opt_h16 = atoi(e) != 0;
   *out = c;
   return HIVF_OK;
 }
