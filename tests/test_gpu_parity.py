@@ -13,6 +13,8 @@ import pytest
 
 import oracle
 
+# process default of option filter_h16 (HIVF_FILTER_H16=0 runs the suite on the fp32 lists)
+H16_DEFAULT = int(os.environ.get("HIVF_FILTER_H16", "1"))
 pytestmark = pytest.mark.gpu
 
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
@@ -281,13 +283,14 @@ def test_auto_escalates_to_split_on_large_norms(ctx):
         first = ctx.stats()
         _check_search(ix, csr, Q, 8, 10)
         second = ctx.stats()
-    finally:
         ctx.set_option("filter_h16", 1)
+        ix2, csr2, X2, centers2 = _random_index(ctx, np.random.default_rng(21), 20000, 256, 32)
+        _check_search(ix2, csr2, Q, 8, 10)
+        h = ctx.stats()
+    finally:
+        ctx.set_option("filter_h16", H16_DEFAULT)
     assert first["scan_kernel"] == 3 and first["scan_filter_bits"] == 32
     assert second["scan_kernel"] == 2 and second["n_fallback"] <= 3, second
-    ix2, csr2, X2, centers2 = _random_index(ctx, np.random.default_rng(21), 20000, 256, 32)
-    _check_search(ix2, csr2, Q, 8, 10)
-    h = ctx.stats()
     assert h["scan_kernel"] == 3 and h["scan_filter_bits"] == 16, h
     assert h["n_fallback"] < first["n_fallback"], (h, first)
 
@@ -460,6 +463,7 @@ def test_fp16_filter_copy_parity_and_out_of_range_queries(ctx):
     out of range (|q| < 2^-46) report no candidates and a -inf threshold, so
     their segments are re-scanned exactly."""
     rng = np.random.default_rng(31)
+    ctx.set_option("filter_h16", 1)  # the index gets the copy whatever the process default
     ix, csr, X, centers = _random_index(ctx, rng, 12000, 100, 24)
     Q = (centers[rng.integers(0, len(centers), 48)] +
          rng.standard_normal((48, 100)).astype(np.float32) * 0.3).astype(np.float32)
@@ -477,5 +481,5 @@ def test_fp16_filter_copy_parity_and_out_of_range_queries(ctx):
         assert st["scan_filter_bits"] == 16
         assert st["n_fallback"] >= 16, st
     finally:
-        ctx.set_option("filter_h16", 1)
+        ctx.set_option("filter_h16", H16_DEFAULT)
         ctx.set_option("scan_kernel", 0)
