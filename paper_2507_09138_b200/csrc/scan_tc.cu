@@ -1415,7 +1415,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
   uint8_t* aring = smem;
   float* md = reinterpret_cast<float*>(smem + SA * kSB);  // merge scratch [kPG groups][4 warps][8 q][8]
   uint32_t* mr = reinterpret_cast<uint32_t*>(md + kPG * kTcEpiWarps * 8 * 8);
-  __shared__ uint64_t full[kTcMaxA], empty[kTcMaxA], pfull[kTcMaxA], tfull[2], tempty[2];
+  // TMEM: 4 slots of 128 columns; a tile takes 1 slot (npad <= 128) or 2 (an
+  // even-aligned pair; an odd slot is skipped), so tiles of <= 128 queries
+  // get 4-deep accumulator buffering instead of 2
+  __shared__ uint64_t full[kTcMaxA], empty[kTcMaxA], pfull[kTcMaxA], tfull[4], tempty[4];
   __shared__ uint64_t ifull[kItemQ], iempty[kItemQ];
   __shared__ ScanItem s_item[kItemQ];
   __shared__ int s_valid[kItemQ];
@@ -1436,7 +1439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
       mbar_init(&empty[i], 1);
       mbar_init(&pfull[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * kPG * kTcEpiWarps);  // both CTAs' epilogue warps
     }
@@ -1462,7 +1465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
   }
 
   uint32_t ra = 0, rpa = 0;
-  uint32_t tb = 0, tph = 0;
+  uint32_t tu = 0;  // TMEM slot uses so far: slot tu & 3, phase (tu >> 2) & 1
   if (warp == 0) {
     // ---------------- producer: static item sequence, own A tiles + own query half ----------------
     if (lane == 0) {
@@ -1534,14 +1537,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
       const uint32_t npt = (ntiles + 1) / 2;
       const uint32_t idesc = h16 ? f16_idesc_m(256, npad) : tf32_idesc_m(256, npad);
       const uint64_t adesc0 = sw64_kmajor_desc(smem_u32(aring));
+      const uint32_t tw = npad > 128 ? 2u : 1u;  // TMEM slots per tile
       for (uint32_t pt = 0; pt < npt; ++pt) {
+        if (tw == 2 && (tu & 1)) {  // a two-slot tile starts on an even slot: skip one
+          if (leader) {
+            mbar_wait_cl(&tempty[tu & 3], ((tu >> 2) & 1) ^ 1);
+            tc_fence_after();
+            if (lane == 0) mma2_commit_both(&tfull[tu & 3]);
+            __syncwarp();
+          }
+          ++tu;
+        }
         if (leader) {
           TC_PROF_T0();
-          mbar_wait_cl(&tempty[tb], tph ^ 1);
+          mbar_wait_cl(&tempty[tu & 3], ((tu >> 2) & 1) ^ 1);
+          if (tw == 2) mbar_wait_cl(&tempty[(tu + 1) & 3], (((tu + 1) >> 2) & 1) ^ 1);
           if (lane == 0) TC_PROF_ADD(2);
           tc_fence_after();
         }
-        const uint32_t d_tmem = tmem_base + tb * 256;
+        const uint32_t d_tmem = tmem_base + (tu & 3) * 128;
         for (uint32_t sg = 0; sg < nstg; ++sg) {
           const uint32_t cn = min((uint32_t)kPCps, nch - sg * kPCps);
           const uint32_t a = ra, pa = rpa;
@@ -1579,10 +1593,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
           if (++ra == SA) { ra = 0; rpa ^= 1; }
         }
         if (leader) {
-          if (lane == 0) mma2_commit_both(&tfull[tb]);
+          if (lane == 0) {
+            mma2_commit_both(&tfull[tu & 3]);
+            if (tw == 2) mma2_commit_both(&tfull[(tu + 1) & 3]);
+          }
           __syncwarp();
         }
-        if (++tb == 2) { tb = 0; tph ^= 1; }
+        tu += tw;
       }
     }
   } else {
@@ -1629,14 +1646,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
         lr[j] = kNoRow;
       }
       float gmin[2] = {kInfF, kInfF};
+      const uint32_t tw = ((item.nq + 15) & ~15u) > 128 ? 2u : 1u;  // TMEM slots per tile (as the MMA warp)
       for (uint32_t pt = 0; pt < npt; ++pt) {
         const uint32_t t = 2 * pt + crank;
         const uint32_t srow = t * kTcTile + quad * 32 + lane;  // segment-local row
         const bool valid = srow < item.nrows;
         const float xn = valid ? __ldg(P.ix.xnorm2 + lbeg + item.row0 + srow) : 0.f;
+        if (tw == 2 && (tu & 1)) {  // the skipped odd slot: pass it back
+          mbar_wait_parked(&tfull[tu & 3], (tu >> 2) & 1);
+          tc_fence_after();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader) mbar_arrive(&tempty[tu & 3]);
+            else mbar_arrive_remote(tempty_leader + (tu & 3) * 8);
+          }
+          ++tu;
+        }
         {
           TC_PROF_T0();
-          mbar_wait_parked(&tfull[tb], tph);
+          mbar_wait_parked(&tfull[tu & 3], (tu >> 2) & 1);
+          if (tw == 2) mbar_wait_parked(&tfull[(tu + 1) & 3], ((tu + 1) >> 2) & 1);
           if (lane == 0) TC_PROF_ADD(8);
         }
         tc_fence_after();
@@ -1652,7 +1682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
           gmin[m] = fminf(gmin[m], gl[m]);
         }
         const uint32_t grow = (uint32_t)(lbeg + item.row0 + srow);
-        const uint32_t ta = tmem_base + ((quad * 32) << 16) + tb * 256 + kPQ * h;
+        const uint32_t ta = tmem_base + ((quad * 32) << 16) + (tu & 3) * 128 + kPQ * h;
 #pragma unroll
         for (int m = 0; m < 2; ++m) {  // 32 query columns at a time
           if (32 * m >= (int)nq) break;
@@ -1688,11 +1718,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1) k_s
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (leader) mbar_arrive(&tempty[tb]);
-          else mbar_arrive_remote(tempty_leader + tb * 8);
+          for (uint32_t u = tu; u < tu + tw; ++u) {
+            if (leader) mbar_arrive(&tempty[u & 3]);
+            else mbar_arrive_remote(tempty_leader + (u & 3) * 8);
+          }
           if (P.prof) atomicAdd(&P.prof[blockIdx.x * 16 + 11], (unsigned long long)(clock64() - _te));
         }
-        if (++tb == 2) { tb = 0; tph ^= 1; }
+        tu += tw;
       }
       // ---- item end: the four warps' 8-lists of each query -> its 32 candidates ----
       const long long _tm = P.prof ? clock64() : 0;
