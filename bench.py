@@ -638,6 +638,14 @@ def run_hivf(args):
             cpu = cpu_baseline_line(info, cfg)
         elif world > 1:
             parity = sharded_parity(ix, cents, cfg, args, pool_np, local_sizes, outs, rank, world)
+    if residency is not None:
+        # the scan's bytes: the fp16 filter copy of every list lives in HBM
+        # (outside the budget), so the scan never crosses PCIe; the budget
+        # governs where the exact re-rank reads the fp32 rows
+        residency["scan_reads"] = ("fp16 filter copy, every list in HBM" if elem == 2
+                                   else "fp32 lists: resident from the HBM pool, cold over PCIe")
+        if elem == 2:
+            residency["exact_rows_from_hbm"] = residency.pop("scanned_bytes_from_hbm")
     if rank != 0:
         return
     clocks = clk.summary()

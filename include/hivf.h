@@ -359,6 +359,8 @@ typedef struct {
   uint32_t scan_group;         /* last call: queries per scan work item (8..32 narrow, 64 / 128 wide,
                                   256 = the CTA-pair scan) */
   uint32_t scan_filter_bits;   /* last call: 16 = the scan read the fp16 filter copy, 32 = the fp32 lists */
+  uint32_t coarse_filter_bits; /* last coarse assign: 16 = tensor-core pass over the fp16 centroid copy,
+                                  32 = FFMA pass, 0 = exact distance to every centroid (nprobe > 4096) */
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",

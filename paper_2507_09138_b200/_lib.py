@@ -57,7 +57,7 @@ class Stats(C.Structure):
                 ("scan_bytes", C.c_uint64), ("timed_calls", C.c_uint32),
                 ("assign_ms", C.c_double), ("scan_ms", C.c_double), ("finalize_ms", C.c_double),
                 ("scan_kernel", C.c_uint32), ("scan_group", C.c_uint32),
-                ("scan_filter_bits", C.c_uint32)]
+                ("scan_filter_bits", C.c_uint32), ("coarse_filter_bits", C.c_uint32)]
 
 
 _lib = None

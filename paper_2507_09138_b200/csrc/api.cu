@@ -178,6 +178,7 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
   // process default of option "filter_h16" (env HIVF_FILTER_H16=0 runs every
   // scan on the fp32 lists, e.g. the whole GPU suite on that path)
   if (const char* e = getenv("HIVF_FILTER_H16")) c->opt_h16 = atoi(e) != 0;
+  if (const char* e = getenv("HIVF_COARSE_TC")) c->opt_coarse_tc = atoi(e) != 0;
   *out = c;
   return HIVF_OK;
 }
@@ -225,6 +226,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->opt_seed_rows = (uint32_t)value;
   } else if (!strcmp(name, "seed_ppl")) {  // probes per list from which the seed runs
     ctx->opt_seed_ppl = (float)value;
+  } else if (!strcmp(name, "coarse_tc")) {  // 1: tensor-core coarse distances (fp16 centroid copy)
+    ctx->opt_coarse_tc = value != 0;
   } else if (!strcmp(name, "filter_h16")) {  // 1: fp16 filter copy built at index finish and used
     ctx->opt_h16 = value != 0;
   } else if (!strcmp(name, "seg_rows")) {  // 0: automatic (auto_seg_rows)
@@ -315,6 +318,7 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
   s.scan_kernel = ctx->last_kind;
   s.scan_group = ctx->last_group;
   s.scan_filter_bits = ctx->last_filter_bits;
+  s.coarse_filter_bits = ctx->last_coarse_bits;
   *out = s;
   return HIVF_OK;
 }
@@ -322,6 +326,33 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out) {
 // ---------------------------------------------------------------------------
 // index build
 // ---------------------------------------------------------------------------
+
+// fp16 centroid copy for the tensor-core coarse pass (scan_tc.cu,
+// k_coarse_dist_tc): one power-of-2 scale from the largest centroid norm
+// bound.  Optional: without it (scale out of range, no memory) the coarse
+// distances stay on the FFMA pass.
+static void build_coarse_h16(hivf_index* ix) {
+  std::vector<float> cn(ix->K);
+  if (cudaMemcpy(cn.data(), ix->cnorm, ix->K * 4ull, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  float cmax = 0.f;
+  for (float v : cn) cmax = std::max(cmax, v);
+  const int e = h16_exp(cmax);
+  if (e < -kH16ExpMax || e > kH16ExpMax) return;
+  const float csc = std::ldexp(1.f, -e);
+  uint8_t* d = nullptr;
+  if (cudaMalloc(&d, coarse_tc_bytes(ix->K, ix->dpad)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return;
+  }
+  launch_pack_coarse_tc(ix->cent, ix->K, ix->dpad, nullptr, csc, d, ix->ctx->stream);
+  if (cudaStreamSynchronize(ix->ctx->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    cudaFree(d);
+    return;
+  }
+  ix->centh = d;
+  ix->csc = csc;
+  ix->cmax = cmax;
+}
 
 hivf_status hivf_index_begin(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n_clusters,
                              const float* centroids, int centroids_on_device,
@@ -410,6 +441,7 @@ hivf_status hivf_index_begin(hivf_ctx* ctx, uint32_t dim, int metric, uint32_t n
   if (tmp) cudaFree(tmp);
   if (e != cudaSuccess) return bail(e, "pack centroids");
   if ((e = cudaGetLastError()) != cudaSuccess) return bail(e, "pack centroids launch");
+  if (ctx->opt_coarse_tc && ctx->tc_conv <= 1) build_coarse_h16(ix);
   *out = ix;
   return HIVF_OK;
 }
@@ -478,10 +510,13 @@ hivf_status hivf_index_get_rows(hivf_index* ix, uint64_t first_row, uint64_t n_r
 
 // fp16 filter copy: per-list power-of-2 scale
 // from the list's norm bound, then the rows rounded to fp16 in the scan layout.
-// Optional: not for tiered (host-backed) indexes, and skipped -- the scan then
-// reads the fp32 lists -- when a list's scale is out of range or HBM is short.
+// Optional: skipped -- the scan then reads the fp32 lists -- when a list's
+// scale is out of range or HBM is short.  Tiered (host-backed) indexes keep
+// the WHOLE filter copy in HBM (half the fp32 bytes, outside hbm_list_budget):
+// every scan streams from HBM, and only the exact re-rank / repair / fallback
+// reads of cold lists' fp32 rows cross PCIe ("two lanes").
 static void build_h16(hivf_index* ix) {
-  if (ix->tiered || ix->N == 0) return;
+  if (ix->N == 0) return;
   cudaStream_t s = ix->ctx->stream;
   std::vector<float> mx(ix->K);
   if (cudaMemcpy(mx.data(), ix->maxnorm_bits, ix->K * 4ull, cudaMemcpyDeviceToHost) != cudaSuccess) return;
@@ -766,17 +801,30 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
     CK(launch_coarse_all(v, qv, nprobe, c->plans.as<uint32_t>(), d_dists, c->coarse_all.p, &need, c->stream));
     CK(cudaMemsetAsync(c->flags_c.p, 0, (size_t)qv.n * 4, c->stream));
     c->stats.kernels_launched += 4;
+    c->last_coarse_bits = 0;
     return HIVF_OK;
   }
-  const uint32_t splits = coarse_dist_splits(v, qv.n);
+  const uint32_t splits = (ix->centh && c->opt_coarse_tc) ? 1u : coarse_dist_splits(v, qv.n);
   float* part = nullptr;
   if (splits > 1) {
     CK(c->coarse_part.ensure((size_t)splits * qv.n * ix->K * 4));
     part = c->coarse_part.as<float>();
   }
-  launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream, part);
+  CoarseBound bd = coarse_bound_ffma(ix->dim);
+  if (ix->centh && c->opt_coarse_tc) {
+    // tensor-core pass: the batch's fp16 query copy, then one kind::f16 GEMM
+    CK(c->qh16.ensure(coarse_tc_bytes(qv.n, ix->dpad)));
+    launch_pack_coarse_tc(qv.qs, qv.n, ix->dpad, qv.qsc, 0.f, c->qh16.as<uint8_t>(), c->stream);
+    CKL();
+    launch_coarse_dist_tc(v, qv, ix->centh, ix->csc, c->qh16.as<uint8_t>(), c->dist32.as<float>(), c->stream);
+    bd = coarse_bound_h16(ix->dim, ix->cmax);
+    c->last_coarse_bits = 16;
+  } else {
+    c->last_coarse_bits = 32;
+    launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream, part);
+  }
   CKL();
-  launch_coarse_select(v, qv, c->dist32.as<float>(), nprobe, c->plans.as<uint32_t>(), d_dists,
+  launch_coarse_select(v, qv, c->dist32.as<float>(), nprobe, bd, c->plans.as<uint32_t>(), d_dists,
                        c->flags_c.as<int>(), c->stream);
   CKL();
   launch_coarse_fallback(v, qv, nprobe, c->plans.as<uint32_t>(), d_dists, c->flags_c.as<int>(), c->stream);

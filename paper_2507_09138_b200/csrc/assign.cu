@@ -14,6 +14,7 @@
 // order and are sorted by (distance, id).  Degenerate inputs (more than
 // kCandCap candidates) take an exact streaming path over all K.
 #include <cfloat>
+#include <cmath>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
 
@@ -197,9 +198,9 @@ __global__ void k_coarse_combine(IndexView ix, QueryView qv, const float* __rest
   }
 }
 
-__device__ __forceinline__ float bound_E(double eps, double ab, float qn, float cn) {
-  const double m = (double)qn + (double)cn;
-  return __double2float_ru(eps * m * m + ab);
+__device__ __forceinline__ float bound_E(const CoarseBound& bd, float qn, float cn) {
+  const double q = qn, c = cn;
+  return __double2float_ru(bd.ea * q * c + bd.eb * (q * q + c * c) + bd.ec + bd.es * q);
 }
 
 // Block-wide radix select: the `want`-th smallest (1-based) of n keys
@@ -283,7 +284,7 @@ __device__ void block_sort_pairs(double* d, uint32_t* id, uint32_t n) {
 // One CTA (512 threads) per query.
 __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView qv,
                                                        const float* __restrict__ dist32,
-                                                       uint32_t nprobe, double eps, double ab,
+                                                       uint32_t nprobe, CoarseBound bd,
                                                        uint32_t* __restrict__ plans,
                                                        double* __restrict__ dists, int* flags) {
   pdl_wait();
@@ -299,12 +300,12 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
   for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)b * ix.dpad + d];
   if (threadIdx.x == 0) s_cnt = 0;
   auto ub_key = [&](uint32_t c) {
-    return f2key(__fadd_ru(row[c], bound_E(eps, ab, qn, ix.cnorm[c])));
+    return f2key(__fadd_ru(row[c], bound_E(bd, qn, ix.cnorm[c])));
   };
   const uint32_t tau_key = block_radix_select(ix.K, nprobe, ub_key, hist);
   const float tau = key2f(tau_key);
   for (uint32_t c = threadIdx.x; c < ix.K; c += blockDim.x) {
-    const float lb = __fsub_rd(row[c], bound_E(eps, ab, qn, ix.cnorm[c]));
+    const float lb = __fsub_rd(row[c], bound_E(bd, qn, ix.cnorm[c]));
     if (lb <= tau) {
       const uint32_t pos = atomicAdd(&s_cnt, 1u);
       if (pos < kCandCap) cid[pos] = c;
@@ -481,16 +482,32 @@ void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32,
     launch_pdl(k_coarse_dist<32>, dim3(dim3((ix.K + 31) / 32, qt)), dim3(64), 0, s, ix, qv, dist32, 0u);
 }
 
+// eps (|q| + |c|)^2 + abs, expanded
+CoarseBound coarse_bound_ffma(uint32_t dim) {
+  const double e = filter_eps(dim);
+  return {2.0 * e, e, filter_abs(dim), 0.0};
+}
+// bound_h16 with x = the centroid (its own norm bound cnorm[c]); bound_h16's
+// subnormal floor 2 sqrt(D) 2^-38 |x||q| is relative to the norm the SCALE was
+// taken from -- here the largest centroid norm cmax, shared by all centroids --
+// so that term is added with cmax (x1.5 headroom and the factor 2 of the
+// distance, as bound_h16 carries it).
+CoarseBound coarse_bound_h16(uint32_t dim, float cmax) {
+  CoarseBound b{};
+  bound_h16(dim, &b.ea, &b.eb, &b.ec);
+  b.es = 1.5 * 2.0 * 2.0 * std::sqrt((double)dim) * 0x1p-38 * 1.01 * (double)cmax;
+  return b;
+}
+
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
-                          uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
+                          uint32_t nprobe, const CoarseBound& bd, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s) {
   const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 8;
   smem_optin((const void*)k_coarse_select, 220 * 1024);
   smem_optin((const void*)k_coarse_fallback, 200 * 1024);
   // 512 threads: fewer (64-256, sized to the candidate count) measured slower
   // (C2 41 -> 61 us, C3 59 -> 75 us)
-  launch_pdl(k_coarse_select, dim3(qv.n), dim3(512), smem, s, ix, qv, dist32, nprobe, filter_eps(ix.dim),
-                                          filter_abs(ix.dim), plans, dists, flags);
+  launch_pdl(k_coarse_select, dim3(qv.n), dim3(512), smem, s, ix, qv, dist32, nprobe, bd, plans, dists, flags);
 }
 
 void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t nprobe,

@@ -112,6 +112,10 @@ struct hivf_ctx {
   // fp16 filter copy (option "filter_h16"): built at index finish when 1 and
   // used by the single-pass tensor-core scan while 1
   int opt_h16 = 1;
+  // coarse distances on the tensor cores (option "coarse_tc", env HIVF_COARSE_TC):
+  // kind::f16 over fp16 copies of centroids and queries, used while 1 by
+  // indexes that have the centroid copy (built at index creation when 1)
+  int opt_coarse_tc = 1;
   // drop-bound seed (launch_seed_bounds): rows per query, and the batch density
   // (pairs per list) from which it runs
   uint32_t opt_seed_rows = 32;
@@ -131,7 +135,7 @@ struct hivf_ctx {
   DBuf qs, qn2, qnorm, qsc, err, dist32, plans, pdists, flags_c, flags_f, pq, pl, list_cnt, list_poff,
       list_cur, list_ioff, sorted_pairs, items, n_items, work_ctr, cand_d, cand_row, cand_thr,
       cand_n, out_ids, qin, x_ids, x_d, x_cnt, x_tot, tau, flags2, qbound, rep_entries, rep_n, rep_cnt,
-      rep_d, rep_ids, qshift, qwide, coarse_all, coarse_part;
+      rep_d, rep_ids, qshift, qwide, coarse_all, coarse_part, qh16;
   HBuf hstage;
   hivf_stats stats{};
   uint32_t last_nq = 0;
@@ -140,6 +144,7 @@ struct hivf_ctx {
   uint32_t last_kind = 0;
   uint32_t last_group = 0;  // queries per scan work item of the last scan
   uint32_t last_filter_bits = 32;  // 16: the last scan read the fp16 filter copy
+  uint32_t last_coarse_bits = 32;  // 16: the last coarse assign ran on the tensor cores
   bool stats_adapted = false;
   // phase timing (option "time_kernels"): one event set per call, resolved lazily
   int opt_time = 0;
@@ -222,6 +227,10 @@ struct hivf_index {
   float* cent = nullptr;
   float* cnorm2 = nullptr;
   float* cnorm = nullptr;
+  // fp16 centroid copy for the tensor-core coarse pass (nullptr: FFMA pass):
+  // tile layout of launch_pack_coarse_tc, shared unscale 2^-e_c, largest norm bound
+  uint8_t* centh = nullptr;
+  float csc = 0.f, cmax = 0.f;
   uint32_t* list_order = nullptr;
   int* d_err = nullptr;
   uint64_t rows_added = 0;
@@ -290,7 +299,7 @@ struct hivf_index {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (tiered && vec) cudaFreeHost(vec);
     else if (vec) cudaFree(vec);
-    for (void* p : {(void*)vech, (void*)lsc, (void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
+    for (void* p : {(void*)centh, (void*)vech, (void*)lsc, (void*)ids, (void*)xnorm2, (void*)d_list_off, (void*)maxnorm_bits, (void*)cent,
                     (void*)cnorm2, (void*)cnorm, (void*)list_order, (void*)d_err, (void*)pool,
                     (void*)d_list_ptr, (void*)loc_ids, (void*)loc_rows})
       if (p) cudaFree(p);

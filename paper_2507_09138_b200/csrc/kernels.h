@@ -184,9 +184,26 @@ void launch_pack_h16(const float* vec, const uint64_t* d_list_off, uint32_t K, u
 uint32_t coarse_dist_splits(const IndexView& ix, uint32_t n_queries);
 void launch_coarse_dist(const IndexView& ix, const QueryView& qv, float* dist32, cudaStream_t s,
                         float* part = nullptr);
+// Filter bound of the coarse distances: |d^ - delta| <= ea |q||c| + eb (|q|^2 + |c|^2)
+// + ec + es |q| (rounded up).  FFMA pass: the fp32 filter's eps (coarse_bound_ffma);
+// tensor-core pass: bound_h16 + the fp16 subnormal floor of the shared centroid
+// scale (coarse_bound_h16).
+struct CoarseBound {
+  double ea, eb, ec, es;
+};
+CoarseBound coarse_bound_ffma(uint32_t dim);
+CoarseBound coarse_bound_h16(uint32_t dim, float cmax);
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
-                          uint32_t nprobe, uint32_t* plans, double* dists, int* flags,
+                          uint32_t nprobe, const CoarseBound& bd, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s);
+// ---- scan_tc.cu: coarse distances on the tensor cores (kind::f16 GEMM over
+// fp16 copies of the centroids and the queries in a 128-row tile layout)
+uint32_t coarse_tc_stages(uint32_t dpad);
+uint64_t coarse_tc_bytes(uint32_t rows, uint32_t dpad);
+void launch_pack_coarse_tc(const float* src, uint32_t n, uint32_t dpad, const float* rsc, float sc, uint8_t* dst,
+                           cudaStream_t s);
+void launch_coarse_dist_tc(const IndexView& ix, const QueryView& qv, const uint8_t* cent_h16, float csc,
+                           const uint8_t* q_h16, float* dist32, cudaStream_t s);
 cudaError_t launch_coarse_all(const IndexView& ix, const QueryView& qv, uint32_t nprobe, uint32_t* plans,
                               double* dists, void* scratch, size_t* scratch_bytes, cudaStream_t s);
 void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t nprobe,

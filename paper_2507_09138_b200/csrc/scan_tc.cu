@@ -2538,3 +2538,187 @@ extern "C" int hivf_debug_bound(int kind, unsigned D, double* e_a, double* e_b, 
 extern "C" int hivf_debug_tc_prof(unsigned long long* out, int n_ctas) {
   return hivf::get_tc_prof(out, n_ctas);
 }
+
+// ===========================================================================
+// Coarse assign on the tensor cores: the distance pass of ivf::select_clusters
+// (/root/reference/proj/src/vector_index.cpp:266-273) for all B x K (query,
+// centroid) pairs as one kind::f16 GEMM over fp16 copies of the centroids and
+// the queries, scaled by powers of two exactly like the fp16 filter copy
+// (DESIGN.md 3a): the centroids share one scale (from the largest centroid
+// norm), each query has its own (qsc, k_prep_queries).  d^ = fma(-2 2^-(e_q+e_c),
+// acc, |c|^2 + |q|^2) -- the scan's fp16 distance, so the scan's bound
+// (bound_h16) holds with x = the centroid; k_coarse_select then filters with it
+// and re-ranks every candidate in the reference's exact double arithmetic, so
+// plans are bit-identical to the FFMA pass (only the candidate superset differs).
+//
+// Tile: 128 centroids (M, TMEM lanes) x 128 queries (N, TMEM columns); 64-dim
+// pipeline stages (two 32-dim SWIZZLE_64B chunk planes per operand, 16 KB
+// each) in a 3-deep ring, one bulk copy per operand per stage.  192 threads:
+// warp 0 producer, warp 1 TMEM allocator + MMA issuer, warps 2-5 epilogue
+// (warp w reads TMEM lane quadrant w % 4).  96 KB of smem: 2 CTAs per SM,
+// so one tile's epilogue overlaps the other's loads.
+// ===========================================================================
+namespace hivf {
+namespace {
+constexpr uint32_t kCdTile = 128;                          // centroids / queries per tile
+constexpr uint32_t kCdCps = 2;                             // 32-dim chunks per stage
+constexpr uint32_t kCdStageDims = kCdCps * 32;             // 64
+constexpr uint32_t kCdOpBytes = kCdTile * kCdStageDims * 2;  // 16 KB per operand per stage
+constexpr uint32_t kCdRing = 3;
+constexpr uint32_t kCdSmem = kCdRing * 2 * kCdOpBytes + 1024 + 128;
+
+// byte offset of the 16-B granule holding dims [d, d + 8) of row r of a tile
+// (layout [tile][stage][chunk][row 0..127][64 B, SWIZZLE_64B: granule g at g ^ ((r >> 1) & 3)])
+__device__ __forceinline__ uint64_t cd_offset(uint32_t tile, uint32_t S, uint32_t r, uint32_t d) {
+  const uint32_t s = d / kCdStageDims, j = (d % kCdStageDims) / 32, g = (d % 32) / 8;
+  return (((uint64_t)tile * S + s) * kCdCps + j) * (kCdTile * 64) + r * 64 + ((g ^ ((r >> 1) & 3u)) << 4);
+}
+
+// rows [0, n_pad) x dims [0, 64 S) of src ([n][dpad] fp32, zero past n / dpad),
+// scaled by 2^e (1 / unscale; per row when rsc != nullptr, else 1 / sc) and
+// rounded to fp16, into the tile layout.  One thread per 16-B granule.
+__global__ void k_pack_cd(const float* __restrict__ src, uint32_t n, uint32_t dpad, uint32_t S, uint32_t n_pad,
+                          const float* __restrict__ rsc, float sc, uint8_t* __restrict__ dst) {
+  pdl_wait();
+  const uint32_t gpr = S * kCdStageDims / 8;
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (uint64_t)n_pad * gpr) return;
+  const uint32_t row = (uint32_t)(gid / gpr), d = (uint32_t)(gid % gpr) * 8;
+  float up = 1.f;
+  if (row < n) {
+    const float u = rsc ? rsc[row] : sc;
+    up = u > 0.f ? 1.f / u : 1.f;  // out-of-range query: results discarded (k_coarse_dist_tc)
+  }
+  __align__(16) __half h[8];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < n && d + p * 4 < dpad) v = *reinterpret_cast<const float4*>(src + (uint64_t)row * dpad + d + p * 4);
+    h[p * 4 + 0] = __float2half_rn(v.x * up);
+    h[p * 4 + 1] = __float2half_rn(v.y * up);
+    h[p * 4 + 2] = __float2half_rn(v.z * up);
+    h[p * 4 + 3] = __float2half_rn(v.w * up);
+  }
+  *reinterpret_cast<uint4*>(dst + cd_offset(row / kCdTile, S, row % kCdTile, d)) = *reinterpret_cast<const uint4*>(h);
+}
+
+struct CdParams {
+  const uint8_t* a;     // centroid copy (tile layout)
+  const uint8_t* b;     // query copy (tile layout)
+  const float* cnorm2;  // [K]
+  const float* qn2;     // [n]
+  const float* qsc;     // [n] 2^-e_q (0: out of range)
+  float csc;            // 2^-e_c
+  float* out;           // [n][K]
+  uint32_t K, n, S;
+};
+
+__global__ void __launch_bounds__(192, 1) k_coarse_dist_tc(CdParams P) {
+  pdl_wait();
+  extern __shared__ uint8_t cd_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(cd_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kCdRing * 2 * kCdOpBytes);
+  uint64_t* empty = full + kCdRing;
+  uint64_t* accf = empty + kCdRing;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(accf + 1);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t ct = blockIdx.x, qt = blockIdx.y, S = P.S;
+  if (tid == 0) {
+    for (uint32_t i = 0; i < kCdRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(accf, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "r"(kCdTile));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  auto stage_a = [&](uint32_t slot) { return sm + slot * 2 * kCdOpBytes; };
+  auto stage_b = [&](uint32_t slot) { return sm + slot * 2 * kCdOpBytes + kCdOpBytes; };
+  if (warp == 0) {
+    if (lane == 0) {
+      for (uint32_t s = 0; s < S; ++s) {
+        const uint32_t slot = s % kCdRing;
+        if (s >= kCdRing) mbar_wait(&empty[slot], ((s / kCdRing) - 1) & 1);
+        mbar_arrive_expect_tx(&full[slot], 2 * kCdOpBytes);
+        bulk_g2s(stage_a(slot), P.a + ((uint64_t)ct * S + s) * kCdOpBytes, kCdOpBytes, &full[slot]);
+        bulk_g2s(stage_b(slot), P.b + ((uint64_t)qt * S + s) * kCdOpBytes, kCdOpBytes, &full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = f16_idesc_m(kCdTile, kCdTile);
+    for (uint32_t s = 0; s < S; ++s) {
+      const uint32_t slot = s % kCdRing;
+      mbar_wait(&full[slot], (s / kCdRing) & 1);
+      tc_fence_after();
+      // chunk planes are 8 KB apart in both operands (+512 in 16-B descriptor units)
+      mma_stage8_f16(tmem, sw64_kmajor_desc(smem_u32(stage_a(slot))), sw64_kmajor_desc(smem_u32(stage_b(slot))),
+                     idesc, s > 0 ? 1u : 0u, kCdCps, 512u);
+      mma_commit_elect(&empty[slot]);
+    }
+    mma_commit_elect(accf);
+  } else {
+    mbar_wait_parked(accf, 0);
+    tc_fence_after();
+    const uint32_t quad = warp & 3;
+    const uint32_t c = ct * kCdTile + quad * 32 + lane;
+    const float cn2 = c < P.K ? P.cnorm2[c] : 0.f;
+#pragma unroll 1
+    for (uint32_t j = 0; j < kCdTile / 32; ++j) {
+      const uint32_t q0 = qt * kCdTile + j * 32;
+      if (q0 >= P.n) break;
+      uint32_t r[32];
+      TMEM_LD32(tmem + ((quad * 32) << 16) + j * 32, r);
+      tmem_wait_ld();
+      if (c < P.K) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t q = q0 + i;
+          if (q < P.n) {
+            const float qs = P.qsc[q];
+            // out-of-range query scale: +inf everywhere sends it to the exact path
+            P.out[(uint64_t)q * P.K + c] =
+                qs > 0.f ? __fmaf_rn(-2.f * qs * P.csc, __uint_as_float(r[i]), __fadd_rn(cn2, P.qn2[q])) : kInfF;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCdTile));
+  }
+}
+}  // namespace
+
+uint32_t coarse_tc_stages(uint32_t dpad) { return (dpad + kCdStageDims - 1) / kCdStageDims; }
+uint64_t coarse_tc_bytes(uint32_t rows, uint32_t dpad) {
+  return (uint64_t)((rows + kCdTile - 1) / kCdTile) * kCdTile * coarse_tc_stages(dpad) * kCdStageDims * 2;
+}
+
+void launch_pack_coarse_tc(const float* src, uint32_t n, uint32_t dpad, const float* rsc, float sc, uint8_t* dst,
+                           cudaStream_t s) {
+  const uint32_t S = coarse_tc_stages(dpad), n_pad = (n + kCdTile - 1) / kCdTile * kCdTile;
+  const uint64_t total = (uint64_t)n_pad * S * kCdStageDims / 8;
+  if (!total) return;
+  launch_pdl(k_pack_cd, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, src, n, dpad, S, n_pad, rsc, sc, dst);
+}
+
+void launch_coarse_dist_tc(const IndexView& ix, const QueryView& qv, const uint8_t* cent_h16, float csc,
+                           const uint8_t* q_h16, float* dist32, cudaStream_t s) {
+  if (!qv.n) return;
+  smem_optin((const void*)k_coarse_dist_tc, kCdSmem);
+  CdParams P{cent_h16, q_h16, ix.cnorm2, qv.qn2, qv.qsc, csc, dist32, ix.K, qv.n, coarse_tc_stages(ix.dpad)};
+  launch_pdl(k_coarse_dist_tc, dim3((ix.K + kCdTile - 1) / kCdTile, (qv.n + kCdTile - 1) / kCdTile), dim3(192),
+             (size_t)kCdSmem, s, P);
+}
+}  // namespace hivf

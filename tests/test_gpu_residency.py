@@ -12,7 +12,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def _setup(budget_frac, seed=3, n=30000, dim=96, K=64):
+def _setup(budget_frac, seed=3, n=30000, dim=96, K=64, options=()):
     import torch
     from paper_2507_09138_b200 import Context, IvfIndex
     rng = np.random.default_rng(seed)
@@ -25,6 +25,8 @@ def _setup(budget_frac, seed=3, n=30000, dim=96, K=64):
     ctx = Context(0, torch.cuda.current_stream())
     total = int(csr.vectors.shape[0]) * ((dim + 15) // 16 * 16) * 4
     ctx.set_option("hbm_list_budget", max(1, int(total * budget_frac)))
+    for name, value in options:
+        ctx.set_option(name, value)
     ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
     Q = (centers[rng.integers(0, 24, 40)] + 0.3 * rng.standard_normal((40, dim))).astype(np.float32)
     return ctx, ix, csr, Q
@@ -89,3 +91,25 @@ def test_tiered_node_split_sub_search():
     for b in range(B):
         assert np.array_equal(hi[b, :hn[b]], oi[b, :oc[b]])
         assert np.array_equal(hd[b, :hn[b]].view(np.uint64), od[b, :oc[b]].view(np.uint64))
+
+
+@pytest.mark.parametrize("h16", [1, 0])
+def test_tiered_two_lanes_fp16_filter_in_hbm(h16):
+    """Tiered index with the fp16 filter copy: the copy of EVERY
+    list stays in HBM, so the tensor-core scan never reads the host backing
+    store; only the exact re-rank of candidates (and repair / fallback) reads
+    cold lists' fp32 rows over PCIe.  Without the copy the scan streams the
+    cold fp32 lists from host memory.  Both give the reference's bits, with
+    nothing, part or all of the exact rows resident."""
+    ctx, ix, csr, Q = _setup(0.3, seed=5, options=(("filter_h16", h16), ("scan_kernel", 3)))
+    _same(ix, csr, Q)
+    st = ctx.stats()
+    assert st["scan_kernel"] == 3 and st["scan_filter_bits"] == (16 if h16 else 32), st
+    plans = ix.select_clusters(Q, 10)
+    hot = np.argsort(-np.bincount(plans.ravel(), minlength=64), kind="stable").astype(np.uint32)
+    ix.set_residency(hot)
+    ix.residency_sync()
+    assert ix.residency().any()
+    _same(ix, csr, Q)
+    _same(ix, csr, Q, nprobe=64, k=20)
+    assert ctx.stats()["scan_filter_bits"] == (16 if h16 else 32)
