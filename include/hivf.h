@@ -364,8 +364,14 @@ typedef struct {
 } hivf_stats;
 hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
 /* Options (0 = default): "seg_rows" rows per scan segment, "force_exact",
- * "hbm_list_budget" (bytes of list storage an index may keep in HBM; the
- * rest stays in pinned host memory, see residency),
+ * "hbm_list_budget" (bytes of fp32 list storage an index may keep in HBM; the
+ * rest stays in pinned host memory, see residency; with "filter_h16" the fp16
+ * filter copy of EVERY list is kept in HBM on top of the budget, so the scan
+ * never crosses PCIe -- only the exact re-rank of cold lists' rows does),
+ * "coarse_tc" (default 1: indexes created while 1 get an fp16 copy of the
+ * centroids and the coarse assign's distance pass runs as one tcgen05
+ * kind::f16 GEMM, filtered with the fp16 bound; 0: FFMA pass; plans identical;
+ * process default from env HIVF_COARSE_TC),
  * "seed_rows" (default 32, 0 = off, <= 64) / "seed_ppl" (default 16): batches
  * with at least seed_ppl probes per list seed each query's shared drop bound
  * with the exact distances of seed_rows rows of its nearest probed list,
