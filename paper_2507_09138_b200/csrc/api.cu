@@ -179,6 +179,7 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
   // scan on the fp32 lists, e.g. the whole GPU suite on that path)
   if (const char* e = getenv("HIVF_FILTER_H16")) c->opt_h16 = atoi(e) != 0;
   if (const char* e = getenv("HIVF_COARSE_TC")) c->opt_coarse_tc = atoi(e) != 0;
+  if (const char* e = getenv("HIVF_COARSE_SET")) c->opt_coarse_set = atoi(e) != 0;
   *out = c;
   return HIVF_OK;
 }
@@ -226,6 +227,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->opt_seed_rows = (uint32_t)value;
   } else if (!strcmp(name, "seed_ppl")) {  // probes per list from which the seed runs
     ctx->opt_seed_ppl = (float)value;
+  } else if (!strcmp(name, "coarse_set")) {  // 1: the search's coarse select re-ranks only its uncertain band
+    ctx->opt_coarse_set = value != 0;
   } else if (!strcmp(name, "coarse_tc")) {  // 1: tensor-core coarse distances (fp16 centroid copy)
     ctx->opt_coarse_tc = value != 0;
   } else if (!strcmp(name, "filter_h16")) {  // 1: fp16 filter copy built at index finish and used
@@ -785,7 +788,10 @@ static hivf_status prep_queries(hivf_index* ix, const float* d_q, uint32_t n, bo
   return HIVF_OK;
 }
 
-static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t nprobe, double* d_dists) {
+// set_mode: the caller needs the plans only as sets (the batched search):
+// k_coarse_select then re-ranks only the centroids its bound cannot place
+static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t nprobe, double* d_dists,
+                              bool set_mode = false) {
   hivf_ctx* c = ix->ctx;
   const IndexView v = ix->view();
   CK(c->dist32.ensure((size_t)qv.n * ix->K * 4));
@@ -825,7 +831,7 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
   }
   CKL();
   launch_coarse_select(v, qv, c->dist32.as<float>(), nprobe, bd, c->plans.as<uint32_t>(), d_dists,
-                       c->flags_c.as<int>(), c->stream);
+                       c->flags_c.as<int>(), c->stream, set_mode && c->opt_coarse_set);
   CKL();
   launch_coarse_fallback(v, qv, nprobe, c->plans.as<uint32_t>(), d_dists, c->flags_c.as<int>(), c->stream);
   CKL();
@@ -969,7 +975,7 @@ static hivf_status search_impl(hivf_index* ix, const float* d_queries, uint32_t 
   if ((st = prep_queries(ix, d_queries, n, true, &qv)) != HIVF_OK) return st;
   const uint32_t np = n * nprobe;
   if (!d_plans) {
-    if ((st = run_assign(ix, qv, nprobe, nullptr)) != HIVF_OK) return st;
+    if ((st = run_assign(ix, qv, nprobe, nullptr, true)) != HIVF_OK) return st;
   } else {
     CK(c->plans.ensure((size_t)np * 4));
     CK(c->flags_c.ensure((size_t)n * 4));  // no coarse fallback in a planned search

@@ -198,10 +198,6 @@ __global__ void k_coarse_combine(IndexView ix, QueryView qv, const float* __rest
   }
 }
 
-__device__ __forceinline__ float bound_E(const CoarseBound& bd, float qn, float cn) {
-  const double q = qn, c = cn;
-  return __double2float_ru(bd.ea * q * c + bd.eb * (q * q + c * c) + bd.ec + bd.es * q);
-}
 
 // Block-wide radix select: the `want`-th smallest (1-based) of n keys
 // produced by key_of(i).  512 threads.
@@ -286,34 +282,68 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
                                                        const float* __restrict__ dist32,
                                                        uint32_t nprobe, CoarseBound bd,
                                                        uint32_t* __restrict__ plans,
-                                                       double* __restrict__ dists, int* flags) {
+                                                       double* __restrict__ dists, int* flags,
+                                                       uint32_t set_mode) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   double* cd = reinterpret_cast<double*>(sm);                       // kCandCap
   uint32_t* cid = reinterpret_cast<uint32_t*>(cd + kCandCap);         // kCandCap
   double* qsh = reinterpret_cast<double*>(cid + kCandCap);            // dpad (widened once)
   __shared__ uint32_t hist[256];
-  __shared__ uint32_t s_cnt;
+  __shared__ uint32_t s_cnt, s_ns, s_wcnt[16];
+  __shared__ unsigned long long s_min;
   const uint32_t b = blockIdx.x;
   const float* row = dist32 + (uint64_t)b * ix.K;
   const float qn = qv.qnorm[b];
   for (uint32_t d = threadIdx.x; d < ix.dpad; d += blockDim.x) qsh[d] = qv.qs[(uint64_t)b * ix.dpad + d];
-  if (threadIdx.x == 0) s_cnt = 0;
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_ns = 0;
+    s_min = ~0ull;
+  }
+  // E(c) = ea q c + eb (q^2 + c^2) + ec + es q = c (c B + A) + C with the
+  // query's constants rounded up once: two round-up fp32 FMAs per key (every
+  // term is >= 0, so each rounding up keeps an upper bound) instead of the
+  // double evaluation per key and radix pass (fp64 issues at ~1/30 the rate)
+  const double qd = qn;
+  const float cA = __double2float_ru(bd.ea * qd), cB = __double2float_ru(bd.eb),
+              cC = __double2float_ru(bd.eb * qd * qd + bd.ec + bd.es * qd);
+  auto bound_E = [&](const CoarseBound&, float, float cn) { return __fmaf_ru(cn, __fmaf_ru(cn, cB, cA), cC); };
   auto ub_key = [&](uint32_t c) {
     return f2key(__fadd_ru(row[c], bound_E(bd, qn, ix.cnorm[c])));
   };
   const uint32_t tau_key = block_radix_select(ix.K, nprobe, ub_key, hist);
   const float tau = key2f(tau_key);
+  // Set mode (the search path: plan order and plan distances unused): L = the
+  // nprobe-th smallest LOWER bound.  A centroid with ub < L is in the top
+  // nprobe for sure -- every centroid at or before it in (d, id) order has
+  // lb <= d <= ub < L, and at most nprobe - 1 centroids have lb < L -- so only
+  // the uncertain band (lb <= tau, ub >= L) needs the exact double; the plan
+  // is the sure set plus the best (nprobe - |sure|) of the band by (d, id),
+  // which is the reference's top-nprobe as a set.
+  float L = -FLT_MAX;
+  if (set_mode) {
+    auto lb_key = [&](uint32_t c) {
+      return f2key(__fsub_rd(row[c], bound_E(bd, qn, ix.cnorm[c])));
+    };
+    L = key2f(block_radix_select(ix.K, nprobe, lb_key, hist));
+  }
   for (uint32_t c = threadIdx.x; c < ix.K; c += blockDim.x) {
-    const float lb = __fsub_rd(row[c], bound_E(bd, qn, ix.cnorm[c]));
+    const float E = bound_E(bd, qn, ix.cnorm[c]);
+    const float lb = __fsub_rd(row[c], E);
     if (lb <= tau) {
-      const uint32_t pos = atomicAdd(&s_cnt, 1u);
-      if (pos < kCandCap) cid[pos] = c;
+      if (set_mode && __fadd_ru(row[c], E) < L) {  // sure
+        atomicAdd(&s_ns, 1u);
+        atomicMin(&s_min, ((unsigned long long)f2key(row[c]) << 32) | c);
+      } else {
+        const uint32_t pos = atomicAdd(&s_cnt, 1u);
+        if (pos < kCandCap) cid[pos] = c;
+      }
     }
   }
   __syncthreads();
-  const uint32_t m = s_cnt;
-  if (m > kCandCap || !(tau <= FLT_MAX)) {  // degenerate: exact streaming path
+  const uint32_t m = s_cnt, ns = s_ns;
+  if (m > kCandCap || !(tau <= FLT_MAX) || ns > nprobe || m + ns < nprobe) {  // degenerate: exact streaming path
     if (threadIdx.x == 0) flags[b] = 1;
     return;
   }
@@ -335,9 +365,40 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
     cid[i] = 0xffffffffu;
   }
   block_sort_pairs(cd, cid, mp);
-  for (uint32_t i = threadIdx.x; i < nprobe; i += blockDim.x) {
-    plans[(uint64_t)b * nprobe + i] = cid[i];
-    if (dists) dists[(uint64_t)b * nprobe + i] = cd[i];
+  if (ns == 0) {
+    for (uint32_t i = threadIdx.x; i < nprobe; i += blockDim.x) {
+      plans[(uint64_t)b * nprobe + i] = cid[i];
+      if (dists) dists[(uint64_t)b * nprobe + i] = cd[i];
+    }
+  } else {
+    // set mode: the sure centroid with the smallest d^ first (the likely
+    // nearest list, which the drop-bound seed reads), the other sure ones in
+    // id order (deterministic), then the band's best by (d, id)
+    uint32_t* out = plans + (uint64_t)b * nprobe;
+    const uint32_t cmin = (uint32_t)(s_min & 0xffffffffu);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t base_pos = 1;
+    for (uint32_t base = 0; base < ix.K; base += blockDim.x) {
+      const uint32_t c = base + threadIdx.x;
+      bool sure = false;
+      if (c < ix.K && c != cmin) {
+        const float E = bound_E(bd, qn, ix.cnorm[c]);
+        sure = __fsub_rd(row[c], E) <= tau && __fadd_ru(row[c], E) < L;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, sure);
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      uint32_t before = base_pos, total = base_pos;
+      for (uint32_t w = 0; w < nw; ++w) {
+        if (w < warp) before += s_wcnt[w];
+        total += s_wcnt[w];
+      }
+      if (sure) out[before + __popc(bal & ((1u << lane) - 1u))] = c;
+      base_pos = total;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = cmin;
+    for (uint32_t i = threadIdx.x; i < nprobe - ns; i += blockDim.x) out[ns + i] = cid[i];
   }
   if (threadIdx.x == 0) flags[b] = 0;
 }
@@ -501,13 +562,14 @@ CoarseBound coarse_bound_h16(uint32_t dim, float cmax) {
 
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
                           uint32_t nprobe, const CoarseBound& bd, uint32_t* plans, double* dists, int* flags,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool set_mode) {
   const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 8;
   smem_optin((const void*)k_coarse_select, 220 * 1024);
   smem_optin((const void*)k_coarse_fallback, 200 * 1024);
   // 512 threads: fewer (64-256, sized to the candidate count) measured slower
   // (C2 41 -> 61 us, C3 59 -> 75 us)
-  launch_pdl(k_coarse_select, dim3(qv.n), dim3(512), smem, s, ix, qv, dist32, nprobe, bd, plans, dists, flags);
+  launch_pdl(k_coarse_select, dim3(qv.n), dim3(512), smem, s, ix, qv, dist32, nprobe, bd, plans, dists, flags,
+             (set_mode && !dists) ? 1u : 0u);
 }
 
 void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t nprobe,

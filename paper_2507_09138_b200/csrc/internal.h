@@ -116,6 +116,9 @@ struct hivf_ctx {
   // kind::f16 over fp16 copies of centroids and queries, used while 1 by
   // indexes that have the centroid copy (built at index creation when 1)
   int opt_coarse_tc = 1;
+  // search path: coarse select in set mode (option "coarse_set", env
+  // HIVF_COARSE_SET): only centroids the bound cannot place get the exact double
+  int opt_coarse_set = 1;
   // drop-bound seed (launch_seed_bounds): rows per query, and the batch density
   // (pairs per list) from which it runs
   uint32_t opt_seed_rows = 32;

@@ -195,7 +195,7 @@ CoarseBound coarse_bound_ffma(uint32_t dim);
 CoarseBound coarse_bound_h16(uint32_t dim, float cmax);
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
                           uint32_t nprobe, const CoarseBound& bd, uint32_t* plans, double* dists, int* flags,
-                          cudaStream_t s);
+                          cudaStream_t s, bool set_mode = false);
 // ---- scan_tc.cu: coarse distances on the tensor cores (kind::f16 GEMM over
 // fp16 copies of the centroids and the queries in a 128-row tile layout)
 uint32_t coarse_tc_stages(uint32_t dpad);

@@ -101,3 +101,33 @@ def test_coarse_tc_search_equals_reference(torch_ok):
     np.testing.assert_array_equal(cnt, oc)
     np.testing.assert_array_equal(ids, oi)
     assert np.array_equal(d.view(np.uint64), od.view(np.uint64))
+
+
+@pytest.mark.parametrize("coarse_tc", [1, 0])
+def test_search_set_mode_duplicate_centroids(torch_ok, coarse_tc):
+    """The search's coarse select in set mode (sure centroids skip the exact
+    double): duplicated centroids put exact ties on the plan boundary (odd
+    nprobe splits a pair), where membership is decided by the lower id; the
+    lists differ, so a wrong member changes the results."""
+    rng = np.random.default_rng(23)
+    dim, K = 64, 64
+    base = rng.standard_normal((K // 2, dim)).astype(np.float32)
+    cents = np.concatenate([base, base])  # centroid i and i + 32 identical
+    X = (base[rng.integers(0, K // 2, 8000)] + 0.4 * rng.standard_normal((8000, dim))).astype(np.float32)
+    ids = np.arange(len(X), dtype=np.uint64) * 7 + 3
+    assign = rng.integers(0, K, len(X)).astype(np.uint32)  # any assignment is an index
+    csr = oracle.CsrIndex.from_assignments(X, ids, cents, assign)
+    from paper_2507_09138_b200 import Context, IvfIndex
+    ctx = Context(0)
+    ctx.set_option("coarse_tc", coarse_tc)
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
+    Q = (base[rng.integers(0, K // 2, 200)] + 0.4 * rng.standard_normal((200, dim))).astype(np.float32)
+    for nprobe, k in ((1, 10), (7, 10), (15, 5), (33, 20)):
+        for set_mode in (1, 0):
+            ctx.set_option("coarse_set", set_mode)
+            gi, gd, gc = ix.search(Q, nprobe, k)
+            oi, od, oc = csr.search(Q, nprobe, k)
+            np.testing.assert_array_equal(gc, oc)
+            np.testing.assert_array_equal(gi, oi)
+            assert np.array_equal(gd.view(np.uint64), od.view(np.uint64))
+    ctx.set_option("coarse_set", 1)
