@@ -358,23 +358,42 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
     const float4* crow = reinterpret_cast<const float4*>(ix.cent + (uint64_t)cid[i] * ix.dpad);
     cd[i] = exact_row_pipelined(ix.dim, qsh, [&](uint32_t g) { return __ldg(crow + g); });
   }
-  uint32_t mp = 1;
-  while (mp < m) mp <<= 1;
-  for (uint32_t i = m + threadIdx.x; i < mp; i += blockDim.x) {
-    cd[i] = DBL_MAX;
-    cid[i] = 0xffffffffu;
-  }
-  block_sort_pairs(cd, cid, mp);
-  if (ns == 0) {
-    for (uint32_t i = threadIdx.x; i < nprobe; i += blockDim.x) {
-      plans[(uint64_t)b * nprobe + i] = cid[i];
-      if (dists) dists[(uint64_t)b * nprobe + i] = cd[i];
+  // the band's best (nprobe - ns) by (d, id) -> plan positions [ns, nprobe)
+  const uint32_t take = nprobe - ns;
+  uint32_t* out = plans + (uint64_t)b * nprobe;
+  if (m <= blockDim.x) {
+    // rank placement: each candidate counts the candidates before it in
+    // (d, id) order (centroid ids are distinct, so ranks are) -- one barrier
+    // instead of the bitonic network's log^2 barriers (which dominated this
+    // kernel's stall samples)
+    __syncthreads();
+    if (threadIdx.x < m) {
+      const double di = cd[threadIdx.x];
+      const uint32_t ii = cid[threadIdx.x];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < m; ++j) r += pair_less(cd[j], cid[j], di, ii) ? 1u : 0u;
+      if (r < take) {
+        out[ns + r] = ii;
+        if (dists) dists[(uint64_t)b * nprobe + r] = di;
+      }
     }
   } else {
+    uint32_t mp = 1;
+    while (mp < m) mp <<= 1;
+    for (uint32_t i = m + threadIdx.x; i < mp; i += blockDim.x) {
+      cd[i] = DBL_MAX;
+      cid[i] = 0xffffffffu;
+    }
+    block_sort_pairs(cd, cid, mp);
+    for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
+      out[ns + i] = cid[i];
+      if (dists) dists[(uint64_t)b * nprobe + i] = cd[i];
+    }
+  }
+  if (ns > 0) {
     // set mode: the sure centroid with the smallest d^ first (the likely
     // nearest list, which the drop-bound seed reads), the other sure ones in
     // id order (deterministic), then the band's best by (d, id)
-    uint32_t* out = plans + (uint64_t)b * nprobe;
     const uint32_t cmin = (uint32_t)(s_min & 0xffffffffu);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     uint32_t base_pos = 1;
@@ -398,7 +417,6 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
       __syncthreads();
     }
     if (threadIdx.x == 0) out[0] = cmin;
-    for (uint32_t i = threadIdx.x; i < nprobe - ns; i += blockDim.x) out[ns + i] = cid[i];
   }
   if (threadIdx.x == 0) flags[b] = 0;
 }

@@ -170,8 +170,22 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
         sn[v] = cand_n[slot0 + sp[v0 + v]];
         sthr[v] = cand_thr[slot0 + sp[v0 + v]];
       }
-      for (uint32_t idx = threadIdx.x; idx < nv * kKP; idx += blockDim.x)
-        sdv[idx] = cand_d[(slot0 + sp[v0 + idx / kKP]) * kKP + (idx % kKP)];
+      // 8 independent loads per thread in flight before the stores (one load
+      // per iteration left every thread waiting out the full latency each time)
+      const uint32_t tot = nv * kKP;
+      for (uint32_t i0 = threadIdx.x; i0 < tot; i0 += 8 * blockDim.x) {
+        float t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t idx = i0 + u * blockDim.x;
+          t[u] = idx < tot ? __ldg(cand_d + (slot0 + sp[v0 + idx / kKP]) * kKP + (idx % kKP)) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t idx = i0 + u * blockDim.x;
+          if (idx < tot) sdv[idx] = t[u];
+        }
+      }
       __syncthreads();
     };
     // 1. tau = k-th smallest upper bound
@@ -306,17 +320,37 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_search(
     });
     cid[i] = ix.ids[crow[i]];
   }
-  uint32_t mp = 1;
-  while (mp < m) mp <<= 1;
-  for (uint32_t i = m + threadIdx.x; i < mp; i += blockDim.x) {
-    cdist[i] = DBL_MAX;
-    cid[i] = ~0ull;
-  }
-  block_sort_pairs(cdist, cid, mp);
   const uint32_t cnt = (uint32_t)min((unsigned long long)k, s_total);
-  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-    ids_out[(uint64_t)b * k + i] = i < cnt ? cid[i] : 0;
-    d_out[(uint64_t)b * k + i] = i < cnt ? cdist[i] : 0.0;
+  if (m <= blockDim.x) {
+    // rank placement (doc ids of distinct rows are distinct, so ranks are):
+    // one barrier instead of the bitonic network's log^2 barriers
+    __syncthreads();
+    if (threadIdx.x < m) {
+      const double di = cdist[threadIdx.x];
+      const uint64_t ii = cid[threadIdx.x];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < m; ++j) r += pair_less(cdist[j], cid[j], di, ii) ? 1u : 0u;
+      if (r < cnt) {
+        ids_out[(uint64_t)b * k + r] = ii;
+        d_out[(uint64_t)b * k + r] = di;
+      }
+    }
+    for (uint32_t i = cnt + threadIdx.x; i < k; i += blockDim.x) {
+      ids_out[(uint64_t)b * k + i] = 0;
+      d_out[(uint64_t)b * k + i] = 0.0;
+    }
+  } else {
+    uint32_t mp = 1;
+    while (mp < m) mp <<= 1;
+    for (uint32_t i = m + threadIdx.x; i < mp; i += blockDim.x) {
+      cdist[i] = DBL_MAX;
+      cid[i] = ~0ull;
+    }
+    block_sort_pairs(cdist, cid, mp);
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+      ids_out[(uint64_t)b * k + i] = i < cnt ? cid[i] : 0;
+      d_out[(uint64_t)b * k + i] = i < cnt ? cdist[i] : 0.0;
+    }
   }
   if (threadIdx.x == 0) {
     counts_out[b] = cnt;
@@ -783,8 +817,12 @@ __global__ void __launch_bounds__(64) k_seed_bounds(IndexView ix, QueryView qv, 
   const float* base = list_base(ix, c, lbeg);
   double acc = __longlong_as_double(0x7ff0000000000000ll);
   if (t < rows) {
-    acc = 0.0;
-    for (uint32_t d = 0; d < ix.dim; ++d) acc = exact_step(acc, base[swz_offset(0, n_c, t, d, ix.dpad)], q[d]);
+    // 16-B loads of the row's swizzled granules, double-buffered ahead of the
+    // sequential chain ((x - q)^2 == (q - x)^2 exactly: the reference's
+    // squared_l2 operand order does not matter)
+    acc = exact_row_pipelined(ix.dim, q, [&](uint32_t g) {
+      return __ldg(reinterpret_cast<const float4*>(base + swz_offset(0, n_c, t, g * 4, ix.dpad)));
+    });
   }
   sd[t] = acc;
   __syncthreads();
