@@ -283,12 +283,12 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
                                                        uint32_t nprobe, CoarseBound bd,
                                                        uint32_t* __restrict__ plans,
                                                        double* __restrict__ dists, int* flags,
-                                                       uint32_t set_mode) {
+                                                       uint32_t set_mode, uint32_t cap) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
-  double* cd = reinterpret_cast<double*>(sm);                       // kCandCap
-  uint32_t* cid = reinterpret_cast<uint32_t*>(cd + kCandCap);         // kCandCap
-  double* qsh = reinterpret_cast<double*>(cid + kCandCap);            // dpad (widened once)
+  double* cd = reinterpret_cast<double*>(sm);                       // cap
+  uint32_t* cid = reinterpret_cast<uint32_t*>(cd + cap);              // cap
+  double* qsh = reinterpret_cast<double*>(cid + cap);                 // dpad (widened once)
   __shared__ uint32_t hist[256];
   __shared__ uint32_t s_cnt, s_ns, s_wcnt[16];
   __shared__ unsigned long long s_min;
@@ -337,13 +337,13 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
         atomicMin(&s_min, ((unsigned long long)f2key(row[c]) << 32) | c);
       } else {
         const uint32_t pos = atomicAdd(&s_cnt, 1u);
-        if (pos < kCandCap) cid[pos] = c;
+        if (pos < cap) cid[pos] = c;
       }
     }
   }
   __syncthreads();
   const uint32_t m = s_cnt, ns = s_ns;
-  if (m > kCandCap || !(tau <= FLT_MAX) || ns > nprobe || m + ns < nprobe) {  // degenerate: exact streaming path
+  if (m > cap || !(tau <= FLT_MAX) || ns > nprobe || m + ns < nprobe) {  // degenerate: exact streaming path
     if (threadIdx.x == 0) flags[b] = 1;
     return;
   }
@@ -581,13 +581,21 @@ CoarseBound coarse_bound_h16(uint32_t dim, float cmax) {
 void launch_coarse_select(const IndexView& ix, const QueryView& qv, const float* dist32,
                           uint32_t nprobe, const CoarseBound& bd, uint32_t* plans, double* dists, int* flags,
                           cudaStream_t s, bool set_mode) {
-  const size_t smem = (size_t)kCandCap * (8 + 4) + (size_t)ix.dpad * 8;
+  // candidate buffer: 4x the plan (>= 1024) -- more candidates take the
+  // exact streaming path -- instead of a fixed kCandCap, so dense batches keep
+  // several CTAs per SM resident while one's exact fp64 chains run
+  uint32_t cap = 1024;
+  while (cap < 4 * nprobe && cap < (uint32_t)kCandCap) cap <<= 1;
+  if (cap < nprobe) cap = nprobe;  // nprobe <= kNprobeMax = kCandCap
+  const size_t smem = (size_t)cap * (8 + 4) + (size_t)ix.dpad * 8;
   smem_optin((const void*)k_coarse_select, 220 * 1024);
   smem_optin((const void*)k_coarse_fallback, 200 * 1024);
-  // 512 threads: fewer (64-256, sized to the candidate count) measured slower
-  // (C2 41 -> 61 us, C3 59 -> 75 us)
-  launch_pdl(k_coarse_select, dim3(qv.n), dim3(512), smem, s, ix, qv, dist32, nprobe, bd, plans, dists, flags,
-             (set_mode && !dists) ? 1u : 0u);
+  // 512 threads for batches up to ~4 per SM (a query's latency is the step's:
+  // fewer threads measured slower, C2 41 -> 61 us, C3 59 -> 75 us); 256 for
+  // dense batches (twice the CTAs resident to cover the fp64 chains)
+  const int threads = qv.n > 4u * (uint32_t)device_sm_count() ? 256 : 512;
+  launch_pdl(k_coarse_select, dim3(qv.n), dim3(threads), smem, s, ix, qv, dist32, nprobe, bd, plans, dists, flags,
+             (set_mode && !dists) ? 1u : 0u, cap);
 }
 
 void launch_coarse_fallback(const IndexView& ix, const QueryView& qv, uint32_t nprobe,
