@@ -368,10 +368,13 @@ hivf_status hivf_last_stats(hivf_ctx* ctx, hivf_stats* out);
  * rest stays in pinned host memory, see residency; with "filter_h16" the fp16
  * filter copy of EVERY list is kept in HBM on top of the budget, so the scan
  * never crosses PCIe -- only the exact re-rank of cold lists' rows does),
- * "coarse_tc" (default 1: indexes created while 1 get an fp16 copy of the
- * centroids and the coarse assign's distance pass runs as one tcgen05
- * kind::f16 GEMM, filtered with the fp16 bound; 0: FFMA pass; plans identical;
- * process default from env HIVF_COARSE_TC),
+ * "coarse_tc" (default 1: indexes created while non-zero get an fp16 copy of
+ * the centroids and the coarse assign's distance pass of batches with at
+ * least 2^26 multiply-adds (B x K x dim) runs as one tcgen05 kind::f16 GEMM,
+ * filtered with the fp16 bound; 2: every batch; 0: FFMA pass; plans identical;
+ * process default from env HIVF_COARSE_TC), "coarse_set" (default 1: the
+ * batched search's coarse select needs its plans only as sets and re-ranks
+ * only the centroids its bound cannot place),
  * "seed_rows" (default 32, 0 = off, <= 64) / "seed_ppl" (default 16): batches
  * with at least seed_ppl probes per list seed each query's shared drop bound
  * with the exact distances of seed_rows rows of its nearest probed list,
