@@ -178,7 +178,7 @@ hivf_status hivf_ctx_create(int device, void* stream, hivf_ctx** out) {
   // process default of option "filter_h16" (env HIVF_FILTER_H16=0 runs every
   // scan on the fp32 lists, e.g. the whole GPU suite on that path)
   if (const char* e = getenv("HIVF_FILTER_H16")) c->opt_h16 = atoi(e) != 0;
-  if (const char* e = getenv("HIVF_COARSE_TC")) c->opt_coarse_tc = atoi(e) != 0;
+  if (const char* e = getenv("HIVF_COARSE_TC")) c->opt_coarse_tc = std::min(2, std::max(0, atoi(e)));
   if (const char* e = getenv("HIVF_COARSE_SET")) c->opt_coarse_set = atoi(e) != 0;
   *out = c;
   return HIVF_OK;
@@ -230,7 +230,8 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
   } else if (!strcmp(name, "coarse_set")) {  // 1: the search's coarse select re-ranks only its uncertain band
     ctx->opt_coarse_set = value != 0;
   } else if (!strcmp(name, "coarse_tc")) {  // 1: tensor-core coarse distances (fp16 centroid copy)
-    ctx->opt_coarse_tc = value != 0;
+    if (value < 0 || value > 2) return fail(HIVF_EINVAL, "coarse_tc must be 0, 1 or 2");
+    ctx->opt_coarse_tc = (int)value;
   } else if (!strcmp(name, "filter_h16")) {  // 1: fp16 filter copy built at index finish and used
     ctx->opt_h16 = value != 0;
   } else if (!strcmp(name, "seg_rows")) {  // 0: automatic (auto_seg_rows)
@@ -810,14 +811,19 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
     c->last_coarse_bits = 0;
     return HIVF_OK;
   }
-  const uint32_t splits = (ix->centh && c->opt_coarse_tc) ? 1u : coarse_dist_splits(v, qv.n);
+  // tensor-core pass from 2^26 multiply-adds (C3 B=256 66 -> 22 us, neutral
+  // at C2); below that the FFMA tile GEMM's single launch is faster (C1: 64
+  // queries x 256 centroids x 128 dims)
+  const bool coarse_tc = ix->centh && (c->opt_coarse_tc == 2 ||
+                                       (c->opt_coarse_tc == 1 && (uint64_t)qv.n * ix->K * ix->dpad >= (1ull << 26)));
+  const uint32_t splits = coarse_tc ? 1u : coarse_dist_splits(v, qv.n);
   float* part = nullptr;
   if (splits > 1) {
     CK(c->coarse_part.ensure((size_t)splits * qv.n * ix->K * 4));
     part = c->coarse_part.as<float>();
   }
   CoarseBound bd = coarse_bound_ffma(ix->dim);
-  if (ix->centh && c->opt_coarse_tc) {
+  if (coarse_tc) {
     // tensor-core pass: the batch's fp16 query copy, then one kind::f16 GEMM
     CK(c->qh16.ensure(coarse_tc_bytes(qv.n, ix->dpad)));
     launch_pack_coarse_tc(qv.qs, qv.n, ix->dpad, qv.qsc, 0.f, c->qh16.as<uint8_t>(), c->stream);

@@ -113,8 +113,9 @@ struct hivf_ctx {
   // used by the single-pass tensor-core scan while 1
   int opt_h16 = 1;
   // coarse distances on the tensor cores (option "coarse_tc", env HIVF_COARSE_TC):
-  // kind::f16 over fp16 copies of centroids and queries, used while 1 by
-  // indexes that have the centroid copy (built at index creation when 1)
+  // kind::f16 over fp16 copies of centroids and queries, for indexes that have
+  // the centroid copy (built at index creation unless 0); 1 = batches of at
+  // least 2^26 multiply-adds, 2 = always, 0 = never
   int opt_coarse_tc = 1;
   // search path: coarse select in set mode (option "coarse_set", env
   // HIVF_COARSE_SET): only centroids the bound cannot place get the exact double

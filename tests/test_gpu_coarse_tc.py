@@ -25,7 +25,7 @@ def torch_ok():
 def _index(coarse_tc, X, cents, metric=0):
     from paper_2507_09138_b200 import Context, IvfIndex
     ctx = Context(0)
-    ctx.set_option("coarse_tc", coarse_tc)
+    ctx.set_option("coarse_tc", 2 if coarse_tc else 0)  # 2: every batch, whatever its size
     ids = np.arange(len(X), dtype=np.uint64) * 7 + 3
     assign = oracle.compute_assignments(X, cents)
     csr = oracle.CsrIndex.from_assignments(X, ids, cents, assign, metric)
@@ -119,7 +119,7 @@ def test_search_set_mode_duplicate_centroids(torch_ok, coarse_tc):
     csr = oracle.CsrIndex.from_assignments(X, ids, cents, assign)
     from paper_2507_09138_b200 import Context, IvfIndex
     ctx = Context(0)
-    ctx.set_option("coarse_tc", coarse_tc)
+    ctx.set_option("coarse_tc", 2 if coarse_tc else 0)
     ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
     Q = (base[rng.integers(0, K // 2, 200)] + 0.4 * rng.standard_normal((200, dim))).astype(np.float32)
     for nprobe, k in ((1, 10), (7, 10), (15, 5), (33, 20)):
@@ -131,3 +131,21 @@ def test_search_set_mode_duplicate_centroids(torch_ok, coarse_tc):
             np.testing.assert_array_equal(gi, oi)
             assert np.array_equal(gd.view(np.uint64), od.view(np.uint64))
     ctx.set_option("coarse_set", 1)
+
+
+def test_coarse_tc_size_threshold(torch_ok):
+    """Default (coarse_tc = 1): the tensor-core pass from 2^26 multiply-adds,
+    the FFMA pass below; plans identical either way."""
+    rng = np.random.default_rng(3)
+    dim, K = 128, 1024
+    X = rng.standard_normal((5000, dim)).astype(np.float32)
+    cents = X[rng.choice(len(X), K, replace=False)].copy()
+    from paper_2507_09138_b200 import Context, IvfIndex
+    ctx = Context(0)
+    ctx.set_option("coarse_tc", 1)
+    ids = np.arange(len(X), dtype=np.uint64)
+    csr = oracle.CsrIndex.from_assignments(X, ids, cents, oracle.compute_assignments(X, cents))
+    ix = IvfIndex.upload(ctx, csr.centroids, csr.off, csr.vectors, csr.ids)
+    for B, bits in ((16, 32), (600, 16)):  # 16 x 1024 x 128 = 2^21; 600 x 1024 x 128 > 2^26
+        Q = rng.standard_normal((B, dim)).astype(np.float32)
+        _check_plans(ctx, ix, csr, Q, 20, bits=bits)
