@@ -2564,8 +2564,11 @@ constexpr uint32_t kCdTile = 128;                          // centroids / querie
 constexpr uint32_t kCdCps = 2;                             // 32-dim chunks per stage
 constexpr uint32_t kCdStageDims = kCdCps * 32;             // 64
 constexpr uint32_t kCdOpBytes = kCdTile * kCdStageDims * 2;  // 16 KB per operand per stage
-constexpr uint32_t kCdRing = 3;
-constexpr uint32_t kCdSmem = kCdRing * 2 * kCdOpBytes + 1024 + 128;
+// ring depth: 3 stages (96 KB, 2 CTAs per SM) for grids that fill the GPU, 6
+// (192 KB, one CTA per SM) for small grids, where each CTA's chain of stage
+// loads is the kernel's latency (C2 / C3 B=256: 16-64 CTAs, 12 stages each)
+template <uint32_t kCdRing>
+constexpr uint32_t cd_smem() { return kCdRing * 2 * kCdOpBytes + 1024 + 128; }
 
 // byte offset of the 16-B granule holding dims [d, d + 8) of row r of a tile
 // (layout [tile][stage][chunk][row 0..127][64 B, SWIZZLE_64B: granule g at g ^ ((r >> 1) & 3)])
@@ -2613,6 +2616,7 @@ struct CdParams {
   uint32_t K, n, S;
 };
 
+template <uint32_t kCdRing>
 __global__ void __launch_bounds__(192, 1) k_coarse_dist_tc(CdParams P) {
   pdl_wait();
   extern __shared__ uint8_t cd_raw[];
@@ -2716,9 +2720,14 @@ void launch_pack_coarse_tc(const float* src, uint32_t n, uint32_t dpad, const fl
 void launch_coarse_dist_tc(const IndexView& ix, const QueryView& qv, const uint8_t* cent_h16, float csc,
                            const uint8_t* q_h16, float* dist32, cudaStream_t s) {
   if (!qv.n) return;
-  smem_optin((const void*)k_coarse_dist_tc, kCdSmem);
   CdParams P{cent_h16, q_h16, ix.cnorm2, qv.qn2, qv.qsc, csc, dist32, ix.K, qv.n, coarse_tc_stages(ix.dpad)};
-  launch_pdl(k_coarse_dist_tc, dim3((ix.K + kCdTile - 1) / kCdTile, (qv.n + kCdTile - 1) / kCdTile), dim3(192),
-             (size_t)kCdSmem, s, P);
+  const dim3 grid((ix.K + kCdTile - 1) / kCdTile, (qv.n + kCdTile - 1) / kCdTile);
+  if ((uint64_t)grid.x * grid.y <= (uint64_t)device_sm_count()) {
+    smem_optin((const void*)k_coarse_dist_tc<6>, cd_smem<6>());
+    launch_pdl(k_coarse_dist_tc<6>, grid, dim3(192), (size_t)cd_smem<6>(), s, P);
+  } else {
+    smem_optin((const void*)k_coarse_dist_tc<3>, cd_smem<3>());
+    launch_pdl(k_coarse_dist_tc<3>, grid, dim3(192), (size_t)cd_smem<3>(), s, P);
+  }
 }
 }  // namespace hivf
