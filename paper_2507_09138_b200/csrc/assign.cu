@@ -308,9 +308,9 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
   const double qd = qn;
   const float cA = __double2float_ru(bd.ea * qd), cB = __double2float_ru(bd.eb),
               cC = __double2float_ru(bd.eb * qd * qd + bd.ec + bd.es * qd);
-  auto bound_E = [&](const CoarseBound&, float, float cn) { return __fmaf_ru(cn, __fmaf_ru(cn, cB, cA), cC); };
+  auto E_of = [&](float cn) { return __fmaf_ru(cn, __fmaf_ru(cn, cB, cA), cC); };
   auto ub_key = [&](uint32_t c) {
-    return f2key(__fadd_ru(row[c], bound_E(bd, qn, ix.cnorm[c])));
+    return f2key(__fadd_ru(row[c], E_of(ix.cnorm[c])));
   };
   const uint32_t tau_key = block_radix_select(ix.K, nprobe, ub_key, hist);
   const float tau = key2f(tau_key);
@@ -324,12 +324,12 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
   float L = -FLT_MAX;
   if (set_mode) {
     auto lb_key = [&](uint32_t c) {
-      return f2key(__fsub_rd(row[c], bound_E(bd, qn, ix.cnorm[c])));
+      return f2key(__fsub_rd(row[c], E_of(ix.cnorm[c])));
     };
     L = key2f(block_radix_select(ix.K, nprobe, lb_key, hist));
   }
   for (uint32_t c = threadIdx.x; c < ix.K; c += blockDim.x) {
-    const float E = bound_E(bd, qn, ix.cnorm[c]);
+    const float E = E_of(ix.cnorm[c]);
     const float lb = __fsub_rd(row[c], E);
     if (lb <= tau) {
       if (set_mode && __fadd_ru(row[c], E) < L) {  // sure
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(512) k_coarse_select(IndexView ix, QueryView q
       const uint32_t c = base + threadIdx.x;
       bool sure = false;
       if (c < ix.K && c != cmin) {
-        const float E = bound_E(bd, qn, ix.cnorm[c]);
+        const float E = E_of(ix.cnorm[c]);
         sure = __fsub_rd(row[c], E) <= tau && __fadd_ru(row[c], E) < L;
       }
       const unsigned bal = __ballot_sync(0xffffffffu, sure);
