@@ -831,6 +831,7 @@ static hivf_status run_assign(hivf_index* ix, const QueryView& qv, uint32_t npro
     launch_coarse_dist_tc(v, qv, ix->centh, ix->csc, c->qh16.as<uint8_t>(), c->dist32.as<float>(), c->stream);
     bd = coarse_bound_h16(ix->dim, ix->cmax);
     c->last_coarse_bits = 16;
+    c->stats.kernels_launched += 1;  // k_pack_cd
   } else {
     c->last_coarse_bits = 32;
     launch_coarse_dist(v, qv, c->dist32.as<float>(), c->stream, part);
