@@ -229,7 +229,7 @@ hivf_status hivf_set_option(hivf_ctx* ctx, const char* name, int64_t value) {
     ctx->opt_seed_ppl = (float)value;
   } else if (!strcmp(name, "coarse_set")) {  // 1: the search's coarse select re-ranks only its uncertain band
     ctx->opt_coarse_set = value != 0;
-  } else if (!strcmp(name, "coarse_tc")) {  // 1: tensor-core coarse distances (fp16 centroid copy)
+  } else if (!strcmp(name, "coarse_tc")) {  // tensor-core coarse pass: 0 never, 1 from 2^26 multiply-adds, 2 always
     if (value < 0 || value > 2) return fail(HIVF_EINVAL, "coarse_tc must be 0, 1 or 2");
     ctx->opt_coarse_tc = (int)value;
   } else if (!strcmp(name, "filter_h16")) {  // 1: fp16 filter copy built at index finish and used
